@@ -1,0 +1,183 @@
+/* hn.h -- C ABI of libhn.so, the sm_100a hot path of the hybrid scattered-regular
+ * RBF-FD method (arXiv 2303.01760), drop-in beneath the reference package
+ * `hybridnodes` (pkg/src/hybridnodes).
+ *
+ * The reference is pure Python over numpy/scipy; its "FFI" for this path is the set of
+ * third-party native calls it makes (scipy cKDTree, LAPACK dgesv via np.linalg.solve,
+ * scipy csr_matvec, SuperLU + bicgstab).  Each entry point below replaces one of them
+ * and cites the reference call site.  Python binds this header with ctypes
+ * (paper_2303_01760_b200/_lib.py); INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - plain C types only; every array is a DEVICE pointer unless its name ends in
+ *     `_host` (small parameter arrays read on the host during the call);
+ *   - every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy stream);
+ *   - return 0 on success, a negative value = -(cudaError_t) on a CUDA failure, a
+ *     positive value for an argument error (documented per call); numerical failures
+ *     (singular systems, non-finite fields) are reported through device `info` arrays;
+ *   - the library never frees caller memory; scratch is caller-provided or taken from
+ *     the stream-ordered allocator and released before the call returns;
+ *   - index arrays are int32 (N < 2^31 nodes); fields and weights are fp64.
+ */
+#ifndef HN_H_
+#define HN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* operator kinds (approx.py:35-52: Laplacian / Partial / NormalDerivative) */
+#define HN_OP_LAPLACIAN 0
+#define HN_OP_PARTIAL 1
+#define HN_OP_NORMAL 2
+
+/* ---------------------------------------------------------------- stencils (K1-K3) */
+
+/* Uniform cell list over positions (N x stride fp64 AoS, stride 2 in 2D / 4 in 3D).
+ * cell_start: ncells+1, cell_items: N, cell_pos: N*stride, scratch_count: ncells,
+ * scratch_point_cell: N, with ncells = prod(dims_host[0..d)).
+ * Replaces: cKDTree(nodeset.positions)  approx.py:386, solver.py:144. */
+int hn_celllist_build(const double* pos, int64_t n, int d, const double* lo_host, double cell,
+                      const int* dims_host, int* cell_start, int* cell_items, double* cell_pos,
+                      int* scratch_count, int* scratch_point_cell, void* stream);
+
+/* n nearest nodes of each query by the key (fl-distance, node index); queries are node
+ * ids (queries, NULL = 0..nq-1) or, when qpos != NULL, points (nq x stride fp64).
+ * out_idx (nq x n) ascending by key, out_dist optional.
+ * exclude (N bytes, nonzero = skip) or NULL.  1 <= n <= 64.
+ * Replaces: _knn_sorted approx.py:133-146 (cKDTree.query + tie widening + lexsort) and
+ * the sub-tree query of _boundary_stencils approx.py:425-431. */
+int hn_knn(const double* pos, int d, const double* lo_host, double cell, const int* dims_host,
+           const int* cell_start, const int* cell_items, const double* cell_pos,
+           const int* queries, const double* qpos, int64_t nq, int n, const uint8_t* exclude,
+           int* out_idx, double* out_dist, void* stream);
+
+/* method per node: -1 boundary, 0 MON, 1 RBF-FD.  lattice_idx (N x d int32, INT32_MIN =
+ * off-lattice) and grid (prod(grid_dims) int32, -1 vacant) may be NULL (no lattice).
+ * Replaces: classify_methods approx.py:332-351. */
+int hn_classify(const int8_t* kind, const int* lattice_idx, const int* grid,
+                const int* grid_dims_host, int64_t n, int d, int8_t* method, void* stream);
+
+/* MON stencils [row, axis neighbours sorted by (distance, index)] -> out (nrows x (2d+1)).
+ * Replaces: _mon_stencils approx.py:360-376. */
+int hn_mon_stencils(const int* rows, int64_t nrows, const double* pos, const int* lattice_idx,
+                    const int* grid, const int* grid_dims_host, int d, int* out, void* stream);
+
+/* ----------------------------------------------------------------- weights (K4-K5) */
+
+/* Outputs go straight into an ELL slab of K rows: out_idx[j*K + k] (ascending node ids),
+ * out_w[(op*n + j)*K + k]; info[k] = 0 or (first zero-pivot step + 1).
+ * op_kind_host/op_axis_host: nops entries; op_normal_host: nops x d (NormalDerivative). */
+
+/* MON (2d+1)^2 collocation solves.  Replaces: _batched_mon_weights approx.py:212-234. */
+int hn_weights_mon(const double* pos, int d, const int* stencils, int64_t K, int nops,
+                   const int* op_kind_host, const int* op_axis_host, const double* op_normal_host,
+                   int* out_idx, double* out_w, int* info, void* stream);
+
+/* RBF-FD PHS r^3 + degree-2 saddle solves ((n+q)^2, q = 6 / 10).  row_normals (K x d) or
+ * NULL: when given, every op must be HN_OP_NORMAL and uses its row's normal (the
+ * `normals` variant, approx.py:260-270).  Tuned warp-cooperative kernels exist for
+ * (d,n) = (2,12), (3,20), (3,30) and 1..4 ops (hn_weights_rbf_is_tuned); other sizes use a
+ * generic thread-per-stencil kernel that needs `workspace` of
+ * hn_weights_rbf_workspace(d, n, nops, K) doubles (returns 3 if workspace is NULL then).
+ * Replaces: _batched_rbf_weights approx.py:237-290. */
+int hn_weights_rbf(const double* pos, int d, const int* stencils, int64_t K, int n, int nops,
+                   const int* op_kind_host, const int* op_axis_host, const double* op_normal_host,
+                   const double* row_normals, double* workspace, int* out_idx, double* out_w,
+                   int* info, void* stream);
+int hn_weights_rbf_is_tuned(int d, int n, int nops);
+/* Launch-shape variant of the tuned 2D kernel (0 = default); a tuning knob, not numerics. */
+void hn_weights_rbf_set_variant(int v);
+int64_t hn_weights_rbf_workspace(int d, int n, int nops, int64_t K);
+
+/* --------------------------------------------------------------- application (K6) */
+
+/* out[o*out_stride + rows_b[k]] = sum_j w_b[(op_sel[o]*W_b + j)*K_b + k] * field[idx_b[j*K_b + k]]
+ * over up to 4 bins b (widths 0,5,7,12,20,30; width 0 writes zeros), 1..4 ops.
+ * Bit-identical to scipy csr_matvec (sequential, ascending columns, no FMA).
+ * Replaces: SparseOperator.apply / apply / divergence operators.py:51-54,80-90. */
+int hn_apply_ell(int nbins, const int64_t* bin_K_host, const int* bin_width_host,
+                 const int* const* bin_rows_host, const int* const* bin_idx_host,
+                 const double* const* bin_w_host, int nops, const int* op_sel_host,
+                 const double* field, double* out, int64_t out_stride, void* stream);
+
+/* ------------------------------------------------------ explicit step (K7, K8, K10, K11) */
+
+/* Bins as in hn_apply_ell over the interior operator table; planes lap_plane and
+ * d_plane_host[0..d) select the Laplacian and d/dx_a weight planes.  State is SoA:
+ * v[c*N + i]. */
+
+/* v* = v + dt*(-(v.grad)v + Pr lap v - buoy_c (T - t_ref)); buoy_host[c] = (Ra*Pr)*g[c].
+ * zero_boundary != 0 fuses apply_velocity_bc (v* = 0 on the width-0 bin rows).
+ * Replaces: momentum_predict + apply_velocity_bc solver.py:250-280. */
+int hn_momentum(int nbins, const int64_t* bin_K_host, const int* bin_width_host,
+                const int* const* bin_rows_host, const int* const* bin_idx_host,
+                const double* const* bin_w_host, int lap_plane, const int* d_plane_host, int d,
+                const double* v, const double* T, int64_t N, double dt, double Pr, double t_ref,
+                const double* buoy_host, int zero_boundary, double* vstar, void* stream);
+
+/* rhs[0..N) = (sum_a D_a v*_a)/dt on interior rows, 0 on boundary rows; rhs[N] = 0.
+ * Replaces: solver.py:295-301. */
+int hn_div_rhs(int nbins, const int64_t* bin_K_host, const int* bin_width_host,
+               const int* const* bin_rows_host, const int* const* bin_idx_host,
+               const double* const* bin_w_host, const int* d_plane_host, int d, const double* vstar,
+               int64_t N, double dt, double* rhs, void* stream);
+
+/* v = v* - dt grad p (0 on boundary); T' = T + dt(-v.grad T + lap T) with the corrected v.
+ * flags[0] |= 1 on any non-finite output, flags[1] = min non-finite T node (init INT_MAX).
+ * Replaces: velocity_correct + temperature_step solver.py:317-331, 345-357. */
+int hn_correct_temperature(int nbins, const int64_t* bin_K_host, const int* bin_width_host,
+                           const int* const* bin_rows_host, const int* const* bin_idx_host,
+                           const double* const* bin_w_host, int lap_plane, const int* d_plane_host, int d,
+                           const double* vstar, const double* p, const double* T, int64_t N, double dt,
+                           double* vout, double* Tout, int* flags, void* stream);
+
+/* T[dir_idx] = dir_val; T[neu_idx[r]] = -(W_r . t0) / neu_diag[r], t0 = T with Neumann
+ * entries zeroed (is_neu mask).  Replaces: apply_temperature_bc solver.py:334-342. */
+int hn_temperature_bc(const int* dir_idx, const double* dir_val, int64_t ndir, const int64_t* neu_rowptr,
+                      const int* neu_cols, const double* neu_vals, const int* neu_idx,
+                      const double* neu_diag, const uint8_t* is_neu, int64_t nneu, double* T,
+                      void* stream);
+
+/* y = A x / y = b - A x for a CSR matrix (int64 rowptr), scipy csr_matvec order. */
+int hn_csr_matvec(const int64_t* rowptr, const int* cols, const double* vals, const double* x,
+                  int64_t nrows, double* y, void* stream);
+int hn_csr_residual(const int64_t* rowptr, const int* cols, const double* vals, const double* x,
+                    const double* b, int64_t nrows, double* y, void* stream);
+
+/* ---------------------------------------------------------------- pressure (K9, K12) */
+
+/* Sync-free triangular solve.  lower != 0: unit-lower L (strict part in CSR), rows 0..n-1;
+ * lower == 0: strict-upper U in CSR + diag, rows n-1..0.  ticket: one device uint64.
+ * Replaces: SuperLU lu.solve inside the bicgstab preconditioner, solver.py:213-214. */
+int hn_sptrsv(int lower, const int64_t* rowptr, const int* cols, const double* vals, const double* diag,
+              const double* b, double* x, int64_t n, unsigned long long* ticket, void* stream);
+
+/* direction 0: out[perm[i]] = in[i]; direction 1: out[i] = in[perm[i]]. */
+int hn_permute(int direction, const int* perm, const double* in, int64_t n, double* out, void* stream);
+
+/* Deterministic reduction into out[0]: op 0 dot(a,b), 1 max|a|, 2 sum|a|, 3 sum a; idx
+ * optional gather; scratch >= 296 doubles. */
+int hn_reduce(int op, const double* a, const double* b, const int* idx, int64_t n, double* scratch,
+              double* out, void* stream);
+
+/* BiCGStab updates in numpy operation order: kind 0 y = ((y - alpha*x)*beta) + r;
+ * kind 1 y = y + alpha*x. */
+int hn_bicg_update(int kind, double* y, const double* x, const double* r, double alpha, double beta,
+                   int64_t n, void* stream);
+
+/* ----------------------------------------------------------- diagnostics / peaks */
+
+/* DFMA throughput probe: `blocks` x 256 threads, `iters` x 16 independent DFMA chains
+ * per thread; out[0] receives a checksum.  Used by bench.py for the fp64 peak. */
+int hn_bench_dfma(double* out, int blocks, int iters, void* stream);
+
+int hn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HN_H_ */

@@ -1,0 +1,214 @@
+"""Device-resident forms of the hot-path data (HBM layout).
+
+* DeviceNodes  -- padded AoS positions (stride 2 in 2D, 4 in 3D), kind, lattice map and
+                  the uniform cell list; one per NodeSet, cached.
+* Bin          -- one ELL slab of rows sharing a stencil width: rows[K], idx[W][K],
+                  w[op][W][K] (column-major so a warp of rows reads each column coalesced).
+* DeviceTable  -- the bins of one weight table (MON / RBF / boundary), with the host
+                  WeightTable arrays produced on demand.
+"""
+
+from __future__ import annotations
+
+import weakref
+
+import numpy as np
+
+from . import _lib as L
+
+INT32_MIN = np.iinfo(np.int32).min
+ELL_WIDTHS = (0, 5, 7, 12, 20, 30)
+
+
+def _pos_stride(dim: int) -> int:
+    return 2 if dim == 2 else 4
+
+
+def pad_positions(positions: np.ndarray) -> np.ndarray:
+    n, d = positions.shape
+    out = np.zeros((n, _pos_stride(d)))
+    out[:, :d] = positions
+    return out
+
+
+class DeviceNodes:
+    """Device copy of a node set plus its cell list (replaces cKDTree, approx.py:386)."""
+
+    def __init__(self, nodeset):
+        t = L.torch()
+        pos = np.asarray(nodeset.positions, dtype=float)
+        self.n, self.dim = pos.shape
+        if self.dim not in (2, 3):
+            raise ValueError("node sets must be 2D or 3D")
+        self.stride = _pos_stride(self.dim)
+        self.pos = L.to_device(pad_positions(pos))
+        self.kind = L.to_device(np.asarray(nodeset.kind, dtype=np.int8))
+        self.lattice_grid = self.lattice_idx = None
+        self.grid_dims = None
+        lat = getattr(nodeset, "lattice", None)
+        lidx = getattr(nodeset, "lattice_idx", None)
+        if lat is not None and lidx is not None:
+            grid = np.asarray(lat.grid)
+            self.grid_dims = list(grid.shape)
+            self.lattice_grid = L.to_device(grid.astype(np.int32))
+            li = np.asarray(lidx)
+            li32 = np.where(li == np.iinfo(np.int64).min, INT32_MIN, li).astype(np.int32)
+            self.lattice_idx = L.to_device(li32)
+        # uniform cell list: ~1 node per cell in 2D, ~2 in 3D
+        lo = pos.min(axis=0) if self.n else np.zeros(self.dim)
+        hi = pos.max(axis=0) if self.n else np.ones(self.dim)
+        ext = np.maximum(hi - lo, 1e-300)
+        vol = float(np.prod(ext))
+        cell = (vol / max(self.n, 1)) ** (1.0 / self.dim) * (1.0 if self.dim == 2 else 1.25)
+        if not np.isfinite(cell) or cell <= 0:
+            cell = float(np.max(ext)) or 1.0
+        dims = [int(np.floor(ext[a] / cell)) + 1 for a in range(self.dim)]
+        while int(np.prod(dims)) > 4 * max(self.n, 1) + 64:
+            cell *= 1.25
+            dims = [int(np.floor(ext[a] / cell)) + 1 for a in range(self.dim)]
+        self.lo, self.cell, self.dims = lo.astype(float), float(cell), dims
+        ncells = int(np.prod(dims))
+        self.cell_start = L.empty(ncells + 1, t.int32)
+        self.cell_items = L.empty(max(self.n, 1), t.int32)
+        self.cell_pos = L.empty((max(self.n, 1), self.stride), t.float64)
+        scratch = L.empty(ncells, t.int32)
+        scratch2 = L.empty(max(self.n, 1), t.int32)
+        L.call("hn_celllist_build", L.ptr(self.pos), self.n, self.dim, L.host_dbls(self.lo), self.cell,
+               L.host_ints(dims), L.ptr(self.cell_start), L.ptr(self.cell_items), L.ptr(self.cell_pos),
+               L.ptr(scratch), L.ptr(scratch2), L.stream_handle())
+        self._keep = (scratch, scratch2)
+
+    def knn(self, n: int, rows=None, points: np.ndarray | None = None, exclude=None, with_dist: bool = False):
+        """n nearest nodes by (fl-distance, index) for node ids `rows` or query `points`."""
+        t = L.torch()
+        qpos = None
+        if points is not None:
+            pts = np.atleast_2d(np.asarray(points, float))
+            nq = len(pts)
+            qpos = L.to_device(pad_positions(pts))
+            q = None
+        elif rows is None:
+            nq = self.n
+            q = None
+        else:
+            q = rows if hasattr(rows, "data_ptr") else L.to_device(np.asarray(rows, dtype=np.int32))
+            nq = int(q.numel())
+        out = L.empty((max(nq, 1), n), t.int32)
+        dist = L.empty((max(nq, 1), n), t.float64) if with_dist else None
+        ex = None
+        if exclude is not None:
+            ex = exclude if hasattr(exclude, "data_ptr") else L.to_device(np.asarray(exclude, dtype=np.uint8))
+        if nq:
+            L.call("hn_knn", L.ptr(self.pos), self.dim, L.host_dbls(self.lo), self.cell, L.host_ints(self.dims),
+                   L.ptr(self.cell_start), L.ptr(self.cell_items), L.ptr(self.cell_pos), L.ptr(q), L.ptr(qpos),
+                   nq, n, L.ptr(ex), L.ptr(out), L.ptr(dist), L.stream_handle())
+        out = out[:nq]
+        return (out, dist[:nq]) if with_dist else out
+
+    def classify(self):
+        t = L.torch()
+        method = L.empty(max(self.n, 1), t.int8)
+        has_lat = self.lattice_grid is not None
+        L.call("hn_classify", L.ptr(self.kind), L.ptr(self.lattice_idx if has_lat else None),
+               L.ptr(self.lattice_grid if has_lat else None),
+               L.host_ints(self.grid_dims if has_lat else [1, 1, 1]), self.n, self.dim, L.ptr(method),
+               L.stream_handle())
+        return method[: self.n]
+
+    def mon_stencils(self, rows):
+        t = L.torch()
+        k = int(rows.numel())
+        out = L.empty((max(k, 1), 2 * self.dim + 1), t.int32)
+        if k:
+            L.call("hn_mon_stencils", L.ptr(rows), k, L.ptr(self.pos), L.ptr(self.lattice_idx),
+                   L.ptr(self.lattice_grid), L.host_ints(self.grid_dims), self.dim, L.ptr(out), L.stream_handle())
+        return out[:k]
+
+
+_NODE_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def device_nodes(nodeset) -> DeviceNodes:
+    """Cached DeviceNodes for a node set (rebuilt if its position array was replaced)."""
+    key_arr = nodeset.positions
+    try:
+        ent = _NODE_CACHE.get(nodeset)
+    except TypeError:
+        ent = None
+    if ent is not None and ent[0] is key_arr and ent[1] == key_arr.shape:
+        return ent[2]
+    dn = DeviceNodes(nodeset)
+    try:
+        _NODE_CACHE[nodeset] = (key_arr, key_arr.shape, dn)
+    except TypeError:
+        pass
+    return dn
+
+
+class Bin:
+    """ELL slab: K rows of stencil width W and n_ops weight planes (device)."""
+
+    def __init__(self, rows_host: np.ndarray, width: int, d_idx, d_w, d_rows=None):
+        self.rows_host = np.asarray(rows_host, dtype=np.int64)
+        self.K = len(self.rows_host)
+        self.width = int(width)
+        self.d_rows = d_rows if d_rows is not None else L.to_device(self.rows_host.astype(np.int32))
+        self.d_idx = d_idx  # (W, K) int32
+        self.d_w = d_w      # (nops, W, K) fp64
+
+
+def bins_args(bins):
+    """ctypes argument block (nbins, K[], W[], rows*[], idx*[], w*[]) for the ELL kernels."""
+    live = [b for b in bins if b.K > 0]
+    return (len(live), L.host_i64([b.K for b in live]), L.host_ints([b.width for b in live]),
+            L.host_ptrs([b.d_rows for b in live]), L.host_ptrs([b.d_idx for b in live]),
+            L.host_ptrs([b.d_w for b in live]), live)
+
+
+class DeviceTable:
+    """All bins of one weight table (rows of every node appear in exactly one bin)."""
+
+    def __init__(self, n: int, dim: int, ops: list, bins: list, n_max: int, method: np.ndarray | None = None):
+        self.n, self.dim, self.ops, self.bins, self.n_max = n, dim, list(ops), bins, n_max
+        self.method = method
+
+    @property
+    def ell_ok(self) -> bool:
+        return all(b.width in ELL_WIDTHS for b in self.bins) and len([b for b in self.bins if b.K]) <= 4
+
+    def sizes(self) -> np.ndarray:
+        s = np.zeros(self.n, dtype=np.int64)
+        for b in self.bins:
+            s[b.rows_host] = b.width
+        return s
+
+    def host_arrays(self):
+        """(indices (N, n_max) int64 -1 padded, sizes, {op: (N, n_max)}) -- the WeightTable layout."""
+        indices = np.full((self.n, self.n_max), -1, dtype=np.int64)
+        weights = {op: np.zeros((self.n, self.n_max)) for op in self.ops}
+        for b in self.bins:
+            if b.K == 0 or b.width == 0:
+                continue
+            idx = b.d_idx.cpu().numpy().T  # (K, W)
+            indices[b.rows_host, : b.width] = idx
+            w = b.d_w.cpu().numpy()        # (nops, W, K)
+            for j, op in enumerate(self.ops):
+                weights[op][b.rows_host, : b.width] = w[j].T
+        return indices, self.sizes(), weights
+
+    @staticmethod
+    def from_host(indices: np.ndarray, sizes: np.ndarray, weights: dict, ops: list, dim: int) -> "DeviceTable":
+        """Bins from WeightTable arrays (rows grouped by stencil size)."""
+        t = L.torch()
+        n, n_max = indices.shape
+        bins = []
+        for w in np.unique(sizes):
+            rows = np.nonzero(sizes == w)[0]
+            w = int(w)
+            if w == 0:
+                bins.append(Bin(rows, 0, L.empty((0, len(rows)), t.int32), L.empty((len(ops), 0, len(rows)), t.float64)))
+                continue
+            idx = np.ascontiguousarray(indices[rows, :w].T.astype(np.int32))
+            wt = np.stack([np.ascontiguousarray(weights[op][rows, :w].T) for op in ops])
+            bins.append(Bin(rows, w, L.to_device(idx), L.to_device(wt)))
+        return DeviceTable(n, dim, ops, bins, n_max)

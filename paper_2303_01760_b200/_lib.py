@@ -1,0 +1,153 @@
+"""ctypes binding of libhn.so (include/hn.h) plus the device-memory plumbing.
+
+torch provides device memory and the current CUDA stream only; every computation on
+the hot path is a libhn.so kernel.  There is no CPU fallback: if the library or a GPU
+is missing, `lib()` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libhn.so"
+
+_c_int_p = C.POINTER(C.c_int)
+_c_i64_p = C.POINTER(C.c_int64)
+_c_dbl_p = C.POINTER(C.c_double)
+_vp = C.c_void_p
+_i = C.c_int
+_i64 = C.c_int64
+_d = C.c_double
+
+# name -> (restype, argtypes); mirrors include/hn.h exactly (tests check the export list)
+SIGNATURES: dict[str, tuple] = {
+    "hn_version": (_i, []),
+    "hn_bench_dfma": (_i, [_vp, _i, _i, _vp]),
+    "hn_celllist_build": (_i, [_vp, _i64, _i, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hn_knn": (_i, [_vp, _i, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp, _vp, _vp, _i64, _i, _vp, _vp, _vp, _vp]),
+    "hn_classify": (_i, [_vp, _vp, _vp, _c_int_p, _i64, _i, _vp, _vp]),
+    "hn_mon_stencils": (_i, [_vp, _i64, _vp, _vp, _vp, _c_int_p, _i, _vp, _vp]),
+    "hn_weights_mon": (_i, [_vp, _i, _vp, _i64, _i, _c_int_p, _c_int_p, _c_dbl_p, _vp, _vp, _vp, _vp]),
+    "hn_weights_rbf": (_i, [_vp, _i, _vp, _i64, _i, _i, _c_int_p, _c_int_p, _c_dbl_p, _vp, _vp, _vp, _vp,
+                            _vp, _vp]),
+    "hn_weights_rbf_is_tuned": (_i, [_i, _i, _i]),
+    "hn_weights_rbf_workspace": (_i64, [_i, _i, _i, _i64]),
+    "hn_weights_rbf_set_variant": (None, [_i]),
+    "hn_apply_ell": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i,
+                          _c_int_p, _vp, _vp, _i64, _vp]),
+    "hn_momentum": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i, _c_int_p,
+                         _i, _vp, _vp, _i64, _d, _d, _d, _c_dbl_p, _i, _vp, _vp]),
+    "hn_div_rhs": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _c_int_p, _i,
+                        _vp, _i64, _d, _vp, _vp]),
+    "hn_correct_temperature": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i,
+                                    _c_int_p, _i, _vp, _vp, _vp, _i64, _d, _vp, _vp, _vp, _vp]),
+    "hn_temperature_bc": (_i, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "hn_csr_matvec": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "hn_csr_residual": (_i, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "hn_sptrsv": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "hn_permute": (_i, [_i, _vp, _vp, _i64, _vp, _vp]),
+    "hn_reduce": (_i, [_i, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "hn_bicg_update": (_i, [_i, _vp, _vp, _vp, _d, _d, _i64, _vp]),
+}
+
+_LIB = None
+
+
+class NativeError(RuntimeError):
+    """A libhn.so call failed (CUDA error or bad argument)."""
+
+
+def lib():
+    """Load libhn.so once; raises if it is missing (no CPU fallback exists)."""
+    global _LIB
+    if _LIB is None:
+        if not LIB_PATH.exists():
+            raise NativeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(python -m paper_2303_01760_b200._build)")
+        handle = C.CDLL(str(LIB_PATH), mode=C.RTLD_GLOBAL)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = handle
+    return _LIB
+
+
+def call(name: str, *args) -> int:
+    rc = getattr(lib(), name)(*args)
+    if rc < 0:
+        raise NativeError(f"{name}: CUDA error {-rc}")
+    if rc > 0:
+        raise NativeError(f"{name}: invalid argument (code {rc})")
+    return rc
+
+
+# ---------------------------------------------------------------- torch plumbing
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        if not t.cuda.is_available():
+            raise NativeError("no CUDA device: the hybridnodes-b200 hot path runs on the GPU only")
+        _torch = t
+    return _torch
+
+
+def device():
+    return torch().device("cuda", torch().cuda.current_device())
+
+
+def stream_handle():
+    return _vp(torch().cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> _vp:
+    """Device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return _vp(0)
+    return _vp(t.data_ptr())
+
+
+def host_ints(vals) -> C.Array:
+    arr = (C.c_int * max(1, len(vals)))(*[int(v) for v in vals])
+    return arr
+
+
+def host_i64(vals) -> C.Array:
+    return (C.c_int64 * max(1, len(vals)))(*[int(v) for v in vals])
+
+
+def host_dbls(vals) -> C.Array:
+    vals = list(vals)
+    return (C.c_double * max(1, len(vals)))(*[float(v) for v in vals])
+
+
+def host_ptrs(tensors) -> C.Array:
+    return (_vp * max(1, len(tensors)))(*[t.data_ptr() if t is not None else 0 for t in tensors])
+
+
+def to_device(a: np.ndarray, dtype=None):
+    """Copy a host array to the current device (pinned staging for large arrays)."""
+    t = torch()
+    arr = np.ascontiguousarray(a if dtype is None else a.astype(dtype, copy=False))
+    return t.from_numpy(arr).to(device(), non_blocking=False)
+
+
+def empty(shape, dtype):
+    return torch().empty(shape, dtype=dtype, device=device())
+
+
+def zeros(shape, dtype):
+    return torch().zeros(shape, dtype=dtype, device=device())
+
+
+def loaded_library_path() -> str:
+    return os.fspath(LIB_PATH)

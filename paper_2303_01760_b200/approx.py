@@ -1,0 +1,487 @@
+"""Stencils and differentiation weights on the GPU (drop-in for hybridnodes.approx).
+
+Same names, signatures, return types and errors as pkg/src/hybridnodes/approx.py; the
+arithmetic runs in libhn.so:
+
+  classify_methods / select_method  -> hn_classify (+ hn_knn probes without a lattice)
+  _mon_stencils / find_stencil      -> hn_mon_stencils / hn_knn  (bit-exact indices)
+  _batched_mon_weights              -> hn_weights_mon   (thread per stencil)
+  _batched_rbf_weights              -> hn_weights_rbf   (warp-cooperative Gauss-Jordan)
+  compute_weights                   -> all of the above, results kept in HBM as ELL bins
+
+`tree` arguments (scipy cKDTree in the reference) are accepted and ignored: the device
+cell list replaces them.  Condition numbers (with_kappa / WeightRow.kappa) are a host
+diagnostic computed with numpy SVD, as in the reference (approx.py:100-105, 229-233).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+from ._device import Bin, DeviceTable, device_nodes
+from .errors import SingularSystemError
+from .nodegen import KIND_REGULAR, LATTICE_NONE
+
+MON_SIZE = {2: 5, 3: 7}
+RBF_SIZE = {2: 12, 3: 30}  # read at call time, like the reference (approx.py:25, 388, 420)
+POLY_COUNT = {2: 6, 3: 10}
+
+METHOD_MON = 0
+METHOD_RBFFD = 1
+METHOD_NONE = -1
+
+
+@dataclass(frozen=True)
+class Laplacian:
+    order: int = 2
+
+
+@dataclass(frozen=True)
+class Partial:
+    axis: int
+    order: int = 1
+
+
+@dataclass(frozen=True)
+class NormalDerivative:
+    normal: tuple
+    order: int = 1
+
+
+@dataclass(frozen=True)
+class StencilSpec:
+    center: int
+    neighbors: np.ndarray
+    method: str
+
+
+@dataclass
+class WeightRow:
+    neighbors: np.ndarray
+    weights: dict
+    kappa: float
+
+
+# ---------------------------------------------------------------- operator codes
+def _op_code(op, dim: int):
+    """(kind, axis, normal) for HN_OP_*; accepts this package's or the reference's op classes."""
+    name = type(op).__name__
+    if name == "Laplacian":
+        return 0, 0, (0.0,) * dim
+    if name == "Partial":
+        return 1, int(op.axis), (0.0,) * dim
+    if name == "NormalDerivative":
+        nrm = tuple(float(v) for v in op.normal)
+        if len(nrm) != dim:
+            raise ValueError("normal has the wrong dimension")
+        return 2, 0, nrm
+    raise TypeError(f"unknown operator kind {op!r}")
+
+
+def _op_args(ops, dim):
+    codes = [_op_code(op, dim) for op in ops]
+    return (L.host_ints([c[0] for c in codes]), L.host_ints([c[1] for c in codes]),
+            L.host_dbls([v for c in codes for v in c[2]]))
+
+
+def _op_order(op) -> int:
+    return int(getattr(op, "order", 2 if type(op).__name__ == "Laplacian" else 1))
+
+
+# ---------------------------------------------------------------- diagnostics (host)
+def condition_number(matrix: np.ndarray) -> float:
+    """Spectral condition number sigma_max / sigma_min (+inf when singular)."""
+    s = np.linalg.svd(np.asarray(matrix, dtype=float), compute_uv=False)
+    if s[-1] == 0.0:
+        return float("inf")
+    return float(s[0] / s[-1])
+
+
+def _exps(dim):
+    out = [(0,) * dim]
+    for a in range(dim):
+        e = [0] * dim
+        e[a] = 1
+        out.append(tuple(e))
+    for a in range(dim):
+        for b in range(a, dim):
+            e = [0] * dim
+            e[a] += 1
+            e[b] += 1
+            out.append(tuple(e))
+    return out
+
+
+def _local(positions, stencils):
+    pts = positions[stencils]
+    rel = pts - pts[:, :1, :]
+    scale = np.max(np.linalg.norm(rel, axis=-1), axis=1)
+    return rel / scale[:, None, None]
+
+
+def _kappa_host(positions: np.ndarray, stencils: np.ndarray, mon: bool) -> np.ndarray:
+    """kappa of the local systems (approx.py:229-233, 285-289); host SVD diagnostic."""
+    loc = _local(positions, stencils)
+    k, n, dim = loc.shape
+    if mon:
+        m = np.empty((k, n, n))
+        m[:, 0, :] = 1.0
+        for a in range(dim):
+            m[:, 1 + a, :] = loc[:, :, a]
+            m[:, 1 + dim + a, :] = loc[:, :, a] ** 2
+    else:
+        ex = _exps(dim)
+        q = len(ex)
+        m = np.zeros((k, n + q, n + q))
+        diff = loc[:, :, None, :] - loc[:, None, :, :]
+        m[:, :n, :n] = np.sqrt(np.sum(diff * diff, axis=-1)) ** 3
+        p = np.ones((k, n, q))
+        for j, e in enumerate(ex):
+            for a in range(dim):
+                if e[a]:
+                    p[:, :, j] *= loc[:, :, a] ** e[a]
+        m[:, :n, n:] = p
+        m[:, n:, :n] = np.transpose(p, (0, 2, 1))
+    s = np.linalg.svd(m, compute_uv=False)
+    with np.errstate(divide="ignore"):
+        return np.where(s[:, -1] > 0, s[:, 0] / s[:, -1], np.inf)
+
+
+# ---------------------------------------------------------------- device solves
+def _solve_bin(dn, stencils_dev, rows_host, ops, mon: bool, row_normals=None, label="") -> Bin:
+    """Weights for a batch of stencils straight into an ELL bin (ascending node order)."""
+    t = L.torch()
+    K, n = int(stencils_dev.shape[0]), int(stencils_dev.shape[1])
+    nops = len(ops)
+    d_idx = L.empty((n, max(K, 1)), t.int32)
+    d_w = L.empty((nops, n, max(K, 1)), t.float64)
+    info = L.zeros(max(K, 1), t.int32)
+    if K:
+        kinds, axes, normals = _op_args(ops, dn.dim)
+        if mon:
+            if n != 2 * dn.dim + 1:
+                raise SingularSystemError(f"singular MON system: stencil size {n} != {2 * dn.dim + 1}")
+            L.call("hn_weights_mon", L.ptr(dn.pos), dn.dim, L.ptr(stencils_dev), K, nops, kinds, axes, normals,
+                   L.ptr(d_idx), L.ptr(d_w), L.ptr(info), L.stream_handle())
+        else:
+            ws = None
+            if L.lib().hn_weights_rbf_is_tuned(dn.dim, n, nops) != 0:
+                ws = L.empty(int(L.lib().hn_weights_rbf_workspace(dn.dim, n, nops, K)), t.float64)
+            rn = L.to_device(np.ascontiguousarray(row_normals, dtype=float)) if row_normals is not None else None
+            L.call("hn_weights_rbf", L.ptr(dn.pos), dn.dim, L.ptr(stencils_dev), K, n, nops, kinds, axes, normals,
+                   L.ptr(rn), L.ptr(ws), L.ptr(d_idx), L.ptr(d_w), L.ptr(info), L.stream_handle())
+        bad = int(t.count_nonzero(info[:K]).item())
+        if bad:
+            first = int(t.nonzero(info[:K])[0].item())
+            kind = "MON" if mon else "RBF-FD saddle"
+            raise SingularSystemError(f"singular {kind} system: Singular matrix ({bad} stencil(s), first at node "
+                                      f"{int(rows_host[first])})")
+    return Bin(rows_host, n, d_idx[:, :K] if K else d_idx[:, :0], d_w[:, :, :K] if K else d_w[:, :, :0],
+               d_rows=L.to_device(np.asarray(rows_host, dtype=np.int32)))
+
+
+def _solve_points(points: np.ndarray, ops, mon: bool, row_normals=None):
+    """Weights of one or more stencils given directly as point arrays (K, n, d)."""
+    pts = np.asarray(points, dtype=float)
+    k, n, dim = pts.shape
+
+    class _Tmp:
+        pass
+
+    tmp = _Tmp()
+    tmp.positions = pts.reshape(k * n, dim)
+    tmp.kind = np.ones(k * n, dtype=np.int8)
+    dn = device_nodes_uncached(tmp)
+    st = L.to_device(np.arange(k * n, dtype=np.int32).reshape(k, n))
+    b = _solve_bin(dn, st, np.arange(k), ops, mon, row_normals)
+    idx = b.d_idx.cpu().numpy().T.reshape(k, n)          # local ids, ascending = stencil order ids
+    w = b.d_w.cpu().numpy().transpose(0, 2, 1)           # (nops, K, n) ascending local id
+    return idx, w
+
+
+def device_nodes_uncached(obj):
+    from ._device import DeviceNodes
+    return DeviceNodes(obj)
+
+
+# ---------------------------------------------------------------- public API
+def select_method(index: int, nodeset, tree=None) -> str:
+    """MON for regular nodes whose 2d axis neighbours all exist; else RBF-FD (approx.py:114-130)."""
+    if nodeset.kind[index] != KIND_REGULAR:
+        return "rbffd"
+    dim = nodeset.dim
+    lat, lidx = getattr(nodeset, "lattice", None), getattr(nodeset, "lattice_idx", None)
+    if lat is not None and lidx is not None and lidx[index][0] != LATTICE_NONE:
+        m = int(device_nodes(nodeset).classify()[index].item())
+        return "mon" if m == METHOD_MON else "rbffd"
+    h = nodeset.spacing[index]
+    pos = nodeset.positions[index]
+    probes = np.concatenate([pos + h * np.eye(dim), pos - h * np.eye(dim)])
+    _, dist = device_nodes(nodeset).knn(1, points=probes, with_dist=True)
+    return "mon" if bool(np.all(dist.cpu().numpy()[:, 0] < 1e-9 * h)) else "rbffd"
+
+
+def find_stencil(center: int, nodeset, n: int, tree=None) -> StencilSpec:
+    """The n nearest nodes (centre included) by (distance, index) (approx.py:149-155)."""
+    total = len(nodeset)
+    if n > total:
+        raise ValueError(f"stencil size {n} exceeds node count {total}")
+    idx = device_nodes(nodeset).knn(n, rows=np.array([center], dtype=np.int32)).cpu().numpy()[0].astype(np.int64)
+    method = "mon" if n == MON_SIZE[nodeset.dim] and nodeset.kind[center] == KIND_REGULAR else "rbffd"
+    return StencilSpec(center, idx, method)
+
+
+def _single(stencil, positions, op, mon: bool) -> WeightRow:
+    nb = np.asarray(stencil.neighbors, dtype=np.int64)
+    pts = np.asarray(positions, float)[nb][None]
+    kappa = float(_kappa_host(np.asarray(positions, float), nb[None], mon)[0])
+    if not np.isfinite(kappa):
+        kind = "MON" if mon else "RBF-FD"
+        raise SingularSystemError(f"singular {kind} system (duplicate nodes?)", kappa)
+    _, w = _solve_points(pts, [op], mon)
+    order = np.argsort(nb)
+    return WeightRow(nb[order], {op: w[0, 0]}, kappa)
+
+
+def mon_weights(stencil: StencilSpec, positions: np.ndarray, op) -> WeightRow:
+    """Monomial collocation weights for one stencil and one operator (approx.py:293-299)."""
+    return _single(stencil, positions, op, True)
+
+
+def rbf_fd_weights(stencil: StencilSpec, positions: np.ndarray, op) -> WeightRow:
+    """PHS + monomial RBF-FD weights for one stencil and one operator (approx.py:302-308)."""
+    return _single(stencil, positions, op, False)
+
+
+class WeightTable:
+    """Per-node stencil indices and weights (approx.py:311-329), resident in HBM.
+
+    The host arrays (indices (N, n_max) -1 padded, sizes, weights {op: (N, n_max)},
+    method, kappa) are materialised from the device bins on first access; assigning a
+    field detaches the table from its device copy so edits are honoured downstream.
+    """
+
+    def __init__(self, indices=None, sizes=None, weights=None, method=None, kappa=None, _device=None):
+        self._dev = _device
+        self._indices, self._sizes, self._weights = indices, sizes, weights
+        self._method = method
+        self.kappa = kappa
+
+    def _materialize(self):
+        if self._indices is None and self._dev is not None:
+            self._indices, self._sizes, self._weights = self._dev.host_arrays()
+
+    def _detach(self):
+        self._materialize()
+        self._dev = None
+
+    @property
+    def indices(self):
+        self._materialize()
+        return self._indices
+
+    @indices.setter
+    def indices(self, v):
+        self._detach()
+        self._indices = v
+
+    @property
+    def sizes(self):
+        if self._sizes is None and self._dev is not None:
+            self._sizes = self._dev.sizes()
+        return self._sizes
+
+    @sizes.setter
+    def sizes(self, v):
+        self._detach()
+        self._sizes = v
+
+    @property
+    def weights(self):
+        self._materialize()
+        return self._weights
+
+    @weights.setter
+    def weights(self, v):
+        self._detach()
+        self._weights = v
+
+    @property
+    def method(self):
+        return self._method
+
+    @method.setter
+    def method(self, v):
+        self._method = v
+
+    @property
+    def ops(self):
+        return self._dev.ops if self._dev is not None else list(self._weights.keys())
+
+    def device_table(self, dim: int) -> DeviceTable:
+        """The HBM bins (rebuilt from the host arrays if the table was edited)."""
+        if self._dev is None:
+            self._dev = DeviceTable.from_host(np.asarray(self._indices), np.asarray(self._sizes),
+                                              self._weights, list(self._weights.keys()), dim)
+            self._dev.method = self._method
+        return self._dev
+
+    def row(self, i: int) -> WeightRow:
+        m = self.sizes[i]
+        w = {op: tab[i, :m].copy() for op, tab in self.weights.items()}
+        return WeightRow(self.indices[i, :m].copy(), w,
+                         float(self.kappa[i]) if self.kappa is not None else float("nan"))
+
+
+def classify_methods(nodeset, tree=None) -> np.ndarray:
+    """METHOD_MON / METHOD_RBFFD per interior node, METHOD_NONE on boundary (approx.py:332-357)."""
+    dn = device_nodes(nodeset)
+    lat, lidx = getattr(nodeset, "lattice", None), getattr(nodeset, "lattice_idx", None)
+    method = dn.classify().cpu().numpy().astype(np.int8)
+    if lat is None or lidx is None:
+        # no lattice map: probe +-h e_a with a 1-NN query (approx.py:124-130)
+        regular = np.nonzero(np.asarray(nodeset.kind) == KIND_REGULAR)[0]
+        if len(regular):
+            dim = nodeset.dim
+            h = np.asarray(nodeset.spacing)[regular]
+            pos = np.asarray(nodeset.positions)[regular]
+            eye = np.concatenate([np.eye(dim), -np.eye(dim)])
+            probes = (pos[:, None, :] + h[:, None, None] * eye[None]).reshape(-1, dim)
+            _, dist = dn.knn(1, points=probes, with_dist=True)
+            ok = np.all(dist.cpu().numpy()[:, 0].reshape(len(regular), 2 * dim) < 1e-9 * h[:, None], axis=1)
+            method[regular[ok]] = METHOD_MON
+    return method
+
+
+def _interior_device_table(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
+    dim = nodeset.dim
+    n = len(nodeset)
+    n_rbf = RBF_SIZE[dim] if n_rbf is None else n_rbf
+    dn = device_nodes(nodeset)
+    method = classify_methods(nodeset)
+    t = L.torch()
+    bins = []
+    mon_rows = np.nonzero(method == METHOD_MON)[0]
+    if len(mon_rows):
+        d_rows = L.to_device(mon_rows.astype(np.int32))
+        if getattr(nodeset, "lattice", None) is not None and getattr(nodeset, "lattice_idx", None) is not None:
+            st = dn.mon_stencils(d_rows)
+        else:
+            st = dn.knn(MON_SIZE[dim], rows=d_rows)
+        bins.append(_solve_bin(dn, st, mon_rows, ops, True))
+    rbf_rows = np.nonzero(method == METHOD_RBFFD)[0]
+    if len(rbf_rows):
+        if n_rbf > n:
+            raise ValueError(f"stencil size {n_rbf} exceeds node count {n}")
+        st = dn.knn(n_rbf, rows=L.to_device(rbf_rows.astype(np.int32)))
+        bins.append(_solve_bin(dn, st, rbf_rows, ops, False))
+    none_rows = np.nonzero(method == METHOD_NONE)[0]
+    if len(none_rows):
+        bins.append(Bin(none_rows, 0, L.empty((0, len(none_rows)), t.int32),
+                        L.empty((len(ops), 0, len(none_rows)), t.float64)))
+    return DeviceTable(n, dim, list(ops), bins, RBF_SIZE[dim], method)
+
+
+def compute_weights(nodeset, ops, with_kappa: bool = False, tree=None) -> WeightTable:
+    """Stencils and weights for every interior node, batched per method (approx.py:379-413)."""
+    ops = list(ops)
+    for op in ops:
+        _op_code(op, nodeset.dim)
+    dev = _interior_device_table(nodeset, ops)
+    table = WeightTable(method=dev.method, _device=dev)
+    if with_kappa:
+        kappa = np.full(len(nodeset), np.nan)
+        for b in dev.bins:
+            if b.width == 0 or b.K == 0:
+                continue
+            idx = table.indices[b.rows_host, : b.width]
+            kappa[b.rows_host] = _kappa_host(np.asarray(nodeset.positions, float), _stencil_order(b.rows_host, idx),
+                                             b.width == MON_SIZE[nodeset.dim] and
+                                             np.all(dev.method[b.rows_host] == METHOD_MON))
+        table.kappa = kappa
+    return table
+
+
+def _stencil_order(rows, idx_sorted):
+    """Centre first (kappa is invariant to the order of the other nodes)."""
+    out = np.empty_like(idx_sorted)
+    for r, (row, ids) in enumerate(zip(rows, idx_sorted)):
+        out[r] = np.concatenate([[row], ids[ids != row]])
+    return out
+
+
+def _boundary_stencils(nodeset, rows: np.ndarray, exclude: np.ndarray | None):
+    """[self] + nearest allowed nodes (exclude given) or plain kNN (approx.py:416-434).
+
+    Returns (device stencils, tie_rows): tie_rows are the requested rows whose
+    (size-1)-th and size-th allowed candidates tie exactly in distance -- where the
+    reference keeps cKDTree's traversal choice instead of the (distance, index) rule
+    (SURVEY §8(a) A5)."""
+    t = L.torch()
+    dim = nodeset.dim
+    size = RBF_SIZE[dim]
+    dn = device_nodes(nodeset)
+    d_rows = L.to_device(rows.astype(np.int32))
+    if exclude is None:
+        if size > len(nodeset):
+            raise ValueError(f"stencil size {size} exceeds node count {len(nodeset)}")
+        return dn.knn(size, rows=d_rows), np.empty(0, dtype=np.int64)
+    exclude = np.asarray(exclude, dtype=bool)
+    if not np.all(exclude[rows]):
+        raise ValueError("exclude mask must cover the requested rows")
+    allowed = int((~exclude).sum())
+    k = min(allowed, size - 1)
+    kq = min(allowed, k + 1)
+    idx, dist = dn.knn(kq, rows=d_rows, exclude=exclude.astype(np.uint8), with_dist=True)
+    tie_rows = np.empty(0, dtype=np.int64)
+    if kq > k and len(rows):
+        dd = dist.cpu().numpy()
+        tie_rows = rows[dd[:, k - 1] == dd[:, k]]
+    st = t.cat([d_rows.view(-1, 1), idx[:, :k]], dim=1).contiguous()
+    return st, tie_rows
+
+
+def _boundary_table(nodeset, rows, exclude, ops, normals: bool) -> tuple[DeviceTable, np.ndarray]:
+    rows = np.asarray(rows, dtype=np.int64)
+    n = len(nodeset)
+    dim = nodeset.dim
+    dn = device_nodes(nodeset)
+    bins = []
+    ties = np.empty(0, dtype=np.int64)
+    size = RBF_SIZE[dim]
+    if len(rows):
+        order = np.argsort(rows, kind="stable")
+        rows_sorted = rows[order]
+        st, ties = _boundary_stencils(nodeset, rows_sorted, exclude)
+        size = int(st.shape[1])
+        rn = np.asarray(nodeset.normals, float)[rows_sorted] if normals else None
+        bins.append(_solve_bin(dn, st, rows_sorted, ops, False, row_normals=rn))
+    rest = np.setdiff1d(np.arange(n), rows)
+    if len(rest):
+        t = L.torch()
+        bins.append(Bin(rest, 0, L.empty((0, len(rest)), t.int32), L.empty((len(ops), 0, len(rest)), t.float64)))
+    method = np.full(n, METHOD_NONE, dtype=np.int8)
+    method[rows] = METHOD_RBFFD
+    return DeviceTable(n, dim, list(ops), bins, size, method), ties
+
+
+def normal_derivative_table(nodeset, rows: np.ndarray, tree=None, exclude: np.ndarray | None = None) -> WeightTable:
+    """One-sided RBF-FD normal-derivative rows at boundary nodes (approx.py:437-465)."""
+    dim = nodeset.dim
+    dev, ties = _boundary_table(nodeset, rows, exclude, [NormalDerivative((0.0,) * dim)], True)
+    dev.ops = ["normal"]
+    t = WeightTable(method=dev.method, _device=dev)
+    t.tie_rows = ties
+    return t
+
+
+def boundary_partial_table(nodeset, rows: np.ndarray, tree=None, exclude: np.ndarray | None = None) -> WeightTable:
+    """One-sided RBF-FD first-derivative rows at boundary nodes, all axes (approx.py:468-491)."""
+    ops = [Partial(a) for a in range(nodeset.dim)]
+    dev, ties = _boundary_table(nodeset, rows, exclude, ops, False)
+    t = WeightTable(method=dev.method, _device=dev)
+    t.tie_rows = ties
+    return t

@@ -1,0 +1,42 @@
+// Library identity and the fp64 peak probe used for the weight-solver roofline.
+#include "hn_common.cuh"
+
+namespace hn {
+
+int sm_count() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+// 16 independent DFMA chains per thread keep the FP64 pipe saturated; the result is
+// folded into a checksum so nothing is dead code.
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters) {
+  double a[16];
+  const double x = 1.0 + 1e-9 * threadIdx.x, y = 0.999999;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = 1e-3 * (i + 1);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = fma(a[i], y, x);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i];
+  if (s == 12345.678) out[0] = s;  // never true; keeps the chains live
+}
+
+}  // namespace hn
+
+HN_EXPORT int hn_version(void) { return 1; }
+
+HN_EXPORT int hn_bench_dfma(double* out, int blocks, int iters, void* stream) {
+  hn::dfma_probe_kernel<<<blocks, 256, 0, hn::as_stream(stream)>>>(out, iters);
+  HN_CHECK_LAUNCH();
+  return 0;
+}

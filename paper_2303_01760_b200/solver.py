@@ -1,0 +1,674 @@
+"""Explicit-Euler natural-convection solver with Chorin projection, GPU-resident.
+
+Drop-in for pkg/src/hybridnodes/solver.py: same dataclasses, OperatorSet attributes,
+step functions and `run`.  Per step, everything runs in libhn.so on HBM-resident state:
+
+  momentum_predict + apply_velocity_bc  -> hn_momentum            (K7)
+  divergence / dt -> Poisson rhs        -> hn_div_rhs             (K8)
+  pressure_solve (bicgstab + LU precond) -> hn_csr_residual/matvec, hn_sptrsv x2, hn_permute,
+                                           hn_reduce, hn_bicg_update   (K9, scipy's algebra)
+  velocity_correct + temperature_step   -> hn_correct_temperature (K10)
+  apply_temperature_bc                  -> hn_temperature_bc      (K11)
+  finite probe / Nusselt / divergence   -> flags + hn_reduce      (K12)
+
+Setup (`build_operators`) computes every weight table on the GPU; the one-time algebra
+that builds the bordered Poisson matrix and its complete LU factorisation stays on the
+host with scipy/SuperLU, exactly as the reference does (solver.py:168-213) -- it is not
+part of the per-step hot path.  The factors are then moved to HBM and
+applied by sync-free triangular solves.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+from scipy import sparse
+from scipy.sparse import linalg as spla
+
+from . import _lib as L
+from ._device import bins_args
+from .approx import (Laplacian, Partial, boundary_partial_table, compute_weights,
+                     normal_derivative_table)
+from .errors import PoissonConvergenceError, SolverDivergenceError
+from .nodegen import ROLE_DIRICHLET, ROLE_NEUMANN
+from .operators import DeviceCSR, FieldState, SparseOperator, assemble
+
+INT32_MAX = np.iinfo(np.int32).max
+
+
+@dataclass
+class PhysicsParams:
+    Ra: float
+    Pr: float
+    g: np.ndarray = None
+    t_ref: float = 0.0
+    dissipation: float = 0.0
+
+    def __post_init__(self):
+        if self.Ra <= 0 or self.Pr <= 0:
+            raise ValueError("Ra and Pr must be positive")
+        if self.g is not None:
+            self.g = np.asarray(self.g, dtype=float)
+            if abs(np.linalg.norm(self.g) - 1.0) > 1e-12:
+                raise ValueError("gravity direction must be a unit vector")
+
+    def gravity(self, dim: int) -> np.ndarray:
+        if self.g is not None:
+            return self.g
+        g = np.zeros(dim)
+        g[-1] = -1.0
+        return g
+
+
+@dataclass
+class TimeControls:
+    dt: float
+    t_end: float
+    steady_tol: float = 1e-6
+    nu_window: int = 40
+    nu_stride: int = 20
+
+    @staticmethod
+    def from_spacing(h_min: float, t_end: float, Ra: float | None = None, **kwargs) -> "TimeControls":
+        """dt = min(0.1 h_min^2 / 2, 40/Ra) (solver.py:60-73)."""
+        dt = 0.1 * h_min ** 2 / 2.0
+        if Ra is not None:
+            dt = min(dt, 40.0 / Ra)
+        return TimeControls(dt=dt, t_end=t_end, **kwargs)
+
+
+@dataclass
+class PoissonSolveSettings:
+    tol: float = 1e-8
+    maxiter: int = 2000
+    gauge: int | None = None
+    stabilization: float = 0.1
+
+    def __post_init__(self):
+        if not 0 < self.tol < 1:
+            raise ValueError("relative tolerance must lie in (0, 1)")
+        if not 0 <= self.stabilization <= 1:
+            raise ValueError("stabilization must lie in [0, 1]")
+
+
+class _DeviceLU:
+    """SuperLU factors Pr A Pc = L U in HBM: strict-lower L, strict-upper U + diag, perms."""
+
+    def __init__(self, lu):
+        Lm = sparse.csr_matrix(lu.L)
+        Um = sparse.csr_matrix(lu.U)
+        self.n = Lm.shape[0]
+        Ls = sparse.tril(Lm, k=-1, format="csr")
+        Us = sparse.triu(Um, k=1, format="csr")
+        Ls.sort_indices()
+        Us.sort_indices()
+        self.L = DeviceCSR(Ls)
+        self.U = DeviceCSR(Us)
+        self.diag = L.to_device(np.asarray(Um.diagonal(), dtype=np.float64))
+        self.perm_r = L.to_device(np.asarray(lu.perm_r, dtype=np.int32))
+        self.perm_c = L.to_device(np.asarray(lu.perm_c, dtype=np.int32))
+        t = L.torch()
+        self.y = L.empty(self.n, t.float64)
+        self.z = L.empty(self.n, t.float64)
+        self.w = L.empty(self.n, t.float64)
+        self.ticket = L.zeros(1, t.int64)
+        self.nnz = self.L.nnz + self.U.nnz + self.n
+
+    def solve(self, b, x):
+        """x = Pc U^-1 L^-1 Pr b (scipy SuperLU.solve semantics)."""
+        s = L.stream_handle()
+        L.call("hn_permute", 0, L.ptr(self.perm_r), L.ptr(b), self.n, L.ptr(self.y), s)
+        L.call("hn_sptrsv", 1, L.ptr(self.L.rowptr), L.ptr(self.L.cols), L.ptr(self.L.vals), None, L.ptr(self.y),
+               L.ptr(self.z), self.n, L.ptr(self.ticket), s)
+        L.call("hn_sptrsv", 0, L.ptr(self.U.rowptr), L.ptr(self.U.cols), L.ptr(self.U.vals), L.ptr(self.diag),
+               L.ptr(self.z), L.ptr(self.w), self.n, L.ptr(self.ticket), s)
+        L.call("hn_permute", 1, L.ptr(self.perm_c), L.ptr(self.w), self.n, L.ptr(x), s)
+        return x
+
+
+class OperatorSet:
+    """Assembled operators, boundary index sets and factorised helpers (solver.py:96-125),
+    with their HBM mirrors."""
+
+    def __init__(self, nodeset, lap, partials, gauge: int, poisson_matrix, poisson_precond, neumann_rows,
+                 neumann_lu, nu_rows, cold_idx, nu_scale, lu=None, neumann_diag=None):
+        self.nodeset = nodeset
+        self.lap = lap
+        self.partials = partials
+        self.gauge = gauge
+        self.poisson_matrix = poisson_matrix
+        self.poisson_precond = poisson_precond
+        self.neumann_lu = neumann_lu
+        self.cold_idx = cold_idx
+        self.nu_scale = nu_scale
+        self._poisson_lambda = 0.0
+        self.interior_idx = np.nonzero(nodeset.interior_mask)[0]
+        self.boundary_idx = np.nonzero(nodeset.boundary_mask)[0]
+        self.dirichlet_idx = np.nonzero(nodeset.role == ROLE_DIRICHLET)[0]
+        self.neumann_idx = np.nonzero(nodeset.role == ROLE_NEUMANN)[0]
+        self._w_neumann = neumann_rows
+        self._nu_rows = nu_rows
+        t = L.torch()
+        n = len(nodeset)
+        self.n = n
+        # ---- HBM mirrors ----
+        self._table = lap._table
+        ops = list(self._table.ops)
+        self._lap_plane = ops.index(lap.kind)
+        self._d_planes = [ops.index(p.kind) for p in partials]
+        self._d_poisson = DeviceCSR(poisson_matrix)
+        self._d_lu = _DeviceLU(lu) if lu is not None else None
+        self._d_dir_idx = L.to_device(self.dirichlet_idx.astype(np.int32))
+        self.dirichlet_values = nodeset.bc_value[self.dirichlet_idx]
+        self._d_neu = None
+        if neumann_rows is not None:
+            self._d_neu = DeviceCSR(neumann_rows)
+            self._d_neu_idx = L.to_device(self.neumann_idx.astype(np.int32))
+            self._d_neu_diag = L.to_device(np.asarray(neumann_diag, dtype=np.float64))
+            mask = np.zeros(n, dtype=np.uint8)
+            mask[self.neumann_idx] = 1
+            self._d_is_neu = L.to_device(mask)
+        self._d_nu = DeviceCSR(nu_rows) if nu_rows is not None else None
+        self._d_interior = L.to_device(self.interior_idx.astype(np.int32))
+        self._red = L.empty(512, t.float64)
+        self._scalar = L.empty(8, t.float64)
+
+    @property
+    def dim(self) -> int:
+        return self.nodeset.dim
+
+    @property
+    def dirichlet_values(self):
+        return self._dirichlet_values
+
+    @dirichlet_values.setter
+    def dirichlet_values(self, v):
+        self._dirichlet_values = np.asarray(v, dtype=float)
+        self._d_dir_val = L.to_device(self._dirichlet_values.astype(np.float64))
+
+    # ---- device helpers ----
+    def _bins(self):
+        return bins_args(self._table.bins)
+
+    def reduce(self, op: int, a, b=None, idx=None, n=None) -> float:
+        n = int(a.numel()) if n is None and idx is None else (int(idx.numel()) if idx is not None else n)
+        L.call("hn_reduce", op, L.ptr(a), L.ptr(b), L.ptr(idx), n, L.ptr(self._red), L.ptr(self._scalar),
+               L.stream_handle())
+        return float(self._scalar[0].item())
+
+
+def _table_to_csr(table, key, n: int) -> sparse.csr_matrix:
+    cols = np.arange(table.indices.shape[1])[None, :] < table.sizes[:, None]
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(table.sizes, out=indptr[1:])
+    return sparse.csr_matrix((table.weights[key][cols], table.indices[cols], indptr), shape=(n, n))
+
+
+def build_operators(nodeset, cold_origins: set, settings: PoissonSolveSettings,
+                    timings: dict | None = None) -> OperatorSet:
+    """Weights on the GPU, one-time host assembly + SuperLU, factors to HBM (solver.py:133-232)."""
+    timings = timings if timings is not None else {}
+    dim = nodeset.dim
+    n = len(nodeset)
+    ops_wanted = [Laplacian()] + [Partial(a) for a in range(dim)]
+    boundary_idx = np.nonzero(nodeset.boundary_mask)[0]
+    neumann_idx = np.nonzero(nodeset.role == ROLE_NEUMANN)[0]
+    cold_idx = np.array([i for i in boundary_idx if nodeset.origin[i] in cold_origins], dtype=np.int64)
+
+    t0 = time.perf_counter()
+    table = compute_weights(nodeset, ops_wanted)
+    boundary_grad = boundary_partial_table(nodeset, boundary_idx, exclude=nodeset.boundary_mask)
+    nu_table = normal_derivative_table(nodeset, cold_idx) if len(cold_idx) else None
+    L.torch().cuda.synchronize()
+    timings["weights"] = time.perf_counter() - t0
+
+    t0 = time.perf_counter()
+    lap = assemble(nodeset, table, Laplacian())
+    partials = [assemble(nodeset, table, Partial(a)) for a in range(dim)]
+    grad_rows = [_table_to_csr(boundary_grad, Partial(a), n) for a in range(dim)]
+    normals_safe = np.where(np.isfinite(nodeset.normals), nodeset.normals, 0.0)
+    normal_matrix = sum(sparse.diags(normals_safe[:, a]) @ grad_rows[a] for a in range(dim)).tocsr()
+
+    interior = nodeset.interior_mask
+    if settings.gauge is None:
+        centroid = nodeset.positions[interior].mean(axis=0)
+        cand = np.nonzero(interior)[0]
+        gauge = int(cand[np.argmin(np.linalg.norm(nodeset.positions[cand] - centroid, axis=1))])
+    else:
+        gauge = int(settings.gauge)
+    grad_full = [p.matrix + g for p, g in zip(partials, grad_rows)]
+    div_grad = sum(p.matrix @ g for p, g in zip(partials, grad_full))
+    beta = settings.stabilization
+    blended = (1.0 - beta) * div_grad + beta * lap.matrix
+    core = (sparse.diags(interior.astype(float)) @ blended
+            + sparse.diags(nodeset.boundary_mask.astype(float)) @ normal_matrix).tocsr()
+    core.eliminate_zeros()
+    core = core.tocoo()
+    n_int = int(interior.sum())
+    rows = np.concatenate([core.row, np.nonzero(interior)[0], [n]])
+    cols = np.concatenate([core.col, np.full(n_int, n), [gauge]])
+    data = np.concatenate([core.data, np.ones(n_int), [1.0]])
+    poisson = sparse.csr_matrix((data, (rows, cols)), shape=(n + 1, n + 1))
+    lu = spla.splu(poisson.tocsc())
+    precond = spla.LinearOperator(poisson.shape, lu.solve)
+
+    neumann_rows = neumann_lu = neumann_diag = None
+    if len(neumann_idx):
+        neumann_rows = normal_matrix[neumann_idx]
+        block = neumann_rows[:, neumann_idx].tocsr()
+        off = block - sparse.diags(block.diagonal())
+        off.eliminate_zeros()
+        if off.nnz:
+            raise NotImplementedError("Neumann reconstruction block is not diagonal; the GPU path solves it "
+                                      "as an elementwise division (boundary stencils must exclude each other)")
+        neumann_diag = block.diagonal()
+        neumann_lu = spla.splu(block.tocsc())
+    nu_rows = _table_to_csr(nu_table, "normal", n)[cold_idx] if nu_table is not None else None
+
+    dirichlet_idx = np.nonzero(nodeset.role == ROLE_DIRICHLET)[0]
+    values = nodeset.bc_value[dirichlet_idx]
+    t_span = (values.max() - values.min()) if len(values) else 1.0
+    nu_scale = float(np.max(nodeset.positions.max(axis=0) - nodeset.positions.min(axis=0)))
+    nu_scale /= t_span if t_span > 0 else 1.0
+    opset = OperatorSet(nodeset, lap, partials, gauge, poisson, precond, neumann_rows, neumann_lu, nu_rows,
+                        cold_idx, nu_scale, lu=lu, neumann_diag=neumann_diag)
+    opset.boundary_tie_rows = getattr(boundary_grad, "tie_rows", np.empty(0, dtype=np.int64))
+    L.torch().cuda.synchronize()
+    timings["solver_setup"] = time.perf_counter() - t0
+    return opset
+
+
+# ============================================================ device step pieces
+def _momentum_dev(ops: OperatorSet, params: PhysicsParams, dt: float, v_soa, T, out, zero_boundary: bool):
+    if params.dissipation:
+        raise NotImplementedError("hyper-dissipation (dissipation != 0) is not on the GPU path")
+    dim = ops.dim
+    g = params.gravity(dim)
+    buoy = [params.Ra * params.Pr * g[c] for c in range(dim)]  # ((Ra*Pr)*g_c), solver.py:270
+    nb, K, W, R, I, Wt, _ = ops._bins()
+    L.call("hn_momentum", nb, K, W, R, I, Wt, ops._lap_plane, L.host_ints(ops._d_planes), dim, L.ptr(v_soa),
+           L.ptr(T), ops.n, float(dt), float(params.Pr), float(params.t_ref), L.host_dbls(buoy),
+           1 if zero_boundary else 0, L.ptr(out), L.stream_handle())
+    return out
+
+
+def _div_rhs_dev(ops: OperatorSet, vstar_soa, dt: float, rhs):
+    nb, K, W, R, I, Wt, _ = ops._bins()
+    L.call("hn_div_rhs", nb, K, W, R, I, Wt, L.host_ints(ops._d_planes), ops.dim, L.ptr(vstar_soa), ops.n,
+           float(dt), L.ptr(rhs), L.stream_handle())
+    return rhs
+
+
+def _correct_temp_dev(ops: OperatorSet, vstar_soa, p, T, dt: float, vout, Tout, flags):
+    nb, K, W, R, I, Wt, _ = ops._bins()
+    L.call("hn_correct_temperature", nb, K, W, R, I, Wt, ops._lap_plane, L.host_ints(ops._d_planes), ops.dim,
+           L.ptr(vstar_soa), L.ptr(p), L.ptr(T), ops.n, float(dt), L.ptr(vout), L.ptr(Tout), L.ptr(flags),
+           L.stream_handle())
+
+
+def _temperature_bc_dev(ops: OperatorSet, T):
+    nd = len(ops.dirichlet_idx)
+    if ops._d_neu is not None:
+        L.call("hn_temperature_bc", L.ptr(ops._d_dir_idx), L.ptr(ops._d_dir_val), nd, L.ptr(ops._d_neu.rowptr),
+               L.ptr(ops._d_neu.cols), L.ptr(ops._d_neu.vals), L.ptr(ops._d_neu_idx), L.ptr(ops._d_neu_diag),
+               L.ptr(ops._d_is_neu), len(ops.neumann_idx), L.ptr(T), L.stream_handle())
+    else:
+        L.call("hn_temperature_bc", L.ptr(ops._d_dir_idx), L.ptr(ops._d_dir_val), nd, None, None, None, None, None,
+               None, 0, L.ptr(T), L.stream_handle())
+    return T
+
+
+class _BiCGStab:
+    """scipy.sparse.linalg.bicgstab (scipy 1.18 _isolve/iterative.py) on device vectors.
+
+    Same iteration, breakdown tests and stopping rule; dot products are device
+    reductions (fixed tree), scalars come back to the host for the control flow."""
+
+    def __init__(self, ops: OperatorSet):
+        t = L.torch()
+        n1 = ops.n + 1
+        self.ops = ops
+        self.n1 = n1
+        for name in ("r", "rt", "p", "phat", "v", "shat", "t", "x"):
+            setattr(self, name, L.empty(n1, t.float64))
+        self.matvecs = 0
+        self.psolves = 0
+
+    def _dot(self, a, b):
+        return self.ops.reduce(0, a, b, n=self.n1)
+
+    def _norm(self, a):
+        return float(np.sqrt(self._dot(a, a)))
+
+    def _axpy(self, y, x, alpha):
+        L.call("hn_bicg_update", 1, L.ptr(y), L.ptr(x), None, float(alpha), 0.0, self.n1, L.stream_handle())
+
+    def _A(self, x, y):
+        self.matvecs += 1
+        self.ops._d_poisson.matvec(x, y)
+
+    def _M(self, x, y):
+        self.psolves += 1
+        self.ops._d_lu.solve(x, y)
+
+    def solve(self, b, x0, rtol: float, maxiter: int):
+        """Returns (x (device, n+1), info)."""
+        bnrm2 = self._norm(b)
+        atol = max(0.0, float(rtol) * float(bnrm2))
+        if bnrm2 == 0:
+            return b.clone(), 0
+        x = self.x
+        if x0 is not None:
+            x.copy_(x0)
+        else:
+            x.zero_()
+        rhotol = np.finfo(np.float64).eps ** 2
+        omegatol = rhotol
+        r, rt, p, phat, v, shat, tt = self.r, self.rt, self.p, self.phat, self.v, self.shat, self.t
+        if x0 is not None and self.ops.reduce(1, x, n=self.n1) > 0:
+            self.matvecs += 1
+            self.ops._d_poisson.residual(x, b, r)
+        else:
+            r.copy_(b)
+        rt.copy_(r)
+        rho_prev = omega = alpha = None
+        for it in range(maxiter):
+            if self._norm(r) < atol:
+                return x, 0
+            rho = self._dot(rt, r)
+            if abs(rho) < rhotol:
+                return x, -10
+            if it > 0:
+                if abs(omega) < omegatol:
+                    return x, -11
+                beta = (rho / rho_prev) * (alpha / omega)
+                L.call("hn_bicg_update", 0, L.ptr(p), L.ptr(v), L.ptr(r), float(omega), float(beta), self.n1,
+                       L.stream_handle())
+            else:
+                p.copy_(r)
+            self._M(p, phat)
+            self._A(phat, v)
+            rv = self._dot(rt, v)
+            if rv == 0:
+                return x, -11
+            alpha = rho / rv
+            self._axpy(r, v, -alpha)
+            if self._norm(r) < atol:
+                self._axpy(x, phat, alpha)
+                return x, 0
+            self._M(r, shat)
+            self._A(shat, tt)
+            omega = self._dot(tt, r) / self._dot(tt, tt)
+            self._axpy(x, phat, alpha)
+            self._axpy(x, shat, omega)
+            self._axpy(r, tt, -omega)
+            rho_prev = rho
+        return x, maxiter
+
+
+def _pressure_dev(ops: OperatorSet, rhs, x0, settings: PoissonSolveSettings, solver: _BiCGStab):
+    x, info = solver.solve(rhs, x0, settings.tol, settings.maxiter)
+    if info != 0:
+        tt = L.torch()
+        res_vec = L.empty(ops.n + 1, tt.float64)
+        ops._d_poisson.residual(x, rhs, res_vec)
+        res = np.sqrt(ops.reduce(0, res_vec, res_vec)) / max(np.sqrt(ops.reduce(0, rhs, rhs)), 1e-300)
+        raise PoissonConvergenceError(f"pressure Poisson solve did not converge (info={info}); the GPU path "
+                                      "has no lgmres retry", residual=float(res))
+    return x
+
+
+# ============================================================ public step functions (host arrays)
+def _soa(v: np.ndarray):
+    return L.to_device(np.ascontiguousarray(np.asarray(v, dtype=np.float64).T))
+
+
+def momentum_predict(state: FieldState, ops: OperatorSet, params: PhysicsParams, dt: float) -> np.ndarray:
+    """Intermediate velocity v* without the pressure gradient (solver.py:250-274)."""
+    t = L.torch()
+    v = _soa(state.velocity)
+    T = L.to_device(np.asarray(state.temperature, dtype=np.float64))
+    out = L.empty((ops.dim, ops.n), t.float64)
+    _momentum_dev(ops, params, dt, v, T, out, zero_boundary=False)
+    return out.cpu().numpy().T.copy()
+
+
+def apply_velocity_bc(v: np.ndarray, ops: OperatorSet) -> np.ndarray:
+    """No-slip on every boundary node (in place, solver.py:277-280)."""
+    v[ops.boundary_idx] = 0.0
+    return v
+
+
+def pressure_solve(vstar: np.ndarray, ops: OperatorSet, settings: PoissonSolveSettings, dt: float,
+                   x0: np.ndarray | None = None, wall_gradient: np.ndarray | None = None) -> np.ndarray:
+    """Solve the bordered Poisson system for p (solver.py:283-314) on the GPU."""
+    t = L.torch()
+    n = ops.n
+    rhs = L.empty(n + 1, t.float64)
+    _div_rhs_dev(ops, _soa(vstar), dt, rhs)
+    if wall_gradient is not None:
+        bidx = L.to_device(ops.boundary_idx.astype(np.int64))
+        rhs.index_copy_(0, bidx, L.to_device(np.broadcast_to(np.asarray(wall_gradient, float),
+                                                             ops.boundary_idx.shape).copy()))
+    x0d = None
+    if x0 is not None and len(x0) == n:
+        x0d = L.to_device(np.concatenate([np.asarray(x0, dtype=np.float64), [ops._poisson_lambda]]))
+    solver = getattr(ops, "_bicg", None) or _BiCGStab(ops)
+    ops._bicg = solver
+    x = _pressure_dev(ops, rhs, x0d, settings, solver)
+    p = x.cpu().numpy()
+    ops._poisson_lambda = float(p[n])
+    return p[:n].copy()
+
+
+def velocity_correct(vstar: np.ndarray, p: np.ndarray, ops: OperatorSet, dt: float) -> np.ndarray:
+    """v = v* - dt grad p inside, no-slip on boundaries (solver.py:317-331)."""
+    t = L.torch()
+    vout = L.empty((ops.dim, ops.n), t.float64)
+    Tout = L.empty(ops.n, t.float64)
+    flags = L.to_device(np.array([0, INT32_MAX], dtype=np.int32))
+    zeros = L.zeros(ops.n, t.float64)
+    _correct_temp_dev(ops, _soa(vstar), L.to_device(np.asarray(p, dtype=np.float64)), zeros, dt, vout, Tout, flags)
+    return vout.cpu().numpy().T.copy()
+
+
+def apply_temperature_bc(t_field: np.ndarray, ops: OperatorSet) -> np.ndarray:
+    """Dirichlet values reset; insulated nodes solved from their Neumann rows (solver.py:334-342)."""
+    T = L.to_device(np.asarray(t_field, dtype=np.float64))
+    _temperature_bc_dev(ops, T)
+    t_field[:] = T.cpu().numpy()
+    return t_field
+
+
+def temperature_step(state: FieldState, ops: OperatorSet, dt: float, dissipation: float = 0.0) -> np.ndarray:
+    """T += dt * (-v . grad T + lap T) inside; boundary values re-imposed (solver.py:345-358)."""
+    if dissipation:
+        raise NotImplementedError("hyper-dissipation (dissipation != 0) is not on the GPU path")
+    t = L.torch()
+    v = _soa(state.velocity)
+    T = L.to_device(np.asarray(state.temperature, dtype=np.float64))
+    vout = L.empty((ops.dim, ops.n), t.float64)
+    Tout = L.empty(ops.n, t.float64)
+    flags = L.to_device(np.array([0, INT32_MAX], dtype=np.int32))
+    zeros = L.zeros(ops.n, t.float64)
+    # with p = 0 the fused kernel's corrected velocity is v itself (v - dt*0 = v)
+    _correct_temp_dev(ops, v, zeros, T, dt, vout, Tout, flags)
+    _temperature_bc_dev(ops, Tout)
+    return Tout.cpu().numpy()
+
+
+def nusselt_average(state: FieldState, ops: OperatorSet) -> float:
+    """Mean of L/(T_H - T_C) |dT/dn| over the cold-boundary nodes (solver.py:361-365)."""
+    if ops._d_nu is None:
+        return float("nan")
+    T = L.to_device(np.asarray(state.temperature, dtype=np.float64))
+    return _nusselt_dev(ops, T)
+
+
+def _nusselt_dev(ops: OperatorSet, T) -> float:
+    t = L.torch()
+    m = ops._d_nu.shape[0]
+    g = L.empty(m, t.float64)
+    ops._d_nu.matvec(T, g)
+    return float(ops.nu_scale * (ops.reduce(2, g, n=m) / m))
+
+
+def interior_divergence(v: np.ndarray, ops: OperatorSet) -> float:
+    t = L.torch()
+    return _interior_divergence_dev(ops, _soa(v))
+
+
+def _interior_divergence_dev(ops: OperatorSet, v_soa) -> float:
+    t = L.torch()
+    rhs = L.empty(ops.n + 1, t.float64)
+    _div_rhs_dev(ops, v_soa, 1.0, rhs)  # div / 1.0 is exact
+    return ops.reduce(1, rhs, idx=ops._d_interior)
+
+
+# ============================================================ device-resident stepping
+class DeviceStepper:
+    """One explicit step = K7 -> K8 -> K9 -> K10 -> K11 on HBM-resident state
+    (replicates the loop body of run(), solver.py:439-452)."""
+
+    def __init__(self, ops: OperatorSet, params: PhysicsParams, settings: PoissonSolveSettings, dt: float,
+                 state: FieldState):
+        t = L.torch()
+        self.ops, self.params, self.settings, self.dt = ops, params, settings, float(dt)
+        n, d = ops.n, ops.dim
+        self.v = _soa(state.velocity)
+        self.T = L.to_device(np.asarray(state.temperature, dtype=np.float64))
+        self.p = L.to_device(np.asarray(state.pressure, dtype=np.float64))
+        self.vstar = L.empty((d, n), t.float64)
+        self.v_next = L.empty((d, n), t.float64)
+        self.T_next = L.empty(n, t.float64)
+        self.rhs = L.empty(n + 1, t.float64)
+        self.x0 = L.empty(n + 1, t.float64)
+        self.flags = L.to_device(np.array([0, INT32_MAX], dtype=np.int32))
+        self.solver = _BiCGStab(ops)
+        self.have_p = False
+        self.steps = 0
+
+    def step(self):
+        ops = self.ops
+        _momentum_dev(ops, self.params, self.dt, self.v, self.T, self.vstar, zero_boundary=True)
+        _div_rhs_dev(ops, self.vstar, self.dt, self.rhs)
+        x0 = None
+        if self.have_p:
+            self.x0[: ops.n].copy_(self.p)
+            self.x0[ops.n] = ops._poisson_lambda
+            x0 = self.x0
+        x = _pressure_dev(ops, self.rhs, x0, self.settings, self.solver)
+        ops._poisson_lambda = float(x[ops.n].item())
+        self.p.copy_(x[: ops.n])
+        self.have_p = True
+        _correct_temp_dev(ops, self.vstar, self.p, self.T, self.dt, self.v_next, self.T_next, self.flags)
+        _temperature_bc_dev(ops, self.T_next)
+        self.v, self.v_next = self.v_next, self.v
+        self.T, self.T_next = self.T_next, self.T
+        self.steps += 1
+
+    def check_finite(self, step: int):
+        f = self.flags.cpu().numpy()
+        if f[0]:
+            node = int(f[1]) if f[1] != INT32_MAX else -1
+            raise SolverDivergenceError(f"non-finite field at step {step}", step=step, node=node)
+
+    def state(self) -> FieldState:
+        return FieldState(self.v.cpu().numpy().T.copy(), self.p.cpu().numpy(), self.T.cpu().numpy())
+
+    def nusselt(self) -> float:
+        return _nusselt_dev(self.ops, self.T) if self.ops._d_nu is not None else float("nan")
+
+    def divergence(self, which: str = "v") -> float:
+        return _interior_divergence_dev(self.ops, self.vstar if which == "vstar" else self.v)
+
+
+@dataclass
+class RunResult:
+    case: str
+    discretization: str
+    final_nu: float
+    nu_steps: np.ndarray
+    nu_times: np.ndarray
+    nu_values: np.ndarray
+    counts: tuple
+    n_total: int
+    timings: dict
+    dt: float
+    steps: int
+    t_final: float
+    status: str = "ok"
+    diagnostics: dict = field(default_factory=dict)
+    state: FieldState | None = None
+    nodeset: object = None
+
+
+def run(config, spec=None, nodeset=None) -> RunResult:
+    """Build operators and integrate the case to t_end (solver.py:395-490), GPU-resident.
+
+    `config` needs the CaseConfig fields run() reads (Ra, Pr, t_cold, t_hot, t_init, t_end,
+    poisson_tol, poisson_maxiter, steady_tol, nu_window, nu_stride, case, discretization)
+    and a `cold_origins(spec)` method or attribute.  Node generation is outside the hot
+    path: pass `nodeset` (any NodeSet-like object); the reference's hybrid_discretize is
+    used only if it is importable."""
+    timings: dict = {}
+    t0 = time.perf_counter()
+    if nodeset is None:
+        try:
+            from hybridnodes.config import build_domain
+            from hybridnodes.nodegen import hybrid_discretize
+        except ImportError as exc:  # pragma: no cover - depends on the environment
+            raise ValueError("run() needs a nodeset: node generation is not part of the GPU path") from exc
+        spec = spec if spec is not None else build_domain(config)
+        nodeset = hybrid_discretize(config, spec)
+    timings["nodegen"] = time.perf_counter() - t0
+    settings = PoissonSolveSettings(tol=config.poisson_tol, maxiter=config.poisson_maxiter)
+    cold = config.cold_origins(spec) if callable(getattr(config, "cold_origins", None)) else set(config.cold_origins)
+    ops = build_operators(nodeset, cold, settings, timings=timings)
+    params = PhysicsParams(config.Ra, config.Pr, t_ref=0.5 * (config.t_cold + config.t_hot))
+    controls = TimeControls.from_spacing(float(np.min(nodeset.spacing)), config.t_end, Ra=config.Ra,
+                                         steady_tol=config.steady_tol, nu_window=config.nu_window,
+                                         nu_stride=config.nu_stride)
+    n = len(nodeset)
+    state = FieldState.zeros(n, nodeset.dim)
+    state.temperature[:] = config.t_init
+    apply_temperature_bc(state.temperature, ops)
+    dt = controls.dt
+    n_steps = max(1, int(np.ceil(controls.t_end / dt - 1e-12)))
+    monitor_stride = max(1, controls.nu_stride)
+    stepper = DeviceStepper(ops, params, settings, dt, state)
+    nu_steps, nu_times, nu_values, div_samples = [], [], [], []
+    t0 = time.perf_counter()
+    step = 0
+    for step in range(1, n_steps + 1):
+        stepper.step()
+        if step % monitor_stride == 0 or step == n_steps:
+            stepper.check_finite(step)
+            nu_steps.append(step)
+            nu_times.append(step * dt)
+            nu_values.append(stepper.nusselt())
+            if len(div_samples) < 64 or step == n_steps:
+                div_samples.append((step, stepper.divergence("vstar"), stepper.divergence("v")))
+            w = controls.nu_window
+            if controls.steady_tol > 0 and len(nu_values) >= 2 * w:
+                m1 = float(np.mean(nu_values[-w:]))
+                m0 = float(np.mean(nu_values[-2 * w:-w]))
+                span = (nu_times[-1] - nu_times[-w - 1]) or 1.0
+                if abs(m1 - m0) / (max(abs(m1), 1e-12) * span) < controls.steady_tol:
+                    break
+    stepper.check_finite(step)
+    L.torch().cuda.synchronize()
+    timings["stepping"] = time.perf_counter() - t0
+    timings["total"] = sum(timings.values())
+    final = stepper.state()
+    nr, ns_, nb = nodeset.counts
+    return RunResult(case=getattr(config, "case", "custom"), discretization=getattr(config, "discretization", ""),
+                     final_nu=nu_values[-1] if nu_values else float("nan"), nu_steps=np.asarray(nu_steps),
+                     nu_times=np.asarray(nu_times), nu_values=np.asarray(nu_values), counts=(nr, ns_, nb),
+                     n_total=n, timings=timings, dt=dt, steps=step, t_final=step * dt,
+                     diagnostics={"divergence_samples": div_samples,
+                                  "temperature_range": (float(final.temperature.min()),
+                                                        float(final.temperature.max()))},
+                     state=final, nodeset=nodeset)
