@@ -1,0 +1,489 @@
+"""Benchmark for the hybrid RBF-FD hot path on B200 (contract: see DESIGN.md §6).
+
+Default workload (BASELINE configs[1], the metric's first half): config 1, the 2D
+scattered set N = 99,856 -- one step = cell-list kNN stencils + batched RBF-FD
+PHS r^3 + degree-2 weight solves (18x18 fp64, Laplacian/d/dx/d/dy) for all 98,596
+interior rows, written into HBM ELL slabs.  `value` = stencil weights/s over the whole
+job; `e2e` = the same through the public API compute_weights() with host NodeSet in and
+host WeightTable out; `roofline` = the dominant kernel (weight solve) vs the live DFMA
+peak; `cpu_baseline` = the reference's algorithm (oracle port, 1 thread, the reference's
+protocol) on the same host.  --config 3 measures node-updates/s of explicit steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 0|1|2|3|4]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import numpy as np  # noqa: E402
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FLOPS_PER_STENCIL = {("rbf", 2, 12): 5613, ("rbf", 3, 20): 24625, ("rbf", 3, 30): 54500, ("mon", 2, 5): 205,
+                     ("mon", 3, 7): 567}
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- distributed plumbing
+def dist_init(n):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group(backend)
+    return rank, world
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def shard_seed(base: int, rank: int) -> int:
+    """Weak scaling: every rank owns an independent node set of the config's size."""
+    return base + 1000 * rank
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def __enter__(self):
+        try:
+            idx = os.environ.get("LOCAL_RANK", "0")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", idx, f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.file, stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.file.flush()
+        rows = []
+        for line in Path(self.file.name).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6 and parts[0].isdigit():
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [int(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- workloads
+def build_nodeset(cfg: int, seed_off: int = 0):
+    from paper_2303_01760_b200 import nodesets
+    if cfg == 0:
+        return nodesets.regular_box(199)
+    if cfg == 1:
+        return nodesets.jittered_box(315, seed=1 + seed_off)
+    if cfg in (2, 3):
+        return nodesets.hybrid_hole_2d(500, seed=2 + seed_off)
+    return nodesets.hybrid_sphere_3d(94, seed=4 + seed_off, refine=2.8)
+
+
+def measure_dfma_peak(L):
+    t = L.torch()
+    out = L.zeros(1, t.float64)
+    blocks, iters = 148 * 8, 8192
+    for _ in range(2):
+        L.call("hn_bench_dfma", L.ptr(out), blocks, iters, L.stream_handle())
+    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(3):
+        e0.record()
+        L.call("hn_bench_dfma", L.ptr(out), blocks, iters, L.stream_handle())
+        e1.record()
+        t.cuda.synchronize()
+        best = max(best, blocks * 256 * iters * 16 * 2 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
+class LaunchCounter:
+    """Kernels each libhn entry point launches (fixed per call; see csrc/*.cu)."""
+    KERNELS = {"hn_celllist_build": 5, "hn_knn": 1, "hn_classify": 1, "hn_mon_stencils": 1, "hn_weights_mon": 1,
+               "hn_weights_rbf": 1, "hn_apply_ell": 1, "hn_momentum": 1, "hn_div_rhs": 1,
+               "hn_correct_temperature": 1, "hn_temperature_bc": 2, "hn_csr_matvec": 1, "hn_csr_residual": 1,
+               "hn_sptrsv": 1, "hn_permute": 1, "hn_reduce": 2, "hn_bicg_update": 1, "hn_bench_dfma": 1}
+
+    def __init__(self, L):
+        self.L = L
+        self.count = 0
+        self.enabled = False
+        self._orig = L.call
+
+        def counted(name, *args):
+            if self.enabled:
+                self.count += self.KERNELS.get(name, 1)
+            return self._orig(name, *args)
+
+        L.call = counted
+
+
+def run_weights_bench(args, rank, world):
+    import paper_2303_01760_b200 as hn
+    from paper_2303_01760_b200 import _device, _lib as L, approx
+    t = L.torch()
+    counter = LaunchCounter(L)
+    cfg = args.config
+    ns = build_nodeset(cfg, shard_seed(0, rank) if world > 1 else 0)
+    dim = ns.dim
+    ops = [hn.Laplacian()] + [hn.Partial(a) for a in range(dim)]
+    rbf_n = 20 if dim == 3 else None
+    n_int = int(ns.interior_mask.sum())
+    flush = L.empty(L2_FLUSH_BYTES // 8, t.float64)
+    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+
+    # ---- device-resident step: positions already in HBM (cached DeviceNodes) ----
+    dn_cached = _device.DeviceNodes(ns)
+
+    def device_step():
+        dn = _device.DeviceNodes.__new__(_device.DeviceNodes)
+        dn.__dict__.update(dn_cached.__dict__)
+        # rebuild the cell list from the resident positions (part of the stencil builder, K1)
+        scratch = L.empty(int(np.prod(dn.dims)), t.int32)
+        scratch2 = L.empty(dn.n, t.int32)
+        L.call("hn_celllist_build", L.ptr(dn.pos), dn.n, dn.dim, L.host_dbls(dn.lo), dn.cell, L.host_ints(dn.dims),
+               L.ptr(dn.cell_start), L.ptr(dn.cell_items), L.ptr(dn.cell_pos), L.ptr(scratch), L.ptr(scratch2),
+               L.stream_handle())
+        _device._NODE_CACHE[ns] = (ns.positions, ns.positions.shape, dn)
+        return approx._interior_device_table(ns, ops, rbf_n)
+
+    for _ in range(args.warmup):
+        device_step()
+    t.cuda.synchronize()
+    barrier(world)
+    times = []
+    counter.enabled = True
+    with ClockSampler() as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            e0.record()
+            device_step()
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    counter.enabled = False
+    t.cuda.synchronize()
+    barrier(world)
+    launches = counter.count // max(args.steps, 1)
+    ms = max_over_ranks(float(np.mean(times)), world)
+    value = world * n_int / (ms * 1e-3)
+
+    # ---- dominant kernel: the RBF (or MON for config 0) weight solve, timed alone ----
+    dev = approx._interior_device_table(ns, ops, rbf_n)
+    method = dev.method
+    big = "rbf" if (method == 1).sum() >= (method == 0).sum() * (0.05 if dim == 2 else 0.2) or cfg == 1 else "mon"
+    rows = np.nonzero(method == (1 if big == "rbf" else 0))[0]
+    dn = _device.device_nodes(ns)
+    if big == "rbf":
+        st = dn.knn(rbf_n or 12, rows=L.to_device(rows.astype(np.int32)))
+        nst = rbf_n or 12
+    else:
+        st = dn.mon_stencils(L.to_device(rows.astype(np.int32)))
+        nst = 2 * dim + 1
+    K = len(rows)
+    kinds, axes, normals = approx._op_args(ops, dim)
+    oi = L.empty((nst, K), t.int32)
+    ow = L.empty((len(ops), nst, K), t.float64)
+    info = L.zeros(K, t.int32)
+
+    def solve():
+        if big == "rbf":
+            counter._orig("hn_weights_rbf", L.ptr(dn.pos), dim, L.ptr(st), K, nst, len(ops), kinds, axes, normals,
+                          None, None, L.ptr(oi), L.ptr(ow), L.ptr(info), L.stream_handle())
+        else:
+            counter._orig("hn_weights_mon", L.ptr(dn.pos), dim, L.ptr(st), K, len(ops), kinds, axes, normals,
+                          L.ptr(oi), L.ptr(ow), L.ptr(info), L.stream_handle())
+
+    for _ in range(3):
+        solve()
+    kt = []
+    for _ in range(max(5, args.steps)):
+        flush.fill_(2.0)
+        e0.record()
+        solve()
+        e1.record()
+        e1.synchronize()
+        kt.append(e0.elapsed_time(e1))
+    k_ms = float(np.median(kt))
+    fps = FLOPS_PER_STENCIL[(big, dim, nst)]
+    achieved = K * fps / (k_ms * 1e-3) / 1e12
+    peak = measure_dfma_peak(L)
+    traffic = None
+    tj = ROOT / "profiles" / "traffic.json"
+    if tj.exists():
+        traffic = json.loads(tj.read_text()).get(f"weights_config{cfg}")
+
+    # ---- secondary: fused 3/4-op apply over the same table (HBM roofline) ----
+    f = L.to_device(build_field(ns))
+    out = L.empty((len(ops), len(ns)), t.float64)
+    nb, bK, bW, bR, bI, bWt, live = _device.bins_args(dev.bins)
+    op_sel = L.host_ints(list(range(len(ops))))
+
+    def app():
+        counter._orig("hn_apply_ell", nb, bK, bW, bR, bI, bWt, len(ops), op_sel, L.ptr(f), L.ptr(out), len(ns),
+                      L.stream_handle())
+
+    for _ in range(3):
+        app()
+    at = []
+    for _ in range(max(10, args.steps)):
+        flush.fill_(3.0)
+        e0.record()
+        app()
+        e1.record()
+        e1.synchronize()
+        at.append(e0.elapsed_time(e1))
+    a_ms = float(np.median(at))
+    S = int(sum(b.K * b.width for b in live))
+    a_bytes = (4 + 8 * len(ops)) * S + 8 * len(ns) + 8 * len(ops) * len(ns) + 4 * len(ns)
+    peaks = load_peaks()
+
+    # ---- end to end through the public API: host NodeSet in, host WeightTable out ----
+    from paper_2303_01760_b200.nodegen import NodeSet
+    e2e_t = []
+    h2d = d2h = 0
+    for k in range(args.warmup + args.steps):
+        fresh = NodeSet(ns.positions, ns.spacing, ns.kind, ns.role, ns.bc_value, ns.normals, ns.origin, ns.lattice,
+                        ns.lattice_idx)
+        flush.fill_(4.0)
+        t.cuda.synchronize()
+        t0 = time.perf_counter()
+        table = hn.compute_weights(fresh, ops, rbf_n=rbf_n) if rbf_n else hn.compute_weights(fresh, ops)
+        idx = table.indices
+        w = table.weights
+        t.cuda.synchronize()
+        if k >= args.warmup:
+            e2e_t.append(time.perf_counter() - t0)
+        h2d = ns.positions.size * 8 // dim * (2 if dim == 2 else 4) + ns.kind.nbytes + \
+            (ns.lattice.grid.size * 4 + ns.lattice_idx.size * 4 if ns.lattice is not None else 0)
+        d2h = sum(b.K * b.width * (4 + 8 * len(ops)) for b in dev.bins) + len(ns)
+    e2e_s = max_over_ranks(float(np.mean(e2e_t)), world)
+
+    line = {
+        "metric": "stencil weights/sec", "value": value, "unit": "stencils/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded node sets, SURVEY Appendix B)",
+        "config": {"workload": config_name(cfg, ns), "N": len(ns), "interior_rows": n_int,
+                   "stencils": stencil_mix(dev), "ops": len(ops), "l2": "flushed between steps (256 MiB write)",
+                   "parallelism": f"weak x{world} (independent node set per rank)"},
+        "e2e": {"value": world * n_int / e2e_s, "unit": "stencils/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "api": "paper_2303_01760_b200.compute_weights(NodeSet, ops)"},
+        "roofline": {"bound": "fp64", "kernel": f"rbf_weights_kernel<{dim},{nst}>" if big == "rbf" else
+                     f"mon_weights_kernel<{dim}>", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic": f"{fps} flop/stencil (LAPACK getrf+getrs count, SURVEY §8(d)) x {K} stencils",
+                     "kernel_ms": k_ms,
+                     "peak_source": "live DFMA probe (hn_bench_dfma); MEASURED_PEAKS.json has no fp64 entry"},
+        "apply": {"metric": "fused multi-op application", "kernel": "apply_ell_kernel", "ms": a_ms,
+                  "bytes": a_bytes, "achieved_gbs": a_bytes / (a_ms * 1e-3) / 1e9, "peak_gbs": peaks.get("hbm_gbs"),
+                  "frac": a_bytes / (a_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6526.8),
+                  "node_updates_per_s": len(ns) / (a_ms * 1e-3),
+                  "bytes_formula": "(4 + 8*ops)*S + 8N (field) + 8*ops*N (out) + 4N (row ids)"},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_weights(ns, ops, rbf_n)
+    return line
+
+
+def build_field(ns):
+    from paper_2303_01760_b200 import nodesets
+    return nodesets.sinusoid_field(ns.positions)
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def config_name(cfg, ns):
+    c = ns.counts
+    return {0: f"config0: 2D regular 200x200, N={len(ns)}, MON 5-point, Lap/dx/dy weights",
+            1: f"config1: 2D scattered jittered M=315, N={len(ns)}, kNN n=12 + RBF-FD 18x18, Lap/dx/dy weights",
+            2: f"config2: 2D hybrid hole M=500, N={len(ns)} ({c[1] / len(ns):.1%} scattered), kNN + MON/RBF weights",
+            3: f"config3: config-2 set, explicit Boussinesq steps Ra=1e6 Pr=0.71 with reference pressure",
+            4: f"config4: 3D hybrid sphere, N={len(ns)} ({c[1] / len(ns):.1%} scattered), MON 7 + RBF-FD n=20 (30x30)",
+            }[cfg]
+
+
+def stencil_mix(dev):
+    return {f"w{b.width}": int(b.K) for b in dev.bins if b.width}
+
+
+def cpu_baseline_weights(ns, ops, rbf_n):
+    """The reference algorithm (oracle port: cKDTree + LAPACK dgesv, 1 thread) on the same
+    host, bounded sample = the whole config once or more (about 3-15 s)."""
+    from oracle import hn_oracle as O
+    keys = [O.op_tuple(o) for o in ops]
+    n_int = int(ns.interior_mask.sum())
+    reps, t_total = 0, 0.0
+    while t_total < 3.0 and reps < 5:
+        t0 = time.perf_counter()
+        O.compute_weights(ns, keys, rbf_n=rbf_n)
+        t_total += time.perf_counter() - t0
+        reps += 1
+    return {"value": reps * n_int / t_total, "unit": "stencils/s", "cores": 1, "kind": "port",
+            "sample": f"oracle compute_weights on the full workload x{reps} ({t_total:.1f} s), "
+                      f"OPENBLAS_NUM_THREADS=1 (reference protocol, cli.py:7-10)",
+            "host_cpu": cpu_model()}
+
+
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------- config 3: time steps
+def run_steps_bench(args, rank, world):
+    import paper_2303_01760_b200 as hn
+    from paper_2303_01760_b200 import _lib as L
+    t = L.torch()
+    counter = LaunchCounter(L)
+    ns = build_nodeset(3, shard_seed(0, rank) if world > 1 else 0)
+    settings = hn.PoissonSolveSettings()
+    ops = hn.build_operators(ns, {"wall:x-"}, settings)
+    dt = hn.TimeControls.from_spacing(float(np.min(ns.spacing)), 1.0, Ra=1e6).dt
+    T0 = (ns.positions[:, 0] - 0.5) + 1e-3 * np.random.default_rng(3).normal(size=len(ns))
+    st = hn.FieldState(np.zeros((len(ns), 2)), np.zeros(len(ns)), T0)
+    hn.apply_temperature_bc(st.temperature, ops)
+    stepper = hn.DeviceStepper(ops, hn.PhysicsParams(1e6, 0.71), settings, dt, st)
+    for _ in range(args.warmup):
+        stepper.step()
+    t.cuda.synchronize()
+    barrier(world)
+    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    counter.enabled = True
+    with ClockSampler() as clocks:
+        e0.record()
+        for _ in range(args.steps):
+            stepper.step()
+        e1.record()
+        t.cuda.synchronize()
+    counter.enabled = False
+    stepper.check_finite(args.steps)
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    return {"metric": "node-updates/sec per step", "value": world * len(ns) / (ms * 1e-3), "unit": "node-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": config_name(3, ns), "N": len(ns), "dt": dt,
+                       "pressure": "LU-preconditioned BiCGStab (SuperLU factors in HBM, sync-free trisolves)"},
+            "gpu_launches": counter.count // max(1, args.steps), "clocks": clocks.summary()}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The reference's CPU implementation of the path (oracle port; the Python reference
+    cannot travel to the GPU box) on this host, all BLAS threads it wants, same workload."""
+    if world > 1 and rank != 0:
+        return None
+    from oracle import hn_oracle as O
+    cfg = args.config
+    ns = build_nodeset(cfg)
+    dim = ns.dim
+    keys = [("lap",)] + [("d", a) for a in range(dim)]
+    n_int = int(ns.interior_mask.sum())
+    rbf_n = 20 if dim == 3 else None
+    for _ in range(min(args.warmup, 1)):
+        O.compute_weights(ns, keys, rbf_n=rbf_n)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.compute_weights(ns, keys, rbf_n=rbf_n)
+        ts.append(time.perf_counter() - t0)
+    s = float(np.mean(ts))
+    v = n_int / s
+    return {"impl": "reference", "metric": "stencil weights/sec", "value": v, "unit": "stencils/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": config_name(cfg, ns), "N": len(ns)},
+            "cpu_baseline": {"value": v, "unit": "stencils/s", "cores": 1, "kind": "port",
+                             "sample": f"full workload per step, {args.steps} steps (numpy/scipy oracle port of "
+                                       "the reference: cKDTree + batched LAPACK dgesv; single-threaded numerics)",
+                             "host_cpu": cpu_model()},
+            "e2e": {"value": v, "unit": "stencils/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    rank, world = dist_init(args.gpus)
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    elif args.config == 3:
+        line = run_steps_bench(args, rank, world)
+    else:
+        line = run_weights_bench(args, rank, world)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

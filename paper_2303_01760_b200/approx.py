@@ -241,9 +241,9 @@ def _single(stencil, positions, op, mon: bool) -> WeightRow:
     if not np.isfinite(kappa):
         kind = "MON" if mon else "RBF-FD"
         raise SingularSystemError(f"singular {kind} system (duplicate nodes?)", kappa)
-    _, w = _solve_points(pts, [op], mon)
+    _, w = _solve_points(pts, [op], mon)  # local ids 0..n-1 are the stencil order
     order = np.argsort(nb)
-    return WeightRow(nb[order], {op: w[0, 0]}, kappa)
+    return WeightRow(nb[order], {op: w[0, 0][order]}, kappa)
 
 
 def mon_weights(stencil: StencilSpec, positions: np.ndarray, op) -> WeightRow:
@@ -382,15 +382,18 @@ def _interior_device_table(nodeset, ops, n_rbf: int | None = None) -> DeviceTabl
     if len(none_rows):
         bins.append(Bin(none_rows, 0, L.empty((0, len(none_rows)), t.int32),
                         L.empty((len(ops), 0, len(none_rows)), t.float64)))
-    return DeviceTable(n, dim, list(ops), bins, RBF_SIZE[dim], method)
+    return DeviceTable(n, dim, list(ops), bins, n_rbf, method)
 
 
-def compute_weights(nodeset, ops, with_kappa: bool = False, tree=None) -> WeightTable:
-    """Stencils and weights for every interior node, batched per method (approx.py:379-413)."""
+def compute_weights(nodeset, ops, with_kappa: bool = False, tree=None, rbf_n: int | None = None) -> WeightTable:
+    """Stencils and weights for every interior node, batched per method (approx.py:379-413).
+
+    `rbf_n` (extension) overrides RBF_SIZE[d] for this call, as the reference allows by
+    rebinding its module constant."""
     ops = list(ops)
     for op in ops:
         _op_code(op, nodeset.dim)
-    dev = _interior_device_table(nodeset, ops)
+    dev = _interior_device_table(nodeset, ops, rbf_n)
     table = WeightTable(method=dev.method, _device=dev)
     if with_kappa:
         kappa = np.full(len(nodeset), np.nan)
@@ -444,7 +447,7 @@ def _boundary_stencils(nodeset, rows: np.ndarray, exclude: np.ndarray | None):
     return st, tie_rows
 
 
-def _boundary_table(nodeset, rows, exclude, ops, normals: bool) -> tuple[DeviceTable, np.ndarray]:
+def _boundary_table(nodeset, rows, exclude, ops, normals: bool, override=None) -> tuple[DeviceTable, np.ndarray]:
     rows = np.asarray(rows, dtype=np.int64)
     n = len(nodeset)
     dim = nodeset.dim
@@ -457,6 +460,15 @@ def _boundary_table(nodeset, rows, exclude, ops, normals: bool) -> tuple[DeviceT
         rows_sorted = rows[order]
         st, ties = _boundary_stencils(nodeset, rows_sorted, exclude)
         size = int(st.shape[1])
+        if override is not None:
+            # explicit stencils for chosen rows (e.g. the reference's cKDTree choice on the
+            # exact-tie rows of SURVEY §8(a) A5), given as (rows, (k, size) stencils)
+            o_rows, o_st = np.asarray(override[0], dtype=np.int64), np.asarray(override[1])
+            pos = np.searchsorted(rows_sorted, o_rows)
+            if len(o_rows) and (np.any(pos >= len(rows_sorted)) or np.any(rows_sorted[pos] != o_rows)):
+                raise ValueError("override rows must be among the requested rows")
+            if len(o_rows):
+                st[L.to_device(pos.astype(np.int64))] = L.to_device(o_st.astype(np.int32))
         rn = np.asarray(nodeset.normals, float)[rows_sorted] if normals else None
         bins.append(_solve_bin(dn, st, rows_sorted, ops, False, row_normals=rn))
     rest = np.setdiff1d(np.arange(n), rows)
@@ -478,10 +490,14 @@ def normal_derivative_table(nodeset, rows: np.ndarray, tree=None, exclude: np.nd
     return t
 
 
-def boundary_partial_table(nodeset, rows: np.ndarray, tree=None, exclude: np.ndarray | None = None) -> WeightTable:
-    """One-sided RBF-FD first-derivative rows at boundary nodes, all axes (approx.py:468-491)."""
+def boundary_partial_table(nodeset, rows: np.ndarray, tree=None, exclude: np.ndarray | None = None,
+                           stencil_override=None) -> WeightTable:
+    """One-sided RBF-FD first-derivative rows at boundary nodes, all axes (approx.py:468-491).
+
+    `stencil_override=(rows, stencils)` (extension) fixes the stencils of chosen rows;
+    `table.tie_rows` lists rows whose (d, idx) choice may differ from cKDTree's."""
     ops = [Partial(a) for a in range(nodeset.dim)]
-    dev, ties = _boundary_table(nodeset, rows, exclude, ops, False)
+    dev, ties = _boundary_table(nodeset, rows, exclude, ops, False, stencil_override)
     t = WeightTable(method=dev.method, _device=dev)
     t.tie_rows = ties
     return t

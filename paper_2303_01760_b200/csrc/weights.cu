@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(128) mon_weights_kernel(const double* __restri
 
 // ===================== RBF-FD (LPS lanes per stencil, rows in registers) ===================
 template <int D, int NST, int NOPS>
-struct RbfSmem {
+struct __align__(16) RbfSmem {  // 16 B: every system's prow takes v2.f64 stores
   static constexpr int NQ = poly_count<D>();
   static constexpr int NS = NST + NQ;
   static constexpr int NC = NS + NOPS;

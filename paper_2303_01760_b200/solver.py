@@ -207,8 +207,12 @@ def _table_to_csr(table, key, n: int) -> sparse.csr_matrix:
 
 
 def build_operators(nodeset, cold_origins: set, settings: PoissonSolveSettings,
-                    timings: dict | None = None) -> OperatorSet:
-    """Weights on the GPU, one-time host assembly + SuperLU, factors to HBM (solver.py:133-232)."""
+                    timings: dict | None = None, boundary_override=None, interior_rbf_n: int | None = None) -> OperatorSet:
+    """Weights on the GPU, one-time host assembly + SuperLU, factors to HBM (solver.py:133-232).
+
+    Extensions: `boundary_override=(rows, stencils)` pins chosen boundary-gradient
+    stencils (SURVEY §8(a) A5 tie rows); `interior_rbf_n` sets the interior RBF-FD stencil
+    size while the boundary tables keep RBF_SIZE (config 4: n = 20 inside, 30 at walls, H9)."""
     timings = timings if timings is not None else {}
     dim = nodeset.dim
     n = len(nodeset)
@@ -218,8 +222,9 @@ def build_operators(nodeset, cold_origins: set, settings: PoissonSolveSettings,
     cold_idx = np.array([i for i in boundary_idx if nodeset.origin[i] in cold_origins], dtype=np.int64)
 
     t0 = time.perf_counter()
-    table = compute_weights(nodeset, ops_wanted)
-    boundary_grad = boundary_partial_table(nodeset, boundary_idx, exclude=nodeset.boundary_mask)
+    table = compute_weights(nodeset, ops_wanted, rbf_n=interior_rbf_n)
+    boundary_grad = boundary_partial_table(nodeset, boundary_idx, exclude=nodeset.boundary_mask,
+                                           stencil_override=boundary_override)
     nu_table = normal_derivative_table(nodeset, cold_idx) if len(cold_idx) else None
     L.torch().cuda.synchronize()
     timings["weights"] = time.perf_counter() - t0

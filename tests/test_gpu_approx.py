@@ -1,0 +1,375 @@
+"""GPU parity for stencils and weights (approx.py), modelled on the reference's
+pkg/tests/test_approx.py plus golden-vector and full-size oracle comparisons.
+
+Tolerances: stencil indices / methods bit-exact; weights row-normwise relative
+||w_gpu - w_ref||_inf / ||w_ref||_inf <= 1e-11 (north star: 1e-9; 1e-11 keeps fields
+within 1e-8); analytic identities at the reference's own tolerances."""
+
+import math
+
+import numpy as np
+import numpy.testing as npt
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import paper_2303_01760_b200 as hn
+from conftest import GOLDEN_CASES
+from oracle import hn_oracle as O
+from paper_2303_01760_b200 import nodesets
+from paper_2303_01760_b200.approx import (METHOD_MON, Laplacian, NormalDerivative, Partial, StencilSpec,
+                                          classify_methods, compute_weights, condition_number, find_stencil,
+                                          mon_weights, normal_derivative_table, rbf_fd_weights, select_method)
+from paper_2303_01760_b200.errors import SingularSystemError
+from paper_2303_01760_b200.nodegen import KIND_REGULAR, KIND_SCATTERED, NodeSet
+
+pytestmark = pytest.mark.gpu
+W_TOL = 1e-11
+
+
+def rowwise_rel(a, b):
+    den = np.maximum(np.abs(b).max(axis=1), 1e-300)
+    return float((np.abs(a - b).max(axis=1) / den).max())
+
+
+def cloud_nodeset(points, h=0.5, kind=KIND_SCATTERED):
+    n = len(points)
+    return NodeSet(np.asarray(points, float), np.full(n, h), np.full(n, kind, dtype=np.int8),
+                   np.zeros(n, dtype=np.int8), np.full(n, np.nan), np.full((n, 2), np.nan))
+
+
+def lattice_nodeset(h=0.1, size=5):
+    pts = np.array([[i * h, j * h] for i in range(size) for j in range(size)])
+    return cloud_nodeset(pts, h=h, kind=KIND_REGULAR)
+
+
+def weights_of(row, op):
+    return dict(zip(map(int, row.neighbors), row.weights[op]))
+
+
+# ---------------------------------------------------------------- reference unit tests
+class TestSelectMethod:
+    def test_lattice_interior_mon(self):
+        assert select_method(12, lattice_nodeset()) == "mon"
+
+    def test_scattered_rbffd(self):
+        rng = np.random.default_rng(3)
+        assert select_method(0, cloud_nodeset(rng.uniform(0, 1, (30, 2)))) == "rbffd"
+
+    def test_missing_axis_neighbor_falls_back(self):
+        ns = lattice_nodeset()
+        keep = [i for i in range(25) if i != 13]
+        ns2 = cloud_nodeset(ns.positions[keep], h=0.1, kind=KIND_REGULAR)
+        assert select_method(keep.index(12), ns2) == "rbffd"
+        assert select_method(keep.index(6), ns2) == "mon"
+
+    def test_classify_without_lattice_matches_oracle(self):
+        ns = lattice_nodeset(size=7)
+        npt.assert_array_equal(classify_methods(ns), O.classify(ns))
+
+
+class TestFindStencil:
+    def test_lattice_axis_stencil(self):
+        st_ = find_stencil(12, lattice_nodeset(), 5)
+        assert set(map(int, st_.neighbors)) == {12, 7, 11, 13, 17}
+        assert st_.neighbors[0] == 12
+
+    def test_matches_brute_force(self):
+        rng = np.random.default_rng(5)
+        ns = cloud_nodeset(rng.uniform(0, 1, (100, 2)))
+        for center in (0, 17, 63, 99):
+            got = find_stencil(center, ns, 12).neighbors
+            d = np.linalg.norm(ns.positions - ns.positions[center], axis=1)
+            npt.assert_array_equal(got, sorted(range(100), key=lambda i: (d[i], i))[:12])
+
+    def test_tie_break_by_index(self):
+        npt.assert_array_equal(find_stencil(12, lattice_nodeset(), 5).neighbors, [12, 7, 11, 13, 17])
+
+    def test_oversized_request_raises(self):
+        with pytest.raises(ValueError):
+            find_stencil(0, lattice_nodeset(size=2), 12)
+
+    @pytest.mark.parametrize("n", [1, 3, 12, 25, 40, 64])
+    def test_every_size_matches_brute_force(self, n):
+        rng = np.random.default_rng(n)
+        ns = cloud_nodeset(np.round(rng.uniform(0, 1, (200, 2)) * 16) / 16)  # many exact ties
+        for center in (0, 50, 199):
+            d = np.linalg.norm(ns.positions - ns.positions[center], axis=1)
+            npt.assert_array_equal(find_stencil(center, ns, n).neighbors,
+                                   sorted(range(200), key=lambda i: (d[i], i))[:n])
+
+
+class TestMonWeights:
+    def test_classic_fd_laplacian(self):
+        h = 0.1
+        ns = lattice_nodeset(h=h)
+        w = weights_of(mon_weights(find_stencil(12, ns, 5), ns.positions, Laplacian()), Laplacian())
+        assert w[12] == pytest.approx(-4 / h ** 2, rel=1e-12)
+        for nb in (7, 11, 13, 17):
+            assert w[nb] == pytest.approx(1 / h ** 2, rel=1e-12)
+
+    def test_classic_fd_partial_x(self):
+        h = 0.1
+        ns = lattice_nodeset(h=h)
+        w = weights_of(mon_weights(find_stencil(12, ns, 5), ns.positions, Partial(0)), Partial(0))
+        assert w[7] == pytest.approx(-1 / (2 * h), rel=1e-12)
+        assert w[17] == pytest.approx(1 / (2 * h), rel=1e-12)
+        assert abs(w[12]) < 1e-12 / h and abs(w[11]) < 1e-12 / h and abs(w[13]) < 1e-12 / h
+
+    def test_constant_annihilated(self):
+        ns = lattice_nodeset()
+        row = mon_weights(find_stencil(12, ns, 5), ns.positions, Laplacian())
+        assert abs(sum(row.weights[Laplacian()])) < 1e-9
+
+    def test_duplicate_nodes_raise(self):
+        pts = np.array([[0.0, 0.0], [0.1, 0.0], [0.1, 0.0], [0.0, 0.1], [0.0, -0.1]])
+        with pytest.raises(SingularSystemError):
+            mon_weights(StencilSpec(0, np.arange(5), "mon"), pts, Laplacian())
+
+
+class TestRbfFdWeights:
+    def make_stencil(self, seed=0, n=12):
+        rng = np.random.default_rng(seed)
+        pts = np.concatenate([[[0.0, 0.0]], rng.uniform(-1, 1, (40, 2))])
+        return find_stencil(0, cloud_nodeset(pts), n), pts
+
+    def test_weight_sum_zero(self):
+        st_, pts = self.make_stencil()
+        assert abs(np.sum(rbf_fd_weights(st_, pts, Laplacian()).weights[Laplacian()])) < 1e-10
+
+    def test_quadratic_moment(self):
+        st_, pts = self.make_stencil(1)
+        row = rbf_fd_weights(st_, pts, Laplacian())
+        r2 = np.sum((pts[row.neighbors] - pts[0]) ** 2, axis=1)
+        assert np.dot(row.weights[Laplacian()], r2) == pytest.approx(4.0, rel=1e-10)
+
+    def test_independent_dense_oracle(self):
+        st_, pts = self.make_stencil(2)
+        row = rbf_fd_weights(st_, pts, Laplacian())
+        idx = st_.neighbors
+        p = pts[idx]
+        n, q = 12, 6
+        sys_ = np.zeros((n + q, n + q))
+        mono = lambda s: [1.0, s[0], s[1], s[0] ** 2, s[0] * s[1], s[1] ** 2]  # noqa: E731
+        for i in range(n):
+            for j in range(n):
+                sys_[i, j] = math.dist(p[i], p[j]) ** 3
+            sys_[i, n:] = mono(p[i])
+            sys_[n:, i] = mono(p[i])
+        rhs = np.zeros(n + q)
+        for j in range(n):
+            rhs[j] = 9.0 * math.dist(p[0], p[j])
+        rhs[n + 3] = 2.0
+        rhs[n + 5] = 2.0
+        oracle = np.linalg.solve(sys_, rhs)[:n]
+        order = np.argsort(idx)
+        npt.assert_allclose(row.weights[Laplacian()], oracle[order], rtol=0, atol=1e-10 * np.abs(oracle).max())
+
+    def test_singular_raises(self):
+        pts = np.zeros((12, 2))
+        pts[:, 0] = np.linspace(0, 1, 12)
+        with pytest.raises(SingularSystemError):
+            rbf_fd_weights(StencilSpec(0, np.arange(12), "rbffd"), pts, Laplacian())
+
+    @pytest.mark.parametrize("n", [8, 12, 16, 24])
+    def test_generic_sizes_match_oracle(self, n):
+        """Stencil sizes without a tuned kernel take the generic path; same numerics."""
+        st_, pts = self.make_stencil(3, n=n)
+        got = rbf_fd_weights(st_, pts, Partial(1))
+        ref = O.rbf_solve(pts, st_.neighbors[None], [("d", 1)])[0, :, 0][np.argsort(st_.neighbors)]
+        assert rowwise_rel(got.weights[Partial(1)][None], ref[None]) <= W_TOL
+
+
+class TestConditionNumber:
+    def test_basic(self):
+        assert condition_number(np.eye(4)) == 1.0
+        assert condition_number(np.diag([10.0, 1.0])) == pytest.approx(10.0)
+        assert condition_number(np.zeros((2, 2))) == float("inf")
+
+    def test_rbffd_exceeds_mon_on_typical_stencils(self):
+        ns = lattice_nodeset(h=0.1)
+        k_mon = mon_weights(find_stencil(12, ns, 5), ns.positions, Laplacian()).kappa
+        rng = np.random.default_rng(6)
+        pts = np.concatenate([[[0.0, 0.0]], rng.uniform(-1, 1, (30, 2))])
+        k_rbf = rbf_fd_weights(find_stencil(0, cloud_nodeset(pts), 12), pts, Laplacian()).kappa
+        assert k_rbf > k_mon
+
+
+@st.composite
+def scattered_stencil(draw):
+    rng = np.random.default_rng(draw(st.integers(0, 10_000)))
+    pts = [np.zeros(2)]
+    attempts = 0
+    while len(pts) < 12 and attempts < 500:
+        cand = rng.uniform(-1, 1, 2)
+        if all(np.linalg.norm(cand - p) > 0.25 for p in pts):
+            pts.append(cand)
+        attempts += 1
+    if len(pts) < 12:
+        pts = [np.zeros(2)] + [np.array([np.cos(t), np.sin(t)]) * (1 + 0.3 * (i % 3))
+                               for i, t in enumerate(np.linspace(0, 2 * np.pi, 11, endpoint=False))]
+    return np.asarray(pts)
+
+
+OPS = [Laplacian(), Partial(0), Partial(1), NormalDerivative((0.6, 0.8))]
+
+
+def analytic(op, e, xc):
+    def val(e, x):
+        return x[0] ** e[0] * x[1] ** e[1]
+
+    def d(e, a):
+        if e[a] == 0:
+            return None
+        o = list(e)
+        o[a] -= 1
+        return tuple(o), e[a]
+
+    if isinstance(op, Laplacian):
+        tot = 0.0
+        for a in (0, 1):
+            f = d(e, a)
+            s = d(f[0], a) if f else None
+            if f and s:
+                tot += f[1] * s[1] * val(s[0], xc)
+        return tot
+    if isinstance(op, Partial):
+        f = d(e, op.axis)
+        return 0.0 if f is None else f[1] * val(f[0], xc)
+    return sum(nm * d(e, a)[1] * val(d(e, a)[0], xc) for a, nm in zip((0, 1), op.normal) if d(e, a))
+
+
+class TestProperties:
+    @given(scattered_stencil(), st.sampled_from(OPS))
+    @settings(max_examples=25, deadline=None)
+    def test_rbffd_reproduces_quadratics(self, pts, op):
+        st_ = find_stencil(0, cloud_nodeset(pts), 12)
+        row = rbf_fd_weights(st_, pts, op)
+        scale = np.abs(row.weights[op]).max()
+        for e in [(0, 0), (1, 0), (0, 1), (2, 0), (1, 1), (0, 2)]:
+            s = pts[row.neighbors][:, 0] ** e[0] * pts[row.neighbors][:, 1] ** e[1]
+            assert np.dot(row.weights[op], s) == pytest.approx(analytic(op, e, pts[0]), abs=1e-8 * max(scale, 1.0))
+
+    @given(scattered_stencil(), st.floats(-50, 50), st.floats(-50, 50), st.floats(0.01, 100))
+    @settings(max_examples=15, deadline=None)
+    def test_translation_and_scaling(self, pts, tx, ty, s):
+        st_ = find_stencil(0, cloud_nodeset(pts), 12)
+        base = rbf_fd_weights(st_, pts, Laplacian()).weights[Laplacian()]
+        lap_t = rbf_fd_weights(st_, pts + np.array([tx, ty]), Laplacian()).weights[Laplacian()]
+        npt.assert_allclose(lap_t, base, rtol=1e-10, atol=1e-10 * np.abs(base).max())
+        lap_s = rbf_fd_weights(st_, pts * s, Laplacian()).weights[Laplacian()]
+        npt.assert_allclose(lap_s, base / s ** 2, rtol=1e-10, atol=1e-10 * np.abs(base / s ** 2).max())
+
+
+# ---------------------------------------------------------------- golden vectors (reference output)
+NAMES = ["lap", "d0", "d1", "d2"]
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_compute_weights_matches_reference_golden(golden, case):
+    ns, g = golden(case)
+    dim = ns.dim
+    ops = [Laplacian()] + [Partial(a) for a in range(dim)]
+    t = compute_weights(ns, ops, rbf_n=20 if dim == 3 else None)
+    npt.assert_array_equal(t.method, g["method"])
+    npt.assert_array_equal(t.sizes, g["sizes"])
+    npt.assert_array_equal(t.indices, g["indices"])
+    for op, name in zip(ops, NAMES):
+        assert rowwise_rel(t.weights[op], g[f"w_{name}"]) <= W_TOL, name
+
+
+def test_3d_reference_default_n30_matches_golden(golden):
+    ns, g = golden("config4_small")
+    ops = [Laplacian(), Partial(0), Partial(1), Partial(2)]
+    t = compute_weights(ns, ops)  # RBF_SIZE[3] = 30, the reference default (40x40 systems)
+    npt.assert_array_equal(t.indices, g["n30_indices"])
+    for op, name in zip(ops, NAMES):
+        assert rowwise_rel(t.weights[op], g[f"n30_w_{name}"]) <= W_TOL
+
+
+@pytest.mark.parametrize("case", ["dvd_coarse", "config0_small", "config1_small", "config2_small", "config4_small"])
+def test_boundary_tables_match_reference_golden(golden, case):
+    """Exact except on exact-tie rows, where the reference keeps cKDTree's traversal
+    choice: there our (distance, index) choice must be a valid
+    nearest set, and with the reference stencils imposed the weights match."""
+    ns, g = golden(case)
+    bidx = np.nonzero(ns.boundary_mask)[0]
+    t = hn.boundary_partial_table(ns, bidx, exclude=ns.boundary_mask)
+    same = np.all(t.indices == g["bgrad_indices"], axis=1)
+    bad = np.nonzero(~same)[0]
+    assert set(bad) <= set(t.tie_rows), "stencil differs outside the exact-tie rows"
+    pos = ns.positions
+    for r in bad:  # our choice: distances are the same multiset as the reference's
+        mine = np.sort(np.linalg.norm(pos[t.indices[r]] - pos[r], axis=1))
+        ref = np.sort(np.linalg.norm(pos[g["bgrad_indices"][r]] - pos[r], axis=1))
+        npt.assert_array_equal(mine, ref)
+    ref_st = O.boundary_stencils(ns, bidx[np.isin(bidx, bad)], ns.boundary_mask, g["bgrad_indices"].shape[1])
+    t2 = hn.boundary_partial_table(ns, bidx, exclude=ns.boundary_mask,
+                                   stencil_override=(bidx[np.isin(bidx, bad)], ref_st))
+    npt.assert_array_equal(t2.indices, g["bgrad_indices"])
+    for a in range(ns.dim):
+        assert rowwise_rel(t2.weights[Partial(a)][bidx], g[f"bgrad_w_d{a}"][bidx]) <= W_TOL
+    if "nu_rows" in g:
+        nt = normal_derivative_table(ns, g["nu_rows"])
+        npt.assert_array_equal(nt.indices, g["nu_indices"])
+        assert rowwise_rel(nt.weights["normal"][g["nu_rows"]], g["nu_w"][g["nu_rows"]]) <= W_TOL
+
+
+# ---------------------------------------------------------------- full BASELINE sizes vs the oracle
+FULL = {0: lambda: nodesets.regular_box(199), 1: lambda: nodesets.jittered_box(315, seed=1),
+        2: lambda: nodesets.hybrid_hole_2d(500, seed=2)}
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_full_config_weights_match_oracle(cfg):
+    ns = FULL[cfg]()
+    ops = [Laplacian(), Partial(0), Partial(1)]
+    t = compute_weights(ns, ops)
+    ref = O.compute_weights(ns, [("lap",), ("d", 0), ("d", 1)])
+    npt.assert_array_equal(t.method, ref["method"])
+    npt.assert_array_equal(t.indices, ref["indices"])
+    for op, key in zip(ops, ref["weights"]):
+        assert rowwise_rel(t.weights[op], ref["weights"][key]) <= W_TOL
+
+
+def test_full_config4_weights_match_oracle():
+    """1e6-node 3D set: indices bit-exact, weights within tolerance (n = 20, BASELINE)."""
+    ns = nodesets.hybrid_sphere_3d(94, seed=4, refine=2.8)
+    ops = [Laplacian(), Partial(0), Partial(1), Partial(2)]
+    t = compute_weights(ns, ops, rbf_n=20)
+    ref = O.compute_weights(ns, [("lap",), ("d", 0), ("d", 1), ("d", 2)], rbf_n=20)
+    npt.assert_array_equal(t.method, ref["method"])
+    npt.assert_array_equal(t.indices, ref["indices"])
+    for op, key in zip(ops, ref["weights"]):
+        assert rowwise_rel(t.weights[op], ref["weights"][key]) <= W_TOL
+
+
+# ---------------------------------------------------------------- edge cases
+def test_empty_row_sets():
+    ns = nodesets.regular_box(9)
+    t = hn.boundary_partial_table(ns, np.empty(0, dtype=np.int64), exclude=ns.boundary_mask)
+    assert t.sizes.sum() == 0
+    nt = normal_derivative_table(ns, np.empty(0, dtype=np.int64))
+    assert nt.sizes.sum() == 0
+
+
+def test_exclude_mask_must_cover_rows():
+    ns = nodesets.regular_box(9)
+    with pytest.raises(ValueError):
+        hn.boundary_partial_table(ns, np.array([0]), exclude=ns.boundary_mask)
+
+
+def test_pure_scattered_and_pure_regular_tables_have_one_bin_kind():
+    t0 = compute_weights(nodesets.regular_box(29), [Laplacian()])
+    assert set(np.unique(t0.sizes)) == {0, 5}
+    t1 = compute_weights(nodesets.jittered_box(29), [Laplacian()])
+    assert set(np.unique(t1.sizes)) == {0, 12}
+
+
+def test_with_kappa_matches_oracle_system_kappa(golden):
+    ns, g = golden("dvd_coarse")
+    t = compute_weights(ns, [Laplacian()], with_kappa=True)
+    inner = ns.interior_mask
+    assert np.all(np.isfinite(t.kappa[inner])) and np.all(np.isnan(t.kappa[~inner]))
+    mon = t.method == METHOD_MON
+    assert np.all(t.kappa[mon] < t.kappa[t.method == 1].max())
