@@ -65,6 +65,11 @@ int hn_classify(const int8_t* kind, const int* lattice_idx, const int* grid,
 int hn_mon_stencils(const int* rows, int64_t nrows, const double* pos, const int* lattice_idx,
                     const int* grid, const int* grid_dims_host, int d, int* out, void* stream);
 
+/* Stable partition of node ids by method: rows_out = [MON asc | RBF-FD asc | NONE asc],
+ * counts_out (3 int32, device) = class sizes; scratch >= 3*ceil(n/256) ints. */
+int hn_partition_methods(const int8_t* method, int64_t n, int* rows_out, int* counts_out, int* scratch,
+                         void* stream);
+
 /* ----------------------------------------------------------------- weights (K4-K5) */
 
 /* Outputs go straight into an ELL slab of K rows: out_idx[j*K + k] (ascending node ids),
@@ -154,6 +159,20 @@ int hn_csr_residual(const int64_t* rowptr, const int* cols, const double* vals, 
  * Replaces: SuperLU lu.solve inside the bicgstab preconditioner, solver.py:213-214. */
 int hn_sptrsv(int lower, const int64_t* rowptr, const int* cols, const double* vals, const double* diag,
               const double* b, double* x, int64_t n, unsigned long long* ticket, void* stream);
+
+/* Scheduled sync-free triangular solve over precomputed tasks (rows in dependency-level
+ * order; rows longer than a chunk split into partial-sum tasks, task_np = -1, combined in
+ * fixed order by the row's final task, task_np = #partials).  divide != 0 divides by diag.
+ * x (n) and partial (npartial) are reset inside.  Deterministic. */
+int hn_sptrsv_tasks(int divide, const int* task_row, const int64_t* task_beg, const int* task_len,
+                    const int* task_part, const int* task_np, int64_t ntasks, const int* cols,
+                    const double* vals, const double* diag, const double* b, double* x, int64_t n,
+                    double* partial, int64_t npartial, unsigned long long* ticket, int warps_per_sm,
+                    void* stream);
+
+/* Setup helper on HOST arrays: dependency level of each row of a triangular CSR
+ * (rows swept increasing when lower != 0, decreasing otherwise). */
+int hn_host_levels(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower, int* levels_host);
 
 /* direction 0: out[perm[i]] = in[i]; direction 1: out[i] = in[perm[i]]. */
 int hn_permute(int direction, const int* perm, const double* in, int64_t n, double* out, void* stream);

@@ -148,13 +148,20 @@ def device_nodes(nodeset) -> DeviceNodes:
 class Bin:
     """ELL slab: K rows of stencil width W and n_ops weight planes (device)."""
 
-    def __init__(self, rows_host: np.ndarray, width: int, d_idx, d_w, d_rows=None):
-        self.rows_host = np.asarray(rows_host, dtype=np.int64)
-        self.K = len(self.rows_host)
+    def __init__(self, rows_host, width: int, d_idx, d_w, d_rows=None, K: int | None = None):
+        self._rows_host = None if rows_host is None else np.asarray(rows_host, dtype=np.int64)
+        self.K = int(K) if K is not None else len(self._rows_host)
         self.width = int(width)
-        self.d_rows = d_rows if d_rows is not None else L.to_device(self.rows_host.astype(np.int32))
+        self.d_rows = d_rows if d_rows is not None else L.to_device(self._rows_host.astype(np.int32))
         self.d_idx = d_idx  # (W, K) int32
         self.d_w = d_w      # (nops, W, K) fp64
+
+    @property
+    def rows_host(self) -> np.ndarray:
+        """Node ids of the bin's rows (copied from HBM on first use)."""
+        if self._rows_host is None:
+            self._rows_host = self.d_rows[: self.K].cpu().numpy().astype(np.int64)
+        return self._rows_host
 
 
 def bins_args(bins):
@@ -168,9 +175,19 @@ def bins_args(bins):
 class DeviceTable:
     """All bins of one weight table (rows of every node appear in exactly one bin)."""
 
-    def __init__(self, n: int, dim: int, ops: list, bins: list, n_max: int, method: np.ndarray | None = None):
+    def __init__(self, n: int, dim: int, ops: list, bins: list, n_max: int, method=None):
         self.n, self.dim, self.ops, self.bins, self.n_max = n, dim, list(ops), bins, n_max
-        self.method = method
+        self._method = method  # host array, or a device tensor copied on first use
+
+    @property
+    def method(self):
+        if self._method is not None and hasattr(self._method, "is_cuda"):
+            self._method = self._method.cpu().numpy().astype(np.int8)
+        return self._method
+
+    @method.setter
+    def method(self, v):
+        self._method = v
 
     @property
     def ell_ok(self) -> bool:

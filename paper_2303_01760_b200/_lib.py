@@ -50,6 +50,10 @@ SIGNATURES: dict[str, tuple] = {
     "hn_csr_matvec": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "hn_csr_residual": (_i, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "hn_sptrsv": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "hn_sptrsv_tasks": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _i,
+                             _vp]),
+    "hn_host_levels": (_i, [_vp, _vp, _i64, _i, _vp]),
+    "hn_partition_methods": (_i, [_vp, _i64, _vp, _vp, _vp, _vp]),
     "hn_permute": (_i, [_i, _vp, _vp, _i64, _vp, _vp]),
     "hn_reduce": (_i, [_i, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "hn_bicg_update": (_i, [_i, _vp, _vp, _vp, _d, _d, _i64, _vp]),

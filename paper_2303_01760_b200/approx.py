@@ -151,8 +151,9 @@ def _kappa_host(positions: np.ndarray, stencils: np.ndarray, mon: bool) -> np.nd
 
 
 # ---------------------------------------------------------------- device solves
-def _solve_bin(dn, stencils_dev, rows_host, ops, mon: bool, row_normals=None, label="") -> Bin:
-    """Weights for a batch of stencils straight into an ELL bin (ascending node order)."""
+def _solve_bin(dn, stencils_dev, d_rows, ops, mon: bool, row_normals=None):
+    """Weights for a batch of stencils straight into an ELL bin (ascending node order).
+    Returns (Bin, info); info[k] != 0 marks a singular stencil (checked by _check_info)."""
     t = L.torch()
     K, n = int(stencils_dev.shape[0]), int(stencils_dev.shape[1])
     nops = len(ops)
@@ -173,14 +174,24 @@ def _solve_bin(dn, stencils_dev, rows_host, ops, mon: bool, row_normals=None, la
             rn = L.to_device(np.ascontiguousarray(row_normals, dtype=float)) if row_normals is not None else None
             L.call("hn_weights_rbf", L.ptr(dn.pos), dn.dim, L.ptr(stencils_dev), K, n, nops, kinds, axes, normals,
                    L.ptr(rn), L.ptr(ws), L.ptr(d_idx), L.ptr(d_w), L.ptr(info), L.stream_handle())
-        bad = int(t.count_nonzero(info[:K]).item())
+    b = Bin(None, n, d_idx[:, :K] if K else d_idx[:, :0], d_w[:, :, :K] if K else d_w[:, :, :0], d_rows=d_rows, K=K)
+    b.mon = mon
+    return b, info[:K]
+
+
+def _check_info(pairs):
+    """One device reduction + one read-back for every bin's singular flags (approx.py:223-226, 278-281)."""
+    pairs = [(b, i) for b, i in pairs if b.K]
+    if not pairs:
+        return
+    t = L.torch()
+    flags = t.stack([t.count_nonzero(i) for _, i in pairs]).cpu().numpy()
+    for (b, info), bad in zip(pairs, flags):
         if bad:
-            first = int(t.nonzero(info[:K])[0].item())
-            kind = "MON" if mon else "RBF-FD saddle"
-            raise SingularSystemError(f"singular {kind} system: Singular matrix ({bad} stencil(s), first at node "
-                                      f"{int(rows_host[first])})")
-    return Bin(rows_host, n, d_idx[:, :K] if K else d_idx[:, :0], d_w[:, :, :K] if K else d_w[:, :, :0],
-               d_rows=L.to_device(np.asarray(rows_host, dtype=np.int32)))
+            first = int(t.nonzero(info)[0].item())
+            kind = "MON" if b.mon else "RBF-FD saddle"
+            raise SingularSystemError(f"singular {kind} system: Singular matrix ({int(bad)} stencil(s), first at "
+                                      f"node {int(b.d_rows[first].item())})")
 
 
 def _solve_points(points: np.ndarray, ops, mon: bool, row_normals=None):
@@ -196,7 +207,8 @@ def _solve_points(points: np.ndarray, ops, mon: bool, row_normals=None):
     tmp.kind = np.ones(k * n, dtype=np.int8)
     dn = device_nodes_uncached(tmp)
     st = L.to_device(np.arange(k * n, dtype=np.int32).reshape(k, n))
-    b = _solve_bin(dn, st, np.arange(k), ops, mon, row_normals)
+    b, info = _solve_bin(dn, st, L.to_device(np.arange(k, dtype=np.int32)), ops, mon, row_normals)
+    _check_info([(b, info)])
     idx = b.d_idx.cpu().numpy().T.reshape(k, n)          # local ids, ascending = stencil order ids
     w = b.d_w.cpu().numpy().transpose(0, 2, 1)           # (nops, K, n) ascending local id
     return idx, w
@@ -276,6 +288,7 @@ class WeightTable:
 
     def _detach(self):
         self._materialize()
+        _ = self.method
         self._dev = None
 
     @property
@@ -311,6 +324,8 @@ class WeightTable:
 
     @property
     def method(self):
+        if self._method is None and self._dev is not None:
+            self._method = self._dev.method
         return self._method
 
     @method.setter
@@ -357,32 +372,41 @@ def classify_methods(nodeset, tree=None) -> np.ndarray:
 
 
 def _interior_device_table(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
+    """classify -> device partition [MON | RBF | NONE] -> stencils -> solves, all in HBM;
+    one 12-byte read-back (the class sizes) and one deferred singular check."""
     dim = nodeset.dim
     n = len(nodeset)
     n_rbf = RBF_SIZE[dim] if n_rbf is None else n_rbf
     dn = device_nodes(nodeset)
-    method = classify_methods(nodeset)
     t = L.torch()
-    bins = []
-    mon_rows = np.nonzero(method == METHOD_MON)[0]
-    if len(mon_rows):
-        d_rows = L.to_device(mon_rows.astype(np.int32))
-        if getattr(nodeset, "lattice", None) is not None and getattr(nodeset, "lattice_idx", None) is not None:
-            st = dn.mon_stencils(d_rows)
-        else:
-            st = dn.knn(MON_SIZE[dim], rows=d_rows)
-        bins.append(_solve_bin(dn, st, mon_rows, ops, True))
-    rbf_rows = np.nonzero(method == METHOD_RBFFD)[0]
-    if len(rbf_rows):
+    has_lattice = getattr(nodeset, "lattice", None) is not None and getattr(nodeset, "lattice_idx", None) is not None
+    if has_lattice or not np.any(np.asarray(nodeset.kind) == KIND_REGULAR):
+        method_d = dn.classify()
+    else:  # probe path without a lattice map (approx.py:352-356)
+        method_d = L.to_device(classify_methods(nodeset))
+    rows_d = L.empty(max(n, 1), t.int32)
+    counts_d = L.empty(3, t.int32)
+    scratch = L.empty(3 * (n // 256 + 1) + 1, t.int32)
+    L.call("hn_partition_methods", L.ptr(method_d), n, L.ptr(rows_d), L.ptr(counts_d), L.ptr(scratch),
+           L.stream_handle())
+    k_mon, k_rbf, k_none = (int(v) for v in counts_d.cpu().numpy())
+    bins, pending = [], []
+    if k_mon:
+        d_rows = rows_d[:k_mon]
+        st = dn.mon_stencils(d_rows) if has_lattice else dn.knn(MON_SIZE[dim], rows=d_rows)
+        pending.append(_solve_bin(dn, st, d_rows, ops, True))
+    if k_rbf:
         if n_rbf > n:
             raise ValueError(f"stencil size {n_rbf} exceeds node count {n}")
-        st = dn.knn(n_rbf, rows=L.to_device(rbf_rows.astype(np.int32)))
-        bins.append(_solve_bin(dn, st, rbf_rows, ops, False))
-    none_rows = np.nonzero(method == METHOD_NONE)[0]
-    if len(none_rows):
-        bins.append(Bin(none_rows, 0, L.empty((0, len(none_rows)), t.int32),
-                        L.empty((len(ops), 0, len(none_rows)), t.float64)))
-    return DeviceTable(n, dim, list(ops), bins, n_rbf, method)
+        d_rows = rows_d[k_mon:k_mon + k_rbf]
+        pending.append(_solve_bin(dn, dn.knn(n_rbf, rows=d_rows), d_rows, ops, False))
+    _check_info(pending)
+    bins = [b for b, _ in pending]
+    if k_none:
+        d_rows = rows_d[k_mon + k_rbf:n]
+        bins.append(Bin(None, 0, L.empty((0, k_none), t.int32), L.empty((len(ops), 0, k_none), t.float64),
+                        d_rows=d_rows, K=k_none))
+    return DeviceTable(n, dim, list(ops), bins, n_rbf, method_d[:n])
 
 
 def compute_weights(nodeset, ops, with_kappa: bool = False, tree=None, rbf_n: int | None = None) -> WeightTable:
@@ -394,7 +418,7 @@ def compute_weights(nodeset, ops, with_kappa: bool = False, tree=None, rbf_n: in
     for op in ops:
         _op_code(op, nodeset.dim)
     dev = _interior_device_table(nodeset, ops, rbf_n)
-    table = WeightTable(method=dev.method, _device=dev)
+    table = WeightTable(_device=dev)
     if with_kappa:
         kappa = np.full(len(nodeset), np.nan)
         for b in dev.bins:
@@ -470,7 +494,10 @@ def _boundary_table(nodeset, rows, exclude, ops, normals: bool, override=None) -
             if len(o_rows):
                 st[L.to_device(pos.astype(np.int64))] = L.to_device(o_st.astype(np.int32))
         rn = np.asarray(nodeset.normals, float)[rows_sorted] if normals else None
-        bins.append(_solve_bin(dn, st, rows_sorted, ops, False, row_normals=rn))
+        b, info = _solve_bin(dn, st, L.to_device(rows_sorted.astype(np.int32)), ops, False, row_normals=rn)
+        b._rows_host = rows_sorted
+        _check_info([(b, info)])
+        bins.append(b)
     rest = np.setdiff1d(np.arange(n), rows)
     if len(rest):
         t = L.torch()

@@ -368,9 +368,81 @@ __global__ void mon_stencil_kernel(const int* __restrict__ rows, int64_t nrows, 
   for (int o = 0; o < M; ++o) out[t * (M + 1) + 1 + o] = nb[o];
 }
 
+// ---- stable partition of node ids by method: [MON | RBF-FD | NONE], ascending in each ----
+constexpr int kPartThreads = 256;
+
+__device__ __forceinline__ int method_class(int8_t m) { return m == 0 ? 0 : (m == 1 ? 1 : 2); }
+
+__global__ void partition_count_kernel(const int8_t* __restrict__ method, int64_t n, int* __restrict__ tile_counts,
+                                       int64_t ntiles) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kPartThreads + threadIdx.x;
+  const int c = i < n ? method_class(method[i]) : 3;
+  __shared__ int cnt[3];
+  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const unsigned b = __ballot_sync(0xffffffffu, c == k);
+    if (lane == 0 && b) atomicAdd(&cnt[k], __popc(b));
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) tile_counts[threadIdx.x * ntiles + blockIdx.x] = cnt[threadIdx.x];
+}
+
+// after the scan: tile_off[k*ntiles + t] = exclusive offset of tile t within class k,
+// tile_off[3*ntiles] = total of class 0..2 laid out contiguously (scan over the flattened array)
+__global__ void partition_scatter_kernel(const int8_t* __restrict__ method, int64_t n,
+                                         const int* __restrict__ tile_off, int64_t ntiles, int* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kPartThreads + threadIdx.x;
+  const int c = i < n ? method_class(method[i]) : 3;
+  __shared__ int warp_cnt[3][kPartThreads / 32];
+  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int rank_in_warp = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const unsigned b = __ballot_sync(0xffffffffu, c == k);
+    if (lane == 0) warp_cnt[k][wid] = __popc(b);
+    if (c == k) rank_in_warp = __popc(b & ((1u << lane) - 1u));
+  }
+  __syncthreads();
+  if (c < 3) {
+    int before = 0;
+    for (int w = 0; w < static_cast<int>(wid); ++w) before += warp_cnt[c][w];
+    out[tile_off[c * ntiles + blockIdx.x] + before + rank_in_warp] = static_cast<int>(i);
+  }
+}
+
+// class sizes: counts[k] = start of class k+1 - start of class k
+__global__ void partition_counts_kernel(const int* __restrict__ tile_off, int64_t ntiles, int* __restrict__ counts) {
+  if (threadIdx.x < 3) counts[threadIdx.x] = tile_off[(threadIdx.x + 1) * ntiles] - tile_off[threadIdx.x * ntiles];
+}
+
 }  // namespace hn
 
 using namespace hn;
+
+// rows_out (n): node ids ordered [MON ascending | RBF ascending | NONE ascending];
+// counts_out (3 int32, device) = class sizes.  scratch: 3*ceil(n/256)+1 ints.
+HN_EXPORT int hn_partition_methods(const int8_t* method, int64_t n, int* rows_out, int* counts_out, int* scratch,
+                                   void* stream) {
+  if (n == 0) return cudaMemsetAsync(counts_out, 0, 3 * sizeof(int), as_stream(stream)) == cudaSuccess ? 0 : -1;
+  cudaStream_t s = as_stream(stream);
+  const int64_t ntiles = ceil_div(n, kPartThreads);
+  int* tile_counts = scratch;                       // 3*ntiles
+  int* tile_off = nullptr;
+  HN_TRY(cudaMallocAsync(&tile_off, sizeof(int) * (3 * ntiles + 1), s));
+  partition_count_kernel<<<ntiles, kPartThreads, 0, s>>>(method, n, tile_counts, ntiles);
+  int rc = exclusive_scan(tile_counts, 3 * ntiles, tile_off, s);
+  if (rc == 0) {
+    partition_scatter_kernel<<<ntiles, kPartThreads, 0, s>>>(method, n, tile_off, ntiles, rows_out);
+    partition_counts_kernel<<<1, 32, 0, s>>>(tile_off, ntiles, counts_out);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(tile_off, s);
+  if (rc) return rc;
+  return e == cudaSuccess ? 0 : -static_cast<int>(e);
+}
 
 static Grid make_grid(const double* lo_host, double cell, const int* dims_host, int d) {
   Grid g{};

@@ -73,6 +73,60 @@ __global__ void __launch_bounds__(256) sptrsv_kernel(const int64_t* __restrict__
   }
 }
 
+// Scheduled variant: tasks in dependency-level order; a row longer than the chunk size is
+// split into partial-sum tasks (np = -1, written to partial[part]) followed by a final
+// task (np = number of partials) that adds them in fixed order -> deterministic.
+// Waiting uses exponential __nanosleep backoff so idle warps do not saturate L2.
+__device__ __forceinline__ double wait_value(const double* p) {
+  double v = ld_acquire_dbl(p);
+  unsigned ns = 32;
+  while (is_sentinel(v)) {
+    __nanosleep(ns);
+    ns = ns < 1024 ? 2 * ns : 1024;
+    v = ld_acquire_dbl(p);
+  }
+  return v;
+}
+
+template <bool DIV>
+__global__ void __launch_bounds__(256) sptrsv_tasks_kernel(
+    const int* __restrict__ task_row, const int64_t* __restrict__ task_beg, const int* __restrict__ task_len,
+    const int* __restrict__ task_part, const int* __restrict__ task_np, int64_t ntasks, const int* __restrict__ cols,
+    const double* __restrict__ vals, const double* __restrict__ diag, const double* __restrict__ b, double* x,
+    double* partial, unsigned long long* ticket) {
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1ull);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= static_cast<unsigned long long>(ntasks)) return;
+    const int row = __ldg(task_row + t);
+    const int64_t e0 = __ldg(task_beg + t);
+    const int len = __ldg(task_len + t);
+    double sum = 0.0;
+    for (int e = lane; e < len; e += 32) {
+      const int c = __ldg(cols + e0 + e);
+      const double v = __ldg(vals + e0 + e);
+      sum = fma(v, wait_value(x + c), sum);
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) {
+      const int np = __ldg(task_np + t);
+      const int part = __ldg(task_part + t);
+      if (np < 0) {
+        st_release_dbl(partial + part, sum);
+      } else {
+        double tot = 0.0;
+        for (int k = 0; k < np; ++k) tot += wait_value(partial + part + k);
+        tot += sum;
+        double r = __ldg(b + row) - tot;
+        if (DIV) r = r / __ldg(diag + row);
+        st_release_dbl(x + row, r);
+      }
+    }
+  }
+}
+
 __global__ void permute_in_kernel(const int* __restrict__ perm_r, const double* __restrict__ b, int64_t n,
                                   double* __restrict__ y) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -171,6 +225,46 @@ HN_EXPORT int hn_sptrsv(int lower, const int64_t* rowptr, const int* cols, const
   if (lower) sptrsv_kernel<true><<<blocks, 256, 0, s>>>(rowptr, cols, vals, diag, b, x, n, ticket);
   else sptrsv_kernel<false><<<blocks, 256, 0, s>>>(rowptr, cols, vals, diag, b, x, n, ticket);
   HN_CHECK_LAUNCH();
+  return 0;
+}
+
+// Scheduled sync-free solve (see sptrsv_tasks_kernel).  divide != 0: x_row /= diag[row].
+// x (n) and partial (npartial) are reset to the sentinel here; warps_per_sm resident warps.
+HN_EXPORT int hn_sptrsv_tasks(int divide, const int* task_row, const int64_t* task_beg, const int* task_len,
+                              const int* task_part, const int* task_np, int64_t ntasks, const int* cols,
+                              const double* vals, const double* diag, const double* b, double* x, int64_t n,
+                              double* partial, int64_t npartial, unsigned long long* ticket, int warps_per_sm,
+                              void* stream) {
+  if (ntasks == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  HN_TRY(cudaMemsetAsync(x, 0xFF, sizeof(double) * n, s));
+  if (npartial > 0) HN_TRY(cudaMemsetAsync(partial, 0xFF, sizeof(double) * npartial, s));
+  HN_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s));
+  const int wps = warps_per_sm > 0 ? warps_per_sm : 16;
+  const int blocks = sm_count() * ((wps + 7) / 8);
+  if (divide)
+    sptrsv_tasks_kernel<true><<<blocks, 256, 0, s>>>(task_row, task_beg, task_len, task_part, task_np, ntasks, cols,
+                                                     vals, diag, b, x, partial, ticket);
+  else
+    sptrsv_tasks_kernel<false><<<blocks, 256, 0, s>>>(task_row, task_beg, task_len, task_part, task_np, ntasks, cols,
+                                                      vals, diag, b, x, partial, ticket);
+  HN_CHECK_LAUNCH();
+  return 0;
+}
+
+// Host helper (setup): dependency level of every row of a triangular CSR, sweeping rows in
+// increasing (lower != 0) or decreasing order.  Host pointers.
+HN_EXPORT int hn_host_levels(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower,
+                             int* levels_host) {
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t i = lower ? k : n - 1 - k;
+    int lev = 0;
+    for (int64_t e = rowptr_host[i]; e < rowptr_host[i + 1]; ++e) {
+      const int l = levels_host[cols_host[e]] + 1;
+      lev = l > lev ? l : lev;
+    }
+    levels_host[i] = lev;
+  }
   return 0;
 }
 

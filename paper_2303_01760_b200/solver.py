@@ -93,8 +93,50 @@ class PoissonSolveSettings:
             raise ValueError("stabilization must lie in [0, 1]")
 
 
+class _TriSchedule:
+    """Task list of a sync-free triangular solve: rows in dependency-level order, rows
+    longer than CHUNK split into partial-sum tasks + one final task (hn_sptrsv_tasks)."""
+
+    CHUNK = 256
+
+    def __init__(self, m: sparse.csr_matrix, lower: bool):
+        plan = plan_triangular_tasks(m, lower, self.CHUNK)
+        self.depth, self.ntasks, self.npartial = plan["depth"], plan["ntasks"], plan["npartial"]
+        self.row, self.beg, self.len = (L.to_device(plan["row"]), L.to_device(plan["beg"]), L.to_device(plan["len"]))
+        self.part, self.np_ = L.to_device(plan["part"]), L.to_device(plan["np"])
+        self.partial = L.empty(max(self.npartial, 1), L.torch().float64)
+
+
+def plan_triangular_tasks(m: sparse.csr_matrix, lower: bool, chunk: int) -> dict:
+    """Host planning of hn_sptrsv_tasks (setup; levels from the native hn_host_levels)."""
+    n = m.shape[0]
+    rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
+    cols = np.ascontiguousarray(m.indices, dtype=np.int32)
+    lev = np.zeros(n, dtype=np.int32)
+    L.call("hn_host_levels", rowptr.ctypes.data_as(L._vp), cols.ctypes.data_as(L._vp), n, 1 if lower else 0,
+           lev.ctypes.data_as(L._vp))
+    order = np.lexsort((np.arange(n), lev))
+    length = np.diff(rowptr)[order]
+    nchunk = np.maximum(1, -(-length // chunk))
+    ntasks = int(nchunk.sum())
+    first = np.concatenate([[0], np.cumsum(nchunk)[:-1]])
+    k = np.arange(ntasks) - np.repeat(first, nchunk)                 # chunk index within its row
+    is_final = k == np.repeat(nchunk, nchunk) - 1
+    part_slot = np.cumsum(~is_final) - 1                              # non-final chunks: own slot
+    row_first = np.repeat(np.concatenate([[0], np.cumsum(nchunk - 1)[:-1]]), nchunk)
+    return {"depth": int(lev.max()) + 1 if n else 0, "levels": lev, "ntasks": ntasks,
+            "npartial": int((~is_final).sum()),
+            "row": np.repeat(order, nchunk).astype(np.int32),
+            "beg": (np.repeat(rowptr[order], nchunk) + k * chunk).astype(np.int64),
+            "len": np.minimum(chunk, np.repeat(length, nchunk) - k * chunk).astype(np.int32),
+            "part": np.where(is_final, row_first, part_slot).astype(np.int32),
+            "np": np.where(is_final, np.repeat(nchunk - 1, nchunk), -1).astype(np.int32)}
+
+
 class _DeviceLU:
     """SuperLU factors Pr A Pc = L U in HBM: strict-lower L, strict-upper U + diag, perms."""
+
+    WARPS_PER_SM = 16
 
     def __init__(self, lu):
         Lm = sparse.csr_matrix(lu.L)
@@ -106,6 +148,8 @@ class _DeviceLU:
         Us.sort_indices()
         self.L = DeviceCSR(Ls)
         self.U = DeviceCSR(Us)
+        self.sL = _TriSchedule(Ls, lower=True)
+        self.sU = _TriSchedule(Us, lower=False)
         self.diag = L.to_device(np.asarray(Um.diagonal(), dtype=np.float64))
         self.perm_r = L.to_device(np.asarray(lu.perm_r, dtype=np.int32))
         self.perm_c = L.to_device(np.asarray(lu.perm_c, dtype=np.int32))
@@ -120,12 +164,15 @@ class _DeviceLU:
         """x = Pc U^-1 L^-1 Pr b (scipy SuperLU.solve semantics)."""
         s = L.stream_handle()
         L.call("hn_permute", 0, L.ptr(self.perm_r), L.ptr(b), self.n, L.ptr(self.y), s)
-        L.call("hn_sptrsv", 1, L.ptr(self.L.rowptr), L.ptr(self.L.cols), L.ptr(self.L.vals), None, L.ptr(self.y),
-               L.ptr(self.z), self.n, L.ptr(self.ticket), s)
-        L.call("hn_sptrsv", 0, L.ptr(self.U.rowptr), L.ptr(self.U.cols), L.ptr(self.U.vals), L.ptr(self.diag),
-               L.ptr(self.z), L.ptr(self.w), self.n, L.ptr(self.ticket), s)
+        self._tri(self.sL, self.L, None, self.y, self.z, s)
+        self._tri(self.sU, self.U, self.diag, self.z, self.w, s)
         L.call("hn_permute", 1, L.ptr(self.perm_c), L.ptr(self.w), self.n, L.ptr(x), s)
         return x
+
+    def _tri(self, sch, m, diag, b, x, s):
+        L.call("hn_sptrsv_tasks", 0 if diag is None else 1, L.ptr(sch.row), L.ptr(sch.beg), L.ptr(sch.len),
+               L.ptr(sch.part), L.ptr(sch.np_), sch.ntasks, L.ptr(m.cols), L.ptr(m.vals), L.ptr(diag), L.ptr(b),
+               L.ptr(x), self.n, L.ptr(sch.partial), sch.npartial, L.ptr(self.ticket), self.WARPS_PER_SM, s)
 
 
 class OperatorSet:

@@ -1,0 +1,99 @@
+"""Host-side logic that needs no GPU: triangular-solve task planning (emulated task by
+task in ticket order, the order the kernel's atomic ticket hands them out), node-set
+generators, operator-code mapping."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+from scipy.sparse.linalg import spsolve_triangular
+
+from paper_2303_01760_b200 import nodesets
+from paper_2303_01760_b200.approx import _op_code, Laplacian, NormalDerivative, Partial
+from paper_2303_01760_b200.solver import plan_triangular_tasks
+
+
+def emulate(plan, m, b, diag=None):
+    """Execute the task list sequentially in ticket order (a valid schedule)."""
+    x = np.full(m.shape[0], np.nan)
+    partial = np.full(max(plan["npartial"], 1), np.nan)
+    for t in range(plan["ntasks"]):
+        r, e0, ln = plan["row"][t], plan["beg"][t], plan["len"][t]
+        cols = m.indices[e0:e0 + ln]
+        assert not np.any(np.isnan(x[cols])), "task ran before a dependency"
+        s = float(np.dot(m.data[e0:e0 + ln], x[cols]))
+        if plan["np"][t] < 0:
+            partial[plan["part"][t]] = s
+        else:
+            p0, k = plan["part"][t], plan["np"][t]
+            assert not np.any(np.isnan(partial[p0:p0 + k]))
+            tot = float(np.sum(partial[p0:p0 + k])) + s
+            x[r] = (b[r] - tot) / (diag[r] if diag is not None else 1.0)
+    return x
+
+
+@pytest.mark.parametrize("lower", [True, False])
+@pytest.mark.parametrize("chunk", [4, 256])
+def test_task_plan_solves_triangular_systems(lower, chunk):
+    rng = np.random.default_rng(0)
+    n = 400
+    a = sp.random(n, n, density=0.05, random_state=1, format="csr")
+    a = a + sp.csr_matrix((np.ones(n), (np.full(n, n - 1 if lower else 0), np.arange(n))), shape=(n, n))
+    tri = sp.tril(a, k=-1, format="csr") if lower else sp.triu(a, k=1, format="csr")
+    tri.sort_indices()
+    b = rng.normal(size=n)
+    diag = rng.uniform(1, 2, size=n)
+    plan = plan_triangular_tasks(tri, lower, chunk)
+    x = emulate(plan, tri, b, None if lower else diag)
+    full = (tri + sp.eye(n)) if lower else (tri + sp.diags(diag))
+    want = spsolve_triangular(full.tocsr(), b, lower=lower)
+    np.testing.assert_allclose(x, want, rtol=1e-10, atol=1e-12)
+    assert plan["ntasks"] >= n
+    if chunk == 4:
+        assert plan["npartial"] > 0
+
+
+def test_generators_match_baseline_sizes():
+    assert len(nodesets.regular_box(199)) == 40_000
+    ns = nodesets.jittered_box(315, seed=1)
+    assert len(ns) == 99_856 and ns.counts == (0, 98_596, 1_260)
+    ns = nodesets.hybrid_hole_2d(500, seed=2)
+    assert 240_000 < len(ns) < 255_000 and 0.2 < ns.counts[1] / len(ns) < 0.26
+
+
+def test_generator_lattice_map_is_consistent():
+    ns = nodesets.hybrid_hole_2d(40, seed=3)
+    grid = ns.lattice.grid
+    ids = grid[grid >= 0]
+    keys = ns.lattice_idx[ids]
+    np.testing.assert_array_equal(grid[keys[:, 0], keys[:, 1]], ids)
+    np.testing.assert_allclose(ns.positions[ids], keys * ns.lattice.step, atol=1e-15)
+
+
+def test_config0_generator_matches_reference_generator():
+    """regular_box(199) is the reference's dvd pure-regular set (counts, roles, lattice)."""
+    import sys
+    from pathlib import Path
+    ref = Path("/root/reference/pkg/src")
+    if not ref.exists():
+        pytest.skip("reference not mounted (GPU box)")
+    sys.path.insert(0, str(ref))
+    from hybridnodes.config import CaseConfig
+    from hybridnodes.nodegen import hybrid_discretize
+    r = hybrid_discretize(CaseConfig(case="dvd", discretization="pure-regular", h_r=1 / 49))
+    ours = nodesets.regular_box(49)
+    assert r.counts == ours.counts
+    np.testing.assert_allclose(np.sort(r.positions, axis=0), np.sort(ours.positions, axis=0), atol=1e-14)
+    assert sorted(r.origin) == sorted(ours.origin)
+    assert (r.role == 1).sum() == (ours.role == 1).sum()
+
+
+def test_operator_codes_accept_foreign_operator_classes():
+    class Laplacian_:  # a class from another package with the same name
+        pass
+    Laplacian_.__name__ = "Laplacian"
+    assert _op_code(Laplacian(), 2)[0] == 0
+    assert _op_code(Laplacian_(), 2)[0] == 0
+    assert _op_code(Partial(1), 3) == (1, 1, (0.0, 0.0, 0.0))
+    assert _op_code(NormalDerivative((0.6, 0.8)), 2) == (2, 0, (0.6, 0.8))
+    with pytest.raises(TypeError):
+        _op_code(object(), 2)
