@@ -82,11 +82,14 @@ __device__ __forceinline__ double wait_value(const double* p) {
   unsigned ns = 32;
   while (is_sentinel(v)) {
     __nanosleep(ns);
-    ns = ns < 1024 ? 2 * ns : 1024;
+    ns = ns < 256 ? 2 * ns : 256;
     v = ld_acquire_dbl(p);
   }
   return v;
 }
+
+constexpr int kTaskChunk = 256;           // nnz per task (host planner uses the same)
+constexpr int kPerLane = kTaskChunk / 32;
 
 template <bool DIV>
 __global__ void __launch_bounds__(256) sptrsv_tasks_kernel(
@@ -103,11 +106,23 @@ __global__ void __launch_bounds__(256) sptrsv_tasks_kernel(
     const int row = __ldg(task_row + t);
     const int64_t e0 = __ldg(task_beg + t);
     const int len = __ldg(task_len + t);
+    // all of the lane's operands are requested before anything waits: one L2 round trip
+    // per task instead of one per element; then spin only on values not yet produced
+    int c[kPerLane];
+    double v[kPerLane], xv[kPerLane];
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      const int e = lane + 32 * k;
+      c[k] = e < len ? __ldg(cols + e0 + e) : -1;
+      v[k] = e < len ? __ldg(vals + e0 + e) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) xv[k] = c[k] >= 0 ? ld_acquire_dbl(x + c[k]) : 0.0;
     double sum = 0.0;
-    for (int e = lane; e < len; e += 32) {
-      const int c = __ldg(cols + e0 + e);
-      const double v = __ldg(vals + e0 + e);
-      sum = fma(v, wait_value(x + c), sum);
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      if (c[k] >= 0 && is_sentinel(xv[k])) xv[k] = wait_value(x + c[k]);
+      sum = fma(v[k], xv[k], sum);
     }
     sum = warp_sum(sum);
     if (lane == 0) {

@@ -318,7 +318,7 @@ struct __align__(16) RbfSmem {  // 16 B: every system's prow takes v2.f64 stores
   static constexpr int NS = NST + NQ;
   static constexpr int NC = NS + NOPS;
   static constexpr int NCP = (NC + 1) & ~1;  // even length keeps every pair 16 B aligned
-  double prow[2][NCP];                          // double-buffered pivot row
+  double prow[2][NCP + 2];                      // double-buffered pivot row; [NCP] = 1/pivot
   double y[NST][D];
   double w[NST][NOPS];
   int sid[NST];
@@ -485,20 +485,33 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
   for (int kk = 0; kk < NS; ++kk) {
     const int buf = kk & 1;
     const unsigned pbase = buf ? pbase1 : pbase0;
-    // pivot search: |a| high word, 6 low bits replaced by the row tag
+    // pivot search: |a| high word, 6 low bits replaced by the row tag.  The lane's local
+    // candidate value is kept so its reciprocal is computed while the reduction runs
+    // (if this lane owns the pivot, its local best IS the pivot).
     unsigned key = 0;
+    double cand = 1.0;
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       const unsigned hi = (static_cast<unsigned>(__double2hiint(a[r][kk])) & 0x7fffffc0u) | tag[r];
-      key = max(key, done[r] ? 0u : hi);
+      const unsigned kr = done[r] ? 0u : hi;
+      cand = kr > key ? a[r][kk] : cand;
+      key = max(key, kr);
     }
+    const double inv_local = fast_rcp(cand);
+    // segmented max (butterfly in segment-relative lane numbers; measured faster than one
+    // REDUX per segment), then broadcast from segment lane 0
 #pragma unroll
     for (int off = 1; off < LPS; off <<= 1) key = max(key, __shfl_sync(0xffffffffu, key, seg_src(off)));
     key = __shfl_sync(0xffffffffu, key, lane_live ? seg_base : lane);
     const unsigned ptag = key & 63u;
     bool isp[RPL];
+    bool own_any = false;
 #pragma unroll
-    for (int r = 0; r < RPL; ++r) isp[r] = (ptag == tag[r]) && lane_live;
+    for (int r = 0; r < RPL; ++r) {
+      isp[r] = (ptag == tag[r]) && lane_live;
+      own_any = own_any || isp[r];
+    }
+    st_pred1(own_any, pbase + 8u * Sm::NCP, inv_local);
     // owner stages the pivot row, columns kk..NC-1
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
@@ -519,7 +532,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
     const double* prow = sm.prow[buf];
     const double piv = prow[kk];
     if (piv == 0.0 && sing == 0) sing = kk + 1;
-    const double inv = fast_rcp(piv);
+    const double inv = prow[Sm::NCP];
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       pcol[r] = isp[r] ? kk : pcol[r];
@@ -715,11 +728,11 @@ static void launch_rbf(const double* pos, const int* st, int64_t K, const OpSpec
                        double* ow, int* info, cudaStream_t s) {
   if constexpr (D == 2 && NST == 12) {
     switch (g_rbf_variant) {
-      case 1: launch_rbf_v<2, 12, NOPS, 6, 3, 4, 3>(pos, st, K, ops, rn, oi, ow, info, s); return;
+      case 1: launch_rbf_v<2, 12, NOPS, 6, 3, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return;
       case 2: launch_rbf_v<2, 12, NOPS, 9, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return;
       case 3: launch_rbf_v<2, 12, NOPS, 9, 2, 4, 4>(pos, st, K, ops, rn, oi, ow, info, s); return;
       case 4: launch_rbf_v<2, 12, NOPS, 6, 3, 2, 5>(pos, st, K, ops, rn, oi, ow, info, s); return;
-      default: break;
+      default: launch_rbf_v<2, 12, NOPS, 6, 3, 4, 3>(pos, st, K, ops, rn, oi, ow, info, s); return;
     }
   }
   launch_rbf_v<D, NST, NOPS, LPS, RPL, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s);
