@@ -170,6 +170,21 @@ int hn_sptrsv_tasks(int divide, const int* task_row, const int64_t* task_beg, co
                     double* partial, int64_t npartial, unsigned long long* ticket, int warps_per_sm,
                     void* stream);
 
+/* Supernodal sync-free triangular solve: blocks [r0, r0+w) (dense in-block triangle, w <=
+ * 4096) given in dependency-level order; one CTA per block pulls the outside part (one
+ * global hop) and solves the dense triangle in 32-column tiles.  lower: unit diagonal;
+ * upper: divides by diag.  Strict CSR with sorted columns.  Deterministic. */
+int hn_sptrsv_super(int lower, const int* blk_r0, const int* blk_w, int64_t nblk, const int64_t* rowptr,
+                    const int* cols, const double* vals, const double* diag, const double* b, double* x,
+                    int64_t n, unsigned long long* ticket, int ctas_per_sm, void* stream);
+
+/* Setup helpers on HOST arrays: dense-triangle row blocks (returns the count; blocks in row
+ * order) and their dependency levels. */
+int64_t hn_host_supernodes(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower, int cap,
+                           int* blk_r0_host, int* blk_w_host);
+int hn_host_block_levels(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower, int64_t nblk,
+                         const int* blk_r0_host, const int* blk_w_host, int* levels_host);
+
 /* Setup helper on HOST arrays: dependency level of each row of a triangular CSR
  * (rows swept increasing when lower != 0, decreasing otherwise). */
 int hn_host_levels(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower, int* levels_host);

@@ -142,6 +142,135 @@ __global__ void __launch_bounds__(256) sptrsv_tasks_kernel(
   }
 }
 
+// ---- supernodal variant -------------------------------------------------------------
+// Rows are grouped into blocks [r0, r0+w) whose in-block triangle is dense (SuperLU
+// supernodes).  One CTA per block: (1) every row's outside part is pulled (warp per row,
+// load-first + spin, one global hop per block), (2) the dense in-block triangle is solved
+// in 32-column tiles: one warp solves the diagonal tile with shuffles, then all warps
+// apply the tile to the remaining rows.  Row layout in the strict CSR (sorted columns):
+//   lower: [outside cols < r0 | inside cols r0..i-1]   (inside count = i - r0)
+//   upper: [inside cols i+1..r1-1 | outside cols >= r1] (inside count = r1-1-i)
+constexpr int kSnThreads = 256;
+constexpr int kSnWarps = kSnThreads / 32;
+constexpr int kSnMaxW = 4096;
+
+__device__ __forceinline__ double row_outside_sum(const int* __restrict__ cols, const double* __restrict__ vals,
+                                                  int64_t e0, int len, const double* x, int lane) {
+  double sum = 0.0;
+  for (int base = 0; base < len; base += kTaskChunk) {
+    int c[kPerLane];
+    double v[kPerLane], xv[kPerLane];
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      const int e = base + lane + 32 * k;
+      c[k] = e < len ? __ldg(cols + e0 + e) : -1;
+      v[k] = e < len ? __ldg(vals + e0 + e) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) xv[k] = c[k] >= 0 ? ld_acquire_dbl(x + c[k]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      if (c[k] >= 0 && is_sentinel(xv[k])) xv[k] = wait_value(x + c[k]);
+      sum = fma(v[k], xv[k], sum);
+    }
+  }
+  return warp_sum(sum);
+}
+
+template <bool LOWER>
+__global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
+    const int* __restrict__ blk_r0, const int* __restrict__ blk_w, int64_t nblk, const int64_t* __restrict__ rowptr,
+    const int* __restrict__ cols, const double* __restrict__ vals, const double* __restrict__ diag,
+    const double* __restrict__ b, double* x, unsigned long long* ticket) {
+  __shared__ double ys[kSnMaxW];
+  __shared__ unsigned long long tk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  while (true) {
+    if (tid == 0) tk = atomicAdd(ticket, 1ull);
+    __syncthreads();
+    const unsigned long long t = tk;
+    __syncthreads();
+    if (t >= static_cast<unsigned long long>(nblk)) return;
+    const int r0 = __ldg(blk_r0 + t), w = __ldg(blk_w + t);
+    // (1) outside contributions, warp per row
+    for (int rr = warp; rr < w; rr += kSnWarps) {
+      const int i = r0 + rr;
+      const int64_t a = __ldg(rowptr + i), z = __ldg(rowptr + i + 1);
+      const int inside = LOWER ? rr : (w - 1 - rr);
+      const int64_t e0 = LOWER ? a : a + inside;
+      const int len = static_cast<int>(z - a) - inside;
+      const double s = row_outside_sum(cols, vals, e0, len, x, lane);
+      if (lane == 0) ys[rr] = __ldg(b + i) - s;
+    }
+    __syncthreads();
+    // (2) dense in-block triangle, 32-column tiles
+    const int ntiles = (w + 31) / 32;
+    for (int tt = 0; tt < ntiles; ++tt) {
+      const int t0 = LOWER ? 32 * tt : 32 * (ntiles - 1 - tt);  // first block row of the tile
+      const int tw = min(32, w - t0);
+      if (warp == (tt % kSnWarps)) {
+        const int rr = t0 + lane;
+        double yv = lane < tw ? ys[rr] : 0.0;
+        const int i = r0 + rr;
+        // this lane's row entries inside the diagonal tile
+        double lv[32];
+        if (lane < tw) {
+          const int64_t a = __ldg(rowptr + i), z = __ldg(rowptr + i + 1);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            double val = 0.0;
+            if (LOWER) {
+              if (k < lane) val = __ldg(vals + (z - rr) + t0 + k);           // col r0 + t0 + k
+            } else {
+              if (k > lane && k < tw) val = __ldg(vals + a + (t0 + k - rr - 1));  // col r0 + t0 + k
+            }
+            lv[k] = val;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) lv[k] = 0.0;
+        }
+        const double dg = (!LOWER && lane < tw) ? __ldg(diag + i) : 1.0;
+        if (LOWER) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const double xk = __shfl_sync(0xffffffffu, yv, k);
+            if (lane > k) yv = fma(-lv[k], xk, yv);
+          }
+        } else {
+#pragma unroll
+          for (int k = 31; k >= 0; --k) {
+            if (lane == k && lane < tw) yv = yv / dg;
+            const double xk = __shfl_sync(0xffffffffu, yv, k);
+            if (lane < k) yv = fma(-lv[k], xk, yv);
+          }
+        }
+        if (lane < tw) {
+          ys[rr] = yv;
+          st_release_dbl(x + i, yv);
+        }
+      }
+      __syncthreads();
+      // apply the solved tile to the rows not yet solved
+      const int lo = LOWER ? t0 + tw : 0;
+      const int hi = LOWER ? w : t0;
+      for (int rr = lo + tid; rr < hi; rr += kSnThreads) {
+        const int i = r0 + rr;
+        double acc = 0.0;
+        if (LOWER) {
+          const double* rowv = vals + (__ldg(rowptr + i + 1) - rr) + t0;  // cols r0+t0 ..
+          for (int k = 0; k < tw; ++k) acc = fma(__ldg(rowv + k), ys[t0 + k], acc);
+        } else {
+          const double* rowv = vals + __ldg(rowptr + i) + (t0 - rr - 1);     // col r0+t0+k at +k
+          for (int k = 0; k < tw; ++k) acc = fma(__ldg(rowv + k), ys[t0 + k], acc);
+        }
+        ys[rr] -= acc;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void permute_in_kernel(const int* __restrict__ perm_r, const double* __restrict__ b, int64_t n,
                                   double* __restrict__ y) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -264,6 +393,90 @@ HN_EXPORT int hn_sptrsv_tasks(int divide, const int* task_row, const int64_t* ta
     sptrsv_tasks_kernel<false><<<blocks, 256, 0, s>>>(task_row, task_beg, task_len, task_part, task_np, ntasks, cols,
                                                       vals, diag, b, x, partial, ticket);
   HN_CHECK_LAUNCH();
+  return 0;
+}
+
+// Supernodal solve over planned blocks (processing order), see sptrsv_super_kernel.
+HN_EXPORT int hn_sptrsv_super(int lower, const int* blk_r0, const int* blk_w, int64_t nblk, const int64_t* rowptr,
+                              const int* cols, const double* vals, const double* diag, const double* b, double* x,
+                              int64_t n, unsigned long long* ticket, int ctas_per_sm, void* stream) {
+  if (nblk == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  HN_TRY(cudaMemsetAsync(x, 0xFF, sizeof(double) * n, s));
+  HN_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s));
+  const int blocks = sm_count() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
+  if (lower) sptrsv_super_kernel<true><<<blocks, kSnThreads, 0, s>>>(blk_r0, blk_w, nblk, rowptr, cols, vals, diag, b, x, ticket);
+  else sptrsv_super_kernel<false><<<blocks, kSnThreads, 0, s>>>(blk_r0, blk_w, nblk, rowptr, cols, vals, diag, b, x, ticket);
+  HN_CHECK_LAUNCH();
+  return 0;
+}
+
+// Host helper (setup): split the rows of a strict triangular CSR (sorted columns) into
+// blocks whose in-block triangle is dense, at most `cap` rows (<= 4096).  Writes blocks in
+// row order (r0 ascending) and returns their number.
+HN_EXPORT int64_t hn_host_supernodes(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower,
+                                     int cap, int* blk_r0_host, int* blk_w_host) {
+  if (cap <= 0 || cap > kSnMaxW) cap = kSnMaxW;
+  int64_t nb = 0;
+  if (lower) {
+    int64_t r0 = 0;
+    for (int64_t i = 1; i <= n; ++i) {
+      bool join = false;
+      if (i < n && i - r0 < cap) {
+        const int64_t cnt = i - r0, a = rowptr_host[i], z = rowptr_host[i + 1];
+        join = (z - a >= cnt) && cols_host[z - cnt] == r0 && cols_host[z - 1] == i - 1;
+      }
+      if (!join) {
+        blk_r0_host[nb] = static_cast<int>(r0);
+        blk_w_host[nb] = static_cast<int>(i - r0);
+        ++nb;
+        r0 = i;
+      }
+    }
+  } else {
+    int64_t r1 = n;  // current block [i+1, r1)
+    for (int64_t i = n - 2; i >= -1; --i) {
+      bool join = false;
+      if (i >= 0 && r1 - 1 - i < cap) {
+        const int64_t cnt = r1 - 1 - i, a = rowptr_host[i], z = rowptr_host[i + 1];
+        join = (z - a >= cnt) && cols_host[a] == i + 1 && cols_host[a + cnt - 1] == r1 - 1;
+      }
+      if (!join) {
+        blk_r0_host[nb] = static_cast<int>(i + 1);
+        blk_w_host[nb] = static_cast<int>(r1 - (i + 1));
+        ++nb;
+        r1 = i + 1;
+      }
+    }
+    // row order ascending
+    for (int64_t k = 0; k < nb / 2; ++k) {
+      int t0 = blk_r0_host[k]; blk_r0_host[k] = blk_r0_host[nb - 1 - k]; blk_r0_host[nb - 1 - k] = t0;
+      int t1 = blk_w_host[k]; blk_w_host[k] = blk_w_host[nb - 1 - k]; blk_w_host[nb - 1 - k] = t1;
+    }
+  }
+  return nb;
+}
+
+// Host helper (setup): dependency level of each block (blocks in row order).
+HN_EXPORT int hn_host_block_levels(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower,
+                                   int64_t nblk, const int* blk_r0_host, const int* blk_w_host, int* levels_host) {
+  int* owner = new int[n];
+  for (int64_t k = 0; k < nblk; ++k)
+    for (int r = 0; r < blk_w_host[k]; ++r) owner[blk_r0_host[k] + r] = static_cast<int>(k);
+  for (int64_t q = 0; q < nblk; ++q) {
+    const int64_t k = lower ? q : nblk - 1 - q;
+    const int r0 = blk_r0_host[k], r1 = r0 + blk_w_host[k];
+    int lev = 0;
+    for (int i = r0; i < r1; ++i)
+      for (int64_t e = rowptr_host[i]; e < rowptr_host[i + 1]; ++e) {
+        const int c = cols_host[e];
+        if (c >= r0 && c < r1) continue;
+        const int l = levels_host[owner[c]] + 1;
+        lev = l > lev ? l : lev;
+      }
+    levels_host[k] = lev;
+  }
+  delete[] owner;
   return 0;
 }
 

@@ -107,6 +107,32 @@ class _TriSchedule:
         self.partial = L.empty(max(self.npartial, 1), L.torch().float64)
 
 
+def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 4096) -> dict:
+    """Host planning of hn_sptrsv_super: dense-triangle row blocks in dependency-level order."""
+    n = m.shape[0]
+    rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
+    cols = np.ascontiguousarray(m.indices, dtype=np.int32)
+    r0 = np.zeros(max(n, 1), dtype=np.int32)
+    w = np.zeros(max(n, 1), dtype=np.int32)
+    vp = L._vp
+    nb = int(L.lib().hn_host_supernodes(rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), n, 1 if lower else 0,
+                                        cap, r0.ctypes.data_as(vp), w.ctypes.data_as(vp)))
+    r0, w = r0[:nb].copy(), w[:nb].copy()
+    lev = np.zeros(nb, dtype=np.int32)
+    L.call("hn_host_block_levels", rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), n, 1 if lower else 0, nb,
+           r0.ctypes.data_as(vp), w.ctypes.data_as(vp), lev.ctypes.data_as(vp))
+    order = np.lexsort((r0, lev))
+    return {"nblk": nb, "r0": r0[order], "w": w[order], "levels": lev[order],
+            "depth": int(lev.max()) + 1 if nb else 0}
+
+
+class _SuperSchedule:
+    def __init__(self, m: sparse.csr_matrix, lower: bool):
+        plan = plan_supernodal_blocks(m, lower)
+        self.nblk, self.depth = plan["nblk"], plan["depth"]
+        self.r0, self.w = L.to_device(plan["r0"]), L.to_device(plan["w"])
+
+
 def plan_triangular_tasks(m: sparse.csr_matrix, lower: bool, chunk: int) -> dict:
     """Host planning of hn_sptrsv_tasks (setup; levels from the native hn_host_levels)."""
     n = m.shape[0]
@@ -137,6 +163,8 @@ class _DeviceLU:
     """SuperLU factors Pr A Pc = L U in HBM: strict-lower L, strict-upper U + diag, perms."""
 
     WARPS_PER_SM = 16
+    CTAS_PER_SM = 2
+    SUPERNODAL = True
 
     def __init__(self, lu):
         Lm = sparse.csr_matrix(lu.L)
@@ -148,8 +176,13 @@ class _DeviceLU:
         Us.sort_indices()
         self.L = DeviceCSR(Ls)
         self.U = DeviceCSR(Us)
-        self.sL = _TriSchedule(Ls, lower=True)
-        self.sU = _TriSchedule(Us, lower=False)
+        self.supernodal = self.SUPERNODAL
+        if self.supernodal:
+            self.sL = _SuperSchedule(Ls, lower=True)
+            self.sU = _SuperSchedule(Us, lower=False)
+        else:
+            self.sL = _TriSchedule(Ls, lower=True)
+            self.sU = _TriSchedule(Us, lower=False)
         self.diag = L.to_device(np.asarray(Um.diagonal(), dtype=np.float64))
         self.perm_r = L.to_device(np.asarray(lu.perm_r, dtype=np.int32))
         self.perm_c = L.to_device(np.asarray(lu.perm_c, dtype=np.int32))
@@ -170,6 +203,11 @@ class _DeviceLU:
         return x
 
     def _tri(self, sch, m, diag, b, x, s):
+        if self.supernodal:
+            L.call("hn_sptrsv_super", 1 if diag is None else 0, L.ptr(sch.r0), L.ptr(sch.w), sch.nblk,
+                   L.ptr(m.rowptr), L.ptr(m.cols), L.ptr(m.vals), L.ptr(diag), L.ptr(b), L.ptr(x), self.n,
+                   L.ptr(self.ticket), self.CTAS_PER_SM, s)
+            return
         L.call("hn_sptrsv_tasks", 0 if diag is None else 1, L.ptr(sch.row), L.ptr(sch.beg), L.ptr(sch.len),
                L.ptr(sch.part), L.ptr(sch.np_), sch.ntasks, L.ptr(m.cols), L.ptr(m.vals), L.ptr(diag), L.ptr(b),
                L.ptr(x), self.n, L.ptr(sch.partial), sch.npartial, L.ptr(self.ticket), self.WARPS_PER_SM, s)

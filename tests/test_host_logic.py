@@ -97,3 +97,44 @@ def test_operator_codes_accept_foreign_operator_classes():
     assert _op_code(NormalDerivative((0.6, 0.8)), 2) == (2, 0, (0.6, 0.8))
     with pytest.raises(TypeError):
         _op_code(object(), 2)
+
+
+def emulate_blocks(plan, m, b, lower, diag=None):
+    """Execute the supernodal plan sequentially in processing order."""
+    n = m.shape[0]
+    x = np.full(n, np.nan)
+    dense = m.toarray()
+    for r0, w in zip(plan["r0"], plan["w"]):
+        rows = np.arange(r0, r0 + w)
+        y = np.empty(w)
+        for k, i in enumerate(rows):
+            c = m.indices[m.indptr[i]:m.indptr[i + 1]]
+            v = m.data[m.indptr[i]:m.indptr[i + 1]]
+            out = (c < r0) if lower else (c >= r0 + w)
+            assert not np.any(np.isnan(x[c[out]])), "block ran before a dependency"
+            inside = ~out
+            assert np.array_equal(np.sort(c[inside]), np.arange(r0, i) if lower else np.arange(i + 1, r0 + w))
+            y[k] = b[i] - np.dot(v[out], x[c[out]])
+        blk = dense[np.ix_(rows, rows)]
+        full = blk + (np.eye(w) if lower else np.diag(diag[rows]))
+        x[rows] = spsolve_triangular(sp.csr_matrix(full), y, lower=lower)
+    return x
+
+
+@pytest.mark.parametrize("lower", [True, False])
+def test_supernodal_plan_solves_triangular_systems(lower):
+    from paper_2303_01760_b200.solver import plan_supernodal_blocks
+    from scipy.sparse import linalg as spla
+    rng = np.random.default_rng(1)
+    n = 300
+    a = sp.random(n, n, density=0.03, random_state=2, format="csc") + sp.eye(n) * 4
+    lu = spla.splu(a.tocsc())
+    tri = sp.tril(sp.csr_matrix(lu.L), k=-1, format="csr") if lower else sp.triu(sp.csr_matrix(lu.U), k=1, format="csr")
+    tri.sort_indices()
+    diag = sp.csr_matrix(lu.U).diagonal()
+    plan = plan_supernodal_blocks(tri, lower, cap=64)
+    assert plan["nblk"] < n and plan["w"].sum() == n
+    b = rng.normal(size=n)
+    x = emulate_blocks(plan, tri, b, lower, diag)
+    full = (tri + sp.eye(n)) if lower else (tri + sp.diags(diag))
+    np.testing.assert_allclose(x, spsolve_triangular(full.tocsr(), b, lower=lower), rtol=1e-9, atol=1e-11)
