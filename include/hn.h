@@ -170,12 +170,16 @@ int hn_sptrsv_tasks(int divide, const int* task_row, const int64_t* task_beg, co
                     double* partial, int64_t npartial, unsigned long long* ticket, int warps_per_sm,
                     void* stream);
 
-/* Supernodal sync-free triangular solve: blocks [r0, r0+w) (dense in-block triangle, w <=
- * 4096) given in dependency-level order; one CTA per block pulls the outside part (one
- * global hop) and solves the dense triangle in 32-column tiles.  lower: unit diagonal;
- * upper: divides by diag.  Strict CSR with sorted columns.  Deterministic. */
-int hn_sptrsv_super(int lower, const int* blk_r0, const int* blk_w, int64_t nblk, const int64_t* rowptr,
-                    const int* cols, const double* vals, const double* diag, const double* b, double* x,
+/* Supernodal sync-free triangular solve over tasks in dependency-level order.  A block
+ * [r0, r0+w) has a dense in-block triangle (w <= 4096).  kind 0: one CTA pulls the block's
+ * outside part (one global hop) and solves the dense triangle in 32-column tiles; kind 1:
+ * helper computing the outside sums of block rows [rb, rb+rc) into ysum (heavy blocks);
+ * kind 2: dense part of a heavy block, fed by its helpers (scheduled just before it).
+ * lower: unit diagonal; upper: divides by diag.  Strict CSR, sorted columns.  x and ysum
+ * (n each) are reset inside.  Deterministic. */
+int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
+                    const int* blk_rc, int64_t nblk, const int64_t* rowptr, const int* cols,
+                    const double* vals, const double* diag, const double* b, double* x, double* ysum,
                     int64_t n, unsigned long long* ticket, int ctas_per_sm, void* stream);
 
 /* Setup helpers on HOST arrays: dense-triangle row blocks (returns the count; blocks in row

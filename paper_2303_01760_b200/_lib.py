@@ -53,7 +53,8 @@ SIGNATURES: dict[str, tuple] = {
     "hn_sptrsv_tasks": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _i,
                              _vp]),
     "hn_host_levels": (_i, [_vp, _vp, _i64, _i, _vp]),
-    "hn_sptrsv_super": (_i, [_i, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i, _vp]),
+    "hn_sptrsv_super": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i,
+                             _vp]),
     "hn_host_supernodes": (_i64, [_vp, _vp, _i64, _i, _i, _vp, _vp]),
     "hn_host_block_levels": (_i, [_vp, _vp, _i64, _i, _i64, _vp, _vp, _vp]),
     "hn_partition_methods": (_i, [_vp, _i64, _vp, _vp, _vp, _vp]),

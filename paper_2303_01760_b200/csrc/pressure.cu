@@ -177,11 +177,15 @@ __device__ __forceinline__ double row_outside_sum(const int* __restrict__ cols, 
   return warp_sum(sum);
 }
 
+// Task kinds: 0 = whole block (outside + dense), 1 = helper (outside sums of rows
+// [rb, rb+rc) of a heavy block -> ysum, sentinel-flagged), 2 = dense part of a heavy block
+// whose outside sums come from its helpers (scheduled right before it).
 template <bool LOWER>
 __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
-    const int* __restrict__ blk_r0, const int* __restrict__ blk_w, int64_t nblk, const int64_t* __restrict__ rowptr,
+    const int* __restrict__ blk_kind, const int* __restrict__ blk_r0, const int* __restrict__ blk_w,
+    const int* __restrict__ blk_rb, const int* __restrict__ blk_rc, int64_t nblk, const int64_t* __restrict__ rowptr,
     const int* __restrict__ cols, const double* __restrict__ vals, const double* __restrict__ diag,
-    const double* __restrict__ b, double* x, unsigned long long* ticket) {
+    const double* __restrict__ b, double* x, double* ysum, unsigned long long* ticket) {
   __shared__ double ys[kSnMaxW];
   __shared__ unsigned long long tk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -191,16 +195,27 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
     const unsigned long long t = tk;
     __syncthreads();
     if (t >= static_cast<unsigned long long>(nblk)) return;
+    const int kind = __ldg(blk_kind + t);
     const int r0 = __ldg(blk_r0 + t), w = __ldg(blk_w + t);
-    // (1) outside contributions, warp per row
-    for (int rr = warp; rr < w; rr += kSnWarps) {
-      const int i = r0 + rr;
-      const int64_t a = __ldg(rowptr + i), z = __ldg(rowptr + i + 1);
-      const int inside = LOWER ? rr : (w - 1 - rr);
-      const int64_t e0 = LOWER ? a : a + inside;
-      const int len = static_cast<int>(z - a) - inside;
-      const double s = row_outside_sum(cols, vals, e0, len, x, lane);
-      if (lane == 0) ys[rr] = __ldg(b + i) - s;
+    if (kind == 2) {
+      for (int rr = tid; rr < w; rr += kSnThreads) ys[rr] = wait_value(ysum + r0 + rr);
+    } else {
+      // (1) outside contributions, warp per row
+      const int rb = kind == 1 ? __ldg(blk_rb + t) : 0;
+      const int re = kind == 1 ? rb + __ldg(blk_rc + t) : w;
+      for (int rr = rb + warp; rr < re; rr += kSnWarps) {
+        const int i = r0 + rr;
+        const int64_t a = __ldg(rowptr + i), z = __ldg(rowptr + i + 1);
+        const int inside = LOWER ? rr : (w - 1 - rr);
+        const int64_t e0 = LOWER ? a : a + inside;
+        const int len = static_cast<int>(z - a) - inside;
+        const double s = row_outside_sum(cols, vals, e0, len, x, lane);
+        if (lane == 0) {
+          if (kind == 1) st_release_dbl(ysum + i, __ldg(b + i) - s);
+          else ys[rr] = __ldg(b + i) - s;
+        }
+      }
+      if (kind == 1) continue;
     }
     __syncthreads();
     // (2) dense in-block triangle, 32-column tiles
@@ -397,16 +412,22 @@ HN_EXPORT int hn_sptrsv_tasks(int divide, const int* task_row, const int64_t* ta
 }
 
 // Supernodal solve over planned blocks (processing order), see sptrsv_super_kernel.
-HN_EXPORT int hn_sptrsv_super(int lower, const int* blk_r0, const int* blk_w, int64_t nblk, const int64_t* rowptr,
-                              const int* cols, const double* vals, const double* diag, const double* b, double* x,
+HN_EXPORT int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
+                              const int* blk_rc, int64_t nblk, const int64_t* rowptr, const int* cols,
+                              const double* vals, const double* diag, const double* b, double* x, double* ysum,
                               int64_t n, unsigned long long* ticket, int ctas_per_sm, void* stream) {
   if (nblk == 0) return 0;
   cudaStream_t s = as_stream(stream);
   HN_TRY(cudaMemsetAsync(x, 0xFF, sizeof(double) * n, s));
+  HN_TRY(cudaMemsetAsync(ysum, 0xFF, sizeof(double) * n, s));
   HN_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s));
   const int blocks = sm_count() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
-  if (lower) sptrsv_super_kernel<true><<<blocks, kSnThreads, 0, s>>>(blk_r0, blk_w, nblk, rowptr, cols, vals, diag, b, x, ticket);
-  else sptrsv_super_kernel<false><<<blocks, kSnThreads, 0, s>>>(blk_r0, blk_w, nblk, rowptr, cols, vals, diag, b, x, ticket);
+  if (lower)
+    sptrsv_super_kernel<true><<<blocks, kSnThreads, 0, s>>>(blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr, cols,
+                                                            vals, diag, b, x, ysum, ticket);
+  else
+    sptrsv_super_kernel<false><<<blocks, kSnThreads, 0, s>>>(blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr,
+                                                             cols, vals, diag, b, x, ysum, ticket);
   HN_CHECK_LAUNCH();
   return 0;
 }

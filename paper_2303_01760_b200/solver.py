@@ -107,7 +107,7 @@ class _TriSchedule:
         self.partial = L.empty(max(self.npartial, 1), L.torch().float64)
 
 
-def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 4096) -> dict:
+def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 4096, helper_nnz: int = 16384) -> dict:
     """Host planning of hn_sptrsv_super: dense-triangle row blocks in dependency-level order."""
     n = m.shape[0]
     rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
@@ -122,15 +122,42 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 4096) -
     L.call("hn_host_block_levels", rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), n, 1 if lower else 0, nb,
            r0.ctypes.data_as(vp), w.ctypes.data_as(vp), lev.ctypes.data_as(vp))
     order = np.lexsort((r0, lev))
-    return {"nblk": nb, "r0": r0[order], "w": w[order], "levels": lev[order],
-            "depth": int(lev.max()) + 1 if nb else 0}
+    r0, w, lev = r0[order], w[order], lev[order]
+    # heavy blocks: their outside sums go to helper tasks (kind 1) that run on other SMs,
+    # the block itself (kind 2) only solves the dense triangle
+    rowlen = np.diff(rowptr)
+    owner_r0 = np.repeat(r0, w)
+    owner_w = np.repeat(w, w)
+    rows = np.concatenate([np.arange(a, a + b) for a, b in zip(r0, w)]) if nb else np.empty(0, np.int64)
+    rr = rows - owner_r0
+    inside = rr if lower else owner_w - 1 - rr
+    outside = rowlen[rows] - inside
+    starts = np.concatenate([[0], np.cumsum(w)[:-1]]) if nb else np.empty(0, np.int64)
+    block_out = np.add.reduceat(outside, starts) if nb else np.empty(0)
+    kinds, tr0, tw, trb, trc = [], [], [], [], []
+    heavy = set(np.nonzero((block_out > helper_nnz) & (w > 1))[0].tolist())
+    for k in range(nb):
+        if k in heavy:
+            o = outside[starts[k]: starts[k] + w[k]]
+            cut = np.searchsorted(np.cumsum(o), np.arange(1, int(np.ceil(o.sum() / helper_nnz))) * helper_nnz)
+            bounds = np.unique(np.concatenate([[0], cut, [w[k]]]))
+            for a, b in zip(bounds[:-1], bounds[1:]):
+                kinds.append(1); tr0.append(r0[k]); tw.append(w[k]); trb.append(a); trc.append(b - a)
+            kinds.append(2); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k])
+        else:
+            kinds.append(0); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k])
+    as32 = lambda v: np.asarray(v, dtype=np.int32)  # noqa: E731
+    return {"nblk": nb, "r0": r0, "w": w, "levels": lev, "depth": int(lev.max()) + 1 if nb else 0,
+            "ntasks": len(kinds), "kind": as32(kinds), "t_r0": as32(tr0), "t_w": as32(tw), "t_rb": as32(trb),
+            "t_rc": as32(trc), "heavy": len(heavy)}
 
 
 class _SuperSchedule:
     def __init__(self, m: sparse.csr_matrix, lower: bool):
         plan = plan_supernodal_blocks(m, lower)
-        self.nblk, self.depth = plan["nblk"], plan["depth"]
-        self.r0, self.w = L.to_device(plan["r0"]), L.to_device(plan["w"])
+        self.nblk, self.depth, self.ntasks = plan["nblk"], plan["depth"], plan["ntasks"]
+        self.kind, self.r0, self.w = L.to_device(plan["kind"]), L.to_device(plan["t_r0"]), L.to_device(plan["t_w"])
+        self.rb, self.rc = L.to_device(plan["t_rb"]), L.to_device(plan["t_rc"])
 
 
 def plan_triangular_tasks(m: sparse.csr_matrix, lower: bool, chunk: int) -> dict:
@@ -191,6 +218,7 @@ class _DeviceLU:
         self.z = L.empty(self.n, t.float64)
         self.w = L.empty(self.n, t.float64)
         self.ticket = L.zeros(1, t.int64)
+        self.ysum = L.empty(self.n, t.float64)
         self.nnz = self.L.nnz + self.U.nnz + self.n
 
     def solve(self, b, x):
@@ -204,9 +232,10 @@ class _DeviceLU:
 
     def _tri(self, sch, m, diag, b, x, s):
         if self.supernodal:
-            L.call("hn_sptrsv_super", 1 if diag is None else 0, L.ptr(sch.r0), L.ptr(sch.w), sch.nblk,
-                   L.ptr(m.rowptr), L.ptr(m.cols), L.ptr(m.vals), L.ptr(diag), L.ptr(b), L.ptr(x), self.n,
-                   L.ptr(self.ticket), self.CTAS_PER_SM, s)
+            L.call("hn_sptrsv_super", 1 if diag is None else 0, L.ptr(sch.kind), L.ptr(sch.r0), L.ptr(sch.w),
+                   L.ptr(sch.rb), L.ptr(sch.rc), sch.ntasks, L.ptr(m.rowptr), L.ptr(m.cols), L.ptr(m.vals),
+                   L.ptr(diag), L.ptr(b), L.ptr(x), L.ptr(self.ysum), self.n, L.ptr(self.ticket), self.CTAS_PER_SM,
+                   s)
             return
         L.call("hn_sptrsv_tasks", 0 if diag is None else 1, L.ptr(sch.row), L.ptr(sch.beg), L.ptr(sch.len),
                L.ptr(sch.part), L.ptr(sch.np_), sch.ntasks, L.ptr(m.cols), L.ptr(m.vals), L.ptr(diag), L.ptr(b),

@@ -100,21 +100,31 @@ def test_operator_codes_accept_foreign_operator_classes():
 
 
 def emulate_blocks(plan, m, b, lower, diag=None):
-    """Execute the supernodal plan sequentially in processing order."""
+    """Execute the supernodal task list sequentially in ticket order (helpers included)."""
     n = m.shape[0]
     x = np.full(n, np.nan)
+    ysum = np.full(n, np.nan)
     dense = m.toarray()
-    for r0, w in zip(plan["r0"], plan["w"]):
+
+    def outside(i, r0, w):
+        c = m.indices[m.indptr[i]:m.indptr[i + 1]]
+        v = m.data[m.indptr[i]:m.indptr[i + 1]]
+        out = (c < r0) if lower else (c >= r0 + w)
+        assert not np.any(np.isnan(x[c[out]])), "task ran before a dependency"
+        assert np.array_equal(np.sort(c[~out]), np.arange(r0, i) if lower else np.arange(i + 1, r0 + w))
+        return b[i] - np.dot(v[out], x[c[out]])
+
+    for kind, r0, w, rb, rc in zip(plan["kind"], plan["t_r0"], plan["t_w"], plan["t_rb"], plan["t_rc"]):
         rows = np.arange(r0, r0 + w)
-        y = np.empty(w)
-        for k, i in enumerate(rows):
-            c = m.indices[m.indptr[i]:m.indptr[i + 1]]
-            v = m.data[m.indptr[i]:m.indptr[i + 1]]
-            out = (c < r0) if lower else (c >= r0 + w)
-            assert not np.any(np.isnan(x[c[out]])), "block ran before a dependency"
-            inside = ~out
-            assert np.array_equal(np.sort(c[inside]), np.arange(r0, i) if lower else np.arange(i + 1, r0 + w))
-            y[k] = b[i] - np.dot(v[out], x[c[out]])
+        if kind == 1:
+            for i in range(r0 + rb, r0 + rb + rc):
+                ysum[i] = outside(i, r0, w)
+            continue
+        if kind == 2:
+            assert not np.any(np.isnan(ysum[rows])), "dense part before its helpers"
+            y = ysum[rows].copy()
+        else:
+            y = np.array([outside(i, r0, w) for i in rows])
         blk = dense[np.ix_(rows, rows)]
         full = blk + (np.eye(w) if lower else np.diag(diag[rows]))
         x[rows] = spsolve_triangular(sp.csr_matrix(full), y, lower=lower)
@@ -132,8 +142,9 @@ def test_supernodal_plan_solves_triangular_systems(lower):
     tri = sp.tril(sp.csr_matrix(lu.L), k=-1, format="csr") if lower else sp.triu(sp.csr_matrix(lu.U), k=1, format="csr")
     tri.sort_indices()
     diag = sp.csr_matrix(lu.U).diagonal()
-    plan = plan_supernodal_blocks(tri, lower, cap=64)
+    plan = plan_supernodal_blocks(tri, lower, cap=64, helper_nnz=40)
     assert plan["nblk"] < n and plan["w"].sum() == n
+    assert plan["heavy"] > 0 and plan["ntasks"] > plan["nblk"]
     b = rng.normal(size=n)
     x = emulate_blocks(plan, tri, b, lower, diag)
     full = (tri + sp.eye(n)) if lower else (tri + sp.diags(diag))
