@@ -40,7 +40,8 @@ L2_FLUSH_BYTES = 256 << 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 200 for weight configs, 50 for config 3)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
@@ -97,7 +98,7 @@ class ClockSampler:
         try:
             idx = os.environ.get("LOCAL_RANK", "0")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", idx, f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=self.file, stderr=subprocess.DEVNULL)
         except (FileNotFoundError, OSError):
             self.proc = None
@@ -157,7 +158,8 @@ def measure_dfma_peak(L):
 
 class LaunchCounter:
     """Kernels each libhn entry point launches (fixed per call; see csrc/*.cu)."""
-    KERNELS = {"hn_celllist_build": 5, "hn_knn": 1, "hn_classify": 1, "hn_mon_stencils": 1, "hn_weights_mon": 1,
+    KERNELS = {"hn_celllist_build": 5, "hn_partition_methods": 6, "hn_sptrsv_super": 1, "hn_sptrsv_tasks": 1,
+               "hn_knn": 1, "hn_classify": 1, "hn_mon_stencils": 1, "hn_weights_mon": 1,
                "hn_weights_rbf": 1, "hn_apply_ell": 1, "hn_momentum": 1, "hn_div_rhs": 1,
                "hn_correct_temperature": 1, "hn_temperature_bc": 2, "hn_csr_matvec": 1, "hn_csr_residual": 1,
                "hn_sptrsv": 1, "hn_permute": 1, "hn_reduce": 2, "hn_bicg_update": 1, "hn_bench_dfma": 1}
@@ -190,39 +192,31 @@ def run_weights_bench(args, rank, world):
     flush = L.empty(L2_FLUSH_BYTES // 8, t.float64)
     e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
 
-    # ---- device-resident step: positions already in HBM (cached DeviceNodes) ----
-    dn_cached = _device.DeviceNodes(ns)
-
-    def device_step():
-        dn = _device.DeviceNodes.__new__(_device.DeviceNodes)
-        dn.__dict__.update(dn_cached.__dict__)
-        # rebuild the cell list from the resident positions (part of the stencil builder, K1)
-        scratch = L.empty(int(np.prod(dn.dims)), t.int32)
-        scratch2 = L.empty(dn.n, t.int32)
-        L.call("hn_celllist_build", L.ptr(dn.pos), dn.n, dn.dim, L.host_dbls(dn.lo), dn.cell, L.host_ints(dn.dims),
-               L.ptr(dn.cell_start), L.ptr(dn.cell_items), L.ptr(dn.cell_pos), L.ptr(scratch), L.ptr(scratch2),
-               L.stream_handle())
-        _device._NODE_CACHE[ns] = (ns.positions, ns.positions.shape, dn)
-        return approx._interior_device_table(ns, ops, rbf_n)
-
+    # ---- device-resident step: positions in HBM; the whole pipeline (cell list ->
+    # classify -> partition -> stencils -> solves) replayed as one CUDA graph ----
+    pipe = approx.WeightsPipeline(ns, ops, rbf_n)
+    counter.enabled = True
+    pipe.run()
+    launches = counter.count  # kernels per step (counted from one eager pass)
+    counter.enabled = False
+    pipe.capture()
     for _ in range(args.warmup):
-        device_step()
+        pipe.replay()
     t.cuda.synchronize()
+    pipe.check()
     barrier(world)
     times = []
-    counter.enabled = True
     with ClockSampler() as clocks:
         for _ in range(args.steps):
             flush.fill_(1.0)
             e0.record()
-            device_step()
+            pipe.replay()
             e1.record()
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
-    counter.enabled = False
     t.cuda.synchronize()
+    pipe.check()
     barrier(world)
-    launches = counter.count // max(args.steps, 1)
     ms = max_over_ranks(float(np.mean(times)), world)
     value = world * n_int / (ms * 1e-3)
 
@@ -255,7 +249,7 @@ def run_weights_bench(args, rank, world):
     for _ in range(3):
         solve()
     kt = []
-    for _ in range(max(5, args.steps)):
+    for _ in range(min(max(5, args.steps), 30)):
         flush.fill_(2.0)
         e0.record()
         solve()
@@ -284,7 +278,7 @@ def run_weights_bench(args, rank, world):
     for _ in range(3):
         app()
     at = []
-    for _ in range(max(10, args.steps)):
+    for _ in range(min(max(10, args.steps), 30)):
         flush.fill_(3.0)
         e0.record()
         app()
@@ -300,7 +294,8 @@ def run_weights_bench(args, rank, world):
     from paper_2303_01760_b200.nodegen import NodeSet
     e2e_t = []
     h2d = d2h = 0
-    for k in range(args.warmup + args.steps):
+    e2e_steps = min(args.steps, 10)
+    for k in range(args.warmup + e2e_steps):
         fresh = NodeSet(ns.positions, ns.spacing, ns.kind, ns.role, ns.bc_value, ns.normals, ns.origin, ns.lattice,
                         ns.lattice_idx)
         flush.fill_(4.0)
@@ -325,7 +320,8 @@ def run_weights_bench(args, rank, world):
                    "stencils": stencil_mix(dev), "ops": len(ops), "l2": "flushed between steps (256 MiB write)",
                    "parallelism": f"weak x{world} (independent node set per rank)"},
         "e2e": {"value": world * n_int / e2e_s, "unit": "stencils/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "api": "paper_2303_01760_b200.compute_weights(NodeSet, ops)"},
+                "d2h_bytes_per_step": int(d2h), "api": "paper_2303_01760_b200.compute_weights(NodeSet, ops)",
+                "samples_ms": [round(1e3 * x, 3) for x in e2e_t]},
         "roofline": {"bound": "fp64", "kernel": f"rbf_weights_kernel<{dim},{nst}>" if big == "rbf" else
                      f"mon_weights_kernel<{dim}>", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -471,6 +467,8 @@ def run_reference(args, rank, world):
 
 def main():
     args = parse()
+    if args.steps is None:
+        args.steps = 50 if args.config == 3 else (3 if args.impl == "reference" else 200)
     rank, world = dist_init(args.gpus)
     if args.impl == "reference":
         line = run_reference(args, rank, world)

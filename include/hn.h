@@ -108,6 +108,14 @@ int hn_apply_ell(int nbins, const int64_t* bin_K_host, const int* bin_width_host
                  const double* const* bin_w_host, int nops, const int* op_sel_host,
                  const double* field, double* out, int64_t out_stride, void* stream);
 
+/* ELL bins -> the reference WeightTable layout (approx.py:311-323): idx_out (N x n_max)
+ * int64 -1 padded, sizes_out (N) int64, w_out (nops x N x n_max) fp64 zero padded; every
+ * node must belong to one bin. */
+int hn_ell_to_table(int nbins, const int64_t* bin_K_host, const int* bin_width_host,
+                    const int* const* bin_rows_host, const int* const* bin_idx_host,
+                    const double* const* bin_w_host, int nops, int n_max, int64_t N, int64_t* idx_out,
+                    int64_t* sizes_out, double* w_out, void* stream);
+
 /* ------------------------------------------------------ explicit step (K7, K8, K10, K11) */
 
 /* Bins as in hn_apply_ell over the interior operator table; planes lap_plane and

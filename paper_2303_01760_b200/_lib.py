@@ -40,6 +40,8 @@ SIGNATURES: dict[str, tuple] = {
     "hn_weights_rbf_set_variant": (None, [_i]),
     "hn_apply_ell": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i,
                           _c_int_p, _vp, _vp, _i64, _vp]),
+    "hn_ell_to_table": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i, _i, _i64,
+                             _vp, _vp, _vp, _vp]),
     "hn_momentum": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i, _c_int_p,
                          _i, _vp, _vp, _i64, _d, _d, _d, _c_dbl_p, _i, _vp, _vp]),
     "hn_div_rhs": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _c_int_p, _i,

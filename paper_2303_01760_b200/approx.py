@@ -409,6 +409,116 @@ def _interior_device_table(nodeset, ops, n_rbf: int | None = None) -> DeviceTabl
     return DeviceTable(n, dim, list(ops), bins, n_rbf, method_d[:n])
 
 
+class WeightsPipeline:
+    """compute_weights for a fixed node set as one host-sync-free launch sequence
+    (cell list -> classify -> partition -> MON stencils + solves -> kNN + RBF-FD solves),
+    with launch sizes frozen from one eager pass, so it can be replayed as a CUDA graph.
+    `check()` verifies the frozen sizes and the singular flags after replays."""
+
+    def __init__(self, nodeset, ops, rbf_n: int | None = None):
+        from ._device import DeviceNodes
+        t = L.torch()
+        self.ops = list(ops)
+        self.dim = dim = nodeset.dim
+        self.n = n = len(nodeset)
+        self.n_rbf = RBF_SIZE[dim] if rbf_n is None else rbf_n
+        self.dn = dn = DeviceNodes(nodeset)
+        self.has_lattice = getattr(nodeset, "lattice", None) is not None and \
+            getattr(nodeset, "lattice_idx", None) is not None
+        if not self.has_lattice and np.any(np.asarray(nodeset.kind) == KIND_REGULAR):
+            raise NotImplementedError("WeightsPipeline needs the lattice map for regular nodes")
+        self.method = L.empty(max(n, 1), t.int8)
+        self.rows = L.empty(max(n, 1), t.int32)
+        self.counts = L.empty(3, t.int32)
+        self.part_scratch = L.empty(3 * (n // 256 + 1) + 1, t.int32)
+        self.cl_scratch = L.empty(int(np.prod(dn.dims)), t.int32)
+        self.cl_scratch2 = L.empty(max(n, 1), t.int32)
+        self._classify_partition()
+        self.k_mon, self.k_rbf, self.k_none = (int(v) for v in self.counts.cpu().numpy())
+        if self.k_rbf and self.n_rbf > n:
+            raise ValueError(f"stencil size {self.n_rbf} exceeds node count {n}")
+        nops = len(self.ops)
+        km, kr = max(self.k_mon, 1), max(self.k_rbf, 1)
+        self.mon_st = L.empty((km, 2 * dim + 1), t.int32)
+        self.rbf_st = L.empty((kr, self.n_rbf), t.int32)
+        self.mon_idx, self.mon_w = L.empty((2 * dim + 1, km), t.int32), L.empty((nops, 2 * dim + 1, km), t.float64)
+        self.rbf_idx, self.rbf_w = L.empty((self.n_rbf, kr), t.int32), L.empty((nops, self.n_rbf, kr), t.float64)
+        self.mon_info, self.rbf_info = L.zeros(km, t.int32), L.zeros(kr, t.int32)
+        self._args = _op_args(self.ops, dim)
+        self.graph = None
+
+    def _classify_partition(self):
+        s = L.stream_handle()
+        dn = self.dn
+        L.call("hn_classify", L.ptr(dn.kind), L.ptr(dn.lattice_idx), L.ptr(dn.lattice_grid),
+               L.host_ints(dn.grid_dims if dn.lattice_grid is not None else [1, 1, 1]), self.n, self.dim,
+               L.ptr(self.method), s)
+        L.call("hn_partition_methods", L.ptr(self.method), self.n, L.ptr(self.rows), L.ptr(self.counts),
+               L.ptr(self.part_scratch), s)
+
+    def run(self):
+        """The whole step, launched on the current stream, no host synchronisation."""
+        s = L.stream_handle()
+        dn = self.dn
+        L.call("hn_celllist_build", L.ptr(dn.pos), dn.n, dn.dim, L.host_dbls(dn.lo), dn.cell, L.host_ints(dn.dims),
+               L.ptr(dn.cell_start), L.ptr(dn.cell_items), L.ptr(dn.cell_pos), L.ptr(self.cl_scratch),
+               L.ptr(self.cl_scratch2), s)
+        self._classify_partition()
+        kinds, axes, normals = self._args
+        nops, dim = len(self.ops), self.dim
+        if self.k_mon:
+            L.call("hn_mon_stencils", L.ptr(self.rows), self.k_mon, L.ptr(dn.pos), L.ptr(dn.lattice_idx),
+                   L.ptr(dn.lattice_grid), L.host_ints(dn.grid_dims), dim, L.ptr(self.mon_st), s)
+            L.call("hn_weights_mon", L.ptr(dn.pos), dim, L.ptr(self.mon_st), self.k_mon, nops, kinds, axes, normals,
+                   L.ptr(self.mon_idx), L.ptr(self.mon_w), L.ptr(self.mon_info), s)
+        if self.k_rbf:
+            q = self.rows[self.k_mon:]
+            L.call("hn_knn", L.ptr(dn.pos), dim, L.host_dbls(dn.lo), dn.cell, L.host_ints(dn.dims),
+                   L.ptr(dn.cell_start), L.ptr(dn.cell_items), L.ptr(dn.cell_pos), L.ptr(q), None, self.k_rbf,
+                   self.n_rbf, None, L.ptr(self.rbf_st), None, s)
+            L.call("hn_weights_rbf", L.ptr(dn.pos), dim, L.ptr(self.rbf_st), self.k_rbf, self.n_rbf, nops, kinds,
+                   axes, normals, None, None, L.ptr(self.rbf_idx), L.ptr(self.rbf_w), L.ptr(self.rbf_info), s)
+
+    def capture(self):
+        t = L.torch()
+        self.run()  # warm every code path on the capture stream's device
+        t.cuda.synchronize()
+        self.graph = t.cuda.CUDAGraph()
+        with t.cuda.graph(self.graph):
+            self.run()
+        return self
+
+    def replay(self):
+        self.graph.replay()
+
+    def check(self):
+        """Frozen sizes still hold and no stencil was singular (one read-back)."""
+        t = L.torch()
+        flags = t.stack([self.counts.to(t.int64)[0], self.counts.to(t.int64)[1],
+                         t.count_nonzero(self.mon_info[: self.k_mon]), t.count_nonzero(self.rbf_info[: self.k_rbf])])
+        k_mon, k_rbf, bad_mon, bad_rbf = (int(v) for v in flags.cpu().numpy())
+        if (k_mon, k_rbf) != (self.k_mon, self.k_rbf):
+            raise RuntimeError("node classification changed under a frozen WeightsPipeline")
+        if bad_mon or bad_rbf:
+            raise SingularSystemError(f"singular systems: {bad_mon} MON, {bad_rbf} RBF-FD")
+
+    def table(self) -> DeviceTable:
+        t = L.torch()
+        bins = []
+        if self.k_mon:
+            b = Bin(None, 2 * self.dim + 1, self.mon_idx[:, : self.k_mon], self.mon_w[:, :, : self.k_mon],
+                    d_rows=self.rows[: self.k_mon], K=self.k_mon)
+            bins.append(b)
+        if self.k_rbf:
+            bins.append(Bin(None, self.n_rbf, self.rbf_idx[:, : self.k_rbf], self.rbf_w[:, :, : self.k_rbf],
+                            d_rows=self.rows[self.k_mon: self.k_mon + self.k_rbf], K=self.k_rbf))
+        if self.k_none:
+            bins.append(Bin(None, 0, L.empty((0, self.k_none), t.int32), L.empty((len(self.ops), 0, self.k_none),
+                                                                                  t.float64),
+                            d_rows=self.rows[self.k_mon + self.k_rbf: self.n], K=self.k_none))
+        return DeviceTable(self.n, self.dim, self.ops, bins, self.n_rbf, self.method[: self.n])
+
+
 def compute_weights(nodeset, ops, with_kappa: bool = False, tree=None, rbf_n: int | None = None) -> WeightTable:
     """Stencils and weights for every interior node, batched per method (approx.py:379-413).
 

@@ -73,9 +73,65 @@ __global__ void __launch_bounds__(256) apply_ell_kernel(ApplyBins b, const doubl
 
 bool supported_width(int w) { return w == 0 || w == 5 || w == 7 || w == 12 || w == 20 || w == 30; }
 
+// ELL bins -> the reference's WeightTable layout (approx.py:311-323): indices (N, n_max)
+// int64 -1 padded, sizes (N,) int64, weights (nops, N, n_max) fp64 zero padded.
+struct TableBins {
+  int nbins;
+  int width[4];
+  int64_t K[4];
+  int64_t block_start[5];
+  const int* rows[4];
+  const int* idx[4];
+  const double* w[4];
+};
+
+__global__ void ell_to_table_kernel(TableBins b, int nops, int n_max, int64_t N, int64_t* __restrict__ idx_out,
+                                    int64_t* __restrict__ sizes_out, double* __restrict__ w_out) {
+  int bin = 0;
+#pragma unroll
+  for (int i = 1; i < 4; ++i)
+    if (i < b.nbins && blockIdx.x >= b.block_start[i]) bin = i;
+  const int64_t k = (static_cast<int64_t>(blockIdx.x) - b.block_start[bin]) * blockDim.x + threadIdx.x;
+  if (k >= b.K[bin]) return;
+  const int64_t K = b.K[bin];
+  const int W = b.width[bin];
+  const int64_t row = __ldg(b.rows[bin] + k);
+  sizes_out[row] = W;
+  for (int j = 0; j < n_max; ++j) idx_out[row * n_max + j] = j < W ? __ldg(b.idx[bin] + j * K + k) : -1;
+  for (int o = 0; o < nops; ++o)
+    for (int j = 0; j < n_max; ++j)
+      w_out[(o * N + row) * n_max + j] = j < W ? __ldg(b.w[bin] + (static_cast<int64_t>(o) * W + j) * K + k) : 0.0;
+}
+
 }  // namespace hn
 
 using namespace hn;
+
+HN_EXPORT int hn_ell_to_table(int nbins, const int64_t* bin_K_host, const int* bin_width_host,
+                              const int* const* bin_rows_host, const int* const* bin_idx_host,
+                              const double* const* bin_w_host, int nops, int n_max, int64_t N, int64_t* idx_out,
+                              int64_t* sizes_out, double* w_out, void* stream) {
+  if (nbins < 1 || nbins > 4) return 1;
+  TableBins b{};
+  b.nbins = nbins;
+  const int threads = 128;
+  int64_t blocks = 0;
+  for (int i = 0; i < nbins; ++i) {
+    if (bin_width_host[i] > n_max) return 2;
+    b.width[i] = bin_width_host[i];
+    b.K[i] = bin_K_host[i];
+    b.rows[i] = bin_rows_host[i];
+    b.idx[i] = bin_idx_host[i];
+    b.w[i] = bin_w_host[i];
+    b.block_start[i] = blocks;
+    blocks += ceil_div(b.K[i], threads);
+  }
+  b.block_start[nbins] = blocks;
+  if (blocks == 0) return 0;
+  ell_to_table_kernel<<<blocks, threads, 0, as_stream(stream)>>>(b, nops, n_max, N, idx_out, sizes_out, w_out);
+  HN_CHECK_LAUNCH();
+  return 0;
+}
 
 HN_EXPORT int hn_apply_ell(int nbins, const int64_t* bin_K_host, const int* bin_width_host,
                            const int* const* bin_rows_host, const int* const* bin_idx_host,
