@@ -219,6 +219,8 @@ int hn_bicg_update(int kind, double* y, const double* x, const double* r, double
 /* DFMA throughput probe: `blocks` x 256 threads, `iters` x 16 independent DFMA chains
  * per thread; out[0] receives a checksum.  Used by bench.py for the fp64 peak. */
 int hn_bench_dfma(double* out, int blocks, int iters, void* stream);
+/* FP64 tensor-core (DMMA m8n8k4) probe: blocks x 8 warps x iters x 4 MMAs of 512 flop. */
+int hn_bench_dmma(double* out, int blocks, int iters, void* stream);
 
 int hn_version(void);
 

@@ -28,6 +28,7 @@ _d = C.c_double
 SIGNATURES: dict[str, tuple] = {
     "hn_version": (_i, []),
     "hn_bench_dfma": (_i, [_vp, _i, _i, _vp]),
+    "hn_bench_dmma": (_i, [_vp, _i, _i, _vp]),
     "hn_celllist_build": (_i, [_vp, _i64, _i, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hn_knn": (_i, [_vp, _i, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp, _vp, _vp, _i64, _i, _vp, _vp, _vp, _vp]),
     "hn_classify": (_i, [_vp, _vp, _vp, _c_int_p, _i64, _i, _vp, _vp]),

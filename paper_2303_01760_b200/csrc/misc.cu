@@ -31,9 +31,34 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters)
   if (s == 12345.678) out[0] = s;  // never true; keeps the chains live
 }
 
+// FP64 tensor-core probe: 4 independent m8n8k4 DMMA accumulators per warp.
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double* out, int iters) {
+  const double a = 1.0 + 1e-9 * threadIdx.x, b = 0.999;
+  double c[4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { c[i][0] = 1e-3 * i; c[i][1] = 2e-3 * i; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 }  // namespace hn
 
 HN_EXPORT int hn_version(void) { return 1; }
+
+// flops per launch = blocks * 8 warps * iters * 4 * (8*8*4*2)
+HN_EXPORT int hn_bench_dmma(double* out, int blocks, int iters, void* stream) {
+  hn::dmma_probe_kernel<<<blocks, 256, 0, hn::as_stream(stream)>>>(out, iters);
+  HN_CHECK_LAUNCH();
+  return 0;
+}
 
 HN_EXPORT int hn_bench_dfma(double* out, int blocks, int iters, void* stream) {
   hn::dfma_probe_kernel<<<blocks, 256, 0, hn::as_stream(stream)>>>(out, iters);
