@@ -54,6 +54,9 @@ int hn_knn(const double* pos, int d, const double* lo_host, double cell, const i
            const int* queries, const double* qpos, int64_t nq, int n, const uint8_t* exclude,
            int* out_idx, double* out_dist, void* stream);
 
+/* kNN kernel variant (tuning knob, identical results): 1 per cell (default), 0 batched rings. */
+void hn_knn_set_variant(int v);
+
 /* method per node: -1 boundary, 0 MON, 1 RBF-FD.  lattice_idx (N x d int32, INT32_MIN =
  * off-lattice) and grid (prod(grid_dims) int32, -1 vacant) may be NULL (no lattice).
  * Replaces: classify_methods approx.py:332-351. */

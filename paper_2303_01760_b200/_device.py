@@ -58,30 +58,65 @@ class DeviceNodes:
         # per-column reductions: numpy's axis-0 reduce over an (N, d) array is ~15x slower
         lo = np.array([pos[:, a].min() for a in range(self.dim)]) if self.n else np.zeros(self.dim)
         hi = np.array([pos[:, a].max() for a in range(self.dim)]) if self.n else np.ones(self.dim)
+        self.lo, self.hi = lo.astype(float), hi.astype(float)
         ext = np.maximum(hi - lo, 1e-300)
         vol = float(np.prod(ext))
         cell = (vol / max(self.n, 1)) ** (1.0 / self.dim) * (1.0 if self.dim == 2 else 1.25)
         if not np.isfinite(cell) or cell <= 0:
             cell = float(np.max(ext)) or 1.0
+        self._grids = {}
+        g = self.grid(cell, exact=True)
+        self.cell, self.dims = g.cell, g.dims
+        self.cell_start, self.cell_items, self.cell_pos = g.start, g.items, g.pos
+        # graded sets: queries on the finest nodes get a grid sized to their own spacing
+        self.fine_cell = None
+        kind = np.asarray(nodeset.kind)
+        spacing = getattr(nodeset, "spacing", None)
+        if spacing is not None and np.any(kind == 1):
+            hs = float(np.mean(np.asarray(spacing)[kind == 1]))
+            fine = hs * (1.0 if self.dim == 2 else 1.25)
+            if fine < 0.7 * self.cell:
+                self.fine_cell = fine
+
+    class _Grid:
+        pass
+
+    def grid(self, cell: float, exact: bool = False):
+        """Uniform cell list with (about) the requested cell size; built once, cached."""
+        t = L.torch()
+        ext = np.maximum(self.hi - self.lo, 1e-300)
         dims = [int(np.floor(ext[a] / cell)) + 1 for a in range(self.dim)]
-        while int(np.prod(dims)) > 4 * max(self.n, 1) + 64:
+        while int(np.prod(dims)) > 8 * max(self.n, 1) + 64:
             cell *= 1.25
             dims = [int(np.floor(ext[a] / cell)) + 1 for a in range(self.dim)]
-        self.lo, self.cell, self.dims = lo.astype(float), float(cell), dims
+        key = round(float(cell), 15)
+        if key in self._grids:
+            return self._grids[key]
+        g = DeviceNodes._Grid()
+        g.cell, g.dims = float(cell), dims
         ncells = int(np.prod(dims))
-        self.cell_start = L.empty(ncells + 1, t.int32)
-        self.cell_items = L.empty(max(self.n, 1), t.int32)
-        self.cell_pos = L.empty((max(self.n, 1), self.stride), t.float64)
-        scratch = L.empty(ncells, t.int32)
-        scratch2 = L.empty(max(self.n, 1), t.int32)
-        L.call("hn_celllist_build", L.ptr(self.pos), self.n, self.dim, L.host_dbls(self.lo), self.cell,
-               L.host_ints(dims), L.ptr(self.cell_start), L.ptr(self.cell_items), L.ptr(self.cell_pos),
-               L.ptr(scratch), L.ptr(scratch2), L.stream_handle())
-        self._keep = (scratch, scratch2)
+        g.start = L.empty(ncells + 1, t.int32)
+        g.items = L.empty(max(self.n, 1), t.int32)
+        g.pos = L.empty((max(self.n, 1), self.stride), t.float64)
+        g.scratch = L.empty(ncells, t.int32)
+        g.scratch2 = L.empty(max(self.n, 1), t.int32)
+        self.build_grid(g)
+        self._grids[key] = g
+        return g
 
-    def knn(self, n: int, rows=None, points: np.ndarray | None = None, exclude=None, with_dist: bool = False):
-        """n nearest nodes by (fl-distance, index) for node ids `rows` or query `points`."""
+    def build_grid(self, g):
+        """(Re)build a cell list from the resident positions (K1)."""
+        L.call("hn_celllist_build", L.ptr(self.pos), self.n, self.dim, L.host_dbls(self.lo), g.cell,
+               L.host_ints(g.dims), L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos), L.ptr(g.scratch),
+               L.ptr(g.scratch2), L.stream_handle())
+
+    def knn(self, n: int, rows=None, points: np.ndarray | None = None, exclude=None, with_dist: bool = False,
+            fine: bool = False):
+        """n nearest nodes by (fl-distance, index) for node ids `rows` or query `points`.
+        fine=True: the queries sit on the finest (scattered) nodes -> use their grid.
+        Any grid gives the same (exact) answer; the choice only changes the work."""
         t = L.torch()
+        g = self.grid(self.fine_cell) if (fine and self.fine_cell is not None) else self.grid(self.cell, exact=True)
         qpos = None
         if points is not None:
             pts = np.atleast_2d(np.asarray(points, float))
@@ -100,8 +135,8 @@ class DeviceNodes:
         if exclude is not None:
             ex = exclude if hasattr(exclude, "data_ptr") else L.to_device(np.asarray(exclude, dtype=np.uint8))
         if nq:
-            L.call("hn_knn", L.ptr(self.pos), self.dim, L.host_dbls(self.lo), self.cell, L.host_ints(self.dims),
-                   L.ptr(self.cell_start), L.ptr(self.cell_items), L.ptr(self.cell_pos), L.ptr(q), L.ptr(qpos),
+            L.call("hn_knn", L.ptr(self.pos), self.dim, L.host_dbls(self.lo), g.cell, L.host_ints(g.dims),
+                   L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos), L.ptr(q), L.ptr(qpos),
                    nq, n, L.ptr(ex), L.ptr(out), L.ptr(dist), L.stream_handle())
         out = out[:nq]
         return (out, dist[:nq]) if with_dist else out

@@ -399,7 +399,7 @@ def _interior_device_table(nodeset, ops, n_rbf: int | None = None) -> DeviceTabl
         if n_rbf > n:
             raise ValueError(f"stencil size {n_rbf} exceeds node count {n}")
         d_rows = rows_d[k_mon:k_mon + k_rbf]
-        pending.append(_solve_bin(dn, dn.knn(n_rbf, rows=d_rows), d_rows, ops, False))
+        pending.append(_solve_bin(dn, dn.knn(n_rbf, rows=d_rows, fine=True), d_rows, ops, False))
     _check_info(pending)
     bins = [b for b, _ in pending]
     if k_none:
@@ -431,8 +431,7 @@ class WeightsPipeline:
         self.rows = L.empty(max(n, 1), t.int32)
         self.counts = L.empty(3, t.int32)
         self.part_scratch = L.empty(3 * (n // 256 + 1) + 1, t.int32)
-        self.cl_scratch = L.empty(int(np.prod(dn.dims)), t.int32)
-        self.cl_scratch2 = L.empty(max(n, 1), t.int32)
+        self.gq = dn.grid(dn.fine_cell) if dn.fine_cell is not None else dn.grid(dn.cell, exact=True)
         self._classify_partition()
         self.k_mon, self.k_rbf, self.k_none = (int(v) for v in self.counts.cpu().numpy())
         if self.k_rbf and self.n_rbf > n:
@@ -460,9 +459,7 @@ class WeightsPipeline:
         """The whole step, launched on the current stream, no host synchronisation."""
         s = L.stream_handle()
         dn = self.dn
-        L.call("hn_celllist_build", L.ptr(dn.pos), dn.n, dn.dim, L.host_dbls(dn.lo), dn.cell, L.host_ints(dn.dims),
-               L.ptr(dn.cell_start), L.ptr(dn.cell_items), L.ptr(dn.cell_pos), L.ptr(self.cl_scratch),
-               L.ptr(self.cl_scratch2), s)
+        dn.build_grid(self.gq)  # the cell list the RBF-FD queries search (K1)
         self._classify_partition()
         kinds, axes, normals = self._args
         nops, dim = len(self.ops), self.dim
@@ -473,8 +470,9 @@ class WeightsPipeline:
                    L.ptr(self.mon_idx), L.ptr(self.mon_w), L.ptr(self.mon_info), s)
         if self.k_rbf:
             q = self.rows[self.k_mon:]
-            L.call("hn_knn", L.ptr(dn.pos), dim, L.host_dbls(dn.lo), dn.cell, L.host_ints(dn.dims),
-                   L.ptr(dn.cell_start), L.ptr(dn.cell_items), L.ptr(dn.cell_pos), L.ptr(q), None, self.k_rbf,
+            g = self.gq
+            L.call("hn_knn", L.ptr(dn.pos), dim, L.host_dbls(dn.lo), g.cell, L.host_ints(g.dims),
+                   L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos), L.ptr(q), None, self.k_rbf,
                    self.n_rbf, None, L.ptr(self.rbf_st), None, s)
             L.call("hn_weights_rbf", L.ptr(dn.pos), dim, L.ptr(self.rbf_st), self.k_rbf, self.n_rbf, nops, kinds,
                    axes, normals, None, None, L.ptr(self.rbf_idx), L.ptr(self.rbf_w), L.ptr(self.rbf_info), s)

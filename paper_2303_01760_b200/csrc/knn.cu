@@ -280,6 +280,136 @@ __global__ void __launch_bounds__(128) knn_kernel(Grid g, const double* __restri
   }
 }
 
+// ---- kNN query v2: batched ring traversal, integer keys ------------------------------
+// Same result as knn_kernel (top n by (fl-distance, index)).  Each ring of cells is walked
+// in batches of KB cells whose [start, end) ranges are loaded together; points are then
+// taken slot-major across the batch so KB independent point loads are in flight.  The
+// top-n network compares fl-distances as uint64 bit patterns (non-negative doubles order
+// like their bits), keeping the FP64 pipe for the distance arithmetic only.
+template <int D, int NMAX>
+__global__ void __launch_bounds__(128) knn2_kernel(Grid g, const double* __restrict__ pos,
+                                                   const int* __restrict__ cell_start,
+                                                   const int* __restrict__ cell_items,
+                                                   const double* __restrict__ cell_pos,
+                                                   const int* __restrict__ queries,
+                                                   const double* __restrict__ qpos, int64_t nq, int n,
+                                                   const uint8_t* __restrict__ exclude,
+                                                   int* __restrict__ out_idx, double* __restrict__ out_dist) {
+  constexpr int KB = 8;
+  constexpr int S = pos_stride<D>();
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nq) return;
+  double q[D];
+  if (qpos) {
+    load_point<D>(qpos, t, q);
+  } else {
+    const int qi = queries ? __ldg(queries + t) : static_cast<int>(t);
+    load_point<D>(pos, qi, q);
+  }
+  int c0[D];
+  cell_coords<D>(g, q, c0);
+  unsigned long long kd[NMAX];
+  int ki[NMAX];
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) {
+    const bool live = j >= NMAX - n;
+    kd[j] = live ? ~0ull : 0ull;  // ~0 > any distance bits; 0 sentinel never displaced
+    ki[j] = live ? INT_MAX : -1;
+  }
+  double thr2 = CUDART_INF;
+  int max_r = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) max_r = max(max_r, max(c0[a], g.dims[a] - 1 - c0[a]));
+
+  for (int R = 0; R <= max_r; ++R) {
+    const int side = 2 * R + 1;
+    int ncube = side * side;
+    if constexpr (D == 3) ncube *= side;
+    for (int base = 0; base < ncube; base += KB) {
+      int cs[KB], ce[KB];
+#pragma unroll
+      for (int b = 0; b < KB; ++b) {
+        int tt = base + b;
+        int o[D];
+        bool ok = tt < ncube;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+          o[a] = tt % side - R;
+          tt /= side;
+        }
+        int m = 0;
+        int64_t cl = 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          m = max(m, abs(o[a]));
+          const int x = c0[a] + o[a];
+          ok = ok && x >= 0 && x < g.dims[a];
+          cl = cl * g.dims[a] + x;
+        }
+        ok = ok && m == R;
+        cs[b] = ok ? __ldg(cell_start + cl) : 0;
+        ce[b] = ok ? __ldg(cell_start + cl + 1) : 0;
+      }
+      for (int slot = 0;; ++slot) {
+        bool any = false;
+        int jj[KB];
+        double pp[KB][D];
+#pragma unroll
+        for (int b = 0; b < KB; ++b) {
+          const int s_ = cs[b] + slot;
+          const bool live = s_ < ce[b];
+          any = any || live;
+          jj[b] = live ? __ldg(cell_items + s_) : -1;
+#pragma unroll
+          for (int a = 0; a < D; ++a) pp[b][a] = live ? __ldg(cell_pos + static_cast<int64_t>(s_) * S + a) : 0.0;
+        }
+        if (!any) break;
+#pragma unroll
+        for (int b = 0; b < KB; ++b) {
+          const int j = jj[b];
+          if (j < 0) continue;
+          if (exclude && __ldg(exclude + j)) continue;
+          const double d2 = exact_dist2<D>(pp[b], q);
+          if (d2 > thr2) continue;
+          const unsigned long long d = static_cast<unsigned long long>(__double_as_longlong(__dsqrt_rn(d2)));
+          if (!(d < kd[NMAX - 1] || (d == kd[NMAX - 1] && j < ki[NMAX - 1]))) continue;
+#pragma unroll
+          for (int mm = NMAX - 1; mm >= 0; --mm) {
+            const bool lt = d < kd[mm] || (d == kd[mm] && j < ki[mm]);
+            if (lt) {
+              const int pm = mm > 0 ? mm - 1 : 0;
+              const bool shift = (mm > 0) && (d < kd[pm] || (d == kd[pm] && j < ki[pm]));
+              kd[mm] = shift ? kd[pm] : d;
+              ki[mm] = shift ? ki[pm] : j;
+            }
+          }
+          const unsigned long long w = kd[NMAX - 1];
+          if (w != ~0ull) {
+            const double wd = __longlong_as_double(static_cast<long long>(w));
+            thr2 = __dmul_rn(__dmul_rn(wd, wd), 1.0 + 1e-15);
+          }
+        }
+      }
+    }
+    double bound = CUDART_INF;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      if (c0[a] - R > 0) bound = fmin(bound, q[a] - (g.lo[a] + (c0[a] - R) * g.cell));
+      if (c0[a] + R + 1 < g.dims[a]) bound = fmin(bound, (g.lo[a] + (c0[a] + R + 1) * g.cell) - q[a]);
+    }
+    const unsigned long long w = kd[NMAX - 1];
+    if (w != ~0ull && __longlong_as_double(static_cast<long long>(w)) < bound - 1e-9 * g.cell) break;
+  }
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) {
+    if (j >= NMAX - n) {
+      const int o = j - (NMAX - n);
+      out_idx[t * n + o] = ki[j];
+      if (out_dist) out_dist[t * n + o] = __longlong_as_double(static_cast<long long>(kd[j]));
+    }
+  }
+}
+
 // ---- classification + lattice stencils ------------------------------------------
 template <int D>
 __device__ __forceinline__ int grid_at(const int* __restrict__ grid, const int* gdims, const int* key) {
@@ -444,6 +574,9 @@ HN_EXPORT int hn_partition_methods(const int8_t* method, int64_t n, int* rows_ou
   return e == cudaSuccess ? 0 : -static_cast<int>(e);
 }
 
+static int g_knn_variant = 1;  // 1: per-cell traversal (knn, default), 0: batched rings (knn2)
+HN_EXPORT void hn_knn_set_variant(int v) { g_knn_variant = v; }
+
 static Grid make_grid(const double* lo_host, double cell, const int* dims_host, int d) {
   Grid g{};
   for (int a = 0; a < 3; ++a) {
@@ -490,6 +623,16 @@ static int launch_knn(const Grid& g, const double* pos, const int* cs, const int
                       double* od, cudaStream_t s) {
   const int th = 128;
   const int64_t bl = ceil_div(nq, th);
+  if (g_knn_variant == 0) {
+    if (n <= 8) knn2_kernel<D, 8><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
+    else if (n <= 16) knn2_kernel<D, 16><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
+    else if (n <= 24) knn2_kernel<D, 24><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
+    else if (n <= 32) knn2_kernel<D, 32><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
+    else if (n <= 48) knn2_kernel<D, 48><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
+    else knn2_kernel<D, 64><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
+    HN_CHECK_LAUNCH();
+    return 0;
+  }
   if (n <= 8) knn_kernel<D, 8><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
   else if (n <= 16) knn_kernel<D, 16><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
   else if (n <= 24) knn_kernel<D, 24><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);

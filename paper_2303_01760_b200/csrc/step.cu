@@ -103,22 +103,13 @@ __device__ __forceinline__ void momentum_row(const StepBins& b, int bin, int64_t
   }
 }
 
-template <int D>
-__global__ void __launch_bounds__(128) momentum_kernel(StepBins b, const double* __restrict__ v,
-                                                       const double* __restrict__ T, int64_t N, MomentumCoef c,
-                                                       double* __restrict__ vstar) {
-  const int bin = find_bin(b);
-  const int64_t k = (static_cast<int64_t>(blockIdx.x) - b.block_start[bin]) * blockDim.x + threadIdx.x;
-  if (k >= b.K[bin]) return;
-  switch (b.width[bin]) {
-    case 0: momentum_row<D, 0>(b, bin, k, v, T, N, c, vstar); break;
-    case 5: momentum_row<D, 5>(b, bin, k, v, T, N, c, vstar); break;
-    case 7: momentum_row<D, 7>(b, bin, k, v, T, N, c, vstar); break;
-    case 12: momentum_row<D, 12>(b, bin, k, v, T, N, c, vstar); break;
-    case 20: momentum_row<D, 20>(b, bin, k, v, T, N, c, vstar); break;
-    case 30: momentum_row<D, 30>(b, bin, k, v, T, N, c, vstar); break;
-    default: break;
-  }
+template <int D, int W>
+__global__ void __launch_bounds__(128, (W <= 7 ? 6 : (W <= 12 ? 3 : 2)))
+momentum_kernel(StepBins b, const double* __restrict__ v, const double* __restrict__ T, int64_t N,
+                MomentumCoef c, double* __restrict__ vstar) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= b.K[0]) return;
+  momentum_row<D, W>(b, 0, k, v, T, N, c, vstar);
 }
 
 // ---- K8: divergence -> Poisson right-hand side (solver.py:295-301) ----
@@ -148,22 +139,14 @@ __device__ __forceinline__ void div_row(const StepBins& b, int bin, int64_t k, c
   }
 }
 
-template <int D>
-__global__ void __launch_bounds__(128) div_rhs_kernel(StepBins b, const double* __restrict__ vs, int64_t N,
-                                                      double dt, double* __restrict__ rhs) {
-  const int bin = find_bin(b);
-  const int64_t k = (static_cast<int64_t>(blockIdx.x) - b.block_start[bin]) * blockDim.x + threadIdx.x;
+template <int D, int W>
+__global__ void __launch_bounds__(128, (W <= 7 ? 8 : (W <= 12 ? 6 : (W <= 20 ? 4 : 2))))
+div_rhs_kernel(StepBins b, const double* __restrict__ vs, int64_t N, double dt,
+               double* __restrict__ rhs) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (blockIdx.x == 0 && threadIdx.x == 0) rhs[N] = 0.0;  // bordered gauge equation
-  if (k >= b.K[bin]) return;
-  switch (b.width[bin]) {
-    case 0: div_row<D, 0>(b, bin, k, vs, N, 0.0, dt, rhs); break;
-    case 5: div_row<D, 5>(b, bin, k, vs, N, 0.0, dt, rhs); break;
-    case 7: div_row<D, 7>(b, bin, k, vs, N, 0.0, dt, rhs); break;
-    case 12: div_row<D, 12>(b, bin, k, vs, N, 0.0, dt, rhs); break;
-    case 20: div_row<D, 20>(b, bin, k, vs, N, 0.0, dt, rhs); break;
-    case 30: div_row<D, 30>(b, bin, k, vs, N, 0.0, dt, rhs); break;
-    default: break;
-  }
+  if (k >= b.K[0]) return;
+  div_row<D, W>(b, 0, k, vs, N, 0.0, dt, rhs);
 }
 
 // ---- K10: velocity correction + temperature advection-diffusion (solver.py:317-331, 345-357) ----
@@ -222,23 +205,14 @@ __device__ __forceinline__ void correct_temp_row(const StepBins& b, int bin, int
   }
 }
 
-template <int D>
-__global__ void __launch_bounds__(128) correct_temp_kernel(StepBins b, const double* __restrict__ vs,
-                                                           const double* __restrict__ p, const double* __restrict__ T,
-                                                           int64_t N, double dt, double* __restrict__ vout,
-                                                           double* __restrict__ Tout, int* __restrict__ flags) {
-  const int bin = find_bin(b);
-  const int64_t k = (static_cast<int64_t>(blockIdx.x) - b.block_start[bin]) * blockDim.x + threadIdx.x;
-  if (k >= b.K[bin]) return;
-  switch (b.width[bin]) {
-    case 0: correct_temp_row<D, 0>(b, bin, k, vs, p, T, N, dt, vout, Tout, flags); break;
-    case 5: correct_temp_row<D, 5>(b, bin, k, vs, p, T, N, dt, vout, Tout, flags); break;
-    case 7: correct_temp_row<D, 7>(b, bin, k, vs, p, T, N, dt, vout, Tout, flags); break;
-    case 12: correct_temp_row<D, 12>(b, bin, k, vs, p, T, N, dt, vout, Tout, flags); break;
-    case 20: correct_temp_row<D, 20>(b, bin, k, vs, p, T, N, dt, vout, Tout, flags); break;
-    case 30: correct_temp_row<D, 30>(b, bin, k, vs, p, T, N, dt, vout, Tout, flags); break;
-    default: break;
-  }
+template <int D, int W>
+__global__ void __launch_bounds__(128, (W <= 7 ? 8 : (W <= 12 ? 6 : (W <= 20 ? 4 : 2))))
+correct_temp_kernel(StepBins b, const double* __restrict__ vs, const double* __restrict__ p,
+                    const double* __restrict__ T, int64_t N, double dt, double* __restrict__ vout,
+                    double* __restrict__ Tout, int* __restrict__ flags) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= b.K[0]) return;
+  correct_temp_row<D, W>(b, 0, k, vs, p, T, N, dt, vout, Tout, flags);
 }
 
 // ---- K11: temperature boundary conditions (solver.py:334-342) ----
@@ -307,6 +281,37 @@ void fill_bins(StepBins& b, int nbins, const int64_t* K, const int* W, const int
   *blocks = acc;
 }
 
+StepBins single_bin(const StepBins& b, int i) {
+  StepBins o = b;
+  o.nbins = 1;
+  o.width[0] = b.width[i];
+  o.K[0] = b.K[i];
+  o.rows[0] = b.rows[i];
+  o.idx[0] = b.idx[i];
+  o.w[0] = b.w[i];
+  o.block_start[0] = 0;
+  o.block_start[1] = ceil_div(b.K[i], 128);
+  return o;
+}
+
+// one template instantiation per (dimension, stencil width): each gets its own registers
+#define HN_WIDTH_DISPATCH(d, w, LAUNCH)                                   \
+  do {                                                                    \
+    if ((d) == 2) {                                                       \
+      switch (w) {                                                        \
+        case 0: LAUNCH(2, 0); break;  case 5: LAUNCH(2, 5); break;        \
+        case 7: LAUNCH(2, 7); break;  case 12: LAUNCH(2, 12); break;      \
+        case 20: LAUNCH(2, 20); break; default: LAUNCH(2, 30); break;     \
+      }                                                                   \
+    } else {                                                              \
+      switch (w) {                                                        \
+        case 0: LAUNCH(3, 0); break;  case 5: LAUNCH(3, 5); break;        \
+        case 7: LAUNCH(3, 7); break;  case 12: LAUNCH(3, 12); break;      \
+        case 20: LAUNCH(3, 20); break; default: LAUNCH(3, 30); break;     \
+      }                                                                   \
+    }                                                                     \
+  } while (0)
+
 }  // namespace hn
 
 using namespace hn;
@@ -334,8 +339,14 @@ HN_EXPORT int hn_momentum(int nbins, const int64_t* bin_K_host, const int* bin_w
   for (int a = 0; a < d; ++a) c.buoy[a] = buoy_host[a];
   if (blocks == 0) return 0;
   cudaStream_t s = as_stream(stream);
-  if (d == 2) momentum_kernel<2><<<blocks, th, 0, s>>>(b, v, T, N, c, vstar);
-  else momentum_kernel<3><<<blocks, th, 0, s>>>(b, v, T, N, c, vstar);
+  for (int i = 0; i < nbins; ++i) {
+    StepBins one = single_bin(b, i);
+    const int64_t bl = ceil_div(one.K[0], th);
+    if (bl == 0) continue;
+#define HN_MOM(DD, WW) momentum_kernel<DD, WW><<<bl, th, 0, s>>>(one, v, T, N, c, vstar)
+    HN_WIDTH_DISPATCH(d, one.width[0], HN_MOM);
+#undef HN_MOM
+  }
   HN_CHECK_LAUNCH();
   return 0;
 }
@@ -352,8 +363,14 @@ HN_EXPORT int hn_div_rhs(int nbins, const int64_t* bin_K_host, const int* bin_wi
   for (int a = 0; a < d; ++a) b.d_plane[a] = d_plane_host[a];
   if (blocks == 0) return 0;
   cudaStream_t s = as_stream(stream);
-  if (d == 2) div_rhs_kernel<2><<<blocks, th, 0, s>>>(b, vstar, N, dt, rhs);
-  else div_rhs_kernel<3><<<blocks, th, 0, s>>>(b, vstar, N, dt, rhs);
+  for (int i = 0; i < nbins; ++i) {
+    StepBins one = single_bin(b, i);
+    const int64_t bl = ceil_div(one.K[0], th);
+    if (bl == 0) continue;
+#define HN_DIV(DD, WW) div_rhs_kernel<DD, WW><<<bl, th, 0, s>>>(one, vstar, N, dt, rhs)
+    HN_WIDTH_DISPATCH(d, one.width[0], HN_DIV);
+#undef HN_DIV
+  }
   HN_CHECK_LAUNCH();
   return 0;
 }
@@ -372,8 +389,14 @@ HN_EXPORT int hn_correct_temperature(int nbins, const int64_t* bin_K_host, const
   for (int a = 0; a < d; ++a) b.d_plane[a] = d_plane_host[a];
   if (blocks == 0) return 0;
   cudaStream_t s = as_stream(stream);
-  if (d == 2) correct_temp_kernel<2><<<blocks, th, 0, s>>>(b, vstar, p, T, N, dt, vout, Tout, flags);
-  else correct_temp_kernel<3><<<blocks, th, 0, s>>>(b, vstar, p, T, N, dt, vout, Tout, flags);
+  for (int i = 0; i < nbins; ++i) {
+    StepBins one = single_bin(b, i);
+    const int64_t bl = ceil_div(one.K[0], th);
+    if (bl == 0) continue;
+#define HN_COR(DD, WW) correct_temp_kernel<DD, WW><<<bl, th, 0, s>>>(one, vstar, p, T, N, dt, vout, Tout, flags)
+    HN_WIDTH_DISPATCH(d, one.width[0], HN_COR);
+#undef HN_COR
+  }
   HN_CHECK_LAUNCH();
   return 0;
 }

@@ -319,6 +319,7 @@ struct __align__(16) RbfSmem {  // 16 B: every system's prow takes v2.f64 stores
   static constexpr int NC = NS + NOPS;
   static constexpr int NCP = (NC + 1) & ~1;  // even length keeps every pair 16 B aligned
   double prow[2][NCP + 2];                      // double-buffered pivot row; [NCP] = 1/pivot
+  double inv_hist[NS + (NS & 1)];               // 1/pivot of every step
   double y[NST][D];
   double w[NST][NOPS];
   int sid[NST];
@@ -463,46 +464,48 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
     }
   }
 
-  // ---- Gauss-Jordan with implicit partial pivoting, branch-free ----
+  // ---- Gauss-Jordan with implicit partial pivoting, branch-free, software-pipelined ----
   // tag[r] = 63 - row id identifies the (lane, slot) of every row; padding rows start done.
+  // Step kk: select + stage pivot row kk, update column kk+1 first, start the pivot
+  // search of step kk+1 (shuffle chain + speculative reciprocal), then the bulk update
+  // runs while that search is in flight.
   unsigned tag[RPL];
   bool done[RPL];
   int pcol[RPL];
-  double pinv[RPL];
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
     const int i = s + r * LPS;
     tag[r] = static_cast<unsigned>(63 - i);
     done[r] = !lane_live || i >= NS;
     pcol[r] = -1;
-    pinv[r] = 0.0;
   }
   const unsigned pbase0 = smem_addr(&sm.prow[0][0]);
   const unsigned pbase1 = smem_addr(&sm.prow[1][0]);
-  int sing = 0;
+  const unsigned hist = smem_addr(&sm.inv_hist[0]);
+
+  unsigned key = 0;
+  double cand = 1.0;
+  auto search = [&](int col) {  // local candidate of column col, then the segmented max
+    key = 0;
+    cand = 1.0;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const unsigned hi = (static_cast<unsigned>(__double2hiint(a[r][col])) & 0x7fffffc0u) | tag[r];
+      const unsigned kr = done[r] ? 0u : hi;
+      cand = kr > key ? a[r][col] : cand;
+      key = max(key, kr);
+    }
+#pragma unroll
+    for (int off = 1; off < LPS; off <<= 1) key = max(key, __shfl_sync(0xffffffffu, key, seg_src(off)));
+    key = __shfl_sync(0xffffffffu, key, lane_live ? seg_base : lane);
+  };
+  search(0);
 
 #pragma unroll
   for (int kk = 0; kk < NS; ++kk) {
     const int buf = kk & 1;
     const unsigned pbase = buf ? pbase1 : pbase0;
-    // pivot search: |a| high word, 6 low bits replaced by the row tag.  The lane's local
-    // candidate value is kept so its reciprocal is computed while the reduction runs
-    // (if this lane owns the pivot, its local best IS the pivot).
-    unsigned key = 0;
-    double cand = 1.0;
-#pragma unroll
-    for (int r = 0; r < RPL; ++r) {
-      const unsigned hi = (static_cast<unsigned>(__double2hiint(a[r][kk])) & 0x7fffffc0u) | tag[r];
-      const unsigned kr = done[r] ? 0u : hi;
-      cand = kr > key ? a[r][kk] : cand;
-      key = max(key, kr);
-    }
-    const double inv_local = fast_rcp(cand);
-    // segmented max (butterfly in segment-relative lane numbers; measured faster than one
-    // REDUX per segment), then broadcast from segment lane 0
-#pragma unroll
-    for (int off = 1; off < LPS; off <<= 1) key = max(key, __shfl_sync(0xffffffffu, key, seg_src(off)));
-    key = __shfl_sync(0xffffffffu, key, lane_live ? seg_base : lane);
+    const double inv_local = fast_rcp(cand);  // = 1/pivot in the owner lane
     const unsigned ptag = key & 63u;
     bool isp[RPL];
     bool own_any = false;
@@ -512,6 +515,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
       own_any = own_any || isp[r];
     }
     st_pred1(own_any, pbase + 8u * Sm::NCP, inv_local);
+    st_pred1(own_any, hist + 8u * kk, inv_local);
     // owner stages the pivot row, columns kk..NC-1
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
@@ -530,27 +534,43 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
     }
     __syncwarp();
     const double* prow = sm.prow[buf];
-    const double piv = prow[kk];
-    if (piv == 0.0 && sing == 0) sing = kk + 1;
     const double inv = prow[Sm::NCP];
+    double l[RPL];
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       pcol[r] = isp[r] ? kk : pcol[r];
-      pinv[r] = isp[r] ? inv : pinv[r];
       done[r] = done[r] || isp[r];
-      const double l = a[r][kk] * (isp[r] ? 0.0 : inv);
+      l[r] = a[r][kk] * (isp[r] ? 0.0 : inv);
+    }
+    if (kk + 1 < NS) {
 #pragma unroll
-      for (int j = kk + 1; j < NC; ++j) a[r][j] = fma(-l, prow[j], a[r][j]);
+      for (int r = 0; r < RPL; ++r) a[r][kk + 1] = fma(-l[r], prow[kk + 1], a[r][kk + 1]);
+      search(kk + 1);
+    }
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+#pragma unroll
+      for (int j = 0; j < NC; ++j)
+        if (j > kk + 1 || (j == kk + 1 && kk + 1 >= NS)) a[r][j] = fma(-l[r], prow[j], a[r][j]);
     }
   }
 
   // ---- solution x_{pcol} = rhs / pivot; stage the n weights (approx.py:282) ----
+  // a zero pivot leaves a non-finite reciprocal in the history: dgesv's singular case
+  __syncwarp();
+  int sing = 0;
+  if (s == 0) {
+#pragma unroll
+    for (int kk = NS - 1; kk >= 0; --kk)
+      if (!isfinite(sm.inv_hist[kk])) sing = kk + 1;
+  }
   const double s2 = s1 * s1;
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
     if (lane_live && pcol[r] >= 0 && pcol[r] < NST) {
+      const double pi = sm.inv_hist[pcol[r]];
 #pragma unroll
-      for (int o = 0; o < NOPS; ++o) sm.w[pcol[r]][o] = a[r][NS + o] * pinv[r];
+      for (int o = 0; o < NOPS; ++o) sm.w[pcol[r]][o] = a[r][NS + o] * pi;
     }
   }
   int sflag = sing;
