@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--phase", default=None, choices=["weights", "steps"],
+                    help="config 4 has both: weight computation (default) or the Boussinesq steps")
     return ap.parse_args()
 
 
@@ -396,19 +398,58 @@ def cpu_model():
 
 
 # ----------------------------------------------------------------------------- config 3: time steps
+def _stepper(hn, ns, factorize, Ra, seed=3):
+    dim = ns.dim
+    settings = hn.PoissonSolveSettings()
+    ops = hn.build_operators(ns, {"wall:x-"}, settings, interior_rbf_n=20 if dim == 3 else None, factorize=factorize)
+    dt = hn.TimeControls.from_spacing(float(np.min(ns.spacing)), 1.0, Ra=Ra).dt
+    T0 = (ns.positions[:, 0] - 0.5) + 1e-3 * np.random.default_rng(seed).normal(size=len(ns))
+    st = hn.FieldState(np.zeros((len(ns), dim)), np.zeros(len(ns)), T0)
+    hn.apply_temperature_bc(st.temperature, ops)
+    return hn.DeviceStepper(ops, hn.PhysicsParams(Ra, 0.71), settings, dt, st), ops, dt
+
+
+def _explicit_roofline(L, stepper, ns, steps, flush):
+    """The HBM-bound explicit part (K7 + K8 + K10 + K11) timed alone, L2 flushed per step."""
+    t = L.torch()
+    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        stepper.explicit_step()
+    ts = []
+    for _ in range(max(10, min(steps, 50))):
+        flush.fill_(5.0)
+        e0.record()
+        stepper.explicit_step()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    d, n = ns.dim, len(ns)
+    S = int(sum(b.K * b.width for b in stepper.ops._table.bins))
+    nbytes = S * (28 + 24 * d) + 40 * n * (d + 1)
+    peak = load_peaks().get("hbm_gbs", 6526.8)
+    return {"kernels": "momentum_kernel + div_rhs_kernel + correct_temp_kernel + temperature BC", "ms": ms,
+            "node_updates_per_s": n / (ms * 1e-3), "bytes": nbytes,
+            "bytes_formula": "S(28+24d) + 40N(d+1) (SURVEY §8(d))", "achieved_gbs": nbytes / (ms * 1e-3) / 1e9,
+            "peak_gbs": peak, "frac": nbytes / (ms * 1e-3) / 1e9 / peak}
+
+
 def run_steps_bench(args, rank, world):
+    """Config 3 (2D, full N, reference pressure treatment) -> node-updates/s of full steps.
+    Config 4 (3D): full steps (with the reference's SuperLU pressure) at a reduced-N twin of
+    the same generator -- SuperLU at N = 1e6 is infeasible -- plus the explicit
+    part at the full N = 1.02e6."""
     import paper_2303_01760_b200 as hn
-    from paper_2303_01760_b200 import _lib as L
+    from paper_2303_01760_b200 import _lib as L, nodesets
     t = L.torch()
     counter = LaunchCounter(L)
-    ns = build_nodeset(3, shard_seed(0, rank) if world > 1 else 0)
-    settings = hn.PoissonSolveSettings()
-    ops = hn.build_operators(ns, {"wall:x-"}, settings)
-    dt = hn.TimeControls.from_spacing(float(np.min(ns.spacing)), 1.0, Ra=1e6).dt
-    T0 = (ns.positions[:, 0] - 0.5) + 1e-3 * np.random.default_rng(3).normal(size=len(ns))
-    st = hn.FieldState(np.zeros((len(ns), 2)), np.zeros(len(ns)), T0)
-    hn.apply_temperature_bc(st.temperature, ops)
-    stepper = hn.DeviceStepper(ops, hn.PhysicsParams(1e6, 0.71), settings, dt, st)
+    flush = L.empty(L2_FLUSH_BYTES // 8, t.float64)
+    off = shard_seed(0, rank) if world > 1 else 0
+    if args.config == 3:
+        ns, Ra = build_nodeset(3, off), 1e6
+    else:
+        ns, Ra = nodesets.hybrid_sphere_3d(24, seed=4 + off, refine=2.8), 1e5
+    stepper, ops, dt = _stepper(hn, ns, True, Ra)
     for _ in range(args.warmup):
         stepper.step()
     t.cuda.synchronize()
@@ -424,12 +465,22 @@ def run_steps_bench(args, rank, world):
     counter.enabled = False
     stepper.check_finite(args.steps)
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
-    return {"metric": "node-updates/sec per step", "value": world * len(ns) / (ms * 1e-3), "unit": "node-updates/s",
+    explicit = _explicit_roofline(L, stepper, ns, args.steps, flush)
+    line = {"metric": "node-updates/sec per step", "value": world * len(ns) / (ms * 1e-3), "unit": "node-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": config_name(3, ns), "N": len(ns), "dt": dt,
-                       "pressure": "LU-preconditioned BiCGStab (SuperLU factors in HBM, sync-free trisolves)"},
+            "config": {"workload": config_name(args.config, ns), "N": len(ns), "dt": dt, "Ra": Ra,
+                       "pressure": "LU-preconditioned BiCGStab (SuperLU factors in HBM, supernodal sync-free "
+                                   "trisolves)"},
+            "explicit": explicit,
             "gpu_launches": counter.count // max(1, args.steps), "clocks": clocks.summary()}
+    if args.config == 4:
+        big = build_nodeset(4, off)
+        st_big, _, _ = _stepper(hn, big, False, Ra)
+        line["explicit_full_N"] = dict(_explicit_roofline(L, st_big, big, args.steps, flush), N=len(big))
+        line["config"]["note"] = ("full steps at a reduced-N twin (hybrid_sphere_3d(24)); the explicit part "
+                                  "also at the full N=%d" % len(big))
+    return line
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -469,10 +520,12 @@ def main():
     args = parse()
     if args.steps is None:
         args.steps = 50 if args.config == 3 else (3 if args.impl == "reference" else 200)
+    if args.phase is None:
+        args.phase = "steps" if args.config == 3 else "weights"
     rank, world = dist_init(args.gpus)
     if args.impl == "reference":
         line = run_reference(args, rank, world)
-    elif args.config == 3:
+    elif args.phase == "steps" and args.config in (3, 4):
         line = run_steps_bench(args, rank, world)
     else:
         line = run_weights_bench(args, rank, world)

@@ -152,10 +152,40 @@ def jittered_box(M: int = 315, seed: int = 1, jitter: float = 0.35, dim: int = 2
     return ns
 
 
-def _graded_band(rng, M, dim, center, radius, band, refine, jitter, regular_keys_mask_fn):
+def _separation_thin(pts, rad, rng):
+    """Random-priority maximal independent set of the conflict graph |p_i - p_j| <
+    max(rad_i, rad_j) (Luby rounds, vectorised): every kept pair is >= its radius apart and
+    every dropped candidate has a kept neighbour inside its radius (Poisson-disk quality)."""
+    from scipy.spatial import cKDTree
+    n = len(pts)
+    if n == 0:
+        return np.zeros(0, bool)
+    pairs = cKDTree(pts).query_pairs(float(rad.max()), output_type="ndarray")
+    if len(pairs):
+        d = np.linalg.norm(pts[pairs[:, 0]] - pts[pairs[:, 1]], axis=1)
+        pairs = pairs[d < np.maximum(rad[pairs[:, 0]], rad[pairs[:, 1]])]
+    a = np.concatenate([pairs[:, 0], pairs[:, 1]]) if len(pairs) else np.zeros(0, np.int64)
+    b = np.concatenate([pairs[:, 1], pairs[:, 0]]) if len(pairs) else np.zeros(0, np.int64)
+    prio = rng.permutation(n)
+    state = np.zeros(n, np.int8)  # 0 open, 1 kept, -1 dropped
+    while (state == 0).any():
+        live = (state[a] == 0) & (state[b] == 0)
+        aa, bb = a[live], b[live]
+        top = np.full(n, -1, dtype=prio.dtype)
+        np.maximum.at(top, aa, prio[bb])
+        win = (state == 0) & (prio > top)
+        state[win] = 1
+        state[bb[win[aa]]] = -1
+    return state == 1
+
+
+def _graded_band(rng, M, dim, center, radius, band, refine, jitter, regular_keys_mask_fn, separation=0.7):
     """Jittered fine lattice (spacing h/refine) inside the band around a round obstacle,
     thinned to a target spacing growing linearly from h/refine at the surface to h at the
-    band edge; candidates too close to the surface or to a kept regular node are dropped."""
+    band edge; candidates too close to the surface or to a kept regular node are dropped.
+    Thinning keeps every pair >= separation * target apart (_separation_thin): random
+    Bernoulli thinning leaves near-coincident pairs whose RBF-FD Laplacian rows carry
+    growing modes under the explicit step (config 3 diverged at step 35 on that set)."""
     h = 1.0 / M
     hf = h / refine
     Mf = int(np.floor(1.0 / hf))
@@ -167,16 +197,16 @@ def _graded_band(rng, M, dim, center, radius, band, refine, jitter, regular_keys
     pts = fk * hf + rng.uniform(-jitter * hf, jitter * hf, fk.shape)
     dist = np.linalg.norm(pts - np.asarray(center), axis=1) - radius
     target = hf + (h - hf) * np.clip(dist / band, 0.0, 1.0)
-    keep_p = (hf / target) ** dim
-    u = rng.random(len(pts))
-    keep = (dist > 0.5 * hf) & (dist < band) & (u < keep_p)
+    keep = (dist > 0.5 * hf) & (dist < band)
     pts, target = pts[keep], target[keep]
     # stay >= 0.5*target away from the nearest lattice node if that node is regular
     near = np.rint(pts / h).astype(np.int64)
     dnear = np.linalg.norm(pts - near * h, axis=1)
     is_reg = regular_keys_mask_fn(near)
     ok = ~(is_reg & (dnear < 0.5 * target))
-    return pts[ok], target[ok]
+    pts, target = pts[ok], target[ok]
+    sel = _separation_thin(pts, separation * target, rng)
+    return pts[sel], target[sel]
 
 
 def hybrid_hole_2d(M: int = 500, seed: int = 2, radius: float = 0.2, band: float = 0.08,

@@ -272,7 +272,7 @@ class OperatorSet:
         ops = list(self._table.ops)
         self._lap_plane = ops.index(lap.kind)
         self._d_planes = [ops.index(p.kind) for p in partials]
-        self._d_poisson = DeviceCSR(poisson_matrix)
+        self._d_poisson = DeviceCSR(poisson_matrix) if poisson_matrix is not None else None
         self._d_lu = _DeviceLU(lu) if lu is not None else None
         self._d_dir_idx = L.to_device(self.dirichlet_idx.astype(np.int32))
         self.dirichlet_values = nodeset.bc_value[self.dirichlet_idx]
@@ -321,12 +321,15 @@ def _table_to_csr(table, key, n: int) -> sparse.csr_matrix:
 
 
 def build_operators(nodeset, cold_origins: set, settings: PoissonSolveSettings,
-                    timings: dict | None = None, boundary_override=None, interior_rbf_n: int | None = None) -> OperatorSet:
+                    timings: dict | None = None, boundary_override=None, interior_rbf_n: int | None = None,
+                    factorize: bool = True) -> OperatorSet:
     """Weights on the GPU, one-time host assembly + SuperLU, factors to HBM (solver.py:133-232).
 
     Extensions: `boundary_override=(rows, stencils)` pins chosen boundary-gradient
     stencils (SURVEY §8(a) A5 tie rows); `interior_rbf_n` sets the interior RBF-FD stencil
-    size while the boundary tables keep RBF_SIZE (config 4: n = 20 inside, 30 at walls, H9)."""
+    size while the boundary tables keep RBF_SIZE (config 4: n = 20 inside, 30 at walls, H9);
+    `factorize=False` skips the bordered Poisson matrix and its LU (explicit kernels only,
+    e.g. config 4 at N = 1e6 where the reference's SuperLU treatment is infeasible, H8)."""
     timings = timings if timings is not None else {}
     dim = nodeset.dim
     n = len(nodeset)
@@ -357,21 +360,23 @@ def build_operators(nodeset, cold_origins: set, settings: PoissonSolveSettings,
         gauge = int(cand[np.argmin(np.linalg.norm(nodeset.positions[cand] - centroid, axis=1))])
     else:
         gauge = int(settings.gauge)
-    grad_full = [p.matrix + g for p, g in zip(partials, grad_rows)]
-    div_grad = sum(p.matrix @ g for p, g in zip(partials, grad_full))
-    beta = settings.stabilization
-    blended = (1.0 - beta) * div_grad + beta * lap.matrix
-    core = (sparse.diags(interior.astype(float)) @ blended
-            + sparse.diags(nodeset.boundary_mask.astype(float)) @ normal_matrix).tocsr()
-    core.eliminate_zeros()
-    core = core.tocoo()
-    n_int = int(interior.sum())
-    rows = np.concatenate([core.row, np.nonzero(interior)[0], [n]])
-    cols = np.concatenate([core.col, np.full(n_int, n), [gauge]])
-    data = np.concatenate([core.data, np.ones(n_int), [1.0]])
-    poisson = sparse.csr_matrix((data, (rows, cols)), shape=(n + 1, n + 1))
-    lu = spla.splu(poisson.tocsc())
-    precond = spla.LinearOperator(poisson.shape, lu.solve)
+    poisson = precond = lu = None
+    if factorize:
+        grad_full = [p.matrix + g for p, g in zip(partials, grad_rows)]
+        div_grad = sum(p.matrix @ g for p, g in zip(partials, grad_full))
+        beta = settings.stabilization
+        blended = (1.0 - beta) * div_grad + beta * lap.matrix
+        core = (sparse.diags(interior.astype(float)) @ blended
+                + sparse.diags(nodeset.boundary_mask.astype(float)) @ normal_matrix).tocsr()
+        core.eliminate_zeros()
+        core = core.tocoo()
+        n_int = int(interior.sum())
+        rows = np.concatenate([core.row, np.nonzero(interior)[0], [n]])
+        cols = np.concatenate([core.col, np.full(n_int, n), [gauge]])
+        data = np.concatenate([core.data, np.ones(n_int), [1.0]])
+        poisson = sparse.csr_matrix((data, (rows, cols)), shape=(n + 1, n + 1))
+        lu = spla.splu(poisson.tocsc())
+        precond = spla.LinearOperator(poisson.shape, lu.solve)
 
     neumann_rows = neumann_lu = neumann_diag = None
     if len(neumann_idx):
@@ -528,6 +533,8 @@ class _BiCGStab:
 
 
 def _pressure_dev(ops: OperatorSet, rhs, x0, settings: PoissonSolveSettings, solver: _BiCGStab):
+    if ops._d_poisson is None or ops._d_lu is None:
+        raise RuntimeError("operators were built with factorize=False: no pressure solve available")
     x, info = solver.solve(rhs, x0, settings.tol, settings.maxiter)
     if info != 0:
         tt = L.torch()
@@ -687,6 +694,17 @@ class DeviceStepper:
         self.v, self.v_next = self.v_next, self.v
         self.T, self.T_next = self.T_next, self.T
         self.steps += 1
+
+    def explicit_step(self):
+        """The explicit part of a step only (K7, K8, K10, K11) with the pressure held at its
+        current value -- for measuring the HBM-bound kernels in isolation (bench)."""
+        ops = self.ops
+        _momentum_dev(ops, self.params, self.dt, self.v, self.T, self.vstar, zero_boundary=True)
+        _div_rhs_dev(ops, self.vstar, self.dt, self.rhs)
+        _correct_temp_dev(ops, self.vstar, self.p, self.T, self.dt, self.v_next, self.T_next, self.flags)
+        _temperature_bc_dev(ops, self.T_next)
+        self.v, self.v_next = self.v_next, self.v
+        self.T, self.T_next = self.T_next, self.T
 
     def check_finite(self, step: int):
         f = self.flags.cpu().numpy()
