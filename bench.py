@@ -302,6 +302,7 @@ def run_weights_bench(args, rank, world):
                         ns.lattice_idx)
         flush.fill_(4.0)
         t.cuda.synchronize()
+        b0 = dict(L.TRAFFIC)
         t0 = time.perf_counter()
         table = hn.compute_weights(fresh, ops, rbf_n=rbf_n) if rbf_n else hn.compute_weights(fresh, ops)
         idx = table.indices
@@ -309,9 +310,8 @@ def run_weights_bench(args, rank, world):
         t.cuda.synchronize()
         if k >= args.warmup:
             e2e_t.append(time.perf_counter() - t0)
-        h2d = ns.positions.size * 8 // dim * (2 if dim == 2 else 4) + ns.kind.nbytes + \
-            (ns.lattice.grid.size * 4 + ns.lattice_idx.size * 4 if ns.lattice is not None else 0)
-        d2h = sum(b.K * b.width * (4 + 8 * len(ops)) for b in dev.bins) + len(ns)
+        # bytes the call moved (package counters: every H2D upload and the result D2H)
+        h2d, d2h = L.TRAFFIC["h2d"] - b0["h2d"], L.TRAFFIC["d2h"] - b0["d2h"]
     e2e_s = max_over_ranks(float(np.mean(e2e_t)), world)
 
     line = {

@@ -41,8 +41,17 @@ class DeviceNodes:
         if self.dim not in (2, 3):
             raise ValueError("node sets must be 2D or 3D")
         self.stride = _pos_stride(self.dim)
-        self.pos = L.to_device(pad_positions(pos))
-        self.kind = L.to_device(np.asarray(nodeset.kind, dtype=np.int8))
+        # raw host arrays go up as they are (pinned DMA); padding, dtype narrowing and the
+        # bounding box / mean scattered spacing are computed on the device, with one small
+        # read-back -- the host-side numpy passes cost ~25 ms at N = 1e6
+        kind_h = np.asarray(nodeset.kind, dtype=np.int8)
+        raw = L.to_device(pos)
+        if self.stride == self.dim:
+            self.pos = raw
+        else:
+            self.pos = L.zeros((self.n, self.stride), t.float64)
+            self.pos[:, : self.dim] = raw
+        self.kind = L.to_device(kind_h)
         self.lattice_grid = self.lattice_idx = None
         self.grid_dims = None
         lat = getattr(nodeset, "lattice", None)
@@ -50,14 +59,25 @@ class DeviceNodes:
         if lat is not None and lidx is not None:
             grid = np.asarray(lat.grid)
             self.grid_dims = list(grid.shape)
-            self.lattice_grid = L.to_device(grid.astype(np.int32))
-            li = np.asarray(lidx)
-            li32 = np.where(li == np.iinfo(np.int64).min, INT32_MIN, li).astype(np.int32)
-            self.lattice_idx = L.to_device(li32)
+            self.lattice_grid = L.to_device(grid).to(t.int32)
+            li = L.to_device(np.asarray(lidx))
+            if li.dtype == t.int64:
+                li = t.where(li == np.iinfo(np.int64).min, INT32_MIN, li)
+            self.lattice_idx = li.to(t.int32).contiguous()
+        spacing = getattr(nodeset, "spacing", None)
+        scattered = self.kind == 1
+        if self.n:
+            stats = [raw.amin(0), raw.amax(0)]
+            if spacing is not None:
+                sp = L.to_device(np.asarray(spacing, dtype=float))
+                cnt = scattered.sum()
+                stats.append(t.stack([t.where(scattered, sp, 0.0).sum(), cnt.to(t.float64)]))
+            st = t.cat(stats).cpu().numpy()
+            lo, hi = st[: self.dim], st[self.dim: 2 * self.dim]
+            mean_h = st[2 * self.dim] / st[2 * self.dim + 1] if spacing is not None and st[-1] > 0 else None
+        else:
+            lo, hi, mean_h = np.zeros(self.dim), np.ones(self.dim), None
         # uniform cell list: ~1 node per cell in 2D, ~2 in 3D
-        # per-column reductions: numpy's axis-0 reduce over an (N, d) array is ~15x slower
-        lo = np.array([pos[:, a].min() for a in range(self.dim)]) if self.n else np.zeros(self.dim)
-        hi = np.array([pos[:, a].max() for a in range(self.dim)]) if self.n else np.ones(self.dim)
         self.lo, self.hi = lo.astype(float), hi.astype(float)
         ext = np.maximum(hi - lo, 1e-300)
         vol = float(np.prod(ext))
@@ -70,11 +90,8 @@ class DeviceNodes:
         self.cell_start, self.cell_items, self.cell_pos = g.start, g.items, g.pos
         # graded sets: queries on the finest nodes get a grid sized to their own spacing
         self.fine_cell = None
-        kind = np.asarray(nodeset.kind)
-        spacing = getattr(nodeset, "spacing", None)
-        if spacing is not None and np.any(kind == 1):
-            hs = float(np.mean(np.asarray(spacing)[kind == 1]))
-            fine = hs * (1.0 if self.dim == 2 else 1.25)
+        if mean_h is not None:
+            fine = float(mean_h) * (1.0 if self.dim == 2 else 1.25)
             if fine < 0.7 * self.cell:
                 self.fine_cell = fine
 
@@ -235,9 +252,12 @@ class DeviceTable:
             s[b.rows_host] = b.width
         return s
 
-    def host_arrays(self):
-        """(indices (N, n_max) int64 -1 padded, sizes, {op: (N, n_max)}) -- the WeightTable
-        layout, produced on the device (hn_ell_to_table) and copied once into pinned memory."""
+    def start_host_copy(self):
+        """Enqueue the WeightTable layout (hn_ell_to_table) and its D2H into pinned memory on
+        the current stream, without waiting: compute_weights issues this before its one
+        synchronising read (the singular flags), so the copy rides on that sync."""
+        if getattr(self, "_pending", None) is not None or getattr(self, "_pinned", None) is not None:
+            return
         t = L.torch()
         n, m, nops = self.n, self.n_max, len(self.ops)
         d_idx = L.empty((max(n, 1), m), t.int64)
@@ -253,8 +273,27 @@ class DeviceTable:
         h_idx.copy_(d_idx, non_blocking=True)
         h_sizes.copy_(d_sizes, non_blocking=True)
         h_w.copy_(d_w, non_blocking=True)
-        t.cuda.current_stream().synchronize()
-        self._pinned = (h_idx, h_sizes, h_w)  # numpy views below keep these alive via this table
+        h_m = None
+        if self._method is not None and hasattr(self._method, "is_cuda"):
+            h_m = t.empty(self._method.shape, dtype=self._method.dtype, pin_memory=True)
+            h_m.copy_(self._method, non_blocking=True)
+        L.TRAFFIC["d2h"] += h_idx.nbytes + h_sizes.nbytes + h_w.nbytes + (h_m.nbytes if h_m is not None else 0)
+        self._pending = (h_idx, h_sizes, h_w, h_m, (d_idx, d_sizes, d_w))
+
+    def host_arrays(self):
+        """(indices (N, n_max) int64 -1 padded, sizes, {op: (N, n_max)}) -- the WeightTable
+        layout, produced on the device (hn_ell_to_table) and copied once into pinned memory."""
+        t = L.torch()
+        self.start_host_copy()
+        if self._pending is not None:
+            t.cuda.current_stream().synchronize()
+            h_idx, h_sizes, h_w, h_m, _ = self._pending
+            self._pending = None
+            self._pinned = (h_idx, h_sizes, h_w)  # numpy views below keep these alive via this table
+            if h_m is not None:
+                self._method = h_m.numpy().astype(np.int8)
+        h_idx, h_sizes, h_w = self._pinned
+        n = self.n
         w_np = h_w.numpy()
         weights = {op: w_np[j, :n] for j, op in enumerate(self.ops)}
         return h_idx.numpy()[:n], h_sizes.numpy()[:n], weights

@@ -146,11 +146,23 @@ def host_ptrs(tensors) -> C.Array:
     return (_vp * max(1, len(tensors)))(*[t.data_ptr() if t is not None else 0 for t in tensors])
 
 
+# host<->device bytes moved by this package (bench.py reports the per-call deltas as e2e traffic)
+TRAFFIC = {"h2d": 0, "d2h": 0}
+
+
 def to_device(a: np.ndarray, dtype=None):
     """Copy a host array to the current device (pinned staging for large arrays)."""
     t = torch()
     arr = np.ascontiguousarray(a if dtype is None else a.astype(dtype, copy=False))
-    return t.from_numpy(arr).to(device(), non_blocking=False)
+    TRAFFIC["h2d"] += arr.nbytes
+    src = t.from_numpy(arr)
+    if arr.nbytes < (64 << 10):
+        return src.to(device(), non_blocking=False)
+    # pinned staging (torch's caching host allocator keeps the block until the copy's
+    # event completes), then an async DMA: no pageable bounce through the driver
+    stage = t.empty(src.shape, dtype=src.dtype, pin_memory=True)
+    stage.copy_(src)
+    return stage.to(device(), non_blocking=True)
 
 
 def empty(shape, dtype):

@@ -23,7 +23,7 @@ import numpy as np
 from . import _lib as L
 from ._device import Bin, DeviceTable, device_nodes
 from .errors import SingularSystemError
-from .nodegen import KIND_REGULAR, LATTICE_NONE
+from .nodegen import KIND_BOUNDARY, KIND_REGULAR, LATTICE_NONE
 
 MON_SIZE = {2: 5, 3: 7}
 RBF_SIZE = {2: 12, 3: 30}  # read at call time, like the reference (approx.py:25, 388, 420)
@@ -371,7 +371,7 @@ def classify_methods(nodeset, tree=None) -> np.ndarray:
     return method
 
 
-def _interior_device_table(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
+def _interior_device_table(nodeset, ops, n_rbf: int | None = None, host_copy: bool = False) -> DeviceTable:
     """classify -> device partition [MON | RBF | NONE] -> stencils -> solves, all in HBM;
     one 12-byte read-back (the class sizes) and one deferred singular check."""
     dim = nodeset.dim
@@ -389,7 +389,14 @@ def _interior_device_table(nodeset, ops, n_rbf: int | None = None) -> DeviceTabl
     scratch = L.empty(3 * (n // 256 + 1) + 1, t.int32)
     L.call("hn_partition_methods", L.ptr(method_d), n, L.ptr(rows_d), L.ptr(counts_d), L.ptr(scratch),
            L.stream_handle())
-    k_mon, k_rbf, k_none = (int(v) for v in counts_d.cpu().numpy())
+    kind = np.asarray(nodeset.kind)
+    if not np.any(kind == KIND_REGULAR):
+        # no regular node: every interior node is RBF-FD (approx.py:346-350), so the class
+        # sizes are known here and the device partition runs without a read-back
+        k_rbf = int(np.count_nonzero(kind != KIND_BOUNDARY))
+        k_mon, k_none = 0, n - k_rbf
+    else:
+        k_mon, k_rbf, k_none = (int(v) for v in counts_d.cpu().numpy())
     bins, pending = [], []
     if k_mon:
         d_rows = rows_d[:k_mon]
@@ -400,13 +407,16 @@ def _interior_device_table(nodeset, ops, n_rbf: int | None = None) -> DeviceTabl
             raise ValueError(f"stencil size {n_rbf} exceeds node count {n}")
         d_rows = rows_d[k_mon:k_mon + k_rbf]
         pending.append(_solve_bin(dn, dn.knn(n_rbf, rows=d_rows, fine=True), d_rows, ops, False))
-    _check_info(pending)
     bins = [b for b, _ in pending]
     if k_none:
         d_rows = rows_d[k_mon + k_rbf:n]
         bins.append(Bin(None, 0, L.empty((0, k_none), t.int32), L.empty((len(ops), 0, k_none), t.float64),
                         d_rows=d_rows, K=k_none))
-    return DeviceTable(n, dim, list(ops), bins, n_rbf, method_d[:n])
+    dev = DeviceTable(n, dim, list(ops), bins, n_rbf, method_d[:n])
+    if host_copy:
+        dev.start_host_copy()  # the result D2H completes under the flag read below
+    _check_info(pending)
+    return dev
 
 
 class WeightsPipeline:
@@ -521,11 +531,18 @@ def compute_weights(nodeset, ops, with_kappa: bool = False, tree=None, rbf_n: in
     """Stencils and weights for every interior node, batched per method (approx.py:379-413).
 
     `rbf_n` (extension) overrides RBF_SIZE[d] for this call, as the reference allows by
-    rebinding its module constant."""
+    rebinding its module constant.  The host arrays are copied back under the
+    call's one synchronisation; operator assembly (solver.build_operators) uses
+    _compute_weights(host_copy=False) and keeps the table in HBM."""
+    return _compute_weights(nodeset, ops, with_kappa, rbf_n, host_copy=True)
+
+
+def _compute_weights(nodeset, ops, with_kappa: bool = False, rbf_n: int | None = None,
+                     host_copy: bool = False) -> WeightTable:
     ops = list(ops)
     for op in ops:
         _op_code(op, nodeset.dim)
-    dev = _interior_device_table(nodeset, ops, rbf_n)
+    dev = _interior_device_table(nodeset, ops, rbf_n, host_copy=host_copy)
     table = WeightTable(_device=dev)
     if with_kappa:
         kappa = np.full(len(nodeset), np.nan)

@@ -32,6 +32,25 @@ constexpr int kWarp = 32;
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Stream-ordered scratch from the device's default pool.  The pool's release threshold is
+// raised once per device so freed scratch stays cached: with the default threshold 0 every
+// synchronize hands it back to the driver and the next cudaMallocAsync costs ~100-250 us.
+inline cudaError_t stream_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static bool kept[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 0 && dev < 64 && !kept[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    kept[dev] = true;
+  }
+  return cudaMallocAsync(p, bytes, s);
+}
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Number of SMs on the current device (cached per process).

@@ -162,7 +162,7 @@ __global__ void scan_tiles_apply(const int* __restrict__ in, int64_t n, const in
 int exclusive_scan(const int* in, int64_t n, int* out, cudaStream_t s) {
   int64_t ntiles = ceil_div(n, kScanTile);
   int* tiles = nullptr;
-  HN_TRY(cudaMallocAsync(&tiles, sizeof(int) * (ntiles + 1), s));
+  HN_TRY(stream_alloc(reinterpret_cast<void**>(&tiles), sizeof(int) * (ntiles + 1), s));
   scan_tile_sums<<<ntiles, kScanThreads, 0, s>>>(in, n, tiles);
   scan_tiles_serial<<<1, 1024, 0, s>>>(tiles, ntiles);
   scan_tiles_apply<<<ntiles, kScanThreads, 0, s>>>(in, n, tiles, out);
@@ -561,7 +561,7 @@ HN_EXPORT int hn_partition_methods(const int8_t* method, int64_t n, int* rows_ou
   const int64_t ntiles = ceil_div(n, kPartThreads);
   int* tile_counts = scratch;                       // 3*ntiles
   int* tile_off = nullptr;
-  HN_TRY(cudaMallocAsync(&tile_off, sizeof(int) * (3 * ntiles + 1), s));
+  HN_TRY(stream_alloc(reinterpret_cast<void**>(&tile_off), sizeof(int) * (3 * ntiles + 1), s));
   partition_count_kernel<<<ntiles, kPartThreads, 0, s>>>(method, n, tile_counts, ntiles);
   int rc = exclusive_scan(tile_counts, 3 * ntiles, tile_off, s);
   if (rc == 0) {

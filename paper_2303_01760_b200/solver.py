@@ -29,7 +29,7 @@ from scipy.sparse import linalg as spla
 
 from . import _lib as L
 from ._device import bins_args
-from .approx import (Laplacian, Partial, boundary_partial_table, compute_weights,
+from .approx import (Laplacian, Partial, _compute_weights, boundary_partial_table, compute_weights,
                      normal_derivative_table)
 from .errors import PoissonConvergenceError, SolverDivergenceError
 from .nodegen import ROLE_DIRICHLET, ROLE_NEUMANN
@@ -339,7 +339,7 @@ def build_operators(nodeset, cold_origins: set, settings: PoissonSolveSettings,
     cold_idx = np.array([i for i in boundary_idx if nodeset.origin[i] in cold_origins], dtype=np.int64)
 
     t0 = time.perf_counter()
-    table = compute_weights(nodeset, ops_wanted, rbf_n=interior_rbf_n)
+    table = _compute_weights(nodeset, ops_wanted, rbf_n=interior_rbf_n)
     boundary_grad = boundary_partial_table(nodeset, boundary_idx, exclude=nodeset.boundary_mask,
                                            stencil_override=boundary_override)
     nu_table = normal_derivative_table(nodeset, cold_idx) if len(cold_idx) else None
