@@ -318,7 +318,7 @@ struct __align__(16) RbfSmem {  // 16 B: every system's prow takes v2.f64 stores
   static constexpr int NS = NST + NQ;
   static constexpr int NC = NS + NOPS;
   static constexpr int NCP = (NC + 1) & ~1;  // even length keeps every pair 16 B aligned
-  double prow[2][NCP + 2];                      // double-buffered pivot row; [NCP] = 1/pivot
+  double prow[2][NCP + 2];                      // double-buffered pivot row (16 B aligned pairs)
   double inv_hist[NS + (NS & 1)];               // 1/pivot of every step
   double y[NST][D];
   double w[NST][NOPS];
@@ -338,15 +338,16 @@ __device__ __forceinline__ void st_pred1(bool p, unsigned addr, double x) {
                :: "r"(static_cast<int>(p)), "r"(addr), "d"(x) : "memory");
 }
 
-// r^3 from r^2: MUFU rsqrt seed + two Newton steps (~1 ulp), exact 0 at r^2 = 0
+// r^3 from r^2: MUFU rsqrt seed + two Newton steps (~1 ulp), exact 0 at r^2 = 0 (the
+// clamp keeps rsqrt finite there: r = 1e-300 * 1e150, and d2 * r = 0 with no select)
 __device__ __forceinline__ double cube_from_sq(double d2) {
+  const double q = fmax(d2, 1e-300);
   double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d2));
-  const double h = 0.5 * d2;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+  const double h = 0.5 * q;
   y = y * fma(-h * y, y, 1.5);
   y = y * fma(-h * y, y, 1.5);
-  const double r = d2 * y;
-  return d2 > 0.0 ? d2 * r : 0.0;
+  return d2 * (q * y);
 }
 
 template <int D, int NST, int NOPS, int LPS, int RPL, int WARPS, int MINB>
@@ -469,14 +470,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
   // Step kk: select + stage pivot row kk, update column kk+1 first, start the pivot
   // search of step kk+1 (shuffle chain + speculative reciprocal), then the bulk update
   // runs while that search is in flight.
-  unsigned tag[RPL];
-  bool done[RPL];
+  // vm[r] = 0x7fffffc0 | tag while row r is live, 0 once it has pivoted: the search key of
+  // a row is then one LOP3, (hi(a) | 63) & vm = (|a| top bits | tag) or 0 (no predicates)
+  unsigned vm[RPL];
   int pcol[RPL];
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
     const int i = s + r * LPS;
-    tag[r] = static_cast<unsigned>(63 - i);
-    done[r] = !lane_live || i >= NS;
+    vm[r] = (!lane_live || i >= NS) ? 0u : (0x7fffffc0u | static_cast<unsigned>(63 - i));
     pcol[r] = -1;
   }
   const unsigned pbase0 = smem_addr(&sm.prow[0][0]);
@@ -484,17 +485,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
   const unsigned hist = smem_addr(&sm.inv_hist[0]);
 
   unsigned key = 0;
-  double cand = 1.0;
-  auto search = [&](int col) {  // local candidate of column col, then the segmented max
+  auto search = [&](int col) {  // local key of column col, then the segmented max
     key = 0;
-    cand = 1.0;
 #pragma unroll
-    for (int r = 0; r < RPL; ++r) {
-      const unsigned hi = (static_cast<unsigned>(__double2hiint(a[r][col])) & 0x7fffffc0u) | tag[r];
-      const unsigned kr = done[r] ? 0u : hi;
-      cand = kr > key ? a[r][col] : cand;
-      key = max(key, kr);
-    }
+    for (int r = 0; r < RPL; ++r)
+      key = max(key, (static_cast<unsigned>(__double2hiint(a[r][col])) | 63u) & vm[r]);
 #pragma unroll
     for (int off = 1; off < LPS; off <<= 1) key = max(key, __shfl_sync(0xffffffffu, key, seg_src(off)));
     key = __shfl_sync(0xffffffffu, key, lane_live ? seg_base : lane);
@@ -505,18 +500,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
   for (int kk = 0; kk < NS; ++kk) {
     const int buf = kk & 1;
     const unsigned pbase = buf ? pbase1 : pbase0;
-    const double inv_local = fast_rcp(cand);  // = 1/pivot in the owner lane
     const unsigned ptag = key & 63u;
     bool isp[RPL];
     bool own_any = false;
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
-      isp[r] = (ptag == tag[r]) && lane_live;
+      // live ptags are >= 46, so a pivoted (vm = 0) row never matches; idle lanes (which
+      // alias segment 0's shared slot) see ptag = 0 and must be excluded explicitly
+      isp[r] = ((vm[r] & 63u) == ptag) && lane_live;
       own_any = own_any || isp[r];
     }
-    st_pred1(own_any, pbase + 8u * Sm::NCP, inv_local);
-    st_pred1(own_any, hist + 8u * kk, inv_local);
-    // owner stages the pivot row, columns kk..NC-1
+    // owner stages the pivot row, columns kk..NC-1 (prow[kk] = the pivot)
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       int j = kk;
@@ -534,12 +528,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
     }
     __syncwarp();
     const double* prow = sm.prow[buf];
-    const double inv = prow[Sm::NCP];
+    const double inv = fast_rcp(prow[kk]);  // every lane: 1/pivot (NaN for a zero pivot)
+    st_pred1(own_any, hist + 8u * kk, inv);
     double l[RPL];
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       pcol[r] = isp[r] ? kk : pcol[r];
-      done[r] = done[r] || isp[r];
+      vm[r] = isp[r] ? 0u : vm[r];
       l[r] = a[r][kk] * (isp[r] ? 0.0 : inv);
     }
     if (kk + 1 < NS) {
@@ -752,6 +747,7 @@ static void launch_rbf(const double* pos, const int* st, int64_t K, const OpSpec
       case 2: launch_rbf_v<2, 12, NOPS, 9, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return;
       case 3: launch_rbf_v<2, 12, NOPS, 9, 2, 4, 4>(pos, st, K, ops, rn, oi, ow, info, s); return;
       case 4: launch_rbf_v<2, 12, NOPS, 6, 3, 2, 5>(pos, st, K, ops, rn, oi, ow, info, s); return;
+      case 5: launch_rbf_v<2, 12, NOPS, 6, 3, 1, 12>(pos, st, K, ops, rn, oi, ow, info, s); return;
       default: launch_rbf_v<2, 12, NOPS, 6, 3, 4, 3>(pos, st, K, ops, rn, oi, ow, info, s); return;
     }
   }

@@ -21,7 +21,7 @@ def main():
     ref = None
     e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
     flush = L.empty(64 * 2 ** 20, t.float64)  # 512 MB > L2
-    for v in [0, 1, 2, 3, 4]:
+    for v in [int(x) for x in (sys.argv[1].split(',') if len(sys.argv) > 1 else '0,1,2,3,4,5'.split(','))]:
         L.lib().hn_weights_rbf_set_variant(v)
         oi = L.empty((12, K), t.int32)
         ow = L.empty((3, 12, K), t.float64)
