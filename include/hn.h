@@ -54,7 +54,17 @@ int hn_knn(const double* pos, int d, const double* lo_host, double cell, const i
            const int* queries, const double* qpos, int64_t nq, int n, const uint8_t* exclude,
            int* out_idx, double* out_dist, void* stream);
 
-/* kNN kernel variant (tuning knob, identical results): 1 per cell (default), 0 batched rings. */
+/* hn_knn with a per-node nominal spacing (N fp64, indexed like the queries: node id, or
+ * query number when qpos != NULL): the box pass sizes each query's first search radius
+ * from its own spacing, which keeps graded node sets on the fast path.  Same results.
+ * Replaces: the same reference calls as hn_knn (nodeset.spacing, nodegen.py:90-179). */
+int hn_knn_spacing(const double* pos, int d, const double* lo_host, double cell, const int* dims_host,
+                   const int* cell_start, const int* cell_items, const double* cell_pos,
+                   const int* queries, const double* qpos, int64_t nq, int n, const uint8_t* exclude,
+                   const double* spacing, int* out_idx, double* out_dist, void* stream);
+
+/* kNN kernel variant (tuning knob, identical results): 0 box pass + exact ring fallback
+ * (default), 1 ring traversal only, 2/3 box pass with a smaller/larger first radius. */
 void hn_knn_set_variant(int v);
 
 /* method per node: -1 boundary, 0 MON, 1 RBF-FD.  lattice_idx (N x d int32, INT32_MIN =

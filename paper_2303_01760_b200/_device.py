@@ -66,10 +66,12 @@ class DeviceNodes:
             self.lattice_idx = li.to(t.int32).contiguous()
         spacing = getattr(nodeset, "spacing", None)
         scattered = self.kind == 1
+        self.spacing = None  # per-node nominal spacing: sizes each kNN query's first radius
         if self.n:
             stats = [raw.amin(0), raw.amax(0)]
             if spacing is not None:
                 sp = L.to_device(np.asarray(spacing, dtype=float))
+                self.spacing = sp
                 cnt = scattered.sum()
                 stats.append(t.stack([t.where(scattered, sp, 0.0).sum(), cnt.to(t.float64)]))
             st = t.cat(stats).cpu().numpy()
@@ -151,7 +153,11 @@ class DeviceNodes:
         ex = None
         if exclude is not None:
             ex = exclude if hasattr(exclude, "data_ptr") else L.to_device(np.asarray(exclude, dtype=np.uint8))
-        if nq:
+        if nq and qpos is None and self.spacing is not None:
+            L.call("hn_knn_spacing", L.ptr(self.pos), self.dim, L.host_dbls(self.lo), g.cell, L.host_ints(g.dims),
+                   L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos), L.ptr(q), None,
+                   nq, n, L.ptr(ex), L.ptr(self.spacing), L.ptr(out), L.ptr(dist), L.stream_handle())
+        elif nq:
             L.call("hn_knn", L.ptr(self.pos), self.dim, L.host_dbls(self.lo), g.cell, L.host_ints(g.dims),
                    L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos), L.ptr(q), L.ptr(qpos),
                    nq, n, L.ptr(ex), L.ptr(out), L.ptr(dist), L.stream_handle())

@@ -31,6 +31,8 @@ SIGNATURES: dict[str, tuple] = {
     "hn_bench_dmma": (_i, [_vp, _i, _i, _vp]),
     "hn_celllist_build": (_i, [_vp, _i64, _i, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hn_knn": (_i, [_vp, _i, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp, _vp, _vp, _i64, _i, _vp, _vp, _vp, _vp]),
+    "hn_knn_spacing": (_i, [_vp, _i, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp, _vp, _vp, _i64, _i, _vp, _vp, _vp, _vp,
+                            _vp]),
     "hn_classify": (_i, [_vp, _vp, _vp, _c_int_p, _i64, _i, _vp, _vp]),
     "hn_mon_stencils": (_i, [_vp, _i64, _vp, _vp, _vp, _c_int_p, _i, _vp, _vp]),
     "hn_weights_mon": (_i, [_vp, _i, _vp, _i64, _i, _c_int_p, _c_int_p, _c_dbl_p, _vp, _vp, _vp, _vp]),

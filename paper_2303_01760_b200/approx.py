@@ -481,9 +481,14 @@ class WeightsPipeline:
         if self.k_rbf:
             q = self.rows[self.k_mon:]
             g = self.gq
-            L.call("hn_knn", L.ptr(dn.pos), dim, L.host_dbls(dn.lo), g.cell, L.host_ints(g.dims),
-                   L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos), L.ptr(q), None, self.k_rbf,
-                   self.n_rbf, None, L.ptr(self.rbf_st), None, s)
+            if dn.spacing is not None:
+                L.call("hn_knn_spacing", L.ptr(dn.pos), dim, L.host_dbls(dn.lo), g.cell, L.host_ints(g.dims),
+                       L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos), L.ptr(q), None, self.k_rbf,
+                       self.n_rbf, None, L.ptr(dn.spacing), L.ptr(self.rbf_st), None, s)
+            else:
+                L.call("hn_knn", L.ptr(dn.pos), dim, L.host_dbls(dn.lo), g.cell, L.host_ints(g.dims),
+                       L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos), L.ptr(q), None, self.k_rbf,
+                       self.n_rbf, None, L.ptr(self.rbf_st), None, s)
             L.call("hn_weights_rbf", L.ptr(dn.pos), dim, L.ptr(self.rbf_st), self.k_rbf, self.n_rbf, nops, kinds,
                    axes, normals, None, None, L.ptr(self.rbf_idx), L.ptr(self.rbf_w), L.ptr(self.rbf_info), s)
 

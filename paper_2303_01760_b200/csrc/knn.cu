@@ -176,45 +176,95 @@ __device__ __forceinline__ bool key_less(double da, int ia, double db, int ib) {
   return da < db || (da == db && ia < ib);
 }
 
-template <int D, int NMAX>
-__global__ void __launch_bounds__(128) knn_kernel(Grid g, const double* __restrict__ pos,
-                                                  const int* __restrict__ cell_start,
-                                                  const int* __restrict__ cell_items,
-                                                  const double* __restrict__ cell_pos,
-                                                  const int* __restrict__ queries,
-                                                  const double* __restrict__ qpos, int64_t nq, int n,
-                                                  const uint8_t* __restrict__ exclude,
-                                                  int* __restrict__ out_idx, double* __restrict__ out_dist) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= nq) return;
-  double q[D];
-  if (qpos) {
-    load_point<D>(qpos, t, q);
-  } else {
-    const int qi = queries ? __ldg(queries + t) : static_cast<int>(t);
-    load_point<D>(pos, qi, q);
-  }
-  int c0[D];
-  cell_coords<D>(g, q, c0);
-
-  // sorted ascending; slots [0, NMAX-n) hold -inf sentinels and are never displaced
-  double kd[NMAX];
-  int ki[NMAX];
+// running top-n: sorted ascending in the last n slots of kd/ki; slots [0, NMAX-n) hold
+// -inf sentinels that are never displaced, so the network has compile-time indices
+template <int NMAX>
+__device__ __forceinline__ void topn_init(double* kd, int* ki, int n) {
 #pragma unroll
   for (int j = 0; j < NMAX; ++j) {
     const bool live = j >= NMAX - n;
     kd[j] = live ? CUDART_INF : -CUDART_INF;
     ki[j] = live ? INT_MAX : -1;
   }
-  double thr2 = CUDART_INF;  // d2 above this cannot enter the window
-  constexpr int S = pos_stride<D>();
+}
 
+// one candidate (node j at p) against the running top-n
+template <int D, int NMAX>
+__device__ __forceinline__ void topn_offer_pt(const uint8_t* __restrict__ exclude, int j, const double* p,
+                                              const double* q, double* kd, int* ki, double& thr2) {
+  if (exclude && __ldg(exclude + j)) return;
+  const double d2 = exact_dist2<D>(p, q);
+  if (d2 > thr2) return;
+  const double d = __dsqrt_rn(d2);
+  if (!key_less(d, j, kd[NMAX - 1], ki[NMAX - 1])) return;
+#pragma unroll
+  for (int m = NMAX - 1; m >= 0; --m) {
+    if (key_less(d, j, kd[m], ki[m])) {
+      const bool shift = (m > 0) && key_less(d, j, kd[m > 0 ? m - 1 : 0], ki[m > 0 ? m - 1 : 0]);
+      kd[m] = shift ? kd[m > 0 ? m - 1 : 0] : d;
+      ki[m] = shift ? ki[m > 0 ? m - 1 : 0] : j;
+    }
+  }
+  const double w = kd[NMAX - 1];
+  if (w != CUDART_INF) thr2 = fmin(thr2, __dmul_rn(__dmul_rn(w, w), 1.0 + 1e-15));
+}
+
+template <int D>
+__device__ __forceinline__ void load_cand(const double* __restrict__ cell_pos, const int* __restrict__ cell_items,
+                                          int s, int& j, double* p) {
+  constexpr int S = pos_stride<D>();
+  j = __ldg(cell_items + s);
+#pragma unroll
+  for (int a = 0; a < D; ++a) p[a] = __ldg(cell_pos + static_cast<int64_t>(s) * S + a);
+}
+
+// point s of the cell-ordered arrays against the running top-n
+template <int D, int NMAX>
+__device__ __forceinline__ void topn_offer(const double* __restrict__ cell_pos, const int* __restrict__ cell_items,
+                                           const uint8_t* __restrict__ exclude, int s, const double* q,
+                                           double* kd, int* ki, double& thr2) {
+  int j;
+  double p[D];
+  load_cand<D>(cell_pos, cell_items, s, j, p);
+  topn_offer_pt<D, NMAX>(exclude, j, p, q, kd, ki, thr2);
+}
+
+// a contiguous run [beg, end) with the next candidate's loads issued before the current
+// one is offered (the offer's compare/insert chain no longer waits on each load)
+template <int D, int NMAX>
+__device__ __forceinline__ void topn_offer_run(const double* __restrict__ cell_pos,
+                                               const int* __restrict__ cell_items,
+                                               const uint8_t* __restrict__ exclude, int beg, int end,
+                                               const double* q, double* kd, int* ki, double& thr2) {
+  if constexpr (D == 2) {  // 2D runs are short (~6 points): the extra registers cost more
+    for (int s = beg; s < end; ++s) topn_offer<D, NMAX>(cell_pos, cell_items, exclude, s, q, kd, ki, thr2);
+    return;
+  }
+  if (beg >= end) return;
+  int jn;
+  double pn[D];
+  load_cand<D>(cell_pos, cell_items, beg, jn, pn);
+  for (int s = beg; s < end; ++s) {
+    const int j = jn;
+    double p[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) p[a] = pn[a];
+    if (s + 1 < end) load_cand<D>(cell_pos, cell_items, s + 1, jn, pn);
+    topn_offer_pt<D, NMAX>(exclude, j, p, q, kd, ki, thr2);
+  }
+}
+
+// Chebyshev rings of cells around the query cell until the current n-th key is strictly
+// closer than any unscanned cell (exact for any grid, any density)
+template <int D, int NMAX>
+__device__ __forceinline__ void ring_scan(const Grid& g, const int* __restrict__ cell_start, const int* __restrict__ cell_items,
+                          const double* __restrict__ cell_pos, const uint8_t* __restrict__ exclude,
+                          const double* q, const int* c0, double* kd, int* ki) {
+  double thr2 = CUDART_INF;  // d2 above this cannot enter the window
   int max_r = 0;
 #pragma unroll
   for (int a = 0; a < D; ++a) max_r = max(max_r, max(c0[a], g.dims[a] - 1 - c0[a]));
-
   for (int R = 0; R <= max_r; ++R) {
-    // visit every cell with Chebyshev offset exactly R
     const int lo1 = -R, hi1 = R;
     for (int o0 = -R; o0 <= R; ++o0) {
       const int x = c0[0] + o0;
@@ -237,27 +287,7 @@ __global__ void __launch_bounds__(128) knn_kernel(Grid g, const double* __restri
           int64_t cl = static_cast<int64_t>(x) * g.dims[1] + y;
           if constexpr (D == 3) cl = cl * g.dims[2] + z;
           const int beg = __ldg(cell_start + cl), end = __ldg(cell_start + cl + 1);
-          for (int s = beg; s < end; ++s) {
-            const int j = __ldg(cell_items + s);
-            if (exclude && __ldg(exclude + j)) continue;
-            double p[D];
-#pragma unroll
-            for (int a = 0; a < D; ++a) p[a] = __ldg(cell_pos + static_cast<int64_t>(s) * S + a);
-            const double d2 = exact_dist2<D>(p, q);
-            if (d2 > thr2) continue;
-            const double d = __dsqrt_rn(d2);
-            if (!key_less(d, j, kd[NMAX - 1], ki[NMAX - 1])) continue;
-#pragma unroll
-            for (int m = NMAX - 1; m >= 0; --m) {
-              if (key_less(d, j, kd[m], ki[m])) {
-                const bool shift = (m > 0) && key_less(d, j, kd[m > 0 ? m - 1 : 0], ki[m > 0 ? m - 1 : 0]);
-                kd[m] = shift ? kd[m > 0 ? m - 1 : 0] : d;
-                ki[m] = shift ? ki[m > 0 ? m - 1 : 0] : j;
-              }
-            }
-            const double w = kd[NMAX - 1];
-            thr2 = (w == CUDART_INF) ? CUDART_INF : __dmul_rn(__dmul_rn(w, w), 1.0 + 1e-15);
-          }
+          for (int s = beg; s < end; ++s) topn_offer<D, NMAX>(cell_pos, cell_items, exclude, s, q, kd, ki, thr2);
         }
       }
     }
@@ -270,6 +300,22 @@ __global__ void __launch_bounds__(128) knn_kernel(Grid g, const double* __restri
     }
     if (kd[NMAX - 1] < bound - 1e-9 * g.cell) break;
   }
+}
+
+template <int D>
+__device__ __forceinline__ void load_query(const double* __restrict__ pos, const int* __restrict__ queries,
+                                           const double* __restrict__ qpos, int64_t t, double* q) {
+  if (qpos) {
+    load_point<D>(qpos, t, q);
+  } else {
+    const int qi = queries ? __ldg(queries + t) : static_cast<int>(t);
+    load_point<D>(pos, qi, q);
+  }
+}
+
+template <int NMAX>
+__device__ __forceinline__ void topn_store(const double* kd, const int* ki, int n, int64_t t, int* out_idx,
+                                           double* out_dist) {
 #pragma unroll
   for (int j = 0; j < NMAX; ++j) {
     if (j >= NMAX - n) {
@@ -280,134 +326,124 @@ __global__ void __launch_bounds__(128) knn_kernel(Grid g, const double* __restri
   }
 }
 
-// ---- kNN query v2: batched ring traversal, integer keys ------------------------------
-// Same result as knn_kernel (top n by (fl-distance, index)).  Each ring of cells is walked
-// in batches of KB cells whose [start, end) ranges are loaded together; points are then
-// taken slot-major across the batch so KB independent point loads are in flight.  The
-// top-n network compares fl-distances as uint64 bit patterns (non-negative doubles order
-// like their bits), keeping the FP64 pipe for the distance arithmetic only.
 template <int D, int NMAX>
-__global__ void __launch_bounds__(128) knn2_kernel(Grid g, const double* __restrict__ pos,
-                                                   const int* __restrict__ cell_start,
-                                                   const int* __restrict__ cell_items,
-                                                   const double* __restrict__ cell_pos,
-                                                   const int* __restrict__ queries,
-                                                   const double* __restrict__ qpos, int64_t nq, int n,
-                                                   const uint8_t* __restrict__ exclude,
-                                                   int* __restrict__ out_idx, double* __restrict__ out_dist) {
-  constexpr int KB = 8;
-  constexpr int S = pos_stride<D>();
+__global__ void __launch_bounds__(128) knn_kernel(Grid g, const double* __restrict__ pos,
+                                                  const int* __restrict__ cell_start,
+                                                  const int* __restrict__ cell_items,
+                                                  const double* __restrict__ cell_pos,
+                                                  const int* __restrict__ queries,
+                                                  const double* __restrict__ qpos, int64_t nq, int n,
+                                                  const uint8_t* __restrict__ exclude,
+                                                  int* __restrict__ out_idx, double* __restrict__ out_dist) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= nq) return;
   double q[D];
-  if (qpos) {
-    load_point<D>(qpos, t, q);
-  } else {
-    const int qi = queries ? __ldg(queries + t) : static_cast<int>(t);
-    load_point<D>(pos, qi, q);
+  load_query<D>(pos, queries, qpos, t, q);
+  int c0[D];
+  cell_coords<D>(g, q, c0);
+  double kd[NMAX];
+  int ki[NMAX];
+  topn_init<NMAX>(kd, ki, n);
+  ring_scan<D, NMAX>(g, cell_start, cell_items, cell_pos, exclude, q, c0, kd, ki);
+  topn_store<NMAX>(kd, ki, n, t, out_idx, out_dist);
+}
+
+// ---- kNN query, box pass ------------------------------------------------------------
+// Same result as knn_kernel.  First pass: every point within the axis box |p - q|_inf <=
+// r0 (r0 ~ 1.3x the expected n-th distance, from the grid's points per cell), scanned as
+// contiguous runs of cells along the grid's fastest axis (one cell_start pair per run
+// instead of per cell) in rows ordered outward from the query, with only d <= r0
+// admitted.  If the n-th key ends within r0 (1 - 1e-12) the result is exact: every point
+// with a smaller key lies inside the box and passed the admission test.  Otherwise the
+// query restarts with the exact ring traversal (sparse corners, excluded regions).
+template <int D, int NMAX>
+__global__ void __launch_bounds__(128, D == 2 ? 7 : 5) knn_box_kernel(Grid g, const double* __restrict__ pos,
+                                                      const int* __restrict__ cell_start,
+                                                      const int* __restrict__ cell_items,
+                                                      const double* __restrict__ cell_pos,
+                                                      const int* __restrict__ queries,
+                                                      const double* __restrict__ qpos, int64_t nq, int n,
+                                                      const uint8_t* __restrict__ exclude, double r0,
+                                                      const double* __restrict__ qh, double rscale,
+                                                      int* __restrict__ out_idx, double* __restrict__ out_dist) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nq) return;
+  double q[D];
+  load_query<D>(pos, queries, qpos, t, q);
+  if (qh) {  // radius from the query's own nominal spacing (graded node sets)
+    const double h = __ldg(qh + (qpos ? t : (queries ? __ldg(queries + t) : t)));
+    if (h > 0.0 && h < CUDART_INF) r0 = rscale * h;
   }
   int c0[D];
   cell_coords<D>(g, q, c0);
-  unsigned long long kd[NMAX];
+  double kd[NMAX];
   int ki[NMAX];
-#pragma unroll
-  for (int j = 0; j < NMAX; ++j) {
-    const bool live = j >= NMAX - n;
-    kd[j] = live ? ~0ull : 0ull;  // ~0 > any distance bits; 0 sentinel never displaced
-    ki[j] = live ? INT_MAX : -1;
-  }
-  double thr2 = CUDART_INF;
-  int max_r = 0;
-#pragma unroll
-  for (int a = 0; a < D; ++a) max_r = max(max_r, max(c0[a], g.dims[a] - 1 - c0[a]));
-
-  for (int R = 0; R <= max_r; ++R) {
-    const int side = 2 * R + 1;
-    int ncube = side * side;
-    if constexpr (D == 3) ncube *= side;
-    for (int base = 0; base < ncube; base += KB) {
-      int cs[KB], ce[KB];
-#pragma unroll
-      for (int b = 0; b < KB; ++b) {
-        int tt = base + b;
-        int o[D];
-        bool ok = tt < ncube;
-#pragma unroll
-        for (int a = D - 1; a >= 0; --a) {
-          o[a] = tt % side - R;
-          tt /= side;
-        }
-        int m = 0;
-        int64_t cl = 0;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          m = max(m, abs(o[a]));
-          const int x = c0[a] + o[a];
-          ok = ok && x >= 0 && x < g.dims[a];
-          cl = cl * g.dims[a] + x;
-        }
-        ok = ok && m == R;
-        cs[b] = ok ? __ldg(cell_start + cl) : 0;
-        ce[b] = ok ? __ldg(cell_start + cl + 1) : 0;
-      }
-      for (int slot = 0;; ++slot) {
-        bool any = false;
-        int jj[KB];
-        double pp[KB][D];
-#pragma unroll
-        for (int b = 0; b < KB; ++b) {
-          const int s_ = cs[b] + slot;
-          const bool live = s_ < ce[b];
-          any = any || live;
-          jj[b] = live ? __ldg(cell_items + s_) : -1;
-#pragma unroll
-          for (int a = 0; a < D; ++a) pp[b][a] = live ? __ldg(cell_pos + static_cast<int64_t>(s_) * S + a) : 0.0;
-        }
-        if (!any) break;
-#pragma unroll
-        for (int b = 0; b < KB; ++b) {
-          const int j = jj[b];
-          if (j < 0) continue;
-          if (exclude && __ldg(exclude + j)) continue;
-          const double d2 = exact_dist2<D>(pp[b], q);
-          if (d2 > thr2) continue;
-          const unsigned long long d = static_cast<unsigned long long>(__double_as_longlong(__dsqrt_rn(d2)));
-          if (!(d < kd[NMAX - 1] || (d == kd[NMAX - 1] && j < ki[NMAX - 1]))) continue;
-#pragma unroll
-          for (int mm = NMAX - 1; mm >= 0; --mm) {
-            const bool lt = d < kd[mm] || (d == kd[mm] && j < ki[mm]);
-            if (lt) {
-              const int pm = mm > 0 ? mm - 1 : 0;
-              const bool shift = (mm > 0) && (d < kd[pm] || (d == kd[pm] && j < ki[pm]));
-              kd[mm] = shift ? kd[pm] : d;
-              ki[mm] = shift ? ki[pm] : j;
-            }
-          }
-          const unsigned long long w = kd[NMAX - 1];
-          if (w != ~0ull) {
-            const double wd = __longlong_as_double(static_cast<long long>(w));
-            thr2 = __dmul_rn(__dmul_rn(wd, wd), 1.0 + 1e-15);
-          }
-        }
-      }
-    }
-    double bound = CUDART_INF;
+  topn_init<NMAX>(kd, ki, n);
+  constexpr int L = D - 1;  // contiguous axis of the cell numbering
+  // gap between q and cell c along axis a (0 inside), shrunk by a rounding margin
+  auto gap = [&](int a, int c) {
+    const double cl = g.lo[a] + c * g.cell;
+    const double gp = fmax(fmax(cl - q[a], q[a] - (cl + g.cell)), 0.0);
+    return fmax(gp - 1e-9 * g.cell, 0.0);
+  };
+  bool exact = false;
+#pragma unroll 1
+  for (int attempt = 0; attempt < 2 && !exact; ++attempt) {
+    const double r = attempt ? 1.7 * r0 : r0;  // one wider retry before the ring fallback
+    if (attempt) topn_init<NMAX>(kd, ki, n);
+    double thr2 = __dmul_rn(__dmul_rn(r, r), 1.0 + 1e-9);
+    // box cells with cell_coords' own formula: fl(sub), fl(mul) and floor are monotone, so
+    // every point whose coordinate lies in [q - r', q + r'] falls in [blo, bhi]
+    const double rm = r * (1.0 + 1e-9);
+    int blo[D], bhi[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      if (c0[a] - R > 0) bound = fmin(bound, q[a] - (g.lo[a] + (c0[a] - R) * g.cell));
-      if (c0[a] + R + 1 < g.dims[a]) bound = fmin(bound, (g.lo[a] + (c0[a] + R + 1) * g.cell) - q[a]);
+      const double lo_p = q[a] - rm, hi_p = q[a] + rm;
+      blo[a] = min(max(static_cast<int>(floor((lo_p - g.lo[a]) * g.inv_cell)), 0), g.dims[a] - 1);
+      bhi[a] = min(max(static_cast<int>(floor((hi_p - g.lo[a]) * g.inv_cell)), 0), g.dims[a] - 1);
     }
-    const unsigned long long w = kd[NMAX - 1];
-    if (w != ~0ull && __longlong_as_double(static_cast<long long>(w)) < bound - 1e-9 * g.cell) break;
-  }
-#pragma unroll
-  for (int j = 0; j < NMAX; ++j) {
-    if (j >= NMAX - n) {
-      const int o = j - (NMAX - n);
-      out_idx[t * n + o] = ki[j];
-      if (out_dist) out_dist[t * n + o] = __longlong_as_double(static_cast<long long>(kd[j]));
+    // cells of the run along the contiguous axis that can hold points within sqrt(rem2)
+    // of q (rem2 = thr2 minus the squared gaps of the other axes; thr2 shrinks as the
+    // window fills, so later runs get shorter)
+    auto run_span = [&](double rem2, int& c_lo, int& c_hi) {
+      const double hw = sqrt(fmax(rem2, 0.0)) * (1.0 + 1e-9) + 1e-12 * g.cell;
+      c_lo = min(max(static_cast<int>(floor((q[L] - hw - g.lo[L]) * g.inv_cell)), blo[L]), bhi[L]);
+      c_hi = min(max(static_cast<int>(floor((q[L] + hw - g.lo[L]) * g.inv_cell)), blo[L]), bhi[L]);
+    };
+    const int w0 = max(c0[0] - blo[0], bhi[0] - c0[0]);
+    for (int k0 = 0; k0 <= 2 * w0; ++k0) {
+      const int x = c0[0] + ((k0 & 1) ? -((k0 + 1) >> 1) : (k0 >> 1));
+      if (x < blo[0] || x > bhi[0]) continue;
+      const double gx = gap(0, x);
+      if (gx * gx > thr2) continue;
+      if constexpr (D == 2) {
+        int ylo, yhi;
+        run_span(thr2 - gx * gx, ylo, yhi);
+        const int64_t cl = static_cast<int64_t>(x) * g.dims[1] + ylo;
+        const int beg = __ldg(cell_start + cl), end = __ldg(cell_start + cl + (yhi - ylo + 1));
+        topn_offer_run<D, NMAX>(cell_pos, cell_items, exclude, beg, end, q, kd, ki, thr2);
+      } else {
+        const int w1 = max(c0[1] - blo[1], bhi[1] - c0[1]);
+        for (int k1 = 0; k1 <= 2 * w1; ++k1) {
+          const int y = c0[1] + ((k1 & 1) ? -((k1 + 1) >> 1) : (k1 >> 1));
+          if (y < blo[1] || y > bhi[1]) continue;
+          const double gy = gap(1, y);
+          if (gx * gx + gy * gy > thr2) continue;
+          int zlo, zhi;
+          run_span(thr2 - gx * gx - gy * gy, zlo, zhi);
+          const int64_t cl = (static_cast<int64_t>(x) * g.dims[1] + y) * g.dims[2] + zlo;
+          const int beg = __ldg(cell_start + cl), end = __ldg(cell_start + cl + (zhi - zlo + 1));
+          topn_offer_run<D, NMAX>(cell_pos, cell_items, exclude, beg, end, q, kd, ki, thr2);
+        }
+      }
     }
+    exact = kd[NMAX - 1] <= r * (1.0 - 1e-12);
   }
+  if (!exact) {  // neither box held n keys (sparse corner, excluded region): exact rings
+    topn_init<NMAX>(kd, ki, n);
+    ring_scan<D, NMAX>(g, cell_start, cell_items, cell_pos, exclude, q, c0, kd, ki);
+  }
+  topn_store<NMAX>(kd, ki, n, t, out_idx, out_dist);
 }
 
 // ---- classification + lattice stencils ------------------------------------------
@@ -574,7 +610,7 @@ HN_EXPORT int hn_partition_methods(const int8_t* method, int64_t n, int* rows_ou
   return e == cudaSuccess ? 0 : -static_cast<int>(e);
 }
 
-static int g_knn_variant = 1;  // 1: per-cell traversal (knn, default), 0: batched rings (knn2)
+static int g_knn_variant = 0;  // 0/2/3: box pass (alpha 1.3/1.0/1.6) + ring fallback; 1: ring traversal only
 HN_EXPORT void hn_knn_set_variant(int v) { g_knn_variant = v; }
 
 static Grid make_grid(const double* lo_host, double cell, const int* dims_host, int d) {
@@ -617,28 +653,50 @@ HN_EXPORT int hn_celllist_build(const double* pos, int64_t n, int d, const doubl
   return 0;
 }
 
-template <int D>
-static int launch_knn(const Grid& g, const double* pos, const int* cs, const int* ci, const double* cp,
-                      const int* queries, const double* qpos, int64_t nq, int n, const uint8_t* excl, int* oi,
-                      double* od, cudaStream_t s) {
+// box-pass radius: alpha x the radius holding n points at density 1/h^d -- h = the grid's
+// design spacing (~1 point per cell in 2D, 1.25^3 in 3D: DeviceNodes' cell rule) or the
+// query's own spacing; any radius gives the exact answer, it only changes the work
+static double radius_per_spacing(int d, int n, double alpha) {
+  if (d == 2) return alpha * sqrt(n / 3.141592653589793);
+  return alpha * cbrt(n / 4.18879020478639);
+}
+static double box_radius(int d, int n, double cell, double alpha) {
+  return radius_per_spacing(d, n, alpha) * (d == 2 ? cell : cell / 1.25);
+}
+
+template <int D, int NMAX>
+static void knn_launch_one(int variant, const Grid& g, const double* pos, const int* cs, const int* ci,
+                           const double* cp, const int* queries, const double* qpos, int64_t nq, int n,
+                           const uint8_t* excl, const double* qh, int* oi, double* od, cudaStream_t s) {
   const int th = 128;
   const int64_t bl = ceil_div(nq, th);
-  if (g_knn_variant == 0) {
-    if (n <= 8) knn2_kernel<D, 8><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
-    else if (n <= 16) knn2_kernel<D, 16><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
-    else if (n <= 24) knn2_kernel<D, 24><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
-    else if (n <= 32) knn2_kernel<D, 32><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
-    else if (n <= 48) knn2_kernel<D, 48><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
-    else knn2_kernel<D, 64><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
-    HN_CHECK_LAUNCH();
-    return 0;
+  if (variant == 1) {
+    knn_kernel<D, NMAX><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
+    return;
   }
-  if (n <= 8) knn_kernel<D, 8><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
-  else if (n <= 16) knn_kernel<D, 16><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
-  else if (n <= 24) knn_kernel<D, 24><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
-  else if (n <= 32) knn_kernel<D, 32><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
-  else if (n <= 48) knn_kernel<D, 48><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
-  else knn_kernel<D, 64><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl, oi, od);
+  const double alpha = variant == 2 ? (D == 2 ? 1.3 : 1.05) : (variant == 3 ? (D == 2 ? 1.6 : 1.3) : (D == 2 ? 1.4 : 1.15));
+  knn_box_kernel<D, NMAX><<<bl, th, 0, s>>>(g, pos, cs, ci, cp, queries, qpos, nq, n, excl,
+                                            box_radius(D, n, g.cell, alpha), qh,
+                                            radius_per_spacing(D, n, alpha), oi, od);
+}
+
+template <int D>
+static int launch_knn(const Grid& g, const double* pos, const int* cs, const int* ci, const double* cp,
+                      const int* queries, const double* qpos, int64_t nq, int n, const uint8_t* excl,
+                      const double* qh, int* oi, double* od, cudaStream_t s) {
+  const int v = g_knn_variant;
+#define HN_KNN(NM) knn_launch_one<D, NM>(v, g, pos, cs, ci, cp, queries, qpos, nq, n, excl, qh, oi, od, s)
+  if (n <= 5) HN_KNN(5);
+  else if (n <= 8) HN_KNN(8);
+  else if (n <= 12) HN_KNN(12);
+  else if (n <= 16) HN_KNN(16);
+  else if (n <= 20) HN_KNN(20);
+  else if (n <= 24) HN_KNN(24);
+  else if (n <= 30) HN_KNN(30);
+  else if (n <= 32) HN_KNN(32);
+  else if (n <= 48) HN_KNN(48);
+  else HN_KNN(64);
+#undef HN_KNN
   HN_CHECK_LAUNCH();
   return 0;
 }
@@ -652,8 +710,27 @@ HN_EXPORT int hn_knn(const double* pos, int d, const double* lo_host, double cel
   if (nq == 0) return 0;
   Grid g = make_grid(lo_host, cell, dims_host, d);
   cudaStream_t s = as_stream(stream);
-  if (d == 2) return launch_knn<2>(g, pos, cell_start, cell_items, cell_pos, queries, qpos, nq, n, exclude, out_idx, out_dist, s);
-  return launch_knn<3>(g, pos, cell_start, cell_items, cell_pos, queries, qpos, nq, n, exclude, out_idx, out_dist, s);
+  if (d == 2)
+    return launch_knn<2>(g, pos, cell_start, cell_items, cell_pos, queries, qpos, nq, n, exclude, nullptr, out_idx,
+                         out_dist, s);
+  return launch_knn<3>(g, pos, cell_start, cell_items, cell_pos, queries, qpos, nq, n, exclude, nullptr, out_idx,
+                       out_dist, s);
+}
+
+HN_EXPORT int hn_knn_spacing(const double* pos, int d, const double* lo_host, double cell, const int* dims_host,
+                             const int* cell_start, const int* cell_items, const double* cell_pos,
+                             const int* queries, const double* qpos, int64_t nq, int n, const uint8_t* exclude,
+                             const double* spacing, int* out_idx, double* out_dist, void* stream) {
+  if (d != 2 && d != 3) return 1;
+  if (n < 1 || n > 64) return 2;
+  if (nq == 0) return 0;
+  Grid g = make_grid(lo_host, cell, dims_host, d);
+  cudaStream_t s = as_stream(stream);
+  if (d == 2)
+    return launch_knn<2>(g, pos, cell_start, cell_items, cell_pos, queries, qpos, nq, n, exclude, spacing, out_idx,
+                         out_dist, s);
+  return launch_knn<3>(g, pos, cell_start, cell_items, cell_pos, queries, qpos, nq, n, exclude, spacing, out_idx,
+                       out_dist, s);
 }
 
 HN_EXPORT int hn_classify(const int8_t* kind, const int* lattice_idx, const int* grid, const int* grid_dims_host,
