@@ -96,18 +96,31 @@ class ClockSampler:
         self.proc = None
         self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
 
+    def _lines(self):
+        self.file.flush()
+        return len([ln for ln in Path(self.file.name).read_text().splitlines() if ln[:1].isdigit()])
+
+    def _wait_for(self, count, timeout):
+        t0 = time.perf_counter()
+        while self._lines() < count and time.perf_counter() - t0 < timeout:
+            time.sleep(0.002)
+
     def __enter__(self):
         try:
             idx = os.environ.get("LOCAL_RANK", "0")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", idx, f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                          "--format=csv,noheader,nounits", "-lms", "10"],
                                          stdout=self.file, stderr=subprocess.DEVNULL)
+            # nvidia-smi needs ~0.1-0.5 s before its first sample: wait for it, so even a short
+            # timed region is bracketed by samples
+            self._wait_for(1, 5.0)
         except (FileNotFoundError, OSError):
             self.proc = None
         return self
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            self._wait_for(self._lines() + 1, 0.5)  # one sample at/after the end of the region
             self.proc.terminate()
             self.proc.wait(timeout=5)
 

@@ -203,6 +203,10 @@ int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int
                     const double* vals, const double* diag, const double* b, double* x, double* ysum,
                     int64_t n, unsigned long long* ticket, int ctas_per_sm, void* stream);
 
+/* Debug: per-task timeline of hn_sptrsv_super launches ([start, outside sums done, end]
+ * in %globaltimer ns, SM id) written to trace (4 u64 per task); NULL switches it off. */
+int hn_debug_sptrsv_trace(unsigned long long* trace);
+
 /* Setup helpers on HOST arrays: dense-triangle row blocks (returns the count; blocks in row
  * order) and their dependency levels. */
 int64_t hn_host_supernodes(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower, int cap,

@@ -14,7 +14,7 @@ from pathlib import Path
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libhn.so"
+LIB_PATH = Path(os.environ.get("HN_LIB_PATH", _PKG / "libhn.so"))  # env override: A/B builds (dev)
 
 _c_int_p = C.POINTER(C.c_int)
 _c_i64_p = C.POINTER(C.c_int64)
@@ -61,6 +61,7 @@ SIGNATURES: dict[str, tuple] = {
     "hn_host_levels": (_i, [_vp, _vp, _i64, _i, _vp]),
     "hn_sptrsv_super": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i,
                              _vp]),
+    "hn_debug_sptrsv_trace": (_i, [_vp]),
     "hn_host_supernodes": (_i64, [_vp, _vp, _i64, _i, _i, _vp, _vp]),
     "hn_host_block_levels": (_i, [_vp, _vp, _i64, _i, _i64, _vp, _vp, _vp]),
     "hn_partition_methods": (_i, [_vp, _i64, _vp, _vp, _vp, _vp]),
@@ -84,7 +85,10 @@ def lib():
             raise NativeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
                               "(python -m paper_2303_01760_b200._build)")
         handle = C.CDLL(str(LIB_PATH), mode=C.RTLD_GLOBAL)
+        ab_build = "HN_LIB_PATH" in os.environ  # dev A/B against an older build: tolerate new symbols
         for name, (res, args) in SIGNATURES.items():
+            if ab_build and not hasattr(handle, name):
+                continue
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args

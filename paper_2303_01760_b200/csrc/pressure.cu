@@ -177,9 +177,86 @@ __device__ __forceinline__ double row_outside_sum(const int* __restrict__ cols, 
   return warp_sum(sum);
 }
 
+// Small block (w <= 32) solved by one warp: lane r owns row r0+r -- its outside part by a
+// serial loop with 4 loads in flight (the planner only batches blocks whose rows are
+// short), then the dense triangle with shuffles.  No shared memory, no CTA barrier.
+template <bool LOWER>
+__device__ __forceinline__ void warp_small_block(const int64_t* __restrict__ rowptr, const int* __restrict__ cols,
+                                                 const double* __restrict__ vals, const double* __restrict__ diag,
+                                                 const double* __restrict__ b, double* x, int r0, int w, int lane) {
+  double yv = 0.0, dg = 1.0;
+  double lv[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) lv[k] = 0.0;
+  if (lane < w) {
+    const int i = r0 + lane;
+    const int64_t a = __ldg(rowptr + i), z = __ldg(rowptr + i + 1);
+    const int inside = LOWER ? lane : (w - 1 - lane);
+    const int64_t e0 = LOWER ? a : a + inside;
+    const int64_t e1 = e0 + (z - a) - inside;
+    double s = 0.0;
+    for (int64_t e = e0; e < e1; e += 4) {
+      int c[4];
+      double v[4], xv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        c[k] = e + k < e1 ? __ldg(cols + e + k) : -1;
+        v[k] = e + k < e1 ? __ldg(vals + e + k) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) xv[k] = c[k] >= 0 ? ld_acquire_dbl(x + c[k]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (c[k] >= 0 && is_sentinel(xv[k])) xv[k] = wait_value(x + c[k]);
+        s = fma(v[k], xv[k], s);
+      }
+    }
+    yv = __ldg(b + i) - s;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (LOWER) {
+        if (k < lane) lv[k] = __ldg(vals + (z - lane) + k);           // col r0 + k
+      } else {
+        if (k > lane && k < w) lv[k] = __ldg(vals + a + (k - lane - 1));  // col r0 + k
+      }
+    }
+    if (!LOWER) dg = __ldg(diag + i);
+  }
+  if (LOWER) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double xk = __shfl_sync(0xffffffffu, yv, k);
+      if (lane > k) yv = fma(-lv[k], xk, yv);
+    }
+  } else {
+#pragma unroll
+    for (int k = 31; k >= 0; --k) {
+      if (lane == k && lane < w) yv = yv / dg;
+      const double xk = __shfl_sync(0xffffffffu, yv, k);
+      if (lane < k) yv = fma(-lv[k], xk, yv);
+    }
+  }
+  if (lane < w) st_release_dbl(x + r0 + lane, yv);
+}
+
 // Task kinds: 0 = whole block (outside + dense), 1 = helper (outside sums of rows
 // [rb, rb+rc) of a heavy block -> ysum, sentinel-flagged), 2 = dense part of a heavy block
-// whose outside sums come from its helpers (scheduled right before it).
+// whose outside sums come from its helpers (scheduled right before it), 3 = batch of up to
+// kSnWarps independent small blocks of one level, warp k solving member rb+k (member
+// entries live past the task list in the same arrays).
+// optional per-task timeline (hn_debug_sptrsv_trace): [start, outside-done, end] ns + SM id
+__device__ unsigned long long* g_sn_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+
 template <bool LOWER>
 __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
     const int* __restrict__ blk_kind, const int* __restrict__ blk_r0, const int* __restrict__ blk_w,
@@ -195,7 +272,23 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
     const unsigned long long t = tk;
     __syncthreads();
     if (t >= static_cast<unsigned long long>(nblk)) return;
+    unsigned long long* tr = g_sn_trace;
+    if (tr && tid == 0) {
+      tr[4 * t] = gtime();
+      tr[4 * t + 3] = smid();
+    }
     const int kind = __ldg(blk_kind + t);
+    if (kind == 3) {
+      const int mb = __ldg(blk_rb + t), mc = __ldg(blk_rc + t);
+      if (warp < mc)
+        warp_small_block<LOWER>(rowptr, cols, vals, diag, b, x, __ldg(blk_r0 + mb + warp), __ldg(blk_w + mb + warp),
+                                lane);
+      if (tr) {
+        __syncthreads();
+        if (tid == 0) tr[4 * t + 2] = gtime();
+      }
+      continue;
+    }
     const int r0 = __ldg(blk_r0 + t), w = __ldg(blk_w + t);
     if (kind == 2) {
       for (int rr = tid; rr < w; rr += kSnThreads) ys[rr] = wait_value(ysum + r0 + rr);
@@ -215,9 +308,16 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
           else ys[rr] = __ldg(b + i) - s;
         }
       }
-      if (kind == 1) continue;
+      if (kind == 1) {
+        if (tr) {
+          __syncthreads();
+          if (tid == 0) tr[4 * t + 2] = gtime();
+        }
+        continue;
+      }
     }
     __syncthreads();
+    if (tr && tid == 0) tr[4 * t + 1] = gtime();
     // (2) dense in-block triangle, 32-column tiles
     const int ntiles = (w + 31) / 32;
     for (int tt = 0; tt < ntiles; ++tt) {
@@ -283,6 +383,7 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
       }
       __syncthreads();
     }
+    if (tr && tid == 0) tr[4 * t + 2] = gtime();
   }
 }
 
@@ -409,6 +510,11 @@ HN_EXPORT int hn_sptrsv_tasks(int divide, const int* task_row, const int64_t* ta
                                                       vals, diag, b, x, partial, ticket);
   HN_CHECK_LAUNCH();
   return 0;
+}
+
+// Debug timeline for hn_sptrsv_super: trace = 4 x ntasks u64 per launch (NULL = off).
+HN_EXPORT int hn_debug_sptrsv_trace(unsigned long long* trace) {
+  return cudaMemcpyToSymbol(g_sn_trace, &trace, sizeof(trace)) == cudaSuccess ? 0 : -1;
 }
 
 // Supernodal solve over planned blocks (processing order), see sptrsv_super_kernel.

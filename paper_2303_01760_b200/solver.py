@@ -107,8 +107,12 @@ class _TriSchedule:
         self.partial = L.empty(max(self.npartial, 1), L.torch().float64)
 
 
-def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 4096, helper_nnz: int = 16384) -> dict:
-    """Host planning of hn_sptrsv_super: dense-triangle row blocks in dependency-level order."""
+def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, helper_nnz: int = 4096,
+                           batch: int = 8, batch_row_nnz: int = 96) -> dict:
+    """Host planning of hn_sptrsv_super: dense-triangle row blocks in dependency-level order.
+    Consecutive small blocks (w <= 32, every row's outside part <= batch_row_nnz) of one
+    level are grouped `batch` to a task (kind 3, one warp each); heavy blocks get helper
+    tasks (kind 1) for their outside sums."""
     n = m.shape[0]
     rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
     cols = np.ascontiguousarray(m.indices, dtype=np.int32)
@@ -135,8 +139,28 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 4096, h
     starts = np.concatenate([[0], np.cumsum(w)[:-1]]) if nb else np.empty(0, np.int64)
     block_out = np.add.reduceat(outside, starts) if nb else np.empty(0)
     kinds, tr0, tw, trb, trc = [], [], [], [], []
+    members = []  # (r0, w) of batched small blocks, appended after the task list (kind 3)
     heavy = set(np.nonzero((block_out > helper_nnz) & (w > 1))[0].tolist())
+    block_maxout = np.maximum.reduceat(outside, starts) if nb else np.empty(0)
+    small = (w <= 32) & (block_maxout <= batch_row_nnz) if batch else np.zeros(nb, bool)
+    pending = []  # consecutive small blocks of one level -> one warp each
+
+    def flush():
+        if len(pending) == 1:
+            k = pending[0]
+            kinds.append(0); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k])
+        elif pending:
+            kinds.append(3); tr0.append(0); tw.append(0); trb.append(len(members)); trc.append(len(pending))
+            members.extend((int(r0[k]), int(w[k])) for k in pending)
+        pending.clear()
+
     for k in range(nb):
+        if small[k] and k not in heavy:
+            if pending and (lev[pending[0]] != lev[k] or len(pending) == batch):
+                flush()
+            pending.append(k)
+            continue
+        flush()
         if k in heavy:
             o = outside[starts[k]: starts[k] + w[k]]
             cut = np.searchsorted(np.cumsum(o), np.arange(1, int(np.ceil(o.sum() / helper_nnz))) * helper_nnz)
@@ -146,15 +170,20 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 4096, h
             kinds.append(2); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k])
         else:
             kinds.append(0); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k])
+    flush()
+    ntasks = len(kinds)
+    for idx, (a, b) in enumerate(members):  # member entries: the kernel never tickets past ntasks
+        kinds.append(4); tr0.append(a); tw.append(b); trb.append(0); trc.append(b)
+    trb = [v + ntasks if kd == 3 else v for kd, v in zip(kinds, trb)]
     as32 = lambda v: np.asarray(v, dtype=np.int32)  # noqa: E731
     return {"nblk": nb, "r0": r0, "w": w, "levels": lev, "depth": int(lev.max()) + 1 if nb else 0,
-            "ntasks": len(kinds), "kind": as32(kinds), "t_r0": as32(tr0), "t_w": as32(tw), "t_rb": as32(trb),
-            "t_rc": as32(trc), "heavy": len(heavy)}
+            "ntasks": ntasks, "kind": as32(kinds), "t_r0": as32(tr0), "t_w": as32(tw), "t_rb": as32(trb),
+            "t_rc": as32(trc), "heavy": len(heavy), "batched": len(members)}
 
 
 class _SuperSchedule:
-    def __init__(self, m: sparse.csr_matrix, lower: bool):
-        plan = plan_supernodal_blocks(m, lower)
+    def __init__(self, m: sparse.csr_matrix, lower: bool, **plan_kw):
+        plan = plan_supernodal_blocks(m, lower, **plan_kw)
         self.nblk, self.depth, self.ntasks = plan["nblk"], plan["depth"], plan["ntasks"]
         self.kind, self.r0, self.w = L.to_device(plan["kind"]), L.to_device(plan["t_r0"]), L.to_device(plan["t_w"])
         self.rb, self.rc = L.to_device(plan["t_rb"]), L.to_device(plan["t_rc"])

@@ -373,3 +373,46 @@ def test_with_kappa_matches_oracle_system_kappa(golden):
     assert np.all(np.isfinite(t.kappa[inner])) and np.all(np.isnan(t.kappa[~inner]))
     mon = t.method == METHOD_MON
     assert np.all(t.kappa[mon] < t.kappa[t.method == 1].max())
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_knn_box_pass_equals_ring_traversal(dim):
+    """The box pass (default) and its retry/ring fallbacks give the ring traversal's exact
+    answer on clustered clouds whose nominal spacing is wrong by 10x either way (forcing
+    the fallback paths), with exclusion masks, and for point queries."""
+    from paper_2303_01760_b200 import _lib as L
+    from paper_2303_01760_b200._device import DeviceNodes
+    rng = np.random.default_rng(11 + dim)
+    pts = np.concatenate([rng.normal(0.3, 0.02, (3000, dim)), rng.uniform(0, 1, (3000, dim)),
+                          rng.normal(0.8, 0.005, (500, dim))])
+    n = len(pts)
+    h = np.full(n, 1.0 / n ** (1.0 / dim))
+    h[:3000] *= 10.0   # clustered nodes claim a coarse spacing: radius far too large
+    h[3000:6000] *= 0.1  # uniform nodes claim a fine spacing: box misses, retry + rings
+    ns = NodeSet(pts, h, np.full(n, KIND_SCATTERED, dtype=np.int8), np.zeros(n, dtype=np.int8),
+                 np.full(n, np.nan), np.full((n, dim), np.nan))
+    dn = DeviceNodes(ns)
+    rows = L.to_device(np.arange(0, n, 3, dtype=np.int32))
+    excl = (rng.random(n) < 0.2).astype(np.uint8)
+    qpts = rng.uniform(-0.1, 1.1, (257, dim))
+    k = 12 if dim == 2 else 20
+    out = {}
+    try:
+        for v in (1, 0, 2, 3):
+            L.lib().hn_knn_set_variant(v)
+            a, da = dn.knn(k, rows=rows, with_dist=True)
+            b = dn.knn(k, rows=rows, exclude=excl)
+            c = dn.knn(k, points=qpts)
+            out[v] = (a.cpu().numpy(), da.cpu().numpy(), b.cpu().numpy(), c.cpu().numpy())
+    finally:
+        L.lib().hn_knn_set_variant(0)
+    for v in (0, 2, 3):
+        for x, y in zip(out[v], out[1]):
+            npt.assert_array_equal(x, y)
+    # and the ring answer is the brute-force (distance, index) order
+    idx = out[1][0]
+    q = pts[np.arange(0, n, 3)]
+    d = np.sqrt(((pts[None, :, :] - q[:50, None, :]) ** 2).sum(-1))
+    for r in range(50):
+        order = np.lexsort((np.arange(n), d[r]))[:k]
+        npt.assert_array_equal(idx[r], order)

@@ -114,8 +114,20 @@ def emulate_blocks(plan, m, b, lower, diag=None):
         assert np.array_equal(np.sort(c[~out]), np.arange(r0, i) if lower else np.arange(i + 1, r0 + w))
         return b[i] - np.dot(v[out], x[c[out]])
 
-    for kind, r0, w, rb, rc in zip(plan["kind"], plan["t_r0"], plan["t_w"], plan["t_rb"], plan["t_rc"]):
+    nt = plan["ntasks"]
+    for kind, r0, w, rb, rc in zip(plan["kind"][:nt], plan["t_r0"][:nt], plan["t_w"][:nt], plan["t_rb"][:nt],
+                                   plan["t_rc"][:nt]):
         rows = np.arange(r0, r0 + w)
+        if kind == 3:  # batch: members run concurrently -> all outside sums before any solve
+            mem = [(plan["t_r0"][k], plan["t_w"][k]) for k in range(rb, rb + rc)]
+            assert all(plan["kind"][k] == 4 for k in range(rb, rb + rc)) and all(mw <= 32 for _, mw in mem)
+            ys = [np.array([outside(i, mr0, mw) for i in range(mr0, mr0 + mw)]) for mr0, mw in mem]
+            for (mr0, mw), y in zip(mem, ys):
+                mrows = np.arange(mr0, mr0 + mw)
+                blk = dense[np.ix_(mrows, mrows)]
+                full = blk + (np.eye(mw) if lower else np.diag(diag[mrows]))
+                x[mrows] = spsolve_triangular(sp.csr_matrix(full), y, lower=lower)
+            continue
         if kind == 1:
             for i in range(r0 + rb, r0 + rb + rc):
                 ysum[i] = outside(i, r0, w)
@@ -144,7 +156,7 @@ def test_supernodal_plan_solves_triangular_systems(lower):
     diag = sp.csr_matrix(lu.U).diagonal()
     plan = plan_supernodal_blocks(tri, lower, cap=64, helper_nnz=40)
     assert plan["nblk"] < n and plan["w"].sum() == n
-    assert plan["heavy"] > 0 and plan["ntasks"] > plan["nblk"]
+    assert plan["heavy"] > 0 and plan["batched"] > 0
     b = rng.normal(size=n)
     x = emulate_blocks(plan, tri, b, lower, diag)
     full = (tri + sp.eye(n)) if lower else (tri + sp.diags(diag))
