@@ -56,6 +56,34 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Number of SMs on the current device (cached per process).
 int sm_count();
 
+// Fork/join of independent launches: launch i > 0 goes to a side stream that waits for
+// everything already queued on s; s waits for every side before anything later runs.
+// Capturable into CUDA graphs (event record/wait become graph edges).
+struct ForkJoin {
+  static constexpr int kSides = 3;
+  cudaStream_t side[kSides];
+  cudaEvent_t done[kSides];
+  cudaEvent_t start;
+};
+ForkJoin& fork_join();
+
+template <typename F>
+inline void launch_forked(cudaStream_t s, int n, F&& launch) {
+  if (n <= 1) {
+    if (n == 1) launch(0, s);
+    return;
+  }
+  ForkJoin& fj = fork_join();
+  const int sides = n - 1 < ForkJoin::kSides ? n - 1 : ForkJoin::kSides;
+  cudaEventRecord(fj.start, s);
+  for (int k = 0; k < sides; ++k) cudaStreamWaitEvent(fj.side[k], fj.start, 0);
+  for (int i = 0; i < n; ++i) launch(i, i == 0 ? s : fj.side[(i - 1) % sides]);
+  for (int k = 0; k < sides; ++k) {
+    cudaEventRecord(fj.done[k], fj.side[k]);
+    cudaStreamWaitEvent(s, fj.done[k], 0);
+  }
+}
+
 // fl(sqrt(((0 + dx*dx) + dy*dy) [+ dz*dz])) -- the distance scipy's cKDTree and
 // np.linalg.norm return for these inputs; no FMA contraction.
 template <int D>

@@ -14,6 +14,25 @@ int sm_count() {
   return cached;
 }
 
+// Side streams for fork/join launches (per device, created on first use; non-blocking so
+// they never serialise against the legacy default stream) and their join events.
+ForkJoin& fork_join() {
+  static ForkJoin fj[16];
+  static bool made[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev = dev < 16 ? dev : 15;
+  if (!made[dev]) {
+    for (int i = 0; i < ForkJoin::kSides; ++i) {
+      cudaStreamCreateWithFlags(&fj[dev].side[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&fj[dev].done[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&fj[dev].start, cudaEventDisableTiming);
+    made[dev] = true;
+  }
+  return fj[dev];
+}
+
 // 16 independent DFMA chains per thread keep the FP64 pipe saturated; the result is
 // folded into a checksum so nothing is dead code.
 __global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters) {

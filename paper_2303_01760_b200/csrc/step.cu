@@ -142,9 +142,9 @@ __device__ __forceinline__ void div_row(const StepBins& b, int bin, int64_t k, c
 template <int D, int W>
 __global__ void __launch_bounds__(128, (W <= 7 ? 8 : (W <= 12 ? 6 : (W <= 20 ? 4 : 2))))
 div_rhs_kernel(StepBins b, const double* __restrict__ vs, int64_t N, double dt,
-               double* __restrict__ rhs) {
+               double* __restrict__ rhs, bool gauge) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (blockIdx.x == 0 && threadIdx.x == 0) rhs[N] = 0.0;  // bordered gauge equation
+  if (gauge && blockIdx.x == 0 && threadIdx.x == 0) rhs[N] = 0.0;  // bordered gauge equation
   if (k >= b.K[0]) return;
   div_row<D, W>(b, 0, k, vs, N, 0.0, dt, rhs);
 }
@@ -215,6 +215,65 @@ correct_temp_kernel(StepBins b, const double* __restrict__ vs, const double* __r
   correct_temp_row<D, W>(b, 0, k, vs, p, T, N, dt, vout, Tout, flags);
 }
 
+// ---- one launch for every bin of a phase (small node sets) ----
+// Blocks map to bins through block_start; a bin's width selects the compile-time body
+// (WA, WB or 0).  At small N the per-bin launches of a phase cost more than the lower
+// occupancy of the shared register budget, so the dispatcher fuses below kFuseRows.
+constexpr int64_t kFuseRows = 600000;
+
+#define HN_FUSED_BODY(ROWFN, ...)                                          \
+  const int bin = find_bin(b);                                             \
+  const int64_t k = static_cast<int64_t>(blockIdx.x - b.block_start[bin]) * blockDim.x + threadIdx.x; \
+  if (k >= b.K[bin]) return;                                               \
+  const int w = b.width[bin];                                              \
+  if (w == WA) ROWFN<D, WA>(b, bin, k, __VA_ARGS__);                       \
+  else if (WB > 0 && w == WB) ROWFN<D, (WB > 0 ? WB : WA)>(b, bin, k, __VA_ARGS__); \
+  else ROWFN<D, 0>(b, bin, k, __VA_ARGS__);
+
+template <int D, int WA, int WB>
+__global__ void __launch_bounds__(128, 3)
+momentum_fused_kernel(StepBins b, const double* __restrict__ v, const double* __restrict__ T, int64_t N,
+                      MomentumCoef c, double* __restrict__ vstar) {
+  HN_FUSED_BODY(momentum_row, v, T, N, c, vstar)
+}
+
+template <int D, int WA, int WB>
+__global__ void __launch_bounds__(128, 4)
+div_rhs_fused_kernel(StepBins b, const double* __restrict__ vs, int64_t N, double dt, double* __restrict__ rhs) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) rhs[N] = 0.0;  // bordered gauge equation
+  HN_FUSED_BODY(div_row, vs, N, 0.0, dt, rhs)
+}
+
+template <int D, int WA, int WB>
+__global__ void __launch_bounds__(128, 4)
+correct_temp_fused_kernel(StepBins b, const double* __restrict__ vs, const double* __restrict__ p,
+                          const double* __restrict__ T, int64_t N, double dt, double* __restrict__ vout,
+                          double* __restrict__ Tout, int* __restrict__ flags) {
+  HN_FUSED_BODY(correct_temp_row, vs, p, T, N, dt, vout, Tout, flags)
+}
+#undef HN_FUSED_BODY
+
+// (WA, WB) pairs with a fused instantiation: the MON/RBF widths of configs 0-4
+#define HN_FUSED_PAIRS(X) X(2, 5, 12) X(2, 5, -1) X(2, 12, -1) X(3, 7, 20) X(3, 7, 30) X(3, 7, -1) X(3, 20, -1) X(3, 30, -1)
+
+// widths of the non-empty bins -> (wa, wb); false if more than two distinct or total too big
+static bool fused_pair(const StepBins& b, int d, int* wa, int* wb) {
+  int64_t rows = 0;
+  *wa = -1;
+  *wb = -1;
+  for (int i = 0; i < b.nbins; ++i) {
+    rows += b.K[i];
+    const int w = b.width[i];
+    if (w == 0 || w == *wa || w == *wb) continue;
+    if (*wa < 0) *wa = w;
+    else if (*wb < 0) *wb = w;
+    else return false;
+  }
+  if (rows > kFuseRows || *wa < 0) return false;
+  if (*wb >= 0 && *wb < *wa) { const int t = *wa; *wa = *wb; *wb = t; }
+  return true;
+}
+
 // ---- K11: temperature boundary conditions (solver.py:334-342) ----
 __global__ void dirichlet_kernel(const int* __restrict__ idx, const double* __restrict__ val, int64_t n,
                                  double* __restrict__ T) {
@@ -225,18 +284,41 @@ __global__ void dirichlet_kernel(const int* __restrict__ idx, const double* __re
 // Insulated rows: T[b] = -(sum_j W_bj t0_j) / W_bb with t0 = T, Neumann entries zeroed.
 // The Neumann block W[:, neu] is diagonal (boundary stencils exclude every other
 // boundary node), so SuperLU's solve of it is an elementwise division.
+// Sequential row dot product sum_e vals[e] * x[cols[e]] in ascending-entry order (scipy
+// csr_matvec: no FMA, one accumulator) with the loads of 8 entries issued before their
+// products are added -- the summation order is unchanged, only the memory latency overlaps.
+template <bool NEU_MASK>
+__device__ __forceinline__ double csr_row_seq(const int* __restrict__ cols, const double* __restrict__ vals,
+                                              const double* __restrict__ x, const uint8_t* __restrict__ is_neu,
+                                              int64_t e, int64_t e1) {
+  double acc = 0.0;
+  for (; e < e1; e += 8) {
+    int c[8];
+    double v[8], xv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      c[k] = e + k < e1 ? __ldg(cols + e + k) : -1;
+      v[k] = e + k < e1 ? __ldg(vals + e + k) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      xv[k] = c[k] >= 0 ? x[c[k]] : 0.0;
+      if (NEU_MASK && c[k] >= 0 && __ldg(is_neu + c[k])) xv[k] = 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (c[k] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[k], xv[k]));
+  }
+  return acc;
+}
+
 __global__ void neumann_kernel(const int64_t* __restrict__ rowptr, const int* __restrict__ cols,
                                const double* __restrict__ vals, const int* __restrict__ neu_idx,
                                const double* __restrict__ diag, const uint8_t* __restrict__ is_neu, int64_t nrows,
                                double* __restrict__ T) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
-  double acc = 0.0;
-  for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
-    const int c = cols[e];
-    const double t0 = is_neu[c] ? 0.0 : T[c];
-    acc = __dadd_rn(acc, __dmul_rn(vals[e], t0));
-  }
+  const double acc = csr_row_seq<true>(cols, vals, T, is_neu, rowptr[r], rowptr[r + 1]);
   T[neu_idx[r]] = __ddiv_rn(-acc, diag[r]);
 }
 
@@ -246,10 +328,7 @@ __global__ void csr_matvec_kernel(const int64_t* __restrict__ rowptr, const int*
                                   double* __restrict__ y) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
-  double acc = 0.0;
-  const int64_t e1 = __ldg(rowptr + r + 1);
-  for (int64_t e = __ldg(rowptr + r); e < e1; ++e) acc = __dadd_rn(acc, __dmul_rn(__ldg(vals + e), __ldg(x + __ldg(cols + e))));
-  y[r] = acc;
+  y[r] = csr_row_seq<false>(cols, vals, x, nullptr, __ldg(rowptr + r), __ldg(rowptr + r + 1));
 }
 
 // y = b - A x  (r0 of BiCGStab; scipy: b - matvec(x))
@@ -258,10 +337,7 @@ __global__ void csr_residual_kernel(const int64_t* __restrict__ rowptr, const in
                                     const double* __restrict__ b, int64_t nrows, double* __restrict__ y) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
-  double acc = 0.0;
-  const int64_t e1 = __ldg(rowptr + r + 1);
-  for (int64_t e = __ldg(rowptr + r); e < e1; ++e) acc = __dadd_rn(acc, __dmul_rn(__ldg(vals + e), __ldg(x + __ldg(cols + e))));
-  y[r] = __dsub_rn(b[r], acc);
+  y[r] = __dsub_rn(b[r], csr_row_seq<false>(cols, vals, x, nullptr, __ldg(rowptr + r), __ldg(rowptr + r + 1)));
 }
 
 void fill_bins(StepBins& b, int nbins, const int64_t* K, const int* W, const int* const* rows, const int* const* idx,
@@ -338,15 +414,23 @@ HN_EXPORT int hn_momentum(int nbins, const int64_t* bin_K_host, const int* bin_w
   MomentumCoef c{dt, Pr, t_ref, {0, 0, 0}, zero_boundary};
   for (int a = 0; a < d; ++a) c.buoy[a] = buoy_host[a];
   if (blocks == 0) return 0;
-  cudaStream_t s = as_stream(stream);
-  for (int i = 0; i < nbins; ++i) {
+  int wa, wb;
+  if (fused_pair(b, d, &wa, &wb)) {
+    cudaStream_t s = as_stream(stream);
+#define HN_X(DD, A, B) \
+    if (d == DD && wa == A && wb == B) { momentum_fused_kernel<DD, A, B><<<blocks, th, 0, s>>>(b, v, T, N, c, vstar); HN_CHECK_LAUNCH(); return 0; }
+    HN_FUSED_PAIRS(HN_X)
+#undef HN_X
+  }
+  // bins are independent row sets: their kernels run concurrently (fork/join)
+  launch_forked(as_stream(stream), nbins, [&](int i, cudaStream_t s) {
     StepBins one = single_bin(b, i);
     const int64_t bl = ceil_div(one.K[0], th);
-    if (bl == 0) continue;
+    if (bl == 0) return;
 #define HN_MOM(DD, WW) momentum_kernel<DD, WW><<<bl, th, 0, s>>>(one, v, T, N, c, vstar)
     HN_WIDTH_DISPATCH(d, one.width[0], HN_MOM);
 #undef HN_MOM
-  }
+  });
   HN_CHECK_LAUNCH();
   return 0;
 }
@@ -362,15 +446,22 @@ HN_EXPORT int hn_div_rhs(int nbins, const int64_t* bin_K_host, const int* bin_wi
   fill_bins(b, nbins, bin_K_host, bin_width_host, bin_rows_host, bin_idx_host, bin_w_host, th, &blocks);
   for (int a = 0; a < d; ++a) b.d_plane[a] = d_plane_host[a];
   if (blocks == 0) return 0;
-  cudaStream_t s = as_stream(stream);
-  for (int i = 0; i < nbins; ++i) {
+  int wa, wb;
+  if (fused_pair(b, d, &wa, &wb)) {
+    cudaStream_t s = as_stream(stream);
+#define HN_X(DD, A, B) \
+    if (d == DD && wa == A && wb == B) { div_rhs_fused_kernel<DD, A, B><<<blocks, th, 0, s>>>(b, vstar, N, dt, rhs); HN_CHECK_LAUNCH(); return 0; }
+    HN_FUSED_PAIRS(HN_X)
+#undef HN_X
+  }
+  launch_forked(as_stream(stream), nbins, [&](int i, cudaStream_t s) {
     StepBins one = single_bin(b, i);
     const int64_t bl = ceil_div(one.K[0], th);
-    if (bl == 0) continue;
-#define HN_DIV(DD, WW) div_rhs_kernel<DD, WW><<<bl, th, 0, s>>>(one, vstar, N, dt, rhs)
+    if (bl == 0) return;
+#define HN_DIV(DD, WW) div_rhs_kernel<DD, WW><<<bl, th, 0, s>>>(one, vstar, N, dt, rhs, i == 0)
     HN_WIDTH_DISPATCH(d, one.width[0], HN_DIV);
 #undef HN_DIV
-  }
+  });
   HN_CHECK_LAUNCH();
   return 0;
 }
@@ -388,15 +479,22 @@ HN_EXPORT int hn_correct_temperature(int nbins, const int64_t* bin_K_host, const
   b.lap_plane = lap_plane;
   for (int a = 0; a < d; ++a) b.d_plane[a] = d_plane_host[a];
   if (blocks == 0) return 0;
-  cudaStream_t s = as_stream(stream);
-  for (int i = 0; i < nbins; ++i) {
+  int wa, wb;
+  if (fused_pair(b, d, &wa, &wb)) {
+    cudaStream_t s = as_stream(stream);
+#define HN_X(DD, A, B) \
+    if (d == DD && wa == A && wb == B) { correct_temp_fused_kernel<DD, A, B><<<blocks, th, 0, s>>>(b, vstar, p, T, N, dt, vout, Tout, flags); HN_CHECK_LAUNCH(); return 0; }
+    HN_FUSED_PAIRS(HN_X)
+#undef HN_X
+  }
+  launch_forked(as_stream(stream), nbins, [&](int i, cudaStream_t s) {
     StepBins one = single_bin(b, i);
     const int64_t bl = ceil_div(one.K[0], th);
-    if (bl == 0) continue;
+    if (bl == 0) return;
 #define HN_COR(DD, WW) correct_temp_kernel<DD, WW><<<bl, th, 0, s>>>(one, vstar, p, T, N, dt, vout, Tout, flags)
     HN_WIDTH_DISPATCH(d, one.width[0], HN_COR);
 #undef HN_COR
-  }
+  });
   HN_CHECK_LAUNCH();
   return 0;
 }
