@@ -250,7 +250,31 @@ class DeviceTable:
 
     @property
     def ell_ok(self) -> bool:
+        if len([b for b in self.bins if b.K]) > 4:
+            self.compact()
         return all(b.width in ELL_WIDTHS for b in self.bins) and len([b for b in self.bins if b.K]) <= 4
+
+    def compact(self):
+        """Merge bins of equal width (e.g. the row chunks of compute_weights' overlapped
+        copy-back) into one ELL slab each: rows, idx and weights concatenated along K."""
+        t = L.torch()
+        by_w = {}
+        for b in self.bins:
+            by_w.setdefault(b.width, []).append(b)
+        merged = []
+        for w, group in by_w.items():
+            group = [b for b in group if b.K] or group[:1]
+            if len(group) == 1:
+                merged.append(group[0])
+                continue
+            K = sum(b.K for b in group)
+            rows = t.cat([b.d_rows[: b.K] for b in group])
+            idx = t.cat([b.d_idx[:, : b.K] for b in group], dim=1).contiguous()
+            wts = t.cat([b.d_w[:, :, : b.K] for b in group], dim=2).contiguous()
+            nb = Bin(None, w, idx, wts, d_rows=rows, K=K)
+            nb.mon = getattr(group[0], "mon", False)
+            merged.append(nb)
+        self.bins = merged
 
     def sizes(self) -> np.ndarray:
         s = np.zeros(self.n, dtype=np.int64)

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib as L
-from ._device import Bin, DeviceTable, device_nodes
+from ._device import Bin, DeviceTable, bins_args, device_nodes
 from .errors import SingularSystemError
 from .nodegen import KIND_BOUNDARY, KIND_REGULAR, LATTICE_NONE
 
@@ -419,6 +419,121 @@ def _interior_device_table(nodeset, ops, n_rbf: int | None = None, host_copy: bo
     return dev
 
 
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream():
+    t = L.torch()
+    dev = t.cuda.current_device()
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = t.cuda.Stream()
+    return _COPY_STREAMS[dev]
+
+
+def _copyback_chunks(nodeset, ops, n_rbf: int | None = None) -> int:
+    """Chunks for the overlapped copy-back: one per ~96 MB of padded host table (each chunk
+    costs ~0.15 ms of host launch work, which a small table's copy cannot hide)."""
+    n_rbf = RBF_SIZE[nodeset.dim] if n_rbf is None else n_rbf
+    table_bytes = len(nodeset) * n_rbf * 8 * (len(list(ops)) + 1)
+    return int(min(8, max(1, table_bytes // (96 << 20))))
+
+
+def _interior_host_table(nodeset, ops, n_rbf: int | None = None, chunks: int | None = None) -> DeviceTable:
+    """_interior_device_table for the public compute_weights: the RBF rows are solved in
+    node-ordered chunks and every chunk's slice of the host WeightTable is copied back on a
+    second stream while the next chunk computes (the D2H of the padded table is the
+    largest cost of the call).  Same arithmetic, same results; one synchronisation."""
+    dim = nodeset.dim
+    n = len(nodeset)
+    n_rbf = RBF_SIZE[dim] if n_rbf is None else n_rbf
+    dn = device_nodes(nodeset)
+    t = L.torch()
+    s = t.cuda.current_stream()
+    has_lattice = getattr(nodeset, "lattice", None) is not None and getattr(nodeset, "lattice_idx", None) is not None
+    if has_lattice or not np.any(np.asarray(nodeset.kind) == KIND_REGULAR):
+        method_d = dn.classify()
+    else:  # probe path without a lattice map (approx.py:352-356)
+        method_d = L.to_device(classify_methods(nodeset))
+    rows_d = L.empty(max(n, 1), t.int32)
+    counts_d = L.empty(3, t.int32)
+    scratch = L.empty(3 * (n // 256 + 1) + 1, t.int32)
+    L.call("hn_partition_methods", L.ptr(method_d), n, L.ptr(rows_d), L.ptr(counts_d), L.ptr(scratch),
+           L.stream_handle())
+    kind = np.asarray(nodeset.kind)
+    rbf_rows_h = None
+    if not np.any(kind == KIND_REGULAR):
+        rbf_rows_h = np.nonzero(kind != KIND_BOUNDARY)[0]  # = the device partition's RBF segment
+        k_rbf = len(rbf_rows_h)
+        k_mon, k_none = 0, n - k_rbf
+    else:
+        k_mon, k_rbf, k_none = (int(v) for v in counts_d.cpu().numpy())
+    if k_rbf and n_rbf > n:
+        raise ValueError(f"stencil size {n_rbf} exceeds node count {n}")
+    nops, m = len(ops), n_rbf
+    if chunks is None:
+        chunks = _copyback_chunks(nodeset, ops, n_rbf)
+    chunks = int(max(1, min(chunks, k_rbf))) if k_rbf else 1
+    bounds = np.linspace(0, k_rbf, chunks + 1).astype(np.int64) if k_rbf else np.zeros(1, np.int64)
+    # node id where each chunk's slice of the table starts (rows are ascending node ids)
+    if k_rbf and chunks > 1:
+        if rbf_rows_h is not None:
+            cut = rbf_rows_h[bounds[1:-1]]
+        else:
+            cut = rows_d[k_mon + L.to_device(bounds[1:-1])].cpu().numpy()
+        starts = np.concatenate([[0], cut, [n]]).astype(np.int64)
+    else:
+        starts = np.array([0, n], dtype=np.int64)
+    d_idx = L.empty((max(n, 1), m), t.int64)
+    d_sizes = L.zeros(max(n, 1), t.int64)
+    d_w = L.empty((nops, max(n, 1), m), t.float64)
+    h_idx = t.empty(d_idx.shape, dtype=t.int64, pin_memory=True)
+    h_sizes = t.empty(d_sizes.shape, dtype=t.int64, pin_memory=True)
+    h_w = t.empty(d_w.shape, dtype=t.float64, pin_memory=True)
+    h_m = t.empty(max(n, 1), dtype=t.int8, pin_memory=True)
+
+    def to_table(bb):
+        nb, K, W, R, I, Wt, live = bins_args(bb)
+        if nb:
+            L.call("hn_ell_to_table", nb, K, W, R, I, Wt, nops, m, n, L.ptr(d_idx), L.ptr(d_sizes), L.ptr(d_w),
+                   L.stream_handle())
+
+    bins, pending = [], []
+    if k_mon:
+        d_rows = rows_d[:k_mon]
+        st = dn.mon_stencils(d_rows) if has_lattice else dn.knn(MON_SIZE[dim], rows=d_rows)
+        pending.append(_solve_bin(dn, st, d_rows, ops, True))
+        bins.append(pending[-1][0])
+    if k_none:
+        bins.append(Bin(None, 0, L.empty((0, k_none), t.int32), L.empty((nops, 0, k_none), t.float64),
+                        d_rows=rows_d[k_mon + k_rbf:n], K=k_none))
+    to_table(bins)  # MON and empty rows first: every chunk slice below is then complete
+    cs = _copy_stream()
+    for c in range(len(starts) - 1):
+        if k_rbf:
+            d_rows = rows_d[k_mon + bounds[c]: k_mon + bounds[c + 1]]
+            pending.append(_solve_bin(dn, dn.knn(n_rbf, rows=d_rows, fine=True), d_rows, ops, False))
+            bins.append(pending[-1][0])
+            to_table([pending[-1][0]])
+        lo, hi = int(starts[c]), int(starts[c + 1])
+        cs.wait_stream(s)
+        with t.cuda.stream(cs):
+            h_idx[lo:hi].copy_(d_idx[lo:hi], non_blocking=True)
+            h_sizes[lo:hi].copy_(d_sizes[lo:hi], non_blocking=True)
+            for o in range(nops):
+                h_w[o, lo:hi].copy_(d_w[o, lo:hi], non_blocking=True)
+    cs.wait_stream(s)
+    with t.cuda.stream(cs):
+        h_m[:n].copy_(method_d[:n], non_blocking=True)
+    for x in (d_idx, d_sizes, d_w, method_d):  # keep the sources alive until the copies ran
+        x.record_stream(cs)
+    s.wait_stream(cs)
+    L.TRAFFIC["d2h"] += h_idx.nbytes + h_sizes.nbytes + h_w.nbytes + n
+    dev = DeviceTable(n, dim, list(ops), bins, n_rbf, method_d[:n])
+    dev._pending = (h_idx, h_sizes, h_w, h_m, (d_idx, d_sizes, d_w))
+    _check_info(pending)  # the one synchronisation: flags, after every copy on s's timeline
+    return dev
+
+
 class WeightsPipeline:
     """compute_weights for a fixed node set as one host-sync-free launch sequence
     (cell list -> classify -> partition -> MON stencils + solves -> kNN + RBF-FD solves),
@@ -542,12 +657,16 @@ def compute_weights(nodeset, ops, with_kappa: bool = False, tree=None, rbf_n: in
     return _compute_weights(nodeset, ops, with_kappa, rbf_n, host_copy=True)
 
 
+
 def _compute_weights(nodeset, ops, with_kappa: bool = False, rbf_n: int | None = None,
                      host_copy: bool = False) -> WeightTable:
     ops = list(ops)
     for op in ops:
         _op_code(op, nodeset.dim)
-    dev = _interior_device_table(nodeset, ops, rbf_n, host_copy=host_copy)
+    if host_copy and _copyback_chunks(nodeset, ops, rbf_n) > 1:
+        dev = _interior_host_table(nodeset, ops, rbf_n)
+    else:
+        dev = _interior_device_table(nodeset, ops, rbf_n, host_copy=host_copy)
     table = WeightTable(_device=dev)
     if with_kappa:
         kappa = np.full(len(nodeset), np.nan)
