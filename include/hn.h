@@ -39,6 +39,13 @@ extern "C" {
  * cell_start: ncells+1, cell_items: N, cell_pos: N*stride, scratch_count: ncells,
  * scratch_point_cell: N, with ncells = prod(dims_host[0..d)).
  * Replaces: cKDTree(nodeset.positions)  approx.py:386, solver.py:144. */
+/* Node-set statistics for the cell-list sizing, one pass: out (device, 2d+2 fp64) =
+ * [min x_a (d) | max x_a (d) | sum of spacing over kind == 1 | count of kind == 1].
+ * pos: N x d fp64 (unpadded); kind / spacing may be NULL; scratch: 8 u64 (device).
+ * Replaces: the np.min/np.max bounding box and mean spacing the host would compute. */
+int hn_node_stats(const double* pos, int64_t n, int d, const int8_t* kind, const double* spacing, double* out,
+                  void* scratch, void* stream);
+
 int hn_celllist_build(const double* pos, int64_t n, int d, const double* lo_host, double cell,
                       const int* dims_host, int* cell_start, int* cell_items, double* cell_pos,
                       int* scratch_count, int* scratch_point_cell, void* stream);

@@ -45,13 +45,16 @@ class DeviceNodes:
         # bounding box / mean scattered spacing are computed on the device, with one small
         # read-back -- the host-side numpy passes cost ~25 ms at N = 1e6
         kind_h = np.asarray(nodeset.kind, dtype=np.int8)
-        raw = L.to_device(pos)
+        spacing = getattr(nodeset, "spacing", None)
+        up = [pos, kind_h] + ([np.asarray(spacing, dtype=float)] if spacing is not None else [])
+        got = L.to_device_many(up)  # one pinned staging buffer, one DMA
+        raw, self.kind = got[0], got[1]
+        self.spacing = got[2] if spacing is not None else None  # per-node spacing: kNN first radius
         if self.stride == self.dim:
             self.pos = raw
         else:
             self.pos = L.zeros((self.n, self.stride), t.float64)
             self.pos[:, : self.dim] = raw
-        self.kind = L.to_device(kind_h)
         self.lattice_grid = self.lattice_idx = None
         self.grid_dims = None
         lat = getattr(nodeset, "lattice", None)
@@ -59,24 +62,20 @@ class DeviceNodes:
         if lat is not None and lidx is not None:
             grid = np.asarray(lat.grid)
             self.grid_dims = list(grid.shape)
-            self.lattice_grid = L.to_device(grid).to(t.int32)
-            li = L.to_device(np.asarray(lidx))
+            g_d, li = L.to_device_many([grid, np.asarray(lidx)])
+            self.lattice_grid = g_d.to(t.int32)
             if li.dtype == t.int64:
                 li = t.where(li == np.iinfo(np.int64).min, INT32_MIN, li)
             self.lattice_idx = li.to(t.int32).contiguous()
-        spacing = getattr(nodeset, "spacing", None)
-        scattered = self.kind == 1
-        self.spacing = None  # per-node nominal spacing: sizes each kNN query's first radius
         if self.n:
-            stats = [raw.amin(0), raw.amax(0)]
-            if spacing is not None:
-                sp = L.to_device(np.asarray(spacing, dtype=float))
-                self.spacing = sp
-                cnt = scattered.sum()
-                stats.append(t.stack([t.where(scattered, sp, 0.0).sum(), cnt.to(t.float64)]))
-            st = t.cat(stats).cpu().numpy()
+            # bounding box + mean scattered spacing in one kernel pass, one small read-back
+            st_d = L.empty(2 * self.dim + 2, t.float64)
+            scratch = L.empty(8, t.int64)
+            L.call("hn_node_stats", L.ptr(raw), self.n, self.dim, L.ptr(self.kind), L.ptr(self.spacing),
+                   L.ptr(st_d), L.ptr(scratch), L.stream_handle())
+            st = st_d.cpu().numpy()
             lo, hi = st[: self.dim], st[self.dim: 2 * self.dim]
-            mean_h = st[2 * self.dim] / st[2 * self.dim + 1] if spacing is not None and st[-1] > 0 else None
+            mean_h = st[2 * self.dim] / st[2 * self.dim + 1] if self.spacing is not None and st[-1] > 0 else None
         else:
             lo, hi, mean_h = np.zeros(self.dim), np.ones(self.dim), None
         # uniform cell list: ~1 node per cell in 2D, ~2 in 3D

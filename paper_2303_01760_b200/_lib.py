@@ -29,6 +29,7 @@ SIGNATURES: dict[str, tuple] = {
     "hn_version": (_i, []),
     "hn_bench_dfma": (_i, [_vp, _i, _i, _vp]),
     "hn_bench_dmma": (_i, [_vp, _i, _i, _vp]),
+    "hn_node_stats": (_i, [_vp, _i64, _i, _vp, _vp, _vp, _vp, _vp]),
     "hn_celllist_build": (_i, [_vp, _i64, _i, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hn_knn": (_i, [_vp, _i, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp, _vp, _vp, _i64, _i, _vp, _vp, _vp, _vp]),
     "hn_knn_spacing": (_i, [_vp, _i, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp, _vp, _vp, _i64, _i, _vp, _vp, _vp, _vp,
@@ -169,6 +170,34 @@ def to_device(a: np.ndarray, dtype=None):
     stage = t.empty(src.shape, dtype=src.dtype, pin_memory=True)
     stage.copy_(src)
     return stage.to(device(), non_blocking=True)
+
+
+def to_device_many(arrays):
+    """Upload several host arrays with one pinned staging buffer and one DMA; returns device
+    tensors (8-byte aligned segments of one allocation)."""
+    t = torch()
+    arrs = [np.ascontiguousarray(a) for a in arrays]
+    offs, total = [], 0
+    for a in arrs:
+        offs.append(total)
+        total += (a.nbytes + 7) // 8 * 8
+    stage = t.empty(max(total, 8), dtype=t.uint8, pin_memory=True)
+    for a, o in zip(arrs, offs):  # torch's CPU copy is multi-threaded (numpy's is not)
+        stage[o:o + a.nbytes].copy_(t.from_numpy(a.reshape(-1).view(np.uint8)))
+    dev = stage.to(device(), non_blocking=True)
+    TRAFFIC["h2d"] += total
+    out = []
+    for a, o in zip(arrs, offs):
+        tt = _np_to_torch_dtype(a.dtype)
+        seg = dev[o:o + (a.nbytes + 7) // 8 * 8].view(tt)
+        out.append(seg[: a.size].view(a.shape))
+    return out
+
+
+def _np_to_torch_dtype(dt):
+    t = torch()
+    return {np.dtype(np.float64): t.float64, np.dtype(np.int64): t.int64, np.dtype(np.int32): t.int32,
+            np.dtype(np.int8): t.int8, np.dtype(np.uint8): t.uint8}[np.dtype(dt)]
 
 
 def empty(shape, dtype):

@@ -624,6 +624,94 @@ static Grid make_grid(const double* lo_host, double cell, const int* dims_host, 
   return g;
 }
 
+namespace hn {
+// ---- node-set statistics for the cell-list sizing: per-axis min/max of the positions and
+// the sum/count of the scattered nodes' spacing, one pass, one launch.  Doubles are
+// min/max-reduced as order-preserving 64-bit keys with integer atomics.
+__device__ __forceinline__ unsigned long long ord_key(double x) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+// out (device, 8 u64): [min key x,y,z | max key x,y,z | sum(spacing) bits | count]
+__global__ void __launch_bounds__(256) node_stats_kernel(const double* __restrict__ pos, int d, int64_t n,
+                                                         const int8_t* __restrict__ kind,
+                                                         const double* __restrict__ spacing,
+                                                         unsigned long long* __restrict__ out) {
+  unsigned long long mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0ull, 0ull, 0ull};
+  double hs = 0.0;
+  unsigned long long cnt = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    for (int a = 0; a < d; ++a) {
+      const unsigned long long k = ord_key(__ldg(pos + i * d + a));
+      mn[a] = min(mn[a], k);
+      mx[a] = max(mx[a], k);
+    }
+    if (spacing && kind && __ldg(kind + i) == 1) {
+      hs += __ldg(spacing + i);
+      ++cnt;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    for (int a = 0; a < 3; ++a) {
+      mn[a] = min(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+      mx[a] = max(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+    }
+    hs += __shfl_xor_sync(0xffffffffu, hs, o);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    for (int a = 0; a < d; ++a) {
+      atomicMin(out + a, mn[a]);
+      atomicMax(out + 3 + a, mx[a]);
+    }
+    if (cnt) {
+      atomicAdd(reinterpret_cast<double*>(out + 6), hs);
+      atomicAdd(out + 7, cnt);
+    }
+  }
+}
+
+__global__ void node_stats_init_kernel(unsigned long long* out) {
+  const int t = threadIdx.x;
+  if (t < 8) out[t] = t < 3 ? ~0ull : 0ull;
+}
+
+__global__ void node_stats_finish_kernel(const unsigned long long* in, double* out, int d) {
+  const int t = threadIdx.x;
+  if (t < d) {
+    out[t] = ord_val(in[t]);
+    out[d + t] = ord_val(in[3 + t]);
+  }
+  if (t == 0) {
+    out[2 * d] = __longlong_as_double(static_cast<long long>(in[6]));
+    out[2 * d + 1] = static_cast<double>(in[7]);
+  }
+}
+
+}  // namespace hn
+
+HN_EXPORT int hn_node_stats(const double* pos, int64_t n, int d, const int8_t* kind, const double* spacing,
+                            double* out, void* scratch, void* stream) {
+  if (d < 1 || d > 3) return 1;
+  cudaStream_t s = as_stream(stream);
+  auto* acc = static_cast<unsigned long long*>(scratch);
+  node_stats_init_kernel<<<1, 32, 0, s>>>(acc);
+  if (n > 0) {
+    const int64_t cap = static_cast<int64_t>(sm_count()) * 4;
+    const int64_t blocks = ceil_div(n, 256) < cap ? ceil_div(n, 256) : cap;
+    node_stats_kernel<<<blocks, 256, 0, s>>>(pos, d, n, kind, spacing, acc);
+  }
+  node_stats_finish_kernel<<<1, 32, 0, s>>>(acc, out, d);
+  HN_CHECK_LAUNCH();
+  return 0;
+}
+
 HN_EXPORT int hn_celllist_build(const double* pos, int64_t n, int d, const double* lo_host, double cell,
                                 const int* dims_host, int* cell_start, int* cell_items, double* cell_pos,
                                 int* scratch_count, int* scratch_point_cell, void* stream) {
