@@ -142,6 +142,10 @@ int hn_ell_to_table(int nbins, const int64_t* bin_K_host, const int* bin_width_h
  * d_plane_host[0..d) select the Laplacian and d/dx_a weight planes.  State is SoA:
  * v[c*N + i]. */
 
+/* Optional hyper-dissipation (PhysicsParams.dissipation != 0, solver.py:235-247): hyper_coef
+ * (N fp64) = -coeff * spacing**3 as numpy computes it, hyper_lap2 = lap(lap(field)) (d x N
+ * for hn_momentum, N for hn_correct_temperature); the term (hyper_coef * |v|) * hyper_lap2
+ * is added to the right-hand side.  Both NULL = off. */
 /* v* = v + dt*(-(v.grad)v + Pr lap v - buoy_c (T - t_ref)); buoy_host[c] = (Ra*Pr)*g[c].
  * zero_boundary != 0 fuses apply_velocity_bc (v* = 0 on the width-0 bin rows).
  * Replaces: momentum_predict + apply_velocity_bc solver.py:250-280. */
@@ -149,7 +153,8 @@ int hn_momentum(int nbins, const int64_t* bin_K_host, const int* bin_width_host,
                 const int* const* bin_rows_host, const int* const* bin_idx_host,
                 const double* const* bin_w_host, int lap_plane, const int* d_plane_host, int d,
                 const double* v, const double* T, int64_t N, double dt, double Pr, double t_ref,
-                const double* buoy_host, int zero_boundary, double* vstar, void* stream);
+                const double* buoy_host, int zero_boundary, const double* hyper_coef,
+                const double* hyper_lap2, double* vstar, void* stream);
 
 /* rhs[0..N) = (sum_a D_a v*_a)/dt on interior rows, 0 on boundary rows; rhs[N] = 0.
  * Replaces: solver.py:295-301. */
@@ -165,7 +170,8 @@ int hn_correct_temperature(int nbins, const int64_t* bin_K_host, const int* bin_
                            const int* const* bin_rows_host, const int* const* bin_idx_host,
                            const double* const* bin_w_host, int lap_plane, const int* d_plane_host, int d,
                            const double* vstar, const double* p, const double* T, int64_t N, double dt,
-                           double* vout, double* Tout, int* flags, void* stream);
+                           double* vout, double* Tout, int* flags, const double* hyper_coef,
+                           const double* hyper_lap2, void* stream);
 
 /* T[dir_idx] = dir_val; T[neu_idx[r]] = -(W_r . t0) / neu_diag[r], t0 = T with Neumann
  * entries zeroed (is_neu mask).  Replaces: apply_temperature_bc solver.py:334-342. */

@@ -364,23 +364,34 @@ def build_operators(ns, cold_origins, beta=0.1, gauge=None, rbf_n=None, table=No
     span = (vals.max() - vals.min()) if len(vals) else 1.0
     o.nu_scale = float(np.max(ns.positions.max(axis=0) - ns.positions.min(axis=0))) / (span if span > 0 else 1.0)
     o.lam = 0.0
+    o.spacing = np.asarray(ns.spacing, dtype=float)
     return o
 
 
-def momentum(o, v, T, Ra, Pr, t_ref, dt, g=None):
-    """v* (no BC) -- reference solver.py:250-274 (dissipation = 0)."""
+def hyper_dissipation(o, field, speed, coeff):
+    """-coeff * h^3 |v| lap(lap(field)), inner boundary rows zeroed -- reference solver.py:235-247."""
+    inner = o.lap @ field
+    inner[o.boundary_idx] = 0.0
+    return -coeff * o.spacing ** 3 * speed * (o.lap @ inner)
+
+
+def momentum(o, v, T, Ra, Pr, t_ref, dt, g=None, dissipation=0.0):
+    """v* (no BC) -- reference solver.py:250-274."""
     dim = o.dim
     if g is None:
         g = np.zeros(dim)
         g[-1] = -1.0
     tdelta = T - t_ref
     out = np.empty_like(v)
+    speed = np.linalg.norm(v, axis=1)
     grads = [[o.d[a] @ v[:, c] for a in range(dim)] for c in range(dim)]
     for c in range(dim):
         adv = v[:, 0] * grads[c][0]
         for a in range(1, dim):
             adv += v[:, a] * grads[c][a]
         rhs = -adv + Pr * (o.lap @ v[:, c]) - Ra * Pr * g[c] * tdelta
+        if dissipation:
+            rhs += hyper_dissipation(o, v[:, c], speed, dissipation)
         out[:, c] = v[:, c] + dt * rhs
     return out
 
@@ -423,12 +434,15 @@ def temperature_bc(o, T):
     return T
 
 
-def temperature(o, v, T, dt):
-    """reference solver.py:345-358 (dissipation = 0)."""
+def temperature(o, v, T, dt, dissipation=0.0):
+    """reference solver.py:345-358."""
     conv = v[:, 0] * (o.d[0] @ T)
     for a in range(1, o.dim):
         conv += v[:, a] * (o.d[a] @ T)
-    out = T + dt * (-conv + (o.lap @ T))
+    rhs = -conv + (o.lap @ T)
+    if dissipation:
+        rhs += hyper_dissipation(o, T, np.linalg.norm(v, axis=1), dissipation)
+    out = T + dt * rhs
     return temperature_bc(o, out)
 
 
@@ -439,14 +453,14 @@ def nusselt(o, T):
     return float(o.nu_scale * np.mean(np.abs(o.nu_rows @ T)))
 
 
-def step(o, state, Ra, Pr, t_ref, dt, p_prev=None, tol=1e-8):
+def step(o, state, Ra, Pr, t_ref, dt, p_prev=None, tol=1e-8, dissipation=0.0):
     """One run() loop body -- reference solver.py:439-452."""
     v, T = state
-    vstar = momentum(o, v, T, Ra, Pr, t_ref, dt)
+    vstar = momentum(o, v, T, Ra, Pr, t_ref, dt, dissipation=dissipation)
     vstar[o.boundary_idx] = 0.0
     p = pressure(o, vstar, dt, x0=p_prev, tol=tol)
     v_new = correct(o, vstar, p, dt)
-    T_new = temperature(o, v_new, T, dt)
+    T_new = temperature(o, v_new, T, dt, dissipation=dissipation)
     probe = float(np.sum(T_new)) + float(np.sum(v_new))
     if not math.isfinite(probe):
         raise FloatingPointError("non-finite field")

@@ -103,7 +103,7 @@ def boundary_block(rns, prefix, cold_origins, size_override=None):
     return out
 
 
-def steps_block(rns, prefix, n_steps, Ra, Pr, seed=11, table_rbf_n=None):
+def steps_block(rns, prefix, n_steps, Ra, Pr, seed=11, table_rbf_n=None, dissipation=0.0):
     """Replicates run()'s loop body (solver.py:439-452) from T = (x - 0.5) + 1e-3 noise."""
     dim = rns.dim
     settings = R_solver.PoissonSolveSettings()
@@ -126,7 +126,7 @@ def steps_block(rns, prefix, n_steps, Ra, Pr, seed=11, table_rbf_n=None):
         R_solver.compute_weights = R_approx.compute_weights
         R_approx.RBF_SIZE.clear()
         R_approx.RBF_SIZE.update(saved)
-    params = R_solver.PhysicsParams(Ra, Pr, t_ref=0.0)
+    params = R_solver.PhysicsParams(Ra, Pr, t_ref=0.0, dissipation=dissipation)
     dt = R_solver.TimeControls.from_spacing(float(np.min(rns.spacing)), 1.0, Ra=Ra).dt
     rng = np.random.default_rng(seed)
     n = len(rns)
@@ -147,12 +147,13 @@ def steps_block(rns, prefix, n_steps, Ra, Pr, seed=11, table_rbf_n=None):
         state.velocity = v_new
         state.pressure = p
         p_prev = p
-        state.temperature = R_solver.temperature_step(state, ops, dt)
+        state.temperature = R_solver.temperature_step(state, ops, dt, params.dissipation)
         if k == 1:
             out[f"{prefix}v1"], out[f"{prefix}T1"], out[f"{prefix}p1"] = v_new.copy(), state.temperature.copy(), p.copy()
     out[f"{prefix}vK"], out[f"{prefix}TK"], out[f"{prefix}pK"] = (state.velocity.copy(), state.temperature.copy(),
                                                                  state.pressure.copy())
     out[f"{prefix}steps"] = n_steps
+    out[f"{prefix}dissipation"] = dissipation
     out[f"{prefix}nuK"] = R_solver.nusselt_average(state, ops)
     return out
 
@@ -176,7 +177,8 @@ def main():
     cfg = CaseConfig(case="dvd", h_r=0.0398)
     ns = R_nodegen.hybrid_discretize(cfg, build_domain(cfg))
     w, _ = weights_block(ns, 2, "", names2)
-    save("dvd_coarse", ns, [w, boundary_block(ns, "", {"wall:x-"}), steps_block(ns, "", 20, 1e6, 0.71)])
+    save("dvd_coarse", ns, [w, boundary_block(ns, "", {"wall:x-"}), steps_block(ns, "", 20, 1e6, 0.71),
+                            steps_block(ns, "hd_", 20, 1e6, 0.71, dissipation=0.05)])
 
     # 2) the reference's pure-scattered fixture (conftest.py:31-36)
     cfg = CaseConfig(case="dvd", h_r=0.05, discretization="pure-scattered")

@@ -45,7 +45,20 @@ struct MomentumCoef {
   double dt, Pr, t_ref;
   double buoy[3];  // (Ra * Pr) * g[c]
   int zero_boundary;
+  // optional hyper-dissipation (solver.py:235-247): hc[i] = -coeff * h_i**3 (host numpy),
+  // l2 = lap(lap(v_c)) per component (SoA); term = (hc * |v|) * l2, added to rhs
+  const double* hc;
+  const double* l2;
 };
+
+// |v_row| as np.linalg.norm(v, axis=1): sqrt((v0*v0 + v1*v1) [+ v2*v2])
+template <int D>
+__device__ __forceinline__ double speed_of(const double* vr) {
+  double s = __dmul_rn(vr[0], vr[0]);
+#pragma unroll
+  for (int a = 1; a < D; ++a) s = __dadd_rn(s, __dmul_rn(vr[a], vr[a]));
+  return __dsqrt_rn(s);
+}
 
 template <int D, int W>
 __device__ __forceinline__ void momentum_row(const StepBins& b, int bin, int64_t k, const double* __restrict__ v,
@@ -68,7 +81,13 @@ __device__ __forceinline__ void momentum_row(const StepBins& b, int bin, int64_t
           adv = (a == 0) ? t : __dadd_rn(adv, t);
         }
         const double tdelta = __dsub_rn(__ldg(T + row), c.t_ref);
-        const double rhs = __dsub_rn(__dadd_rn(-adv, __dmul_rn(c.Pr, 0.0)), __dmul_rn(c.buoy[cc], tdelta));
+        double rhs = __dsub_rn(__dadd_rn(-adv, __dmul_rn(c.Pr, 0.0)), __dmul_rn(c.buoy[cc], tdelta));
+        if (c.hc) {
+          double vr[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) vr[a] = __ldg(v + a * N + row);
+          rhs = __dadd_rn(rhs, __dmul_rn(__dmul_rn(__ldg(c.hc + row), speed_of<D>(vr)), __ldg(c.l2 + cc * N + row)));
+        }
         out = __dadd_rn(vc, __dmul_rn(c.dt, rhs));
       }
       vstar[cc * N + row] = out;
@@ -97,7 +116,9 @@ __device__ __forceinline__ void momentum_row(const StepBins& b, int bin, int64_t
         adv = (a == 0) ? t : __dadd_rn(adv, t);
       }
       const double lap = ssum<W>(wb + b.lap_plane * ps, K, k, fv);
-      const double rhs = __dsub_rn(__dadd_rn(-adv, __dmul_rn(c.Pr, lap)), __dmul_rn(c.buoy[cc], tdelta));
+      double rhs = __dsub_rn(__dadd_rn(-adv, __dmul_rn(c.Pr, lap)), __dmul_rn(c.buoy[cc], tdelta));
+      if (c.hc)
+        rhs = __dadd_rn(rhs, __dmul_rn(__dmul_rn(__ldg(c.hc + row), speed_of<D>(vi)), __ldg(c.l2 + cc * N + row)));
       vstar[cc * N + row] = __dadd_rn(vi[cc], __dmul_rn(c.dt, rhs));
     }
   }
@@ -150,11 +171,16 @@ div_rhs_kernel(StepBins b, const double* __restrict__ vs, int64_t N, double dt,
 }
 
 // ---- K10: velocity correction + temperature advection-diffusion (solver.py:317-331, 345-357) ----
+struct HyperT {  // optional hyper-dissipation of T: hc = -coeff * h**3, l2 = lap(lap(T))
+  const double* hc;
+  const double* l2;
+};
+
 template <int D, int W>
 __device__ __forceinline__ void correct_temp_row(const StepBins& b, int bin, int64_t k, const double* __restrict__ vs,
                                                  const double* __restrict__ p, const double* __restrict__ T,
                                                  int64_t N, double dt, double* __restrict__ vout,
-                                                 double* __restrict__ Tout, int* __restrict__ flags) {
+                                                 double* __restrict__ Tout, int* __restrict__ flags, HyperT hy) {
   const int64_t K = b.K[bin];
   const int row = __ldg(b.rows[bin] + k);
   double vn[D];
@@ -164,7 +190,9 @@ __device__ __forceinline__ void correct_temp_row(const StepBins& b, int bin, int
     for (int a = 0; a < D; ++a) vn[a] = 0.0;
     // empty operator rows: conv = 0, lap = 0  ->  T + dt * (-0 + 0)
     const double Ti = __ldg(T + row);
-    tn = __dadd_rn(Ti, __dmul_rn(dt, __dadd_rn(-0.0, 0.0)));
+    double r = __dadd_rn(-0.0, 0.0);
+    if (hy.hc) r = __dadd_rn(r, __dmul_rn(__dmul_rn(__ldg(hy.hc + row), speed_of<D>(vn)), __ldg(hy.l2 + row)));
+    tn = __dadd_rn(Ti, __dmul_rn(dt, r));
   } else {
     int id[W];
 #pragma unroll
@@ -190,7 +218,9 @@ __device__ __forceinline__ void correct_temp_row(const StepBins& b, int bin, int
       conv = (a == 0) ? t : __dadd_rn(conv, t);
     }
     const double lap = ssum<W>(wb + b.lap_plane * ps, K, k, ft);
-    tn = __dadd_rn(__ldg(T + row), __dmul_rn(dt, __dadd_rn(-conv, lap)));
+    double r = __dadd_rn(-conv, lap);
+    if (hy.hc) r = __dadd_rn(r, __dmul_rn(__dmul_rn(__ldg(hy.hc + row), speed_of<D>(vn)), __ldg(hy.l2 + row)));
+    tn = __dadd_rn(__ldg(T + row), __dmul_rn(dt, r));
   }
   bool bad = !isfinite(tn);
 #pragma unroll
@@ -209,10 +239,10 @@ template <int D, int W>
 __global__ void __launch_bounds__(128, (W <= 7 ? 8 : (W <= 12 ? 6 : (W <= 20 ? 4 : 2))))
 correct_temp_kernel(StepBins b, const double* __restrict__ vs, const double* __restrict__ p,
                     const double* __restrict__ T, int64_t N, double dt, double* __restrict__ vout,
-                    double* __restrict__ Tout, int* __restrict__ flags) {
+                    double* __restrict__ Tout, int* __restrict__ flags, HyperT hy) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= b.K[0]) return;
-  correct_temp_row<D, W>(b, 0, k, vs, p, T, N, dt, vout, Tout, flags);
+  correct_temp_row<D, W>(b, 0, k, vs, p, T, N, dt, vout, Tout, flags, hy);
 }
 
 // ---- one launch for every bin of a phase (small node sets) ----
@@ -248,8 +278,8 @@ template <int D, int WA, int WB>
 __global__ void __launch_bounds__(128, 4)
 correct_temp_fused_kernel(StepBins b, const double* __restrict__ vs, const double* __restrict__ p,
                           const double* __restrict__ T, int64_t N, double dt, double* __restrict__ vout,
-                          double* __restrict__ Tout, int* __restrict__ flags) {
-  HN_FUSED_BODY(correct_temp_row, vs, p, T, N, dt, vout, Tout, flags)
+                          double* __restrict__ Tout, int* __restrict__ flags, HyperT hy) {
+  HN_FUSED_BODY(correct_temp_row, vs, p, T, N, dt, vout, Tout, flags, hy)
 }
 #undef HN_FUSED_BODY
 
@@ -403,7 +433,8 @@ HN_EXPORT int hn_momentum(int nbins, const int64_t* bin_K_host, const int* bin_w
                           const int* const* bin_rows_host, const int* const* bin_idx_host,
                           const double* const* bin_w_host, int lap_plane, const int* d_plane_host, int d,
                           const double* v, const double* T, int64_t N, double dt, double Pr, double t_ref,
-                          const double* buoy_host, int zero_boundary, double* vstar, void* stream) {
+                          const double* buoy_host, int zero_boundary, const double* hyper_coef,
+                          const double* hyper_lap2, double* vstar, void* stream) {
   if (!ok_bins(nbins, bin_width_host) || (d != 2 && d != 3)) return 1;
   StepBins b{};
   int64_t blocks;
@@ -411,7 +442,8 @@ HN_EXPORT int hn_momentum(int nbins, const int64_t* bin_K_host, const int* bin_w
   fill_bins(b, nbins, bin_K_host, bin_width_host, bin_rows_host, bin_idx_host, bin_w_host, th, &blocks);
   b.lap_plane = lap_plane;
   for (int a = 0; a < d; ++a) b.d_plane[a] = d_plane_host[a];
-  MomentumCoef c{dt, Pr, t_ref, {0, 0, 0}, zero_boundary};
+  if ((hyper_coef == nullptr) != (hyper_lap2 == nullptr)) return 2;
+  MomentumCoef c{dt, Pr, t_ref, {0, 0, 0}, zero_boundary, hyper_coef, hyper_lap2};
   for (int a = 0; a < d; ++a) c.buoy[a] = buoy_host[a];
   if (blocks == 0) return 0;
   int wa, wb;
@@ -470,8 +502,11 @@ HN_EXPORT int hn_correct_temperature(int nbins, const int64_t* bin_K_host, const
                                      const int* const* bin_rows_host, const int* const* bin_idx_host,
                                      const double* const* bin_w_host, int lap_plane, const int* d_plane_host, int d,
                                      const double* vstar, const double* p, const double* T, int64_t N, double dt,
-                                     double* vout, double* Tout, int* flags, void* stream) {
+                                     double* vout, double* Tout, int* flags, const double* hyper_coef,
+                                     const double* hyper_lap2, void* stream) {
   if (!ok_bins(nbins, bin_width_host) || (d != 2 && d != 3)) return 1;
+  if ((hyper_coef == nullptr) != (hyper_lap2 == nullptr)) return 2;
+  const HyperT hy{hyper_coef, hyper_lap2};
   StepBins b{};
   int64_t blocks;
   const int th = 128;
@@ -483,7 +518,7 @@ HN_EXPORT int hn_correct_temperature(int nbins, const int64_t* bin_K_host, const
   if (fused_pair(b, d, &wa, &wb)) {
     cudaStream_t s = as_stream(stream);
 #define HN_X(DD, A, B) \
-    if (d == DD && wa == A && wb == B) { correct_temp_fused_kernel<DD, A, B><<<blocks, th, 0, s>>>(b, vstar, p, T, N, dt, vout, Tout, flags); HN_CHECK_LAUNCH(); return 0; }
+    if (d == DD && wa == A && wb == B) { correct_temp_fused_kernel<DD, A, B><<<blocks, th, 0, s>>>(b, vstar, p, T, N, dt, vout, Tout, flags, hy); HN_CHECK_LAUNCH(); return 0; }
     HN_FUSED_PAIRS(HN_X)
 #undef HN_X
   }
@@ -491,7 +526,7 @@ HN_EXPORT int hn_correct_temperature(int nbins, const int64_t* bin_K_host, const
     StepBins one = single_bin(b, i);
     const int64_t bl = ceil_div(one.K[0], th);
     if (bl == 0) return;
-#define HN_COR(DD, WW) correct_temp_kernel<DD, WW><<<bl, th, 0, s>>>(one, vstar, p, T, N, dt, vout, Tout, flags)
+#define HN_COR(DD, WW) correct_temp_kernel<DD, WW><<<bl, th, 0, s>>>(one, vstar, p, T, N, dt, vout, Tout, flags, hy)
     HN_WIDTH_DISPATCH(d, one.width[0], HN_COR);
 #undef HN_COR
   });

@@ -434,16 +434,41 @@ def build_operators(nodeset, cold_origins: set, settings: PoissonSolveSettings,
 
 
 # ============================================================ device step pieces
+def _lap2_dev(ops: OperatorSet, f, out):
+    """out = lap(lap(f)) with the inner result's boundary rows at 0 (solver.py:245-247): two
+    bit-exact ELL applies; boundary rows have empty stencils, so they already give 0."""
+    t = L.torch()
+    tmp = L.empty(ops.n, t.float64)
+    nb, K, W, R, I, Wt, _ = ops._bins()
+    sel = L.host_ints([ops._lap_plane])
+    L.call("hn_apply_ell", nb, K, W, R, I, Wt, 1, sel, L.ptr(f), L.ptr(tmp), ops.n, L.stream_handle())
+    L.call("hn_apply_ell", nb, K, W, R, I, Wt, 1, sel, L.ptr(tmp), L.ptr(out), ops.n, L.stream_handle())
+    return out
+
+
+def _hyper_coef(ops: OperatorSet, coeff: float):
+    """-coeff * spacing**3, evaluated by numpy exactly as the reference does (cached in HBM)."""
+    cache = ops.__dict__.setdefault("_hyper_cache", {})
+    if coeff not in cache:
+        cache[coeff] = L.to_device(-coeff * np.asarray(ops.nodeset.spacing, dtype=float) ** 3)
+    return cache[coeff]
+
+
 def _momentum_dev(ops: OperatorSet, params: PhysicsParams, dt: float, v_soa, T, out, zero_boundary: bool):
-    if params.dissipation:
-        raise NotImplementedError("hyper-dissipation (dissipation != 0) is not on the GPU path")
     dim = ops.dim
     g = params.gravity(dim)
     buoy = [params.Ra * params.Pr * g[c] for c in range(dim)]  # ((Ra*Pr)*g_c), solver.py:270
+    hc = l2 = None
+    if params.dissipation:  # hyper-dissipation (solver.py:235-247, 271-272)
+        t = L.torch()
+        hc = _hyper_coef(ops, float(params.dissipation))
+        l2 = L.empty((dim, ops.n), t.float64)
+        for c in range(dim):
+            _lap2_dev(ops, v_soa[c], l2[c])
     nb, K, W, R, I, Wt, _ = ops._bins()
     L.call("hn_momentum", nb, K, W, R, I, Wt, ops._lap_plane, L.host_ints(ops._d_planes), dim, L.ptr(v_soa),
            L.ptr(T), ops.n, float(dt), float(params.Pr), float(params.t_ref), L.host_dbls(buoy),
-           1 if zero_boundary else 0, L.ptr(out), L.stream_handle())
+           1 if zero_boundary else 0, L.ptr(hc), L.ptr(l2), L.ptr(out), L.stream_handle())
     return out
 
 
@@ -454,11 +479,16 @@ def _div_rhs_dev(ops: OperatorSet, vstar_soa, dt: float, rhs):
     return rhs
 
 
-def _correct_temp_dev(ops: OperatorSet, vstar_soa, p, T, dt: float, vout, Tout, flags):
+def _correct_temp_dev(ops: OperatorSet, vstar_soa, p, T, dt: float, vout, Tout, flags, dissipation: float = 0.0):
+    hc = l2 = None
+    if dissipation:  # hyper-dissipation of T with the corrected velocity's speed (solver.py:355-356)
+        t = L.torch()
+        hc = _hyper_coef(ops, float(dissipation))
+        l2 = _lap2_dev(ops, T, L.empty(ops.n, t.float64))
     nb, K, W, R, I, Wt, _ = ops._bins()
     L.call("hn_correct_temperature", nb, K, W, R, I, Wt, ops._lap_plane, L.host_ints(ops._d_planes), ops.dim,
            L.ptr(vstar_soa), L.ptr(p), L.ptr(T), ops.n, float(dt), L.ptr(vout), L.ptr(Tout), L.ptr(flags),
-           L.stream_handle())
+           L.ptr(hc), L.ptr(l2), L.stream_handle())
 
 
 def _temperature_bc_dev(ops: OperatorSet, T):
@@ -639,8 +669,6 @@ def apply_temperature_bc(t_field: np.ndarray, ops: OperatorSet) -> np.ndarray:
 
 def temperature_step(state: FieldState, ops: OperatorSet, dt: float, dissipation: float = 0.0) -> np.ndarray:
     """T += dt * (-v . grad T + lap T) inside; boundary values re-imposed (solver.py:345-358)."""
-    if dissipation:
-        raise NotImplementedError("hyper-dissipation (dissipation != 0) is not on the GPU path")
     t = L.torch()
     v = _soa(state.velocity)
     T = L.to_device(np.asarray(state.temperature, dtype=np.float64))
@@ -649,7 +677,7 @@ def temperature_step(state: FieldState, ops: OperatorSet, dt: float, dissipation
     flags = L.to_device(np.array([0, INT32_MAX], dtype=np.int32))
     zeros = L.zeros(ops.n, t.float64)
     # with p = 0 the fused kernel's corrected velocity is v itself (v - dt*0 = v)
-    _correct_temp_dev(ops, v, zeros, T, dt, vout, Tout, flags)
+    _correct_temp_dev(ops, v, zeros, T, dt, vout, Tout, flags, dissipation)
     _temperature_bc_dev(ops, Tout)
     return Tout.cpu().numpy()
 
@@ -718,7 +746,8 @@ class DeviceStepper:
         ops._poisson_lambda = float(x[ops.n].item())
         self.p.copy_(x[: ops.n])
         self.have_p = True
-        _correct_temp_dev(ops, self.vstar, self.p, self.T, self.dt, self.v_next, self.T_next, self.flags)
+        _correct_temp_dev(ops, self.vstar, self.p, self.T, self.dt, self.v_next, self.T_next, self.flags,
+                          self.params.dissipation)
         _temperature_bc_dev(ops, self.T_next)
         self.v, self.v_next = self.v_next, self.v
         self.T, self.T_next = self.T_next, self.T
@@ -730,7 +759,8 @@ class DeviceStepper:
         ops = self.ops
         _momentum_dev(ops, self.params, self.dt, self.v, self.T, self.vstar, zero_boundary=True)
         _div_rhs_dev(ops, self.vstar, self.dt, self.rhs)
-        _correct_temp_dev(ops, self.vstar, self.p, self.T, self.dt, self.v_next, self.T_next, self.flags)
+        _correct_temp_dev(ops, self.vstar, self.p, self.T, self.dt, self.v_next, self.T_next, self.flags,
+                          self.params.dissipation)
         _temperature_bc_dev(ops, self.T_next)
         self.v, self.v_next = self.v_next, self.v
         self.T, self.T_next = self.T_next, self.T

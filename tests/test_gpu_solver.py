@@ -269,6 +269,32 @@ def test_steps_match_reference_golden(golden, case):
     assert stepper.nusselt() == pytest.approx(float(g["nuK"]), rel=1e-8)
 
 
+def test_hyper_dissipation_steps_match_reference_golden(golden):
+    """PhysicsParams.dissipation != 0 (solver.py:235-247): the reference's own 20 steps with the
+    fourth-difference term (it moves v by 14 % here, so the path is exercised)."""
+    ns, g = golden("dvd_coarse")
+    settings = PoissonSolveSettings()
+    ops = build_operators(ns, {"wall:x-"}, settings, boundary_override=tie_override(ns))
+    dt, Ra, Pr = float(g["hd_dt"]), float(g["hd_Ra"]), float(g["hd_Pr"])
+    state = FieldState(np.zeros((len(ns), ns.dim)), np.zeros(len(ns)), g["hd_T0"].copy())
+    stepper = DeviceStepper(ops, PhysicsParams(Ra, Pr, dissipation=float(g["hd_dissipation"])), settings, dt, state)
+    for _ in range(int(g["hd_steps"])):
+        stepper.step()
+    sK = stepper.state()
+    for got, ref, name in ((sK.velocity, g["hd_vK"], "v"), (sK.temperature, g["hd_TK"], "T"),
+                           (sK.pressure, g["hd_pK"], "p")):
+        assert rel(got, ref) <= FIELD_TOL, name
+    # the standalone API functions take the same path
+    st0 = FieldState(np.zeros((len(ns), 2)) + 0.01, np.zeros(len(ns)), g["hd_T0"].copy())
+    params = PhysicsParams(Ra, Pr, dissipation=float(g["hd_dissipation"]))
+    o = O.build_operators(ns, {"wall:x-"})
+    o_mom = O.momentum(o, st0.velocity, st0.temperature, Ra, Pr, 0.0, dt, dissipation=params.dissipation)
+    assert rel(momentum_predict(st0, ops, params, dt), o_mom) <= 1e-12
+    o_t = O.temperature(o, st0.velocity, st0.temperature.copy(), dt, dissipation=params.dissipation)
+    inner = ns.interior_mask  # boundary values come from the tie-row stencils (A5), compared above
+    assert rel(temperature_step(st0, ops, dt, params.dissipation)[inner], o_t[inner]) <= 1e-12
+
+
 def test_stepper_bitwise_deterministic(golden):
     ns, g = golden("dvd_coarse")
     settings = PoissonSolveSettings()

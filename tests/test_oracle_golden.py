@@ -89,6 +89,18 @@ def test_oracle_steps_match_reference(golden, case):
     assert O.nusselt(o, state[1]) == pytest.approx(float(g["nuK"]), rel=1e-8)
 
 
+def test_oracle_hyper_dissipation_steps_match_reference(golden):
+    """The oracle's dissipation term (solver.py:235-247) against the reference's own steps."""
+    ns, g = golden("dvd_coarse")
+    o = O.build_operators(ns, {"wall:x-"})
+    dt, Ra, Pr, diss = float(g["hd_dt"]), float(g["hd_Ra"]), float(g["hd_Pr"]), float(g["hd_dissipation"])
+    state, p = (np.zeros((len(ns), ns.dim)), g["hd_T0"].copy()), None
+    for _ in range(int(g["hd_steps"])):
+        state, p = O.step(o, state, Ra, Pr, 0.0, dt, p_prev=p, dissipation=diss)
+    for got, ref in ((state[0], g["hd_vK"]), (state[1], g["hd_TK"]), (p, g["hd_pK"])):
+        np.testing.assert_allclose(got, ref, rtol=0, atol=1e-8 * max(np.abs(ref).max(), 1e-300))
+
+
 def test_oracle_knn_brute_force_tie_order():
     """kNN key = (fl-distance, index), as the reference's own brute-force oracle
     (pkg/tests/test_approx.py:70-83)."""
