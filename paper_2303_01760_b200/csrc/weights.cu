@@ -185,15 +185,150 @@ __device__ __forceinline__ double fast_rcp(double x) {
 }
 
 // ============================ MON (thread per stencil) ============================
+// Fast path for a lattice MON stencil [centre, the 2d axis neighbours]: with the columns in
+// canonical order (centre, -x, +x, -y, +y, ...) every such system has one structure whose
+// partial-pivoting choices are known -- column 0 -> row 0 (basis 1), column -a -> row 1+a
+// (y_a, pivot -1), column +a -> row 1+D+a (y_a^2, pivot 2) -- so it is eliminated in that
+// static order: no pivot search, no row swaps (their selects were 3/4 of the general
+// path's instructions), reciprocal multiplies.  Returns false (nothing written) for any
+// other stencil or any pivot below 1/4 of its column; the caller then runs the general
+// partial-pivoting path.  Weights agree with dgesv's to rounding (kappa ~ 10).
+template <int D, int NOPS>
+__device__ __forceinline__ bool mon_static(const double* __restrict__ pos, const int* sid, const double* c,
+                                           int64_t K, int64_t k, const OpSpec& ops, int* __restrict__ out_idx,
+                                           double* __restrict__ out_w) {
+  constexpr int N = 2 * D + 1;
+  constexpr int NC = N + NOPS;
+  // slots and scale from the stencil-order offsets (sign/axis are scale-invariant)
+  int cn[N];
+#pragma unroll
+  for (int s = 0; s < N; ++s) cn[s] = -1;
+  cn[0] = sid[0];
+  double scale = 0.0;
+  bool ok = true;
+  unsigned used = 1u;
+#pragma unroll
+  for (int j = 1; j < N; ++j) {
+    double p[D], yj[D];
+    load_point<D>(pos, sid[j], p);
+#pragma unroll
+    for (int a = 0; a < D; ++a) yj[a] = __dsub_rn(p[a], c[a]);
+    scale = fmax(scale, norm_rn<D>(yj));
+    int ax = 0;
+    double best = fabs(yj[0]);
+    int nz = best != 0.0;
+#pragma unroll
+    for (int a = 1; a < D; ++a) {
+      nz += fabs(yj[a]) != 0.0;
+      const bool g = fabs(yj[a]) > best;
+      best = g ? fabs(yj[a]) : best;
+      ax = g ? a : ax;
+    }
+    const int sl = 1 + 2 * ax + (pick_axis<D>(yj, ax) > 0.0 ? 1 : 0);
+    ok = ok && nz == 1 && !(used & (1u << sl));
+    used |= 1u << sl;
+#pragma unroll
+    for (int s = 1; s < N; ++s) cn[s] = (s == sl) ? sid[j] : cn[s];
+  }
+  if (!ok) return false;
+  // In canonical order the system is block-structured with exact zeros (a neighbour along
+  // axis a has y_b = 0 exactly for b != a, the centre has y = 0): row 0 (basis 1) couples
+  // every column, and axis a only couples rows (y_a, y_a^2) with columns (-a, +a).  The
+  // static elimination (pivot rows 0, 1+a, 1+D+a) therefore reduces to one 2x2 solve per
+  // axis plus the row-0 back substitution -- the same operations the dense static
+  // elimination performs on its nonzeros, in the same order.
+  double x[N][NOPS];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double pm[D], pp[D];
+    load_point<D>(pos, cn[1 + 2 * a], pm);
+    load_point<D>(pos, cn[2 + 2 * a], pp);
+    const double u = __ddiv_rn(__dsub_rn(pick_axis<D>(pm, a), c[a]), scale);  // y_a at -a (pivot)
+    const double v = __ddiv_rn(__dsub_rn(pick_axis<D>(pp, a), c[a]), scale);  // y_a at +a
+    const double su = __dmul_rn(u, u), sv = __dmul_rn(v, v);
+    if (!(fabs(u) >= 0.25 * fmax(fabs(u), fabs(su)) && u != 0.0)) return false;
+    const double inv_u = fast_rcp(u);
+    const double l = su * inv_u;
+    const double p2 = fma(-l, v, sv);
+    if (p2 == 0.0) return false;
+    const double inv_p = fast_rcp(p2);
+#pragma unroll
+    for (int o = 0; o < NOPS; ++o) {
+      const int kind = ops.kind[o];
+      const double lin = kind == kOpPartial ? ((a == ops.axis[o]) ? 1.0 : 0.0)
+                                            : (kind == kOpNormal ? ops.normal[o][a] : 0.0);
+      const double sq = kind == kOpLaplacian ? 2.0 : 0.0;
+      const double xp = fma(-l, lin, sq) * inv_p;
+      x[2 + 2 * a][o] = xp;
+      x[1 + 2 * a][o] = fma(-v, xp, lin) * inv_u;
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < NOPS; ++o) {
+    double acc = 0.0;
+#pragma unroll
+    for (int s2 = 1; s2 < N; ++s2) acc = fma(-1.0, x[s2][o], acc);
+    x[0][o] = acc;
+  }
+  const double r1 = 1.0 / scale, r2 = 1.0 / __dmul_rn(scale, scale);
+#pragma unroll
+  for (int s = 0; s < N; ++s) {
+    int rank = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) rank += (sid[i] < cn[s]);  // lattice stencils have distinct ids
+    out_idx[rank * K + k] = cn[s];
+#pragma unroll
+    for (int o = 0; o < NOPS; ++o)
+      out_w[(static_cast<int64_t>(o) * N + rank) * K + k] = x[s][o] * (ops.order[o] == 2 ? r2 : r1);
+  }
+  return true;
+}
+
+// Fast kernel: canonical lattice stencils (mon_static); any other row is flagged
+// (flag[k] = 1) for mon_general_kernel, which runs the general partial-pivoting path.
+// Two kernels, so the general path's register budget does not set the fast path's
+// occupancy (a called device function would).
 template <int D, int NOPS>
 __global__ void __launch_bounds__(128) mon_weights_kernel(const double* __restrict__ pos,
                                                           const int* __restrict__ stencils, int64_t K,
                                                           OpSpec ops, int* __restrict__ out_idx,
-                                                          double* __restrict__ out_w, int* __restrict__ info) {
+                                                          double* __restrict__ out_w, int* __restrict__ info,
+                                                          int* __restrict__ flag) {
   constexpr int N = 2 * D + 1;
-  constexpr int NC = N + NOPS;
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= K) return;
+  int sid[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) sid[j] = __ldg(stencils + k * N + j);
+  double c[D];
+  load_point<D>(pos, sid[0], c);
+  const bool done = mon_static<D, NOPS>(pos, sid, c, K, k, ops, out_idx, out_w);
+  flag[k] = done ? 0 : 1;
+  if (done && info) info[k] = 0;
+}
+
+template <int D, int NOPS>
+__device__ __forceinline__ void mon_general(const double* __restrict__ pos, const int* __restrict__ stencils,
+                                            int64_t K, int64_t k, const OpSpec& ops, int* __restrict__ out_idx,
+                                            double* __restrict__ out_w, int* __restrict__ info);
+
+template <int D, int NOPS>
+__global__ void __launch_bounds__(128) mon_general_kernel(const double* __restrict__ pos,
+                                                          const int* __restrict__ stencils, int64_t K,
+                                                          OpSpec ops, int* __restrict__ out_idx,
+                                                          double* __restrict__ out_w, int* __restrict__ info,
+                                                          const int* __restrict__ flag) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= K || !flag[k]) return;
+  mon_general<D, NOPS>(pos, stencils, K, k, ops, out_idx, out_w, info);
+}
+
+template <int D, int NOPS>
+__device__ __forceinline__ void mon_general(const double* __restrict__ pos, const int* __restrict__ stencils,
+                                            int64_t K, int64_t k, const OpSpec& ops, int* __restrict__ out_idx,
+                                            double* __restrict__ out_w, int* __restrict__ info) {
+  constexpr int N = 2 * D + 1;
+  constexpr int NC = N + NOPS;
   int sid[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) sid[j] = __ldg(stencils + k * N + j);
@@ -714,13 +849,20 @@ HN_EXPORT int hn_weights_mon(const double* pos, int d, const int* stencils, int6
   cudaStream_t s = as_stream(stream);
   const int th = 128;
   const int64_t bl = ceil_div(K, th);
-#define HN_MON(DD, NO) mon_weights_kernel<DD, NO><<<bl, th, 0, s>>>(pos, stencils, K, ops, out_idx, out_w, info)
+  int* flag = nullptr;
+  HN_TRY(stream_alloc(reinterpret_cast<void**>(&flag), sizeof(int) * K, s));
+#define HN_MON(DD, NO)                                                                                  \
+  do {                                                                                                  \
+    mon_weights_kernel<DD, NO><<<bl, th, 0, s>>>(pos, stencils, K, ops, out_idx, out_w, info, flag);    \
+    mon_general_kernel<DD, NO><<<bl, th, 0, s>>>(pos, stencils, K, ops, out_idx, out_w, info, flag);    \
+  } while (0)
   if (d == 2) {
     switch (nops) { case 1: HN_MON(2, 1); break; case 2: HN_MON(2, 2); break; case 3: HN_MON(2, 3); break; default: HN_MON(2, 4); }
   } else {
     switch (nops) { case 1: HN_MON(3, 1); break; case 2: HN_MON(3, 2); break; case 3: HN_MON(3, 3); break; default: HN_MON(3, 4); }
   }
 #undef HN_MON
+  cudaFreeAsync(flag, s);
   HN_CHECK_LAUNCH();
   return 0;
 }

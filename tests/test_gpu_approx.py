@@ -416,3 +416,49 @@ def test_knn_box_pass_equals_ring_traversal(dim):
     for r in range(50):
         order = np.lexsort((np.arange(n), d[r]))[:k]
         npt.assert_array_equal(idx[r], order)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_mon_fast_and_general_paths_match_oracle(dim):
+    """The MON kernel's static-pivot fast path (canonical lattice stencils) and its general
+    partial-pivoting path (any other 2d+1 stencil) both agree with dgesv (oracle) to 1e-12;
+    one launch mixes both kinds of rows."""
+    from paper_2303_01760_b200 import _lib as L
+    from paper_2303_01760_b200.approx import device_nodes_uncached
+    rng = np.random.default_rng(3 + dim)
+    n = 2 * dim + 1
+    K = 400
+    h = 0.01
+    centres = rng.uniform(0.2, 0.8, (K, dim))
+    offs = np.concatenate([np.zeros((1, dim)), np.repeat(np.eye(dim), 2, axis=0) * np.tile([-1, 1], dim)[:, None]])
+    pts = centres[:, None, :] + h * offs[None]
+    j0 = 1 + int(rng.integers(0, 2 * dim))
+    pts[1::2, j0] += 0.3 * h * rng.normal(size=(K // 2, dim))  # odd stencils: one neighbour off-axis
+    perm = np.array([np.concatenate([[0], 1 + rng.permutation(n - 1)]) for _ in range(K)])
+    pts = np.take_along_axis(pts, perm[:, :, None], axis=1)  # neighbours in arbitrary order
+    flat = pts.reshape(-1, dim)
+
+    class Tmp:
+        pass
+    tmp = Tmp()
+    tmp.positions, tmp.kind = flat, np.ones(len(flat), dtype=np.int8)
+    dn = device_nodes_uncached(tmp)
+    st = np.arange(K * n, dtype=np.int32).reshape(K, n)
+    ops = [("lap",)] + [("d", a) for a in range(dim)]
+    t = L.torch()
+    oi = L.empty((n, K), t.int32)
+    ow = L.empty((len(ops), n, K), t.float64)
+    info = L.zeros(K, t.int32)
+    L.call("hn_weights_mon", L.ptr(dn.pos), dim, L.ptr(L.to_device(st)), K, len(ops), L.host_ints([0] + [1] * dim),
+           L.host_ints([0] + list(range(dim))), L.host_dbls([0.0] * (len(ops) * dim)), L.ptr(oi), L.ptr(ow),
+           L.ptr(info), L.stream_handle())
+    assert int(info.sum().item()) == 0
+    idx = oi.cpu().numpy().T
+    w = ow.cpu().numpy().transpose(2, 1, 0)  # (K, n, ops), ascending node order
+    ref = O.mon_solve(flat, st.astype(np.int64), ops)  # stencil order
+    for k in range(K):
+        order = np.argsort(st[k])
+        np.testing.assert_array_equal(idx[k], st[k][order])
+        for o in range(len(ops)):
+            r = ref[k, order, o]
+            assert np.abs(w[k, :, o] - r).max() <= 1e-12 * np.abs(r).max()
