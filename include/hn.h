@@ -74,6 +74,30 @@ int hn_knn_spacing(const double* pos, int d, const double* lo_host, double cell,
  * (default), 1 ring traversal only, 2/3 box pass with a smaller/larger first radius. */
 void hn_knn_set_variant(int v);
 
+/* compute_weights' whole device sequence in one call: classify -> partition [MON | RBF |
+ * NONE] -> (class sizes: k_rbf_host >= 0 when the caller knows them -- no regular node --
+ * else one read-back) -> MON stencils + solves -> kNN (spacing-sized, on the given grid) +
+ * RBF-FD solves -> WeightTable layout (tab_*) -> async copy into pinned host memory (h_*,
+ * skipped when h_idx is NULL).  Bins are written with stride K into capacity buffers;
+ * counts_host (host, 3) receives (K_mon, K_rbf, K_none); summary (device, 4 int) and its
+ * copy h_summary (pinned, may be NULL) = [MON singular count, first MON row, RBF count,
+ * first RBF row].  chunks > 1 splits the RBF rows into node-ordered chunks whose table
+ * slices are copied back on a side stream while the next chunk computes; cut_host (host,
+ * chunks-1 node ids where chunks 1.. start) or NULL (read back).  Returns without synchronising
+ * (unless sizes were read back); info arrays flag singular stencils as in hn_weights_*.
+ * Requires a tuned RBF size (hn_weights_rbf_is_tuned == 0).
+ * Replaces: compute_weights approx.py:379-413 (orchestration of the calls above). */
+int hn_weights_pipeline(const double* pos, int d, int64_t n, const int8_t* kind, const int* lattice_idx,
+                        const int* lattice_grid, const int* grid_dims_host, const double* lo_host, double cell,
+                        const int* dims_host, const int* cell_start, const int* cell_items, const double* cell_pos,
+                        const double* spacing, int nops, const int* op_kind_host, const int* op_axis_host,
+                        const double* op_normal_host, int n_rbf, int64_t k_rbf_host, int8_t* method, int* rows,
+                        int* counts, int* part_scratch, int* mon_st, int* mon_idx, double* mon_w, int* mon_info,
+                        int* rbf_st, int* rbf_idx, double* rbf_w, int* rbf_info, int64_t* tab_idx,
+                        int64_t* tab_sizes, double* tab_w, int64_t* h_idx, int64_t* h_sizes, double* h_w,
+                        int8_t* h_method, int64_t* counts_host, int* summary, int* h_summary, int chunks,
+                        const int64_t* cut_host, void* stream);
+
 /* method per node: -1 boundary, 0 MON, 1 RBF-FD.  lattice_idx (N x d int32, INT32_MIN =
  * off-lattice) and grid (prod(grid_dims) int32, -1 vacant) may be NULL (no lattice).
  * Replaces: classify_methods approx.py:332-351. */

@@ -430,6 +430,102 @@ def _copy_stream():
     return _COPY_STREAMS[dev]
 
 
+NATIVE_CHUNKS = 8  # RBF chunks of the native pipeline's overlapped copy-back
+
+
+def _native_ok(nodeset, ops, n_rbf: int | None = None) -> bool:
+    """hn_weights_pipeline covers the lattice / no-regular-node cases with a tuned RBF size."""
+    dim = nodeset.dim
+    n_rbf = RBF_SIZE[dim] if n_rbf is None else n_rbf
+    has_lattice = getattr(nodeset, "lattice", None) is not None and getattr(nodeset, "lattice_idx", None) is not None
+    return (has_lattice or not np.any(np.asarray(nodeset.kind) == KIND_REGULAR)) and len(nodeset) >= n_rbf and \
+        L.lib().hn_weights_rbf_is_tuned(dim, n_rbf, len(list(ops))) == 0
+
+
+def _interior_native(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
+    """_interior_device_table(host_copy=True) as one native call (hn_weights_pipeline): the
+    same library kernels in the same order, without the per-stage Python host work."""
+    dim = nodeset.dim
+    n = len(nodeset)
+    n_rbf = RBF_SIZE[dim] if n_rbf is None else n_rbf
+    nops = len(ops)
+    dn = device_nodes(nodeset)
+    t = L.torch()
+    g = dn.grid(dn.fine_cell) if dn.fine_cell is not None else dn.grid(dn.cell, exact=True)
+    kind = np.asarray(nodeset.kind)
+    rbf_rows_h = np.flatnonzero(kind != KIND_BOUNDARY) if not np.any(kind == KIND_REGULAR) else None
+    k_rbf_host = len(rbf_rows_h) if rbf_rows_h is not None else -1
+    has_lat = dn.lattice_grid is not None
+    nmon = 2 * dim + 1
+    cap_mon = n if k_rbf_host < 0 else 1  # no regular node -> no MON rows
+    cap_rbf = n
+    # three device pools + two pinned pools (allocation count is this call's host cost)
+    i32_sizes = [max(n, 1), 3, 3 * (n // 256 + 1) + 1, nmon * cap_mon, nmon * cap_mon, cap_mon,
+                 n_rbf * cap_rbf, n_rbf * cap_rbf, cap_rbf, 4]
+    pool_i = L.empty(sum(i32_sizes), t.int32)
+    rows, counts, scratch, mon_st, mon_idx, mon_info, rbf_st, rbf_idx, rbf_info, summary = \
+        t.split(pool_i, i32_sizes)
+    pool_f = L.empty(nops * nmon * cap_mon + nops * n_rbf * cap_rbf + nops * max(n, 1) * n_rbf, t.float64)
+    mon_w, rbf_w, d_w = t.split(pool_f, [nops * nmon * cap_mon, nops * n_rbf * cap_rbf, nops * max(n, 1) * n_rbf])
+    pool_l = L.empty(max(n, 1) * (n_rbf + 1), t.int64)
+    d_idx, d_sizes = pool_l[: max(n, 1) * n_rbf], pool_l[max(n, 1) * n_rbf:]
+    method = L.empty(max(n, 1), t.int8)
+    h_l = t.empty(max(n, 1) * (n_rbf + 1), dtype=t.int64, pin_memory=True)
+    h_w = t.empty((nops, max(n, 1), n_rbf), dtype=t.float64, pin_memory=True)
+    h_small = t.empty(16 + max(n, 1), dtype=t.int8, pin_memory=True)  # 4 int32 summary + method
+    h_idx, h_sizes = h_l[: max(n, 1) * n_rbf].view(max(n, 1), n_rbf), h_l[max(n, 1) * n_rbf:]
+    h_sum, h_m = h_small[:16].view(t.int32), h_small[16:]
+    kinds, axes, normals = _op_args(ops, dim)
+    cnt = (L.C.c_int64 * 3)()
+    # node-ordered RBF chunks: each chunk's table slice is copied back while the next computes
+    chunks = NATIVE_CHUNKS if k_rbf_host != 0 else 1
+    cut = None
+    if rbf_rows_h is not None and chunks > 1:
+        kb = (k_rbf_host * np.arange(1, chunks)) // chunks
+        cut = L.host_i64(rbf_rows_h[kb])
+    L.call("hn_weights_pipeline", L.ptr(dn.pos), dim, n, L.ptr(dn.kind), L.ptr(dn.lattice_idx if has_lat else None),
+           L.ptr(dn.lattice_grid if has_lat else None), L.host_ints(dn.grid_dims if has_lat else [1, 1, 1]),
+           L.host_dbls(dn.lo), g.cell, L.host_ints(g.dims), L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos),
+           L.ptr(dn.spacing), nops, kinds, axes, normals, n_rbf, k_rbf_host, L.ptr(method), L.ptr(rows),
+           L.ptr(counts), L.ptr(scratch), L.ptr(mon_st), L.ptr(mon_idx), L.ptr(mon_w), L.ptr(mon_info),
+           L.ptr(rbf_st), L.ptr(rbf_idx), L.ptr(rbf_w), L.ptr(rbf_info), L.ptr(d_idx), L.ptr(d_sizes), L.ptr(d_w),
+           L.ptr(h_idx), L.ptr(h_sizes), L.ptr(h_w), L.ptr(h_m), cnt, L.ptr(summary), L.ptr(h_sum),
+           chunks, cut, L.stream_handle())
+    k_mon, k_rbf, k_none = int(cnt[0]), int(cnt[1]), int(cnt[2])
+    chunks = max(1, min(chunks, k_rbf, 64)) if k_rbf else 1
+    kb = [(k_rbf * c) // chunks for c in range(chunks + 1)]
+    L.TRAFFIC["d2h"] += h_idx.nbytes + h_sizes.nbytes + h_w.nbytes + n + 16
+    bins = []
+    if k_mon:
+        b = Bin(None, nmon, mon_idx[: nmon * k_mon].view(nmon, k_mon),
+                mon_w[: nops * nmon * k_mon].view(nops, nmon, k_mon), d_rows=rows[:k_mon], K=k_mon)
+        b.mon = True
+        bins.append(b)
+    for c in range(chunks if k_rbf else 0):  # one ELL bin per chunk (DeviceTable.compact merges them)
+        k0, kc = kb[c], kb[c + 1] - kb[c]
+        if not kc:
+            continue
+        b = Bin(None, n_rbf, rbf_idx[n_rbf * k0: n_rbf * (k0 + kc)].view(n_rbf, kc),
+                rbf_w[nops * n_rbf * k0: nops * n_rbf * (k0 + kc)].view(nops, n_rbf, kc),
+                d_rows=rows[k_mon + k0:k_mon + k0 + kc], K=kc)
+        b.mon = False
+        bins.append(b)
+    if k_none:
+        bins.append(Bin(None, 0, L.empty((0, k_none), t.int32), L.empty((nops, 0, k_none), t.float64),
+                        d_rows=rows[k_mon + k_rbf:n], K=k_none))
+    dev = DeviceTable(n, dim, list(ops), bins, n_rbf, method[:n])
+    d_w3 = d_w.view(nops, max(n, 1), n_rbf)
+    dev._pending = (h_idx, h_sizes, h_w, h_m, (d_idx, d_sizes, d_w3))
+    t.cuda.current_stream().synchronize()  # the one synchronisation (flags + table copies)
+    hs = h_sum.numpy()
+    for cnt_, first, kind_, off in ((hs[0], hs[1], "MON", 0), (hs[2], hs[3], "RBF-FD saddle", k_mon)):
+        if cnt_:
+            node = int(rows[off + int(first)].item())
+            raise SingularSystemError(f"singular {kind_} system: Singular matrix ({int(cnt_)} stencil(s), first at "
+                                      f"node {node})")
+    return dev
+
+
 def _copyback_chunks(nodeset, ops, n_rbf: int | None = None) -> int:
     """Chunks for the overlapped copy-back: one per ~96 MB of padded host table (each chunk
     costs ~0.15 ms of host launch work, which a small table's copy cannot hide)."""
@@ -665,6 +761,8 @@ def _compute_weights(nodeset, ops, with_kappa: bool = False, rbf_n: int | None =
         _op_code(op, nodeset.dim)
     if host_copy and _copyback_chunks(nodeset, ops, rbf_n) > 1:
         dev = _interior_host_table(nodeset, ops, rbf_n)
+    elif host_copy and _native_ok(nodeset, ops, rbf_n):
+        dev = _interior_native(nodeset, ops, rbf_n)
     else:
         dev = _interior_device_table(nodeset, ops, rbf_n, host_copy=host_copy)
     table = WeightTable(_device=dev)
