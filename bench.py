@@ -333,6 +333,7 @@ def run_weights_bench(args, rank, world):
             e2e_t.append(time.perf_counter() - t0)
         # bytes the call moved (package counters: every H2D upload and the result D2H)
         h2d, d2h = L.TRAFFIC["h2d"] - b0["h2d"], L.TRAFFIC["d2h"] - b0["d2h"]
+        del table, idx, w  # the caller is done with this table: its pinned pages go back to the cache
     e2e_s = max_over_ranks(float(np.mean(e2e_t)), world)
 
     line = {

@@ -759,10 +759,10 @@ def _compute_weights(nodeset, ops, with_kappa: bool = False, rbf_n: int | None =
     ops = list(ops)
     for op in ops:
         _op_code(op, nodeset.dim)
-    if host_copy and _copyback_chunks(nodeset, ops, rbf_n) > 1:
-        dev = _interior_host_table(nodeset, ops, rbf_n)
-    elif host_copy and _native_ok(nodeset, ops, rbf_n):
+    if host_copy and _native_ok(nodeset, ops, rbf_n):
         dev = _interior_native(nodeset, ops, rbf_n)
+    elif host_copy and _copyback_chunks(nodeset, ops, rbf_n) > 1:
+        dev = _interior_host_table(nodeset, ops, rbf_n)
     else:
         dev = _interior_device_table(nodeset, ops, rbf_n, host_copy=host_copy)
     table = WeightTable(_device=dev)
