@@ -24,9 +24,6 @@ import threading
 import time
 from pathlib import Path
 
-for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
-    os.environ.setdefault(_v, "1")
-
 import numpy as np  # noqa: E402
 
 ROOT = Path(__file__).resolve().parent
@@ -398,14 +395,18 @@ def cpu_baseline_weights(ns, ops, rbf_n):
     """The reference algorithm (oracle port: cKDTree + LAPACK dgesv, 1 thread) on the same
     host, bounded sample = the whole config once or more (about 3-15 s)."""
     from oracle import hn_oracle as O
+    from threadpoolctl import threadpool_limits
     keys = [O.op_tuple(o) for o in ops]
     n_int = int(ns.interior_mask.sum())
     reps, t_total = 0, 0.0
-    while t_total < 3.0 and reps < 5:
-        t0 = time.perf_counter()
-        O.compute_weights(ns, keys, rbf_n=rbf_n)
-        t_total += time.perf_counter() - t0
-        reps += 1
+    # one BLAS thread for the oracle only (the reference's protocol); a process-wide
+    # OMP_NUM_THREADS=1 would also serialise torch's host copies on the GPU arm's e2e path
+    with threadpool_limits(1):
+        while t_total < 3.0 and reps < 5:
+            t0 = time.perf_counter()
+            O.compute_weights(ns, keys, rbf_n=rbf_n)
+            t_total += time.perf_counter() - t0
+            reps += 1
     return {"value": reps * n_int / t_total, "unit": "stencils/s", "cores": 1, "kind": "port",
             "sample": f"oracle compute_weights on the full workload x{reps} ({t_total:.1f} s), "
                       f"OPENBLAS_NUM_THREADS=1 (reference protocol, cli.py:7-10)",
