@@ -462,3 +462,37 @@ def test_mon_fast_and_general_paths_match_oracle(dim):
         for o in range(len(ops)):
             r = ref[k, order, o]
             assert np.abs(w[k, :, o] - r).max() <= 1e-12 * np.abs(r).max()
+
+
+@pytest.mark.parametrize("case", ["config1", "config2", "config4"])
+def test_native_pipeline_equals_stepwise_path(case):
+    """hn_weights_pipeline (one native call, chunked copy-back) returns exactly the table of the
+    stage-by-stage path: same kernels in the same order, so bit-identical arrays."""
+    from paper_2303_01760_b200 import approx
+    ns = {"config1": lambda: nodesets.jittered_box(120, seed=1),
+          "config2": lambda: nodesets.hybrid_hole_2d(160, seed=2),
+          "config4": lambda: nodesets.hybrid_sphere_3d(24, seed=4, refine=2.8)}[case]()
+    ops = [Laplacian()] + [Partial(a) for a in range(ns.dim)]
+    rbf_n = 20 if ns.dim == 3 else None
+    assert approx._native_ok(ns, ops, rbf_n)
+    a = approx._interior_native(ns, ops, rbf_n)
+    b = approx._interior_device_table(ns, ops, rbf_n, host_copy=True)
+    ia, sa, wa = a.host_arrays()
+    ib, sb, wb = b.host_arrays()
+    npt.assert_array_equal(ia, ib)
+    npt.assert_array_equal(sa, sb)
+    for op in ops:
+        npt.assert_array_equal(wa[op], wb[op])
+    npt.assert_array_equal(a.method, b.method)
+    assert a.ell_ok  # chunk bins merge back into one slab per width for device applies
+
+
+def test_all_boundary_node_set_gives_empty_rows():
+    """No interior node: every row is empty (size 0, -1 indices, zero weights), as the reference."""
+    n = 40
+    pts = np.random.default_rng(2).uniform(0, 1, (n, 2))
+    ns = NodeSet(pts, np.full(n, 0.1), np.full(n, 2, dtype=np.int8), np.ones(n, dtype=np.int8),
+                 np.zeros(n), np.tile([1.0, 0.0], (n, 1)))
+    t = compute_weights(ns, [Laplacian(), Partial(0)])
+    assert (t.sizes == 0).all() and (t.indices == -1).all()
+    assert all((w == 0).all() for w in t.weights.values())
