@@ -178,7 +178,7 @@ __device__ __forceinline__ double row_outside_sum(const int* __restrict__ cols, 
 }
 
 // Small block (w <= 32) solved by one warp: lane r owns row r0+r -- its outside part by a
-// serial loop with 4 loads in flight (the planner only batches blocks whose rows are
+// serial loop with 8 loads in flight (the planner only batches blocks whose rows are
 // short), then the dense triangle with shuffles.  No shared memory, no CTA barrier.
 template <bool LOWER>
 __device__ __forceinline__ void warp_small_block(const int64_t* __restrict__ rowptr, const int* __restrict__ cols,
@@ -195,18 +195,18 @@ __device__ __forceinline__ void warp_small_block(const int64_t* __restrict__ row
     const int64_t e0 = LOWER ? a : a + inside;
     const int64_t e1 = e0 + (z - a) - inside;
     double s = 0.0;
-    for (int64_t e = e0; e < e1; e += 4) {
-      int c[4];
-      double v[4], xv[4];
+    for (int64_t e = e0; e < e1; e += 8) {
+      int c[8];
+      double v[8], xv[8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < 8; ++k) {
         c[k] = e + k < e1 ? __ldg(cols + e + k) : -1;
         v[k] = e + k < e1 ? __ldg(vals + e + k) : 0.0;
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) xv[k] = c[k] >= 0 ? ld_acquire_dbl(x + c[k]) : 0.0;
+      for (int k = 0; k < 8; ++k) xv[k] = c[k] >= 0 ? ld_acquire_dbl(x + c[k]) : 0.0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < 8; ++k) {
         if (c[k] >= 0 && is_sentinel(xv[k])) xv[k] = wait_value(x + c[k]);
         s = fma(v[k], xv[k], s);
       }

@@ -108,7 +108,7 @@ class _TriSchedule:
 
 
 def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, helper_nnz: int = 4096,
-                           batch: int = 8, batch_row_nnz: int = 96) -> dict:
+                           batch: int = 8, batch_row_nnz: int = 32) -> dict:
     """Host planning of hn_sptrsv_super: dense-triangle row blocks in dependency-level order.
     Consecutive small blocks (w <= 32, every row's outside part <= batch_row_nnz) of one
     level are grouped `batch` to a task (kind 3, one warp each); heavy blocks get helper

@@ -33,12 +33,14 @@ def main():
     e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
     caps = [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "4096,512,256,128,64").split(",")]
     hel = [int(v) for v in (sys.argv[3] if len(sys.argv) > 3 else "16384").split(",")]
+    brn = [int(v) for v in (sys.argv[4] if len(sys.argv) > 4 else "96").split(",")]
     for cap in caps:
-      for helper in hel:
+     for helper in hel:
+      for brow in brn:
         batch = 8
         t0 = time.perf_counter()
-        lu.sL = solver._SuperSchedule(Lh, lower=True, batch=batch, cap=cap, helper_nnz=helper)
-        lu.sU = solver._SuperSchedule(Uh, lower=False, batch=batch, cap=cap, helper_nnz=helper)
+        lu.sL = solver._SuperSchedule(Lh, lower=True, batch=batch, cap=cap, helper_nnz=helper, batch_row_nnz=brow)
+        lu.sU = solver._SuperSchedule(Uh, lower=False, batch=batch, cap=cap, helper_nnz=helper, batch_row_nnz=brow)
         plan_s = time.perf_counter() - t0
         for cps in (2,):
             lu.CTAS_PER_SM = cps
@@ -52,7 +54,7 @@ def main():
                 t.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1))
             err = np.abs(x.cpu().numpy() - want).max() / np.abs(want).max()
-            print(f"cap {cap} helper {helper} ctas/SM {cps}: precond {np.median(ts):.3f} ms (min {min(ts):.3f})  tasks L "
+            print(f"cap {cap} helper {helper} batch_row_nnz {brow} ctas/SM {cps}: precond {np.median(ts):.3f} ms (min {min(ts):.3f})  tasks L "
                   f"{lu.sL.ntasks} U {lu.sU.ntasks}  rel err vs SuperLU {err:.1e}  (plan {plan_s:.1f}s)", flush=True)
 
 
