@@ -143,6 +143,9 @@ int64_t hn_weights_rbf_workspace(int d, int n, int nops, int64_t K);
 
 /* --------------------------------------------------------------- application (K6) */
 
+/* Threads per block of hn_apply_ell (64, 128 or 256; tuning knob, identical results). */
+void hn_apply_set_threads(int threads);
+
 /* out[o*out_stride + rows_b[k]] = sum_j w_b[(op_sel[o]*W_b + j)*K_b + k] * field[idx_b[j*K_b + k]]
  * over up to 4 bins b (widths 0,5,7,12,20,30; width 0 writes zeros), 1..4 ops.
  * Bit-identical to scipy csr_matvec (sequential, ascending columns, no FMA).

@@ -47,6 +47,7 @@ SIGNATURES: dict[str, tuple] = {
     "hn_weights_rbf_workspace": (_i64, [_i, _i, _i, _i64]),
     "hn_weights_rbf_set_variant": (None, [_i]),
     "hn_knn_set_variant": (None, [_i]),
+    "hn_apply_set_threads": (None, [_i]),
     "hn_apply_ell": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i,
                           _c_int_p, _vp, _vp, _i64, _vp]),
     "hn_ell_to_table": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i, _i, _i64,

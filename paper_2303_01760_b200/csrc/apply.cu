@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(256) apply_ell_kernel(ApplyBins b, const doubl
   }
 }
 
+int g_apply_threads = 128;  // tuning knob (hn_apply_set_threads); results identical
+
 bool supported_width(int w) { return w == 0 || w == 5 || w == 7 || w == 12 || w == 20 || w == 30; }
 
 // ELL bins -> the reference's WeightTable layout (approx.py:311-323): indices (N, n_max)
@@ -133,6 +135,8 @@ HN_EXPORT int hn_ell_to_table(int nbins, const int64_t* bin_K_host, const int* b
   return 0;
 }
 
+HN_EXPORT void hn_apply_set_threads(int t) { g_apply_threads = (t == 64 || t == 128 || t == 256) ? t : 128; }
+
 HN_EXPORT int hn_apply_ell(int nbins, const int64_t* bin_K_host, const int* bin_width_host,
                            const int* const* bin_rows_host, const int* const* bin_idx_host,
                            const double* const* bin_w_host, int nops, const int* op_sel_host,
@@ -142,7 +146,7 @@ HN_EXPORT int hn_apply_ell(int nbins, const int64_t* bin_K_host, const int* bin_
   b.nbins = nbins;
   b.nops = nops;
   b.out_stride = out_stride;
-  const int threads = 256;
+  const int threads = g_apply_threads;
   int64_t blocks = 0;
   for (int i = 0; i < nbins; ++i) {
     if (!supported_width(bin_width_host[i])) return 2;
