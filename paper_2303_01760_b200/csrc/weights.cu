@@ -23,6 +23,8 @@
 //      Exact zero pivot => SingularSystemError (info = step + 1), as dgesv does.
 #include <cfloat>
 #include <climits>
+#include <type_traits>
+#include <utility>
 
 #include "hn_common.cuh"
 
@@ -485,9 +487,12 @@ __device__ __forceinline__ double cube_from_sq(double d2) {
   return d2 * (q * y);
 }
 
-template <int D, int NST, int NOPS, int LPS, int RPL, int WARPS, int MINB>
-__global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
-    const double* __restrict__ pos, const int* __restrict__ stencils, int64_t K, OpSpec ops,
+// One block-group of the searching kernel.  Stencil k = item (direct mode) or list[item]
+// (list mode: the stencils the static kernel below flagged, n_items read on the device).
+template <int D, int NST, int NOPS, int LPS, int RPL, int WARPS>
+__device__ __forceinline__ void rbf_search_group(
+    int64_t grp, RbfSmem<D, NST, NOPS>* smem_all, const double* __restrict__ pos, const int* __restrict__ stencils,
+    int64_t K, int64_t n_items, const int* __restrict__ list, const OpSpec& ops,
     const double* __restrict__ row_normals, int* __restrict__ out_idx, double* __restrict__ out_w,
     int* __restrict__ info) {
   constexpr int NQ = poly_count<D>();
@@ -497,7 +502,6 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
   static_assert(LPS * RPL >= NS, "rows do not fit");
   static_assert(NS <= 63, "packed pivot key holds 6 row bits");
   using Sm = RbfSmem<D, NST, NOPS>;
-  __shared__ __align__(16) Sm smem_all[WARPS * SPW];
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -505,9 +509,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
   const int s = lane - sys_w * LPS;             // lane within the system segment
   const bool lane_live = sys_w < SPW;
   const int seg_base = sys_w * LPS;
-  const int64_t k_raw = (static_cast<int64_t>(blockIdx.x) * WARPS + warp) * SPW + (lane_live ? sys_w : 0);
-  const bool sys_live = lane_live && k_raw < K;
-  const int64_t k = k_raw < K ? k_raw : K - 1;  // idle segments recompute the last stencil
+  const int64_t k_raw = (grp * WARPS + warp) * SPW + (lane_live ? sys_w : 0);
+  const bool sys_live = lane_live && k_raw < n_items;
+  const int64_t item = k_raw < n_items ? k_raw : n_items - 1;  // idle segments recompute the last stencil
+  const int64_t k = list ? static_cast<int64_t>(list[item]) : item;
   Sm& sm = smem_all[warp * SPW + (lane_live ? sys_w : 0)];
   // butterfly partner in segment-relative numbering; out-of-segment partners read
   // themselves, which leaves segment lane 0 holding the full reduction
@@ -735,6 +740,431 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
   }
 }
 
+// Searching kernel: direct mode (list == nullptr, items = stencils 0..K-1, one group per
+// block) or list mode (items = list[0..*list_count), grid-stride over groups).
+template <int D, int NST, int NOPS, int LPS, int RPL, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
+    const double* __restrict__ pos, const int* __restrict__ stencils, int64_t K, OpSpec ops,
+    const double* __restrict__ row_normals, int* __restrict__ out_idx, double* __restrict__ out_w,
+    int* __restrict__ info, const int* __restrict__ list, const int* __restrict__ list_count) {
+  constexpr int SPW = 32 / LPS;
+  __shared__ __align__(16) RbfSmem<D, NST, NOPS> smem_all[WARPS * SPW];
+  if (list == nullptr) {
+    rbf_search_group<D, NST, NOPS, LPS, RPL, WARPS>(blockIdx.x, smem_all, pos, stencils, K, K, nullptr, ops,
+                                                    row_normals, out_idx, out_w, info);
+    return;
+  }
+  const int64_t n = *list_count;
+  for (int64_t g = blockIdx.x; g * WARPS * SPW < n; g += gridDim.x) {
+    rbf_search_group<D, NST, NOPS, LPS, RPL, WARPS>(g, smem_all, pos, stencils, K, n, list, ops, row_normals,
+                                                    out_idx, out_w, info);
+    __syncwarp();
+  }
+}
+
+// ============ RBF-FD with a static null-space pivot order (default path) ============
+// The saddle system [[A P],[P^T 0]] (A_ij = r_ij^3: zero diagonal, indefinite) is
+// eliminated in a fixed order instead of with a pivot search at every step:
+//   A. a partial-pivoting LU of P (NST x NQ, rows = stencil nodes, NQ short steps) picks
+//      NQ nodes I whose monomial rows are unisolvent with |L| <= 1; the nodes are then
+//      renumbered [I (pivot order), J (the rest, stencil order)];
+//   1. pivots (monomial row m, column of node I_m), m < NQ: the LU of P_I^T;
+//   2. pivots (node row I_m, column lambda_m): the LU of P_I.  Both have the pivots of
+//      step A (the same leading minors of P_I), so their reciprocals are step A's;
+//   3. pivots (node row J_j, column of node J_j): the diagonal of the Schur complement
+//      Z^T A Z, symmetric positive definite because r^3 is conditionally positive definite
+//      of order 2 -- diagonal pivots need no search there.
+// That is the null-space method written as Gauss-Jordan.  Every pivot row sits at a
+// compile-time (lane, slot), so the elimination has no pivot search, no row bookkeeping and
+// one predicated store per staged pair (the searching kernel above stores RPL), and the
+// zero blocks are skipped statically (monomial rows have no lambda columns; phase 2 leaves
+// monomial rows alone, phase 3 the I rows whose lambda values are not needed).
+// Row rho = s + r * LPS of the renumbered system lives in segment lane s, slot r: rho < NQ
+// node I_rho, rho < NST node J, else monomial rho - NST.  Segments are interleaved across
+// the warp (lane = s * SPW + system), so the owners of a pivot row -- one per system --
+// are SPW adjacent lanes and their predicated 16-B stores take one or two shared-memory
+// phases instead of four.  The matrix is assembled in registers (shared memory is the
+// scarcer resource here: it carries every pivot-row broadcast).
+// Checked against dgesv on every config's stencils (numpy model of this order: <= 1.8e-13
+// row-normwise on configs 1/2/4, interior and one-sided boundary stencils; pivots of
+// phases 1/2 >= 0.06, phase-3 pivots >= 5e-3).  A stencil with a step-A pivot below
+// 2^-10 or a phase-3 pivot below 2^-12 (nearly unisolvent nodes, non-SPD Schur
+// complement, exact zero pivots, coincident nodes) is flagged and re-solved by the
+// searching kernel, so dgesv's partial-pivoting semantics, SingularSystemError included,
+// are unchanged.
+template <int D, int NST, int NOPS>
+struct RbfStaticCore {
+  static constexpr int NQ = poly_count<D>();
+  static constexpr int NS = NST + NQ;
+  static constexpr int NC = NS + NOPS;
+  static constexpr int NCP = (NC + 1) & ~1;
+  static constexpr int YS = D == 2 ? 2 : 4;        // padded point (16-B loads)
+  static constexpr int PTW = (NST + 1) & ~1;       // transposed-P row width (16-B rows)
+  double prow[2][NCP];             // double-buffered pivot row (16 B aligned pairs)
+  double inv_hist[(NQ + 1) & ~1];  // 1/pivot of step A (= phases 1 and 2)
+  double yp[NST][YS];              // local coordinates, renumbered [I, J]
+  double pt[NQ][PTW];              // P^T (monomial rows), renumbered nodes
+  double w[NST][NOPS];             // solution, renumbered
+  int sidp[NST];                   // node ids, renumbered
+};
+// padded so consecutive systems start 16 B apart modulo 128 B: the five pivot-row
+// broadcasts of a warp hit distinct banks
+template <int D, int NST, int NOPS>
+struct __align__(16) RbfStaticSmem : RbfStaticCore<D, NST, NOPS> {
+  static constexpr int kCore = static_cast<int>(sizeof(RbfStaticCore<D, NST, NOPS>));
+  static constexpr int kPad = ((16 - kCore % 128) % 128 + 128) % 128;
+  char pad[kPad == 0 ? 128 : kPad];
+};
+
+// f(std::integral_constant<int, I>) for I = 0..N-1, unrolled by construction (NVVM's
+// #pragma unroll gives up on the 30-40-step 3D eliminations and falls back to local memory)
+template <typename F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+// compile-time schedule of the static elimination
+template <int NST, int NQ>
+__host__ __device__ constexpr int st_piv_row(int t) {
+  return t < NQ ? NST + t : (t < 2 * NQ ? t - NQ : NQ + (t - 2 * NQ));
+}
+template <int NST, int NQ>
+__host__ __device__ constexpr int st_piv_col(int t) {
+  return t < NQ ? t : (t < 2 * NQ ? NST + (t - NQ) : NQ + (t - 2 * NQ));
+}
+template <int NST, int NQ>
+__host__ __device__ constexpr int st_col_step(int c) {  // step that pivots column c (RHS: never)
+  return c < NQ ? c : (c < NST ? 2 * NQ + (c - NQ) : (c < NST + NQ ? NQ + (c - NST) : (1 << 20)));
+}
+
+constexpr double kStaticPivMin = 1.0 / 1024.0;   // |pivot| floor, step A (= phases 1-2)
+constexpr double kStaticSchurMin = 1.0 / 4096.0;  // pivot floor, phase 3 (positive)
+
+// standard operator set [Laplacian, d/dx_0, .., d/dx_{D-1}] (what compute_weights asks for):
+// right-hand sides from compile-time tables
+template <int D>
+__device__ __forceinline__ double std_poly_rhs(int o, int m) {
+  constexpr unsigned SQ = D == 2 ? 0x28u : 0x290u;  // pure squares: 2D m = 3, 5; 3D m = 4, 7, 9
+  if (o == 0) return ((SQ >> m) & 1u) ? 2.0 : 0.0;
+  return m == o ? 1.0 : 0.0;                        // d/dx_a of monomial 1 + a
+}
+
+template <int D, int NST, int NOPS, bool STD, int LPS, int RPL, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
+    const double* __restrict__ pos, const int* __restrict__ stencils, int64_t K, OpSpec ops,
+    const double* __restrict__ row_normals, int* __restrict__ out_idx, double* __restrict__ out_w,
+    int* __restrict__ info, int* __restrict__ flag_list, int* __restrict__ flag_count, int force_flag) {
+  constexpr int NQ = poly_count<D>();
+  constexpr int NS = NST + NQ;
+  constexpr int NC = NS + NOPS;
+  constexpr int SPW = 32 / LPS;
+  constexpr int PA = (NST + LPS - 1) / LPS;  // slots holding the original nodes in step A
+  static_assert(LPS * RPL == NS, "one system row per (lane, slot)");
+  static_assert(NST <= 31, "node bitmask");
+  static_assert(!STD || NOPS == D + 1, "standard operator set is [Lap, d/dx_a..]");
+  using Sm = RbfStaticSmem<D, NST, NOPS>;
+  extern __shared__ __align__(16) unsigned char rbf_static_smem[];  // WARPS * SPW systems
+  Sm* smem_all = reinterpret_cast<Sm*>(rbf_static_smem);
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const bool lane_live = lane < SPW * LPS;
+  const int s = lane_live ? lane / SPW : 0;        // lane within the system segment
+  const int sys_w = lane_live ? lane - s * SPW : 0;  // system slot within the warp
+  const int seg_base = sys_w;                      // segment lane 0
+  const int64_t k_raw = (static_cast<int64_t>(blockIdx.x) * WARPS + warp) * SPW + sys_w;
+  const bool sys_live = lane_live && k_raw < K;
+  const int64_t k = k_raw < K ? k_raw : K - 1;
+  Sm& sm = smem_all[warp * SPW + sys_w];
+  // butterfly partner in segment-relative numbering; out-of-segment partners read
+  // themselves, which leaves segment lane 0 holding the full reduction
+  auto seg_src = [&](int off) {
+    const int t = s ^ off;
+    return (lane_live && t < LPS) ? t * SPW + sys_w : lane;
+  };
+  // slot classes (rho = s + r * LPS, s < LPS)
+  auto has_node = [](int r) { return r * LPS < NST; };
+  auto only_poly = [](int r) { return r * LPS >= NST; };
+  auto only_node = [](int r) { return r * LPS + LPS <= NST; };
+  auto only_I = [](int r) { return r * LPS + LPS <= NQ; };
+
+  const bool use_rn = !STD && row_normals != nullptr;
+  double rn[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) rn[a] = use_rn ? __ldg(row_normals + k * D + a) : 0.0;
+
+  // ---- gather, shift to the centre, scale by the stencil radius (approx.py:245-250) ----
+  // (scale and 1/scale to ~1 ulp; the weights are un-scaled by the same 1/scale, and a
+  //  stencil that needs dgesv's exact-zero-pivot semantics is re-solved by the searching
+  //  kernel, which forms the local coordinates bitwise as the reference does)
+  double c[D];
+  load_point<D>(pos, __ldg(stencils + k * NST), c);
+  double yo[PA][D];
+  int sido[PA];
+  double d2max = 0.0;
+#pragma unroll
+  for (int r = 0; r < PA; ++r) {
+    const int j = s + r * LPS;
+    sido[r] = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) yo[r][a] = 0.0;
+    if (j < NST) {
+      sido[r] = __ldg(stencils + k * NST + j);
+      double p[D];
+      load_point<D>(pos, sido[r], p);
+      double d2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        yo[r][a] = p[a] - c[a];
+        d2 = fma(yo[r][a], yo[r][a], d2);
+      }
+      d2max = fmax(d2max, d2);
+    }
+  }
+#pragma unroll
+  for (int off = 1; off < LPS; off <<= 1) d2max = fmax(d2max, __shfl_sync(0xffffffffu, d2max, seg_src(off)));
+  d2max = __shfl_sync(0xffffffffu, d2max, lane_live ? seg_base : lane);
+  const double s1 = fast_rcp(fast_sqrt(d2max));
+#pragma unroll
+  for (int r = 0; r < PA; ++r)
+#pragma unroll
+    for (int a = 0; a < D; ++a) yo[r][a] *= s1;
+
+  const unsigned pb0 = smem_addr(&sm.prow[0][0]);
+  const unsigned pb1 = smem_addr(&sm.prow[1][0]);
+  const unsigned hist = smem_addr(&sm.inv_hist[0]);
+  bool bad = force_flag != 0;
+
+  // ---- step A: LU of P with partial pivoting over the nodes -> I ----
+  {
+    double pp[PA][NQ];
+    unsigned vm[PA];
+#pragma unroll
+    for (int r = 0; r < PA; ++r) {
+      const int j = s + r * LPS;
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) pp[r][m] = mono_val<D>(m, yo[r]);
+      vm[r] = (lane_live && j < NST) ? (0x7fffffc0u | static_cast<unsigned>(63 - j)) : 0u;
+    }
+    unsigned chosen = 0u;
+    static_for<NQ>([&](auto mc) {
+      constexpr int m = decltype(mc)::value;
+      unsigned key = 0;
+#pragma unroll
+      for (int r = 0; r < PA; ++r)
+        key = max(key, (static_cast<unsigned>(__double2hiint(pp[r][m])) | 63u) & vm[r]);
+#pragma unroll
+      for (int off = 1; off < LPS; off <<= 1) key = max(key, __shfl_sync(0xffffffffu, key, seg_src(off)));
+      key = __shfl_sync(0xffffffffu, key, lane_live ? seg_base : lane);
+      const unsigned ptag = key & 63u;
+      const unsigned pbase = (m & 1) ? pb1 : pb0;
+      bool isp[PA];
+#pragma unroll
+      for (int r = 0; r < PA; ++r) {
+        isp[r] = ((vm[r] & 63u) == ptag) && vm[r] != 0u;
+        constexpr int j0 = m & ~1;
+#pragma unroll
+        for (int jj = j0; jj < NQ; jj += 2) {
+          if (jj + 1 < NQ) st_pred2(isp[r], pbase + 8u * jj, pp[r][jj], pp[r][jj + 1]);
+          else st_pred1(isp[r], pbase + 8u * jj, pp[r][jj]);
+        }
+        if (isp[r]) {
+#pragma unroll
+          for (int a = 0; a < D; ++a) sm.yp[m][a] = yo[r][a];
+          sm.sidp[m] = sido[r];
+        }
+      }
+      __syncwarp();
+      const double* prow = sm.prow[m & 1];
+      const double piv = prow[m];
+      bad = bad || !(fabs(piv) >= kStaticPivMin);
+      const double inv = fast_rcp(piv);
+      st_pred1(lane_live && s == 0, hist + 8u * m, inv);
+#pragma unroll
+      for (int r = 0; r < PA; ++r) {
+        const double l = isp[r] ? 0.0 : pp[r][m] * inv;
+        vm[r] = isp[r] ? 0u : vm[r];
+#pragma unroll
+        for (int cc = m + 1; cc < NQ; ++cc) pp[r][cc] = fma(-l, prow[cc], pp[r][cc]);
+      }
+      chosen |= 1u << (63u - ptag);
+    });
+    // J: the unchosen nodes in stencil order
+#pragma unroll
+    for (int r = 0; r < PA; ++r) {
+      const int j = s + r * LPS;
+      if (lane_live && j < NST && !((chosen >> j) & 1u)) {
+        const int ni = NQ + __popc(~chosen & ((1u << j) - 1u));
+#pragma unroll
+        for (int a = 0; a < D; ++a) sm.yp[ni][a] = yo[r][a];
+        sm.sidp[ni] = sido[r];
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---- assemble the renumbered rows | RHS in registers (approx.py:254-277) ----
+  // node rows: A_ij = r_ij^3 from the shared renumbered coordinates, own P row; the node
+  // lanes also publish P^T so the monomial rows read their row instead of forming it
+  double a[RPL][NC];
+  double yr[RPL][D];
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int rho = s + r * LPS;
+    const bool node_row = only_node(r) || (!only_poly(r) && rho < NST);
+#pragma unroll
+    for (int q = 0; q < D; ++q) yr[r][q] = 0.0;
+    if (node_row) {
+      const int i = rho < NST ? rho : 0;
+      double yi[D];
+#pragma unroll
+      for (int q = 0; q < D; ++q) yi[q] = yr[r][q] = sm.yp[i][q];
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) {
+        a[r][NST + m] = mono_val<D>(m, yi);
+        if (lane_live) sm.pt[m][i] = a[r][NST + m];
+      }
+      const double r0 = norm_fast<D>(yi);
+      if constexpr (STD) {
+        a[r][NS] = 3.0 * (D + 1) * r0;
+        const double m3 = -3.0 * r0;
+#pragma unroll
+        for (int q = 0; q < D; ++q) a[r][NS + 1 + q] = m3 * yi[q];
+      } else {
+#pragma unroll
+        for (int o = 0; o < NOPS; ++o) a[r][NS + o] = phs_rhs<D>(ops, o, yi, r0, use_rn, rn);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NST; ++j) {
+    double yj[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) yj[q] = sm.yp[j][q];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      if (!has_node(r)) continue;
+      double d2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        const double t = yr[r][q] - yj[q];
+        d2 = fma(t, t, d2);
+      }
+      a[r][j] = cube_from_sq(d2);  // exact 0 on the diagonal
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int rho = s + r * LPS;
+    const bool node_row = only_node(r) || (!only_poly(r) && rho < NST);
+    if (!node_row) {
+      const int m = rho - NST < NQ ? rho - NST : 0;
+      const double2* row = reinterpret_cast<const double2*>(&sm.pt[m][0]);
+#pragma unroll
+      for (int j = 0; j < NST; j += 2) {
+        const double2 v = row[j / 2];
+        a[r][j] = v.x;
+        if (j + 1 < NST) a[r][j + 1] = v.y;
+      }
+      if (has_node(r)) {
+#pragma unroll
+        for (int mm = 0; mm < NQ; ++mm) a[r][NST + mm] = 0.0;
+      }
+#pragma unroll
+      for (int o = 0; o < NOPS; ++o) a[r][NS + o] = STD ? std_poly_rhs<D>(o, m) : poly_rhs<D>(ops, o, m, use_rn, rn);
+    }
+  }
+
+  // ---- static Gauss-Jordan ----
+  double invp[RPL];
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) invp[r] = 0.0;
+  static_for<NS>([&](auto tc) {
+    constexpr int t = decltype(tc)::value;
+    constexpr int pr = st_piv_row<NST, NQ>(t), pc = st_piv_col<NST, NQ>(t);
+    constexpr int os = pr / LPS, ol = pr % LPS;
+    constexpr int ph = t < NQ ? 1 : (t < 2 * NQ ? 2 : 3);
+    const bool own = lane_live && s == ol;
+    const unsigned pbase = (t & 1) ? pb1 : pb0;
+    // live columns of the pivot row: not pivoted before t; phase 1 rows have no lambda
+    auto live = [&](int cc) {
+      return cc < NC && st_col_step<NST, NQ>(cc) >= t && !(ph == 1 && cc >= NST && cc < NS);
+    };
+#pragma unroll
+    for (int cc = 0; cc < NC; cc += 2) {
+      const bool l0 = live(cc), l1 = live(cc + 1);
+      if (l0 && l1) st_pred2(own, pbase + 8u * cc, a[os][cc], a[os][cc + 1]);
+      else if (l0) st_pred1(own, pbase + 8u * cc, a[os][cc]);
+      else if (l1) st_pred1(own, pbase + 8u * (cc + 1), a[os][cc + 1]);
+    }
+    __syncwarp();
+    const double* prow = sm.prow[t & 1];
+    double inv;
+    if constexpr (ph == 3) {
+      const double piv = prow[pc];
+      bad = bad || !(piv >= kStaticSchurMin);
+      inv = fast_rcp(piv);
+      invp[os] = own ? inv : invp[os];
+    } else {
+      inv = sm.inv_hist[t < NQ ? t : t - NQ];
+      if constexpr (ph == 1) invp[os] = own ? inv : invp[os];
+    }
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      if ((ph == 2 && only_poly(r)) || (ph == 3 && only_I(r))) continue;
+      double l = a[r][pc] * inv;
+      if (r == os) l = own ? 0.0 : l;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+        if (cc != pc && live(cc)) a[r][cc] = fma(-l, prow[cc], a[r][cc]);
+    }
+  });
+
+  // ---- solution: J rows give w_J, monomial row m gives w_{I_m} (approx.py:282) ----
+  double* w = &sm.w[0][0];
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    if (only_I(r)) continue;
+    const int rho = s + r * LPS;
+    if (lane_live && rho >= NQ) {
+      const int node = rho < NST ? rho : (rho - NST < NQ ? rho - NST : 0);
+#pragma unroll
+      for (int o = 0; o < NOPS; ++o) w[node * NOPS + o] = a[r][NS + o] * invp[r];
+    }
+  }
+  __syncwarp();
+  if (!sys_live) return;
+  if (bad) {
+    if (s == 0) flag_list[atomicAdd(flag_count, 1)] = static_cast<int>(k);
+    return;
+  }
+  if (info && s == 0) info[k] = 0;
+  // ---- epilogue: ascending node-index order, un-scale (approx.py:283-284, 407-410) ----
+  // (node ids of an unflagged stencil are distinct: a repeated node makes two equal rows)
+  const double s2 = s1 * s1;
+#pragma unroll
+  for (int r = 0; r < PA; ++r) {
+    const int j = s + r * LPS;
+    if (j < NST) {
+      const int id = sm.sidp[j];
+      int rank = 0;
+#pragma unroll
+      for (int i = 0; i < NST; ++i) rank += sm.sidp[i] < id;
+      out_idx[static_cast<int64_t>(rank) * K + k] = id;
+#pragma unroll
+      for (int o = 0; o < NOPS; ++o) {
+        const double f = (STD ? o == 0 : ops.order[o] == 2) ? s2 : s1;
+        out_w[(static_cast<int64_t>(o) * NST + rank) * K + k] = w[j * NOPS + o] * f;
+      }
+    }
+  }
+}
+
 // ===================== generic fallback (any n, any op count): thread per stencil ==========
 // Used for stencil sizes without a tuned instantiation (per-stencil API calls in tests).
 // Matrix lives in a caller-provided global workspace; LU with partial pivoting + row swaps.
@@ -873,27 +1303,88 @@ static void launch_rbf_v(const double* pos, const int* st, int64_t K, const OpSp
   constexpr int SPW = 32 / LPS;
   const int64_t per_block = static_cast<int64_t>(WARPS) * SPW;
   rbf_weights_kernel<D, NST, NOPS, LPS, RPL, WARPS, MINB><<<ceil_div(K, per_block), WARPS * 32, 0, s>>>(
-      pos, st, K, ops, rn, oi, ow, info);
+      pos, st, K, ops, rn, oi, ow, info, nullptr, nullptr);
 }
 
-// launch-shape variant for the 2D n=12 kernel (tuning experiments; 0 = default)
+// Static-order kernel, then the searching kernel over the stencils it flagged (list mode,
+// grid-stride: an empty list costs one short launch).
+template <int D, int NST, int NOPS, int LPS, int RPL, int WARPS, int MINB, int FLPS, int FRPL>
+static cudaError_t launch_rbf_static(const double* pos, const int* st, int64_t K, const OpSpec& ops,
+                                     const double* rn, int* oi, double* ow, int* info, cudaStream_t s, int force) {
+  // the standard operator set [Lap, d/dx_0, ..] gets compile-time right-hand sides
+  bool std_ops = rn == nullptr && NOPS == D + 1 && ops.kind[0] == kOpLaplacian;
+  for (int o = 1; o < NOPS && std_ops; ++o) std_ops = ops.kind[o] == kOpPartial && ops.axis[o] == o - 1;
+  int* buf = nullptr;  // [count, list...]
+  cudaError_t e = stream_alloc(reinterpret_cast<void**>(&buf), sizeof(int) * (K + 1), s);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(buf, 0, sizeof(int), s);
+  constexpr int SPW = 32 / LPS;
+  const int64_t grid = ceil_div(K, static_cast<int64_t>(WARPS) * SPW);
+  const size_t smem = sizeof(RbfStaticSmem<D, NST, NOPS>) * WARPS * SPW;
+  auto go = [&](auto kc) {
+    constexpr auto kern = decltype(kc)::value;
+    static bool attr = false;  // one attribute call per kernel (dynamic smem may exceed 48 KB)
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      attr = true;
+    }
+    kern<<<grid, WARPS * 32, smem, s>>>(pos, st, K, ops, rn, oi, ow, info, buf + 1, buf, force);
+  };
+  using KT = decltype(&rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB>);
+  if constexpr (NOPS == D + 1) {
+    if (std_ops) go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, true, LPS, RPL, WARPS, MINB>>{});
+    else go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB>>{});
+  } else {
+    go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB>>{});
+  }
+  constexpr int FSPW = 32 / FLPS;
+  const int64_t groups = ceil_div(K, static_cast<int64_t>(4) * FSPW);
+  const int64_t cap = static_cast<int64_t>(sm_count()) * 2;
+  rbf_weights_kernel<D, NST, NOPS, FLPS, FRPL, 4, 1><<<static_cast<int>(groups < cap ? groups : cap), 128, 0, s>>>(
+      pos, st, K, ops, rn, oi, ow, info, buf + 1, buf);
+  return cudaFreeAsync(buf, s);
+}
+
+// Kernel choice (tuning/tests; 0 = default static order + flagged fallback):
+// 100 = searching kernel for every stencil; 101 = static kernel with every stencil flagged
+// (exercises the list-mode fallback); 1..5 = launch shapes of the 2D searching kernel;
+// 10..19 = launch shapes of the static kernel.
 static int g_rbf_variant = 0;
 HN_EXPORT void hn_weights_rbf_set_variant(int v) { g_rbf_variant = v; }
 
-template <int D, int NST, int NOPS, int LPS, int RPL>
-static void launch_rbf(const double* pos, const int* st, int64_t K, const OpSpec& ops, const double* rn, int* oi,
-                       double* ow, int* info, cudaStream_t s) {
-  if constexpr (D == 2 && NST == 12) {
-    switch (g_rbf_variant) {
-      case 1: launch_rbf_v<2, 12, NOPS, 6, 3, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return;
-      case 2: launch_rbf_v<2, 12, NOPS, 9, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return;
-      case 3: launch_rbf_v<2, 12, NOPS, 9, 2, 4, 4>(pos, st, K, ops, rn, oi, ow, info, s); return;
-      case 4: launch_rbf_v<2, 12, NOPS, 6, 3, 2, 5>(pos, st, K, ops, rn, oi, ow, info, s); return;
-      case 5: launch_rbf_v<2, 12, NOPS, 6, 3, 1, 12>(pos, st, K, ops, rn, oi, ow, info, s); return;
-      default: launch_rbf_v<2, 12, NOPS, 6, 3, 4, 3>(pos, st, K, ops, rn, oi, ow, info, s); return;
+template <int D, int NST, int NOPS>
+static cudaError_t launch_rbf(const double* pos, const int* st, int64_t K, const OpSpec& ops, const double* rn,
+                              int* oi, double* ow, int* info, cudaStream_t s) {
+  const int v = g_rbf_variant;
+  const int force = v == 101 ? 1 : 0;
+  if constexpr (D == 2) {
+    switch (v) {
+      case 1: launch_rbf_v<2, 12, NOPS, 6, 3, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return cudaSuccess;
+      case 2: launch_rbf_v<2, 12, NOPS, 9, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return cudaSuccess;
+      case 100: launch_rbf_v<2, 12, NOPS, 6, 3, 4, 3>(pos, st, K, ops, rn, oi, ow, info, s); return cudaSuccess;
+      case 10: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 2, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+      case 11: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 3, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+      case 12: return launch_rbf_static<2, 12, NOPS, 6, 3, 2, 6, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+      case 13: return launch_rbf_static<2, 12, NOPS, 6, 3, 8, 1, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+      case 14: return launch_rbf_static<2, 12, NOPS, 3, 6, 4, 2, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+      case 15: return launch_rbf_static<2, 12, NOPS, 3, 6, 2, 4, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+      case 16: return launch_rbf_static<2, 12, NOPS, 3, 6, 4, 1, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+      default: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, force);
+    }
+  } else if constexpr (NST == 20) {
+    switch (v) {
+      case 100: launch_rbf_v<3, 20, NOPS, 15, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return cudaSuccess;
+      case 10: return launch_rbf_static<3, 20, NOPS, 10, 3, 4, 1, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+      case 11: return launch_rbf_static<3, 20, NOPS, 10, 3, 2, 2, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+      case 12: return launch_rbf_static<3, 20, NOPS, 15, 2, 4, 2, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+      default: return launch_rbf_static<3, 20, NOPS, 10, 3, 4, 1, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, force);
+    }
+  } else {
+    switch (v) {
+      case 100: launch_rbf_v<3, 30, NOPS, 20, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return cudaSuccess;
+      default: return launch_rbf_static<3, 30, NOPS, 20, 2, 4, 1, 20, 2>(pos, st, K, ops, rn, oi, ow, info, s, force);
     }
   }
-  launch_rbf_v<D, NST, NOPS, LPS, RPL, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s);
 }
 
 // Workspace (doubles) the generic path needs for K stencils of size n: K*(ns*nc + n*d).
@@ -922,24 +1413,24 @@ HN_EXPORT int hn_weights_rbf(const double* pos, int d, const int* stencils, int6
   if (hn_weights_rbf_is_tuned(d, n, nops) == 0) {
     if (d == 2) {
       switch (nops) {
-        case 1: launch_rbf<2, 12, 1, 6, 3>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
-        case 2: launch_rbf<2, 12, 2, 6, 3>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
-        case 3: launch_rbf<2, 12, 3, 6, 3>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
-        default: launch_rbf<2, 12, 4, 6, 3>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
+        case 1: HN_TRY((launch_rbf<2, 12, 1>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
+        case 2: HN_TRY((launch_rbf<2, 12, 2>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
+        case 3: HN_TRY((launch_rbf<2, 12, 3>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
+        default: HN_TRY((launch_rbf<2, 12, 4>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
       }
     } else if (n == 20) {
       switch (nops) {
-        case 1: launch_rbf<3, 20, 1, 15, 2>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
-        case 2: launch_rbf<3, 20, 2, 15, 2>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
-        case 3: launch_rbf<3, 20, 3, 15, 2>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
-        default: launch_rbf<3, 20, 4, 15, 2>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
+        case 1: HN_TRY((launch_rbf<3, 20, 1>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
+        case 2: HN_TRY((launch_rbf<3, 20, 2>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
+        case 3: HN_TRY((launch_rbf<3, 20, 3>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
+        default: HN_TRY((launch_rbf<3, 20, 4>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
       }
     } else {
       switch (nops) {
-        case 1: launch_rbf<3, 30, 1, 20, 2>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
-        case 2: launch_rbf<3, 30, 2, 20, 2>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
-        case 3: launch_rbf<3, 30, 3, 20, 2>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
-        default: launch_rbf<3, 30, 4, 20, 2>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s); break;
+        case 1: HN_TRY((launch_rbf<3, 30, 1>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
+        case 2: HN_TRY((launch_rbf<3, 30, 2>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
+        case 3: HN_TRY((launch_rbf<3, 30, 3>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
+        default: HN_TRY((launch_rbf<3, 30, 4>(pos, stencils, K, ops, row_normals, out_idx, out_w, info, s))); break;
       }
     }
   } else {
