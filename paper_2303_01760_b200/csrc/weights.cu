@@ -853,7 +853,7 @@ __device__ __forceinline__ double std_poly_rhs(int o, int m) {
   return m == o ? 1.0 : 0.0;                        // d/dx_a of monomial 1 + a
 }
 
-template <int D, int NST, int NOPS, bool STD, int LPS, int RPL, int WARPS, int MINB>
+template <int D, int NST, int NOPS, bool STD, int LPS, int RPL, int WARPS, int MINB, bool ILV>
 __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
     const double* __restrict__ pos, const int* __restrict__ stencils, int64_t K, OpSpec ops,
     const double* __restrict__ row_normals, int* __restrict__ out_idx, double* __restrict__ out_w,
@@ -867,15 +867,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
   static_assert(NST <= 31, "node bitmask");
   static_assert(!STD || NOPS == D + 1, "standard operator set is [Lap, d/dx_a..]");
   using Sm = RbfStaticSmem<D, NST, NOPS>;
+  // flagged systems are re-solved in this kernel when the searching layout is the same
+  static constexpr bool kInlineFallback = D == 2 && NST == 12 && LPS == 6 && RPL == 3 && !ILV;
   extern __shared__ __align__(16) unsigned char rbf_static_smem[];  // WARPS * SPW systems
   Sm* smem_all = reinterpret_cast<Sm*>(rbf_static_smem);
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const bool lane_live = lane < SPW * LPS;
-  const int s = lane_live ? lane / SPW : 0;        // lane within the system segment
-  const int sys_w = lane_live ? lane - s * SPW : 0;  // system slot within the warp
-  const int seg_base = sys_w;                      // segment lane 0
+  // ILV: lane = s * SPW + system (owners adjacent); else lane = system * LPS + s
+  const int s = lane_live ? (ILV ? lane / SPW : lane % LPS) : 0;      // lane within the segment
+  const int sys_w = lane_live ? (ILV ? lane % SPW : lane / LPS) : 0;  // system slot in the warp
+  const int seg_base = ILV ? sys_w : sys_w * LPS;                     // segment lane 0
   const int64_t k_raw = (static_cast<int64_t>(blockIdx.x) * WARPS + warp) * SPW + sys_w;
   const bool sys_live = lane_live && k_raw < K;
   const int64_t k = k_raw < K ? k_raw : K - 1;
@@ -884,7 +887,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
   // themselves, which leaves segment lane 0 holding the full reduction
   auto seg_src = [&](int off) {
     const int t = s ^ off;
-    return (lane_live && t < LPS) ? t * SPW + sys_w : lane;
+    return (lane_live && t < LPS) ? (ILV ? t * SPW + sys_w : sys_w * LPS + t) : lane;
   };
   // slot classes (rho = s + r * LPS, s < LPS)
   auto has_node = [](int r) { return r * LPS < NST; };
@@ -1080,33 +1083,65 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
     }
   }
 
-  // ---- static Gauss-Jordan ----
+  // ---- static Gauss-Jordan, one step of look-ahead ----
+  // Step t updates the slot holding pivot row t+1 first, stages that row and issues its
+  // loads, then updates the other slots while the loads are in flight: the shared-memory
+  // round trip of the next pivot row overlaps this step's bulk update.
+  // live(t, c): column c of pivot row t is needed (not pivoted before t; phase-1 pivot rows
+  // are monomial rows, zero in the lambda columns)
+  auto live_at = [](int tt, int cc) {
+    const int phh = tt < NQ ? 1 : (tt < 2 * NQ ? 2 : 3);
+    return cc < NC && st_col_step<NST, NQ>(cc) >= tt && !(phh == 1 && cc >= NST && cc < NS);
+  };
+  auto stage = [&](auto tc2) {  // owner of pivot row t2 writes its live columns
+    constexpr int t2 = decltype(tc2)::value;
+    constexpr int pr2 = st_piv_row<NST, NQ>(t2);
+    constexpr int os2 = pr2 / LPS, ol2 = pr2 % LPS;
+    const bool own2 = lane_live && s == ol2;
+    const unsigned pbase = (t2 & 1) ? pb1 : pb0;
+#pragma unroll
+    for (int cc = 0; cc < NC; cc += 2) {
+      const bool l0 = live_at(t2, cc), l1 = live_at(t2, cc + 1);
+      if (l0 && l1) st_pred2(own2, pbase + 8u * cc, a[os2][cc], a[os2][cc + 1]);
+      else if (l0) st_pred1(own2, pbase + 8u * cc, a[os2][cc]);
+      else if (l1) st_pred1(own2, pbase + 8u * (cc + 1), a[os2][cc + 1]);
+    }
+  };
+  auto load = [&](auto tc2, double* v) {
+    constexpr int t2 = decltype(tc2)::value;
+    const double* prow = sm.prow[t2 & 1];
+#pragma unroll
+    for (int cc = 0; cc < NC; cc += 2) {
+      const bool l0 = live_at(t2, cc), l1 = live_at(t2, cc + 1);
+      if (l0 && l1) {
+        const double2 q = *reinterpret_cast<const double2*>(prow + cc);
+        v[cc] = q.x;
+        v[cc + 1] = q.y;
+      } else if (l0) {
+        v[cc] = prow[cc];
+      } else if (l1) {
+        v[cc + 1] = prow[cc + 1];
+      }
+    }
+  };
   double invp[RPL];
 #pragma unroll
   for (int r = 0; r < RPL; ++r) invp[r] = 0.0;
+  double pv[NC];  // pivot row of the current step
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc) pv[cc] = 0.0;
+  stage(std::integral_constant<int, 0>{});
+  __syncwarp();
+  load(std::integral_constant<int, 0>{}, pv);
   static_for<NS>([&](auto tc) {
     constexpr int t = decltype(tc)::value;
     constexpr int pr = st_piv_row<NST, NQ>(t), pc = st_piv_col<NST, NQ>(t);
     constexpr int os = pr / LPS, ol = pr % LPS;
     constexpr int ph = t < NQ ? 1 : (t < 2 * NQ ? 2 : 3);
     const bool own = lane_live && s == ol;
-    const unsigned pbase = (t & 1) ? pb1 : pb0;
-    // live columns of the pivot row: not pivoted before t; phase 1 rows have no lambda
-    auto live = [&](int cc) {
-      return cc < NC && st_col_step<NST, NQ>(cc) >= t && !(ph == 1 && cc >= NST && cc < NS);
-    };
-#pragma unroll
-    for (int cc = 0; cc < NC; cc += 2) {
-      const bool l0 = live(cc), l1 = live(cc + 1);
-      if (l0 && l1) st_pred2(own, pbase + 8u * cc, a[os][cc], a[os][cc + 1]);
-      else if (l0) st_pred1(own, pbase + 8u * cc, a[os][cc]);
-      else if (l1) st_pred1(own, pbase + 8u * (cc + 1), a[os][cc + 1]);
-    }
-    __syncwarp();
-    const double* prow = sm.prow[t & 1];
     double inv;
     if constexpr (ph == 3) {
-      const double piv = prow[pc];
+      const double piv = pv[pc];
       bad = bad || !(piv >= kStaticSchurMin);
       inv = fast_rcp(piv);
       invp[os] = own ? inv : invp[os];
@@ -1114,14 +1149,31 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
       inv = sm.inv_hist[t < NQ ? t : t - NQ];
       if constexpr (ph == 1) invp[os] = own ? inv : invp[os];
     }
-#pragma unroll
-    for (int r = 0; r < RPL; ++r) {
-      if ((ph == 2 && only_poly(r)) || (ph == 3 && only_I(r))) continue;
+    auto active = [&](int r) { return !((ph == 2 && only_poly(r)) || (ph == 3 && only_I(r))); };
+    auto update = [&](int r) {
       double l = a[r][pc] * inv;
       if (r == os) l = own ? 0.0 : l;
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc)
-        if (cc != pc && live(cc)) a[r][cc] = fma(-l, prow[cc], a[r][cc]);
+        if (cc != pc && live_at(t, cc)) a[r][cc] = fma(-l, pv[cc], a[r][cc]);
+    };
+    if constexpr (t + 1 < NS) {
+      constexpr int os_next = st_piv_row<NST, NQ>(t + 1) / LPS;
+      if (active(os_next)) update(os_next);
+      stage(std::integral_constant<int, t + 1>{});
+      __syncwarp();
+      double pn[NC];
+      load(std::integral_constant<int, t + 1>{}, pn);
+#pragma unroll
+      for (int r = 0; r < RPL; ++r)
+        if (r != os_next && active(r)) update(r);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+        if (live_at(t + 1, cc)) pv[cc] = pn[cc];
+    } else {
+#pragma unroll
+      for (int r = 0; r < RPL; ++r)
+        if (active(r)) update(r);
     }
   });
 
@@ -1138,6 +1190,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
     }
   }
   __syncwarp();
+  if constexpr (kInlineFallback) {
+    // same lane layout as the searching kernel: a warp with a flagged system re-solves its
+    // whole group with partial pivoting, in its own part of shared memory (no second launch)
+    if (__any_sync(0xffffffffu, sys_live && bad)) {
+      using SmS = RbfSmem<D, NST, NOPS>;
+      static_assert(sizeof(SmS) <= sizeof(Sm), "searching layout must fit the warp's shared memory");
+      SmS* mine = reinterpret_cast<SmS*>(smem_all + warp * SPW);
+      rbf_search_group<D, NST, NOPS, LPS, RPL, WARPS>(blockIdx.x, mine - warp * SPW, pos, stencils, K, K, nullptr,
+                                                      ops, row_normals, out_idx, out_w, info);
+      return;
+    }
+  }
   if (!sys_live) return;
   if (bad) {
     if (s == 0) flag_list[atomicAdd(flag_count, 1)] = static_cast<int>(k);
@@ -1308,16 +1372,20 @@ static void launch_rbf_v(const double* pos, const int* st, int64_t K, const OpSp
 
 // Static-order kernel, then the searching kernel over the stencils it flagged (list mode,
 // grid-stride: an empty list costs one short launch).
-template <int D, int NST, int NOPS, int LPS, int RPL, int WARPS, int MINB, int FLPS, int FRPL>
+template <int D, int NST, int NOPS, int LPS, int RPL, int WARPS, int MINB, int FLPS, int FRPL, bool ILV = false>
 static cudaError_t launch_rbf_static(const double* pos, const int* st, int64_t K, const OpSpec& ops,
                                      const double* rn, int* oi, double* ow, int* info, cudaStream_t s, int force) {
   // the standard operator set [Lap, d/dx_0, ..] gets compile-time right-hand sides
   bool std_ops = rn == nullptr && NOPS == D + 1 && ops.kind[0] == kOpLaplacian;
   for (int o = 1; o < NOPS && std_ops; ++o) std_ops = ops.kind[o] == kOpPartial && ops.axis[o] == o - 1;
-  int* buf = nullptr;  // [count, list...]
-  cudaError_t e = stream_alloc(reinterpret_cast<void**>(&buf), sizeof(int) * (K + 1), s);
-  if (e != cudaSuccess) return e;
-  cudaMemsetAsync(buf, 0, sizeof(int), s);
+  // same lane layout as the searching kernel: flagged systems are re-solved in the kernel
+  constexpr bool inline_fb = D == 2 && NST == 12 && LPS == 6 && RPL == 3 && !ILV;
+  int* buf = nullptr;  // [count, list...] of flagged stencils (second launch)
+  if (!inline_fb) {
+    cudaError_t e = stream_alloc(reinterpret_cast<void**>(&buf), sizeof(int) * (K + 1), s);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(buf, 0, sizeof(int), s);
+  }
   constexpr int SPW = 32 / LPS;
   const int64_t grid = ceil_div(K, static_cast<int64_t>(WARPS) * SPW);
   const size_t smem = sizeof(RbfStaticSmem<D, NST, NOPS>) * WARPS * SPW;
@@ -1328,15 +1396,16 @@ static cudaError_t launch_rbf_static(const double* pos, const int* st, int64_t K
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       attr = true;
     }
-    kern<<<grid, WARPS * 32, smem, s>>>(pos, st, K, ops, rn, oi, ow, info, buf + 1, buf, force);
+    kern<<<grid, WARPS * 32, smem, s>>>(pos, st, K, ops, rn, oi, ow, info, buf ? buf + 1 : nullptr, buf, force);
   };
-  using KT = decltype(&rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB>);
+  using KT = decltype(&rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB, ILV>);
   if constexpr (NOPS == D + 1) {
-    if (std_ops) go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, true, LPS, RPL, WARPS, MINB>>{});
-    else go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB>>{});
+    if (std_ops) go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, true, LPS, RPL, WARPS, MINB, ILV>>{});
+    else go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB, ILV>>{});
   } else {
-    go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB>>{});
+    go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB, ILV>>{});
   }
+  if constexpr (inline_fb) return cudaGetLastError();
   constexpr int FSPW = 32 / FLPS;
   const int64_t groups = ceil_div(K, static_cast<int64_t>(4) * FSPW);
   const int64_t cap = static_cast<int64_t>(sm_count()) * 2;
@@ -1347,8 +1416,8 @@ static cudaError_t launch_rbf_static(const double* pos, const int* st, int64_t K
 
 // Kernel choice (tuning/tests; 0 = default static order + flagged fallback):
 // 100 = searching kernel for every stencil; 101 = static kernel with every stencil flagged
-// (exercises the list-mode fallback); 1..5 = launch shapes of the 2D searching kernel;
-// 10..19 = launch shapes of the static kernel.
+// (exercises the fallback: in-kernel for 2D, list mode for 3D); 10..14 = launch shapes of
+// the static kernel.
 static int g_rbf_variant = 0;
 HN_EXPORT void hn_weights_rbf_set_variant(int v) { g_rbf_variant = v; }
 
@@ -1357,33 +1426,40 @@ static cudaError_t launch_rbf(const double* pos, const int* st, int64_t K, const
                               int* oi, double* ow, int* info, cudaStream_t s) {
   const int v = g_rbf_variant;
   const int force = v == 101 ? 1 : 0;
+  constexpr bool tune = NOPS == D + 1;  // launch-shape variants only for the standard op count
   if constexpr (D == 2) {
-    switch (v) {
-      case 1: launch_rbf_v<2, 12, NOPS, 6, 3, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return cudaSuccess;
-      case 2: launch_rbf_v<2, 12, NOPS, 9, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return cudaSuccess;
-      case 100: launch_rbf_v<2, 12, NOPS, 6, 3, 4, 3>(pos, st, K, ops, rn, oi, ow, info, s); return cudaSuccess;
-      case 10: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 2, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-      case 11: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 3, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-      case 12: return launch_rbf_static<2, 12, NOPS, 6, 3, 2, 6, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-      case 13: return launch_rbf_static<2, 12, NOPS, 6, 3, 8, 1, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-      case 14: return launch_rbf_static<2, 12, NOPS, 3, 6, 4, 2, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-      case 15: return launch_rbf_static<2, 12, NOPS, 3, 6, 2, 4, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-      case 16: return launch_rbf_static<2, 12, NOPS, 3, 6, 4, 1, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-      default: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, force);
+    if (v == 100) {
+      launch_rbf_v<2, 12, NOPS, 6, 3, 4, 3>(pos, st, K, ops, rn, oi, ow, info, s);
+      return cudaSuccess;
     }
+    if constexpr (tune) {
+      switch (v) {
+        case 10: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 2, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+        case 11: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 3, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+        case 14: return launch_rbf_static<2, 12, NOPS, 3, 6, 4, 2, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+        default: break;
+      }
+    }
+    return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, force);
   } else if constexpr (NST == 20) {
-    switch (v) {
-      case 100: launch_rbf_v<3, 20, NOPS, 15, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return cudaSuccess;
-      case 10: return launch_rbf_static<3, 20, NOPS, 10, 3, 4, 1, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-      case 11: return launch_rbf_static<3, 20, NOPS, 10, 3, 2, 2, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-      case 12: return launch_rbf_static<3, 20, NOPS, 15, 2, 4, 2, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-      default: return launch_rbf_static<3, 20, NOPS, 10, 3, 4, 1, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, force);
+    if (v == 100) {
+      launch_rbf_v<3, 20, NOPS, 15, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s);
+      return cudaSuccess;
     }
+    if constexpr (tune) {
+      switch (v) {
+        case 11: return launch_rbf_static<3, 20, NOPS, 10, 3, 2, 2, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+        case 12: return launch_rbf_static<3, 20, NOPS, 15, 2, 4, 2, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+        default: break;
+      }
+    }
+    return launch_rbf_static<3, 20, NOPS, 10, 3, 4, 1, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, force);
   } else {
-    switch (v) {
-      case 100: launch_rbf_v<3, 30, NOPS, 20, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s); return cudaSuccess;
-      default: return launch_rbf_static<3, 30, NOPS, 20, 2, 4, 1, 20, 2>(pos, st, K, ops, rn, oi, ow, info, s, force);
+    if (v == 100) {
+      launch_rbf_v<3, 30, NOPS, 20, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s);
+      return cudaSuccess;
     }
+    return launch_rbf_static<3, 30, NOPS, 20, 2, 4, 1, 20, 2>(pos, st, K, ops, rn, oi, ow, info, s, force);
   }
 }
 

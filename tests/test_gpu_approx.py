@@ -496,3 +496,78 @@ def test_all_boundary_node_set_gives_empty_rows():
     t = compute_weights(ns, [Laplacian(), Partial(0)])
     assert (t.sizes == 0).all() and (t.indices == -1).all()
     assert all((w == 0).all() for w in t.weights.values())
+
+
+# ---------------------------------------------------------------- RBF kernel variants
+@pytest.mark.parametrize("dim,n", [(2, 12), (3, 20), (3, 30)])
+def test_rbf_static_order_and_fallbacks_match_dgesv(dim, n):
+    """The static null-space elimination (default), the partial-pivoting searching kernel
+    (variant 100) and the static kernel with every stencil flagged (variant 101: in-kernel
+    fallback in 2D, list-mode second launch in 3D) all match dgesv; the flagged path is
+    bit-identical to the searching kernel."""
+    from paper_2303_01760_b200 import _lib as L
+    from paper_2303_01760_b200._device import DeviceNodes
+
+    rng = np.random.default_rng(5 + n)
+    m = 24 if dim == 2 else 11
+    g = np.stack(np.meshgrid(*([np.arange(1, m) / m] * dim), indexing="ij"), -1).reshape(-1, dim)
+    pts = g + rng.uniform(-0.35, 0.35, g.shape) / m
+    ns = cloud_nodeset(pts, h=1.0 / m)
+    if dim == 3:
+        ns = NodeSet(pts, np.full(len(pts), 1.0 / m), np.full(len(pts), KIND_SCATTERED, dtype=np.int8),
+                     np.zeros(len(pts), dtype=np.int8), np.full(len(pts), np.nan), np.full((len(pts), 3), np.nan))
+    dn = DeviceNodes(ns)
+    rows = np.arange(len(pts), dtype=np.int32)
+    st_d = dn.knn(n, rows=L.to_device(rows))
+    st_h = st_d.cpu().numpy().astype(np.int64)
+    K, nops = len(rows), dim + 1
+    t = L.torch()
+    ops = [("lap",)] + [("d", a) for a in range(dim)]
+    want = O.rbf_solve(ns.positions, st_h, ops)
+    order = np.argsort(st_h, axis=1, kind="stable")
+    want = np.take_along_axis(want, order[:, :, None], 1)
+    res = {}
+    try:
+        for v in (0, 100, 101):
+            L.lib().hn_weights_rbf_set_variant(v)
+            oi = L.empty((n, K), t.int32)
+            ow = L.empty((nops, n, K), t.float64)
+            info = L.zeros(K, t.int32)
+            L.call("hn_weights_rbf", L.ptr(dn.pos), dim, L.ptr(st_d), K, n, nops, L.host_ints([0] + [1] * dim),
+                   L.host_ints([0] + list(range(dim))), L.host_dbls([0.0] * (3 * nops)), None, None, L.ptr(oi),
+                   L.ptr(ow), L.ptr(info), L.stream_handle())
+            t.cuda.synchronize()
+            res[v] = (oi.cpu().numpy(), ow.cpu().numpy(), info.cpu().numpy())
+    finally:
+        L.lib().hn_weights_rbf_set_variant(0)
+    for v, (oi, ow, info) in res.items():
+        npt.assert_array_equal(oi.T, np.take_along_axis(st_h, order, 1))
+        assert not info.any()
+        for o in range(nops):
+            assert rowwise_rel(ow[o].T, want[:, :, o]) <= W_TOL, (v, o)
+    npt.assert_array_equal(res[101][1], res[100][1])
+
+
+def test_rbf_static_kernel_flags_singular_stencils():
+    """A stencil with a repeated node (exactly singular) is flagged by the static kernel and
+    re-solved with partial pivoting, which reports dgesv's exact zero pivot."""
+    from paper_2303_01760_b200 import _lib as L
+    from paper_2303_01760_b200._device import DeviceNodes
+
+    rng = np.random.default_rng(2)
+    pts = rng.uniform(0, 1, (400, 2))
+    ns = cloud_nodeset(pts, h=0.05)
+    dn = DeviceNodes(ns)
+    st_d = dn.knn(12, rows=L.to_device(np.arange(400, dtype=np.int32)))
+    st_h = st_d.cpu().numpy()
+    st_h[7, 5] = st_h[7, 4]  # repeated node -> two identical rows and columns
+    t = L.torch()
+    st_d = L.to_device(st_h.astype(np.int32))
+    oi = L.empty((12, 400), t.int32)
+    ow = L.empty((3, 12, 400), t.float64)
+    info = L.zeros(400, t.int32)
+    L.call("hn_weights_rbf", L.ptr(dn.pos), 2, L.ptr(st_d), 400, 12, 3, L.host_ints([0, 1, 1]), L.host_ints([0, 0, 1]),
+           L.host_dbls([0.0] * 9), None, None, L.ptr(oi), L.ptr(ow), L.ptr(info), L.stream_handle())
+    t.cuda.synchronize()
+    inf = info.cpu().numpy()
+    assert inf[7] != 0 and np.count_nonzero(inf) == 1
