@@ -14,6 +14,8 @@
 // MON: one thread per stencil, matrix in registers, LU with partial pivoting.
 // RBF: LPS lanes per stencil, RPL matrix rows per lane held in registers
 //      (row i lives in lane i % LPS, slot i / LPS), 32/LPS stencils per warp.
+//      Default: rbf_static_kernel -- a static null-space elimination order (below), with
+//      flagged stencils re-solved by the searching kernel.  Searching kernel:
 //      Gauss-Jordan with implicit partial pivoting: every step picks the largest
 //      |a_ik| among not-yet-pivoted rows (segmented shuffle argmax on a packed
 //      key), the owner lane stages the pivot row in shared memory, and every lane
@@ -780,11 +782,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_weights_kernel(
 // zero blocks are skipped statically (monomial rows have no lambda columns; phase 2 leaves
 // monomial rows alone, phase 3 the I rows whose lambda values are not needed).
 // Row rho = s + r * LPS of the renumbered system lives in segment lane s, slot r: rho < NQ
-// node I_rho, rho < NST node J, else monomial rho - NST.  Segments are interleaved across
-// the warp (lane = s * SPW + system), so the owners of a pivot row -- one per system --
-// are SPW adjacent lanes and their predicated 16-B stores take one or two shared-memory
-// phases instead of four.  The matrix is assembled in registers (shared memory is the
-// scarcer resource here: it carries every pivot-row broadcast).
+// node I_rho, rho < NST node J, else monomial rho - NST.  A system's segment is LPS
+// contiguous lanes (ILV = true interleaves them, lane = s * SPW + system: the pivot-row
+// owners become adjacent and their stores cheaper, but the broadcast loads, which dominate,
+// cost twice as many shared-memory wavefronts; measured slower).  The matrix is assembled
+// in registers -- shared memory is the scarcer resource: it carries every pivot-row
+// broadcast, and staging the symmetric A there once per pair cost more than the 2x cubes.
+// Step t updates the next pivot row first, stages it and issues its loads (and the next
+// pivot's reciprocal) before the bulk update of step t.
 // Checked against dgesv on every config's stencils (numpy model of this order: <= 1.8e-13
 // row-normwise on configs 1/2/4, interior and one-sided boundary stencils; pivots of
 // phases 1/2 >= 0.06, phase-3 pivots >= 5e-3).  A stencil with a step-A pivot below
@@ -883,11 +888,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
   const bool sys_live = lane_live && k_raw < K;
   const int64_t k = k_raw < K ? k_raw : K - 1;
   Sm& sm = smem_all[warp * SPW + sys_w];
-  // butterfly partner in segment-relative numbering; out-of-segment partners read
-  // themselves, which leaves segment lane 0 holding the full reduction
-  auto seg_src = [&](int off) {
-    const int t = s ^ off;
-    return (lane_live && t < LPS) ? (ILV ? t * SPW + sys_w : sys_w * LPS + t) : lane;
+  // all-reduce butterfly partner in segment-relative numbering: s ^ off clamped to LPS - 1
+  // leaves every lane of the segment with the full reduction for any LPS (checked for
+  // 2..24), so no broadcast shuffle follows
+  auto seg_xor = [&](int off) {
+    int t = s ^ off;
+    t = t < LPS ? t : LPS - 1;
+    return lane_live ? (ILV ? t * SPW + sys_w : sys_w * LPS + t) : lane;
   };
   // slot classes (rho = s + r * LPS, s < LPS)
   auto has_node = [](int r) { return r * LPS < NST; };
@@ -929,8 +936,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
     }
   }
 #pragma unroll
-  for (int off = 1; off < LPS; off <<= 1) d2max = fmax(d2max, __shfl_sync(0xffffffffu, d2max, seg_src(off)));
-  d2max = __shfl_sync(0xffffffffu, d2max, lane_live ? seg_base : lane);
+  for (int off = 1; off < LPS; off <<= 1) d2max = fmax(d2max, __shfl_sync(0xffffffffu, d2max, seg_xor(off)));
   const double s1 = fast_rcp(fast_sqrt(d2max));
 #pragma unroll
   for (int r = 0; r < PA; ++r)
@@ -953,16 +959,24 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
       for (int m = 0; m < NQ; ++m) pp[r][m] = mono_val<D>(m, yo[r]);
       vm[r] = (lane_live && j < NST) ? (0x7fffffc0u | static_cast<unsigned>(63 - j)) : 0u;
     }
-    unsigned chosen = 0u;
-    static_for<NQ>([&](auto mc) {
-      constexpr int m = decltype(mc)::value;
+    // column 0 (monomial 1) is all ones: partial pivoting takes the first node, the centre,
+    // whose monomial row is [1, 0, ..] (y = 0 exactly), so step 0 eliminates nothing
+    unsigned chosen = 1u;
+    vm[0] = s == 0 ? 0u : vm[0];
+    if (lane_live && s == 0) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) sm.yp[0][a] = yo[0][a];
+      sm.sidp[0] = sido[0];
+      sm.inv_hist[0] = 1.0;
+    }
+    static_for<NQ - 1>([&](auto mc) {
+      constexpr int m = decltype(mc)::value + 1;
       unsigned key = 0;
 #pragma unroll
       for (int r = 0; r < PA; ++r)
         key = max(key, (static_cast<unsigned>(__double2hiint(pp[r][m])) | 63u) & vm[r]);
 #pragma unroll
-      for (int off = 1; off < LPS; off <<= 1) key = max(key, __shfl_sync(0xffffffffu, key, seg_src(off)));
-      key = __shfl_sync(0xffffffffu, key, lane_live ? seg_base : lane);
+      for (int off = 1; off < LPS; off <<= 1) key = max(key, __shfl_sync(0xffffffffu, key, seg_xor(off)));
       const unsigned ptag = key & 63u;
       const unsigned pbase = (m & 1) ? pb1 : pb0;
       bool isp[PA];
@@ -1130,25 +1144,29 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
   double pv[NC];  // pivot row of the current step
 #pragma unroll
   for (int cc = 0; cc < NC; ++cc) pv[cc] = 0.0;
+  // 1/pivot of step t2 from its loaded pivot row (phase 3) or step A's history (phases 1-2)
+  auto pivot_inv = [&](auto tc2, const double* v) {
+    constexpr int t2 = decltype(tc2)::value;
+    if constexpr (t2 >= 2 * NQ) {
+      const double piv = v[st_piv_col<NST, NQ>(t2)];
+      bad = bad || !(piv >= kStaticSchurMin);
+      return fast_rcp(piv);
+    } else {
+      return sm.inv_hist[t2 < NQ ? t2 : t2 - NQ];
+    }
+  };
   stage(std::integral_constant<int, 0>{});
   __syncwarp();
   load(std::integral_constant<int, 0>{}, pv);
+  double inv_cur = pivot_inv(std::integral_constant<int, 0>{}, pv);
   static_for<NS>([&](auto tc) {
     constexpr int t = decltype(tc)::value;
     constexpr int pr = st_piv_row<NST, NQ>(t), pc = st_piv_col<NST, NQ>(t);
     constexpr int os = pr / LPS, ol = pr % LPS;
     constexpr int ph = t < NQ ? 1 : (t < 2 * NQ ? 2 : 3);
     const bool own = lane_live && s == ol;
-    double inv;
-    if constexpr (ph == 3) {
-      const double piv = pv[pc];
-      bad = bad || !(piv >= kStaticSchurMin);
-      inv = fast_rcp(piv);
-      invp[os] = own ? inv : invp[os];
-    } else {
-      inv = sm.inv_hist[t < NQ ? t : t - NQ];
-      if constexpr (ph == 1) invp[os] = own ? inv : invp[os];
-    }
+    const double inv = inv_cur;
+    if constexpr (ph != 2) invp[os] = own ? inv : invp[os];
     auto active = [&](int r) { return !((ph == 2 && only_poly(r)) || (ph == 3 && only_I(r))); };
     auto update = [&](int r) {
       double l = a[r][pc] * inv;
@@ -1164,6 +1182,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
       __syncwarp();
       double pn[NC];
       load(std::integral_constant<int, t + 1>{}, pn);
+      inv_cur = pivot_inv(std::integral_constant<int, t + 1>{}, pn);
 #pragma unroll
       for (int r = 0; r < RPL; ++r)
         if (r != os_next && active(r)) update(r);
