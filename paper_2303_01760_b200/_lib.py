@@ -99,6 +99,8 @@ def lib():
             fn.restype = res
             fn.argtypes = args
         _LIB = handle
+        if os.environ.get("HN_RBF_VARIANT"):  # dev A/B of the weight kernels (tools/ab_rbf.py)
+            handle.hn_weights_rbf_set_variant(int(os.environ["HN_RBF_VARIANT"]))
     return _LIB
 
 
