@@ -103,19 +103,41 @@ __device__ __forceinline__ void momentum_row(const StepBins& b, int bin, int64_t
 #pragma unroll
     for (int a = 0; a < D; ++a) vi[a] = __ldg(v + a * N + row);
     const double tdelta = __dsub_rn(__ldg(T + row), c.t_ref);
+    // every gather of the row first (D components), then each weight loaded once and
+    // applied to all components: D * (D + 1) sequential sums, each in ascending-j order
+    double fv[D][W];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc)
+#pragma unroll
+      for (int j = 0; j < W; ++j) fv[cc][j] = __ldg(v + cc * N + id[j]);
+    double gs[D][D], ls[D];
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) {
-      double fv[W];
+      ls[cc] = 0.0;
 #pragma unroll
-      for (int j = 0; j < W; ++j) fv[j] = __ldg(v + cc * N + id[j]);
+      for (int a = 0; a < D; ++a) gs[cc][a] = 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double wa = __ldg(wb + b.d_plane[a] * ps + j * K + k);
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) gs[cc][a] = __dadd_rn(gs[cc][a], __dmul_rn(wa, fv[cc][j]));
+      }
+      const double wl = __ldg(wb + b.lap_plane * ps + j * K + k);
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) ls[cc] = __dadd_rn(ls[cc], __dmul_rn(wl, fv[cc][j]));
+    }
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) {
       double adv = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        const double g = ssum<W>(wb + b.d_plane[a] * ps, K, k, fv);
-        const double t = __dmul_rn(vi[a], g);
+        const double t = __dmul_rn(vi[a], gs[cc][a]);
         adv = (a == 0) ? t : __dadd_rn(adv, t);
       }
-      const double lap = ssum<W>(wb + b.lap_plane * ps, K, k, fv);
+      const double lap = ls[cc];
       double rhs = __dsub_rn(__dadd_rn(-adv, __dmul_rn(c.Pr, lap)), __dmul_rn(c.buoy[cc], tdelta));
       if (c.hc)
         rhs = __dadd_rn(rhs, __dmul_rn(__dmul_rn(__ldg(c.hc + row), speed_of<D>(vi)), __ldg(c.l2 + cc * N + row)));
@@ -342,13 +364,37 @@ __device__ __forceinline__ double csr_row_seq(const int* __restrict__ cols, cons
   return acc;
 }
 
+// Rows of at most 32 entries (every boundary stencil: n = 12 in 2D, 30 in 3D) issue all
+// their column/value loads, then all their gathers, before the sequential sum: three
+// memory round trips per row instead of one per batch of 8.
+__device__ __forceinline__ double csr_row_seq32_neu(const int* __restrict__ cols, const double* __restrict__ vals,
+                                                   const double* __restrict__ x, const uint8_t* __restrict__ is_neu,
+                                                   int64_t e, int len) {
+  int c[32];
+  double v[32], xv[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    c[k] = k < len ? __ldg(cols + e + k) : -1;
+    v[k] = k < len ? __ldg(vals + e + k) : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) xv[k] = (c[k] >= 0 && !__ldg(is_neu + c[k])) ? x[c[k]] : 0.0;
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    if (k < len) acc = __dadd_rn(acc, __dmul_rn(v[k], xv[k]));
+  return acc;
+}
+
 __global__ void neumann_kernel(const int64_t* __restrict__ rowptr, const int* __restrict__ cols,
                                const double* __restrict__ vals, const int* __restrict__ neu_idx,
                                const double* __restrict__ diag, const uint8_t* __restrict__ is_neu, int64_t nrows,
                                double* __restrict__ T) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
-  const double acc = csr_row_seq<true>(cols, vals, T, is_neu, rowptr[r], rowptr[r + 1]);
+  const int64_t e0 = __ldg(rowptr + r), e1 = __ldg(rowptr + r + 1);
+  const double acc = e1 - e0 <= 32 ? csr_row_seq32_neu(cols, vals, T, is_neu, e0, static_cast<int>(e1 - e0))
+                                   : csr_row_seq<true>(cols, vals, T, is_neu, e0, e1);
   T[neu_idx[r]] = __ddiv_rn(-acc, diag[r]);
 }
 
