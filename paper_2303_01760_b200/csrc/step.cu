@@ -169,13 +169,15 @@ __device__ __forceinline__ void div_row(const StepBins& b, int bin, int64_t k, c
 #pragma unroll
     for (int j = 0; j < W; ++j) id[j] = __ldg(b.idx[bin] + j * K + k);
     const int64_t ps = static_cast<int64_t>(W) * K;
+    double fv[D][W];  // every gather first
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int j = 0; j < W; ++j) fv[a][j] = __ldg(vs + a * N + id[j]);
     double div = 0.0;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      double fv[W];
-#pragma unroll
-      for (int j = 0; j < W; ++j) fv[j] = __ldg(vs + a * N + id[j]);
-      const double s = ssum<W>(b.w[bin] + b.d_plane[a] * ps, K, k, fv);
+      const double s = ssum<W>(b.w[bin] + b.d_plane[a] * ps, K, k, fv[a]);
       div = (a == 0) ? s : __dadd_rn(div, s);
     }
     rhs[row] = __ddiv_rn(div, dt);
@@ -227,19 +229,28 @@ __device__ __forceinline__ void correct_temp_row(const StepBins& b, int bin, int
       fp[j] = __ldg(p + id[j]);
       ft[j] = __ldg(T + id[j]);
     }
+    // each derivative weight loaded once for both fields: 2D + 1 sequential sums in j order
+    double gp[D], gt[D], lap = 0.0;
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
-      const double gp = ssum<W>(wb + b.d_plane[a] * ps, K, k, fp);
-      vn[a] = __dsub_rn(__ldg(vs + a * N + row), __dmul_rn(dt, gp));
+    for (int a = 0; a < D; ++a) gp[a] = gt[a] = 0.0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double wa = __ldg(wb + b.d_plane[a] * ps + j * K + k);
+        gp[a] = __dadd_rn(gp[a], __dmul_rn(wa, fp[j]));
+        gt[a] = __dadd_rn(gt[a], __dmul_rn(wa, ft[j]));
+      }
+      lap = __dadd_rn(lap, __dmul_rn(__ldg(wb + b.lap_plane * ps + j * K + k), ft[j]));
     }
+#pragma unroll
+    for (int a = 0; a < D; ++a) vn[a] = __dsub_rn(__ldg(vs + a * N + row), __dmul_rn(dt, gp[a]));
     double conv = 0.0;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      const double gt = ssum<W>(wb + b.d_plane[a] * ps, K, k, ft);
-      const double t = __dmul_rn(vn[a], gt);
+      const double t = __dmul_rn(vn[a], gt[a]);
       conv = (a == 0) ? t : __dadd_rn(conv, t);
     }
-    const double lap = ssum<W>(wb + b.lap_plane * ps, K, k, ft);
     double r = __dadd_rn(-conv, lap);
     if (hy.hc) r = __dadd_rn(r, __dmul_rn(__dmul_rn(__ldg(hy.hc + row), speed_of<D>(vn)), __ldg(hy.l2 + row)));
     tn = __dadd_rn(__ldg(T + row), __dmul_rn(dt, r));
