@@ -858,7 +858,7 @@ __device__ __forceinline__ double std_poly_rhs(int o, int m) {
   return m == o ? 1.0 : 0.0;                        // d/dx_a of monomial 1 + a
 }
 
-template <int D, int NST, int NOPS, bool STD, int LPS, int RPL, int WARPS, int MINB, bool ILV>
+template <int D, int NST, int NOPS, bool STD, int LPS, int RPL, int WARPS, int MINB, bool ILV, bool SHB = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
     const double* __restrict__ pos, const int* __restrict__ stencils, int64_t K, OpSpec ops,
     const double* __restrict__ row_normals, int* __restrict__ out_idx, double* __restrict__ out_w,
@@ -1121,6 +1121,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
       else if (l1) st_pred1(own2, pbase + 8u * (cc + 1), a[os2][cc + 1]);
     }
   };
+  // SHB: the pivot row goes from the owner's registers to its segment by shuffles (one
+  // SHFL pair per value, no shared-memory round trip) instead of a staged store + load
+  auto bcast = [&](auto tc2, double* v) {
+    constexpr int t2 = decltype(tc2)::value;
+    constexpr int pr2 = st_piv_row<NST, NQ>(t2);
+    constexpr int os2 = pr2 / LPS, ol2 = pr2 % LPS;
+    const int src = lane_live ? (ILV ? ol2 * SPW + sys_w : sys_w * LPS + ol2) : lane;
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+      if (live_at(t2, cc)) v[cc] = __shfl_sync(0xffffffffu, a[os2][cc], src);
+  };
   auto load = [&](auto tc2, double* v) {
     constexpr int t2 = decltype(tc2)::value;
     const double* prow = sm.prow[t2 & 1];
@@ -1155,9 +1166,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
       return sm.inv_hist[t2 < NQ ? t2 : t2 - NQ];
     }
   };
-  stage(std::integral_constant<int, 0>{});
-  __syncwarp();
-  load(std::integral_constant<int, 0>{}, pv);
+  if constexpr (SHB) {
+    bcast(std::integral_constant<int, 0>{}, pv);
+  } else {
+    stage(std::integral_constant<int, 0>{});
+    __syncwarp();
+    load(std::integral_constant<int, 0>{}, pv);
+  }
   double inv_cur = pivot_inv(std::integral_constant<int, 0>{}, pv);
   static_for<NS>([&](auto tc) {
     constexpr int t = decltype(tc)::value;
@@ -1178,10 +1193,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
     if constexpr (t + 1 < NS) {
       constexpr int os_next = st_piv_row<NST, NQ>(t + 1) / LPS;
       if (active(os_next)) update(os_next);
-      stage(std::integral_constant<int, t + 1>{});
-      __syncwarp();
       double pn[NC];
-      load(std::integral_constant<int, t + 1>{}, pn);
+      if constexpr (SHB) {
+        bcast(std::integral_constant<int, t + 1>{}, pn);
+      } else {
+        stage(std::integral_constant<int, t + 1>{});
+        __syncwarp();
+        load(std::integral_constant<int, t + 1>{}, pn);
+      }
       inv_cur = pivot_inv(std::integral_constant<int, t + 1>{}, pn);
 #pragma unroll
       for (int r = 0; r < RPL; ++r)
@@ -1391,7 +1410,8 @@ static void launch_rbf_v(const double* pos, const int* st, int64_t K, const OpSp
 
 // Static-order kernel, then the searching kernel over the stencils it flagged (list mode,
 // grid-stride: an empty list costs one short launch).
-template <int D, int NST, int NOPS, int LPS, int RPL, int WARPS, int MINB, int FLPS, int FRPL, bool ILV = false>
+template <int D, int NST, int NOPS, int LPS, int RPL, int WARPS, int MINB, int FLPS, int FRPL, bool ILV = false,
+          bool SHB = false>
 static cudaError_t launch_rbf_static(const double* pos, const int* st, int64_t K, const OpSpec& ops,
                                      const double* rn, int* oi, double* ow, int* info, cudaStream_t s, int force) {
   // the standard operator set [Lap, d/dx_0, ..] gets compile-time right-hand sides
@@ -1417,12 +1437,12 @@ static cudaError_t launch_rbf_static(const double* pos, const int* st, int64_t K
     }
     kern<<<grid, WARPS * 32, smem, s>>>(pos, st, K, ops, rn, oi, ow, info, buf ? buf + 1 : nullptr, buf, force);
   };
-  using KT = decltype(&rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB, ILV>);
+  using KT = decltype(&rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB, ILV, SHB>);
   if constexpr (NOPS == D + 1) {
-    if (std_ops) go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, true, LPS, RPL, WARPS, MINB, ILV>>{});
-    else go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB, ILV>>{});
+    if (std_ops) go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, true, LPS, RPL, WARPS, MINB, ILV, SHB>>{});
+    else go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB, ILV, SHB>>{});
   } else {
-    go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB, ILV>>{});
+    go(std::integral_constant<KT, &rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB, ILV, SHB>>{});
   }
   if constexpr (inline_fb) return cudaGetLastError();
   constexpr int FSPW = 32 / FLPS;
@@ -1456,10 +1476,14 @@ static cudaError_t launch_rbf(const double* pos, const int* st, int64_t K, const
         case 10: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 2, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
         case 11: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 3, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
         case 14: return launch_rbf_static<2, 12, NOPS, 3, 6, 4, 2, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+        case 15: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+        case 16: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 3, 6, 3, false, true>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+        case 17: return launch_rbf_static<2, 12, NOPS, 3, 6, 4, 2, 6, 3, false, true>(pos, st, K, ops, rn, oi, ow, info, s, 0);
         default: break;
       }
     }
-    return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, force);
+    // 2D default: pivot rows broadcast by shuffles (3D rows are 34 wide: shared memory wins)
+    return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3, false, true>(pos, st, K, ops, rn, oi, ow, info, s, force);
   } else if constexpr (NST == 20) {
     if (v == 100) {
       launch_rbf_v<3, 20, NOPS, 15, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s);
@@ -1469,6 +1493,7 @@ static cudaError_t launch_rbf(const double* pos, const int* st, int64_t K, const
       switch (v) {
         case 11: return launch_rbf_static<3, 20, NOPS, 10, 3, 2, 2, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
         case 12: return launch_rbf_static<3, 20, NOPS, 15, 2, 4, 2, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+        case 13: return launch_rbf_static<3, 20, NOPS, 10, 3, 4, 1, 15, 2, false, true>(pos, st, K, ops, rn, oi, ow, info, s, 0);
         default: break;
       }
     }
