@@ -128,16 +128,21 @@ int hn_weights_mon(const double* pos, int d, const int* stencils, int64_t K, int
 /* RBF-FD PHS r^3 + degree-2 saddle solves ((n+q)^2, q = 6 / 10).  row_normals (K x d) or
  * NULL: when given, every op must be HN_OP_NORMAL and uses its row's normal (the
  * `normals` variant, approx.py:260-270).  Tuned warp-cooperative kernels exist for
- * (d,n) = (2,12), (3,20), (3,30) and 1..4 ops (hn_weights_rbf_is_tuned); other sizes use a
- * generic thread-per-stencil kernel that needs `workspace` of
- * hn_weights_rbf_workspace(d, n, nops, K) doubles (returns 3 if workspace is NULL then).
- * Replaces: _batched_rbf_weights approx.py:237-290. */
+ * (d,n) = (2,12), (3,20), (3,30) and 1..4 ops (hn_weights_rbf_is_tuned): a static
+ * null-space elimination order (pivoted LU of P, then a fixed Gauss-Jordan order whose last
+ * phase pivots on the SPD Schur complement) with the partial-pivoting kernel re-solving any
+ * stencil whose static pivots fall below their floors -- so the exact-zero-pivot semantics
+ * of dgesv (info[k] != 0) are kept.  Other sizes use a generic thread-per-stencil kernel
+ * that needs `workspace` of hn_weights_rbf_workspace(d, n, nops, K) doubles (returns 3 if
+ * workspace is NULL then).  Replaces: _batched_rbf_weights approx.py:237-290. */
 int hn_weights_rbf(const double* pos, int d, const int* stencils, int64_t K, int n, int nops,
                    const int* op_kind_host, const int* op_axis_host, const double* op_normal_host,
                    const double* row_normals, double* workspace, int* out_idx, double* out_w,
                    int* info, void* stream);
 int hn_weights_rbf_is_tuned(int d, int n, int nops);
-/* Launch-shape variant of the tuned 2D kernel (0 = default); a tuning knob, not numerics. */
+/* Kernel variant (0 = default).  100 = partial-pivoting kernel for every stencil, 101 = static
+ * kernel with every stencil flagged (exercises the fallback), 10..19 = launch shapes (tuning).
+ * Every variant matches dgesv to ~1e-13; a tuning/testing knob, not a numerics switch. */
 void hn_weights_rbf_set_variant(int v);
 int64_t hn_weights_rbf_workspace(int d, int n, int nops, int64_t K);
 
