@@ -57,6 +57,12 @@ def main():
     t.Tensor.cpu = tcpu
     for _ in range(3):
         call()
+    t0 = EV[0][1]
+    for e in EV:  # timeline of the last traced call
+        if len(e) == 2:
+            print(f"{(e[1] - t0) * 1e3:8.3f} ms  {e[0]}")
+        else:
+            print(f"{(e[1] - t0) * 1e3:8.3f} ms  +{(e[2] - e[1]) * 1e3:6.3f}  {e[0]}")
     # plain timing for several chunk counts of the native pipeline
     t.cuda.Stream.synchronize = orig_sync
     t.Tensor.cpu = orig_cpu
