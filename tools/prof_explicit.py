@@ -18,11 +18,11 @@ def main():
     t = L.torch()
     ns = bench.build_nodeset(cfg, 0)
     st, _, _ = bench._stepper(hn, ns, False, 1e5 if cfg == 4 else 1e6)
-    flush = L.empty(bench.L2_FLUSH_BYTES // 8, t.float64)
+    flush = bench.L2Flush(L)
     e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
     ts = []
     for _ in range(reps):
-        flush.fill_(1.0)
+        flush(1.0)
         e0.record()
         st.explicit_step()
         e1.record()
