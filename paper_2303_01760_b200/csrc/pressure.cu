@@ -320,6 +320,66 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
     if (tr && tid == 0) tr[4 * t + 1] = gtime();
     // (2) dense in-block triangle, 32-column tiles
     const int ntiles = (w + 31) / 32;
+    if (w <= kSnThreads) {
+      // thread tid owns block row tid: it loads its 32 entries of the next tile while the
+      // current tile is solved (the diagonal tile by the warp that owns its rows, lane =
+      // row - t0), so the apply of a tile never waits on memory; same arithmetic and order
+      const bool has = tid < w;
+      const int i = r0 + tid;
+      const int64_t ra = has ? __ldg(rowptr + i) : 0, rz = has ? __ldg(rowptr + i + 1) : 0;
+      auto tile_t0 = [&](int tt) { return LOWER ? 32 * tt : 32 * (ntiles - 1 - tt); };
+      auto load_tile = [&](int t0, double* v) {
+        const int tw = min(32, w - t0);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int c = t0 + k;
+          const bool ok = has && k < tw && (LOWER ? c < tid : c > tid);
+          v[k] = ok ? __ldg(vals + (LOWER ? (rz - tid) + c : ra + (c - tid - 1))) : 0.0;
+        }
+      };
+      double cur[32], nxt[32];
+      load_tile(tile_t0(0), cur);
+      for (int tt = 0; tt < ntiles; ++tt) {
+        const int t0 = tile_t0(tt);
+        const int tw = min(32, w - t0);
+        if (tt + 1 < ntiles) load_tile(tile_t0(tt + 1), nxt);
+        if (warp == t0 / 32) {  // the diagonal tile's rows: lane = row - t0
+          double yv = lane < tw ? ys[tid] : 0.0;
+          const double dg = (!LOWER && lane < tw) ? __ldg(diag + i) : 1.0;
+          if (LOWER) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const double xk = __shfl_sync(0xffffffffu, yv, k);
+              if (lane > k) yv = fma(-cur[k], xk, yv);
+            }
+          } else {
+#pragma unroll
+            for (int k = 31; k >= 0; --k) {
+              if (lane == k && lane < tw) yv = yv / dg;
+              const double xk = __shfl_sync(0xffffffffu, yv, k);
+              if (lane < k) yv = fma(-cur[k], xk, yv);
+            }
+          }
+          if (lane < tw) {
+            ys[tid] = yv;
+            st_release_dbl(x + i, yv);
+          }
+        }
+        __syncthreads();
+        if (has && (LOWER ? tid >= t0 + tw : tid < t0)) {  // apply the solved tile to my row
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (k < tw) acc = fma(cur[k], ys[t0 + k], acc);
+          ys[tid] -= acc;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) cur[k] = nxt[k];
+      }
+      if (tr && tid == 0) tr[4 * t + 2] = gtime();
+      continue;
+    }
     for (int tt = 0; tt < ntiles; ++tt) {
       const int t0 = LOWER ? 32 * tt : 32 * (ntiles - 1 - tt);  // first block row of the tile
       const int tw = min(32, w - t0);
