@@ -222,6 +222,7 @@ __device__ __forceinline__ void warp_small_block(const int64_t* __restrict__ row
     }
     if (!LOWER) dg = __ldg(diag + i);
   }
+  const double rdg = 1.0 / dg;  // off the dependency chain below (x * (1/d): <= 1 ulp from x / d)
   if (LOWER) {
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
@@ -231,7 +232,7 @@ __device__ __forceinline__ void warp_small_block(const int64_t* __restrict__ row
   } else {
 #pragma unroll
     for (int k = 31; k >= 0; --k) {
-      if (lane == k && lane < w) yv = yv / dg;
+      if (lane == k && lane < w) yv = yv * rdg;
       const double xk = __shfl_sync(0xffffffffu, yv, k);
       if (lane < k) yv = fma(-lv[k], xk, yv);
     }
@@ -346,6 +347,7 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
         if (warp == t0 / 32) {  // the diagonal tile's rows: lane = row - t0
           double yv = lane < tw ? ys[tid] : 0.0;
           const double dg = (!LOWER && lane < tw) ? __ldg(diag + i) : 1.0;
+          const double rdg = 1.0 / dg;
           if (LOWER) {
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
           } else {
 #pragma unroll
             for (int k = 31; k >= 0; --k) {
-              if (lane == k && lane < tw) yv = yv / dg;
+              if (lane == k && lane < tw) yv = yv * rdg;
               const double xk = __shfl_sync(0xffffffffu, yv, k);
               if (lane < k) yv = fma(-cur[k], xk, yv);
             }
@@ -406,6 +408,7 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
           for (int k = 0; k < 32; ++k) lv[k] = 0.0;
         }
         const double dg = (!LOWER && lane < tw) ? __ldg(diag + i) : 1.0;
+        const double rdg = 1.0 / dg;
         if (LOWER) {
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
         } else {
 #pragma unroll
           for (int k = 31; k >= 0; --k) {
-            if (lane == k && lane < tw) yv = yv / dg;
+            if (lane == k && lane < tw) yv = yv * rdg;
             const double xk = __shfl_sync(0xffffffffu, yv, k);
             if (lane < k) yv = fma(-lv[k], xk, yv);
           }
