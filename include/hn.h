@@ -248,6 +248,19 @@ int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int
                     const double* vals, const double* diag, const double* b, double* x, double* ysum,
                     int64_t n, unsigned long long* ticket, int ctas_per_sm, void* stream);
 
+/* hn_sptrsv_super with tinv (n x 32 doubles, or NULL = substitution): every row's row of the
+ * inverse of its 32-row diagonal tile (tiles start at each block's r0, r0+32, ..), from
+ * hn_host_tile_inverse; the in-tile triangle is then one matrix-vector product per tile. */
+int hn_sptrsv_super_inv(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
+                        const int* blk_rc, int64_t nblk, const int64_t* rowptr, const int* cols,
+                        const double* vals, const double* diag, const double* tinv, const double* b, double* x,
+                        double* ysum, int64_t n, unsigned long long* ticket, int ctas_per_sm, void* stream);
+/* Host (setup): the tile inverses hn_sptrsv_super_inv reads, from the strict CSR (sorted
+ * columns; lower: unit diagonal, upper: diag) and the block list (r0, w) of nb blocks. */
+int hn_host_tile_inverse(const int64_t* rowptr_host, const int* cols_host, const double* vals_host,
+                         const double* diag_host, int64_t n, int lower, int64_t nb, const int* r0_host,
+                         const int* w_host, double* tinv_host);
+
 /* Debug: per-task timeline of hn_sptrsv_super launches ([start, outside sums done, end]
  * in %globaltimer ns, SM id) written to trace (4 u64 per task); NULL switches it off. */
 int hn_debug_sptrsv_trace(unsigned long long* trace);

@@ -67,6 +67,9 @@ SIGNATURES: dict[str, tuple] = {
     "hn_host_levels": (_i, [_vp, _vp, _i64, _i, _vp]),
     "hn_sptrsv_super": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i,
                              _vp]),
+    "hn_sptrsv_super_inv": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
+                                 _vp, _i, _vp]),
+    "hn_host_tile_inverse": (_i, [_vp, _vp, _vp, _vp, _i64, _i, _i64, _vp, _vp, _vp]),
     "hn_debug_sptrsv_trace": (_i, [_vp]),
     "hn_host_supernodes": (_i64, [_vp, _vp, _i64, _i, _i, _vp, _vp]),
     "hn_host_block_levels": (_i, [_vp, _vp, _i64, _i, _i64, _vp, _vp, _vp]),

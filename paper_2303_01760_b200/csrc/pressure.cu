@@ -183,7 +183,8 @@ __device__ __forceinline__ double row_outside_sum(const int* __restrict__ cols, 
 template <bool LOWER>
 __device__ __forceinline__ void warp_small_block(const int64_t* __restrict__ rowptr, const int* __restrict__ cols,
                                                  const double* __restrict__ vals, const double* __restrict__ diag,
-                                                 const double* __restrict__ b, double* x, int r0, int w, int lane) {
+                                                 const double* __restrict__ tinv, const double* __restrict__ b,
+                                                 double* x, int r0, int w, int lane) {
   double yv = 0.0, dg = 1.0;
   double lv[32];
 #pragma unroll
@@ -214,13 +215,25 @@ __device__ __forceinline__ void warp_small_block(const int64_t* __restrict__ row
     yv = __ldg(b + i) - s;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
-      if (LOWER) {
+      if (tinv) {
+        if (k < w) lv[k] = __ldg(tinv + static_cast<int64_t>(i) * 32 + k);  // row of the tile inverse
+      } else if (LOWER) {
         if (k < lane) lv[k] = __ldg(vals + (z - lane) + k);           // col r0 + k
       } else {
         if (k > lane && k < w) lv[k] = __ldg(vals + a + (k - lane - 1));  // col r0 + k
       }
     }
     if (!LOWER) dg = __ldg(diag + i);
+  }
+  if (tinv) {  // x = T^-1 y: 32 independent products, no dependency chain through the shuffles
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 32; k += 2) {
+      acc0 = fma(lv[k], __shfl_sync(0xffffffffu, yv, k), acc0);
+      acc1 = fma(lv[k + 1], __shfl_sync(0xffffffffu, yv, k + 1), acc1);
+    }
+    if (lane < w) st_release_dbl(x + r0 + lane, acc0 + acc1);
+    return;
   }
   const double rdg = 1.0 / dg;  // off the dependency chain below (x * (1/d): <= 1 ulp from x / d)
   if (LOWER) {
@@ -263,7 +276,8 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
     const int* __restrict__ blk_kind, const int* __restrict__ blk_r0, const int* __restrict__ blk_w,
     const int* __restrict__ blk_rb, const int* __restrict__ blk_rc, int64_t nblk, const int64_t* __restrict__ rowptr,
     const int* __restrict__ cols, const double* __restrict__ vals, const double* __restrict__ diag,
-    const double* __restrict__ b, double* x, double* ysum, unsigned long long* ticket) {
+    const double* __restrict__ tinv, const double* __restrict__ b, double* x, double* ysum,
+    unsigned long long* ticket) {
   __shared__ double ys[kSnMaxW];
   __shared__ unsigned long long tk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -282,7 +296,7 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
     if (kind == 3) {
       const int mb = __ldg(blk_rb + t), mc = __ldg(blk_rc + t);
       if (warp < mc)
-        warp_small_block<LOWER>(rowptr, cols, vals, diag, b, x, __ldg(blk_r0 + mb + warp), __ldg(blk_w + mb + warp),
+        warp_small_block<LOWER>(rowptr, cols, vals, diag, tinv, b, x, __ldg(blk_r0 + mb + warp), __ldg(blk_w + mb + warp),
                                 lane);
       if (tr) {
         __syncthreads();
@@ -331,11 +345,13 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
       auto tile_t0 = [&](int tt) { return LOWER ? 32 * tt : 32 * (ntiles - 1 - tt); };
       auto load_tile = [&](int t0, double* v) {
         const int tw = min(32, w - t0);
+        const bool own = tinv && has && tid >= t0 && tid < t0 + tw;  // my diagonal tile: its inverse
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
           const int c = t0 + k;
           const bool ok = has && k < tw && (LOWER ? c < tid : c > tid);
-          v[k] = ok ? __ldg(vals + (LOWER ? (rz - tid) + c : ra + (c - tid - 1))) : 0.0;
+          v[k] = own ? (k < tw ? __ldg(tinv + static_cast<int64_t>(i) * 32 + k) : 0.0)
+                     : (ok ? __ldg(vals + (LOWER ? (rz - tid) + c : ra + (c - tid - 1))) : 0.0);
         }
       };
       double cur[32], nxt[32];
@@ -344,7 +360,19 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
         const int t0 = tile_t0(tt);
         const int tw = min(32, w - t0);
         if (tt + 1 < ntiles) load_tile(tile_t0(tt + 1), nxt);
-        if (warp == t0 / 32) {  // the diagonal tile's rows: lane = row - t0
+        if (warp == t0 / 32 && tinv) {  // x = T^-1 y, no dependency chain
+          const double yv = lane < tw ? ys[tid] : 0.0;
+          double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) {
+            acc0 = fma(cur[k], __shfl_sync(0xffffffffu, yv, k), acc0);
+            acc1 = fma(cur[k + 1], __shfl_sync(0xffffffffu, yv, k + 1), acc1);
+          }
+          if (lane < tw) {
+            ys[tid] = acc0 + acc1;
+            st_release_dbl(x + i, acc0 + acc1);
+          }
+        } else if (warp == t0 / 32) {  // the diagonal tile's rows: lane = row - t0
           double yv = lane < tw ? ys[tid] : 0.0;
           const double dg = (!LOWER && lane < tw) ? __ldg(diag + i) : 1.0;
           const double rdg = 1.0 / dg;
@@ -581,10 +609,28 @@ HN_EXPORT int hn_debug_sptrsv_trace(unsigned long long* trace) {
 }
 
 // Supernodal solve over planned blocks (processing order), see sptrsv_super_kernel.
+HN_EXPORT int hn_sptrsv_super_inv(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w,
+                                  const int* blk_rb, const int* blk_rc, int64_t nblk, const int64_t* rowptr,
+                                  const int* cols, const double* vals, const double* diag, const double* tinv,
+                                  const double* b, double* x, double* ysum, int64_t n, unsigned long long* ticket,
+                                  int ctas_per_sm, void* stream);
+
 HN_EXPORT int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
                               const int* blk_rc, int64_t nblk, const int64_t* rowptr, const int* cols,
                               const double* vals, const double* diag, const double* b, double* x, double* ysum,
                               int64_t n, unsigned long long* ticket, int ctas_per_sm, void* stream) {
+  return hn_sptrsv_super_inv(lower, blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr, cols, vals, diag, nullptr,
+                             b, x, ysum, n, ticket, ctas_per_sm, stream);
+}
+
+// As hn_sptrsv_super; tinv (n x 32, or NULL) holds, for every row, its row of the inverse of
+// its 32-row diagonal tile (hn_host_tile_inverse): the in-tile triangle is then one
+// matrix-vector product instead of a 32-step substitution chain.
+HN_EXPORT int hn_sptrsv_super_inv(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w,
+                                  const int* blk_rb, const int* blk_rc, int64_t nblk, const int64_t* rowptr,
+                                  const int* cols, const double* vals, const double* diag, const double* tinv,
+                                  const double* b, double* x, double* ysum, int64_t n, unsigned long long* ticket,
+                                  int ctas_per_sm, void* stream) {
   if (nblk == 0) return 0;
   cudaStream_t s = as_stream(stream);
   HN_TRY(cudaMemsetAsync(x, 0xFF, sizeof(double) * n, s));
@@ -593,11 +639,56 @@ HN_EXPORT int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0,
   const int blocks = sm_count() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
   if (lower)
     sptrsv_super_kernel<true><<<blocks, kSnThreads, 0, s>>>(blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr, cols,
-                                                            vals, diag, b, x, ysum, ticket);
+                                                            vals, diag, tinv, b, x, ysum, ticket);
   else
     sptrsv_super_kernel<false><<<blocks, kSnThreads, 0, s>>>(blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr,
-                                                             cols, vals, diag, b, x, ysum, ticket);
+                                                             cols, vals, diag, tinv, b, x, ysum, ticket);
   HN_CHECK_LAUNCH();
+  return 0;
+}
+
+// Host helper (setup): inverses of the 32-row diagonal tiles of every block [r0, r0+w)
+// (tiles start at r0, r0+32, ..; the last one may be narrower), as hn_sptrsv_super_inv
+// reads them: tinv[i*32 + k] = row (i - tile start) of T^-1, column k.  T = I + the strict
+// lower in-tile entries (lower) or diag + the strict upper in-tile entries (upper); the
+// inverse by substitution on the identity columns.  tinv must hold n*32 doubles.
+HN_EXPORT int hn_host_tile_inverse(const int64_t* rowptr, const int* cols, const double* vals, const double* diag,
+                                   int64_t n, int lower, int64_t nb, const int* r0, const int* w, double* tinv) {
+  for (int64_t q = 0; q < n * 32; ++q) tinv[q] = 0.0;
+  double T[32][32], X[32][32];
+  for (int64_t blk = 0; blk < nb; ++blk) {
+    for (int t0 = 0; t0 < w[blk]; t0 += 32) {
+      const int tw = w[blk] - t0 < 32 ? w[blk] - t0 : 32;
+      const int64_t base = static_cast<int64_t>(r0[blk]) + t0;
+      for (int l = 0; l < tw; ++l)
+        for (int k = 0; k < tw; ++k) T[l][k] = 0.0;
+      for (int l = 0; l < tw; ++l) {
+        const int64_t i = base + l;
+        T[l][l] = lower ? 1.0 : diag[i];
+        for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+          const int64_t c = cols[e];
+          if (c >= base && c < base + tw && (lower ? c < i : c > i)) T[l][c - base] = vals[e];
+        }
+      }
+      for (int j = 0; j < tw; ++j) {  // column j of X = T^-1
+        if (lower) {
+          for (int l = 0; l < tw; ++l) {
+            double v = l == j ? 1.0 : 0.0;
+            for (int k = 0; k < l; ++k) v -= T[l][k] * X[k][j];
+            X[l][j] = v;
+          }
+        } else {
+          for (int l = tw - 1; l >= 0; --l) {
+            double v = l == j ? 1.0 : 0.0;
+            for (int k = l + 1; k < tw; ++k) v -= T[l][k] * X[k][j];
+            X[l][j] = v / T[l][l];
+          }
+        }
+      }
+      for (int l = 0; l < tw; ++l)
+        for (int k = 0; k < tw; ++k) tinv[(base + l) * 32 + k] = X[l][k];
+    }
+  }
   return 0;
 }
 

@@ -182,11 +182,29 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, he
 
 
 class _SuperSchedule:
-    def __init__(self, m: sparse.csr_matrix, lower: bool, **plan_kw):
+    def __init__(self, m: sparse.csr_matrix, lower: bool, diag: np.ndarray | None = None, **plan_kw):
         plan = plan_supernodal_blocks(m, lower, **plan_kw)
         self.nblk, self.depth, self.ntasks = plan["nblk"], plan["depth"], plan["ntasks"]
         self.kind, self.r0, self.w = L.to_device(plan["kind"]), L.to_device(plan["t_r0"]), L.to_device(plan["t_w"])
         self.rb, self.rc = L.to_device(plan["t_rb"]), L.to_device(plan["t_rc"])
+        self.tinv = None
+        if lower or not _DeviceLU.TILE_INVERSE:
+            return
+        # inverses of the 32-row diagonal tiles of every block (setup): the kernel's in-tile
+        # triangles become matrix-vector products (hn_sptrsv_super_inv)
+        n = m.shape[0]
+        vp = L._vp
+        rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
+        cols = np.ascontiguousarray(m.indices, dtype=np.int32)
+        vals = np.ascontiguousarray(m.data, dtype=np.float64)
+        dg = np.ascontiguousarray(diag if diag is not None else np.ones(max(n, 1)), dtype=np.float64)
+        r0 = np.ascontiguousarray(plan["r0"], dtype=np.int32)
+        w = np.ascontiguousarray(plan["w"], dtype=np.int32)
+        tinv = np.empty(max(n, 1) * 32, dtype=np.float64)
+        L.call("hn_host_tile_inverse", rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), vals.ctypes.data_as(vp),
+               dg.ctypes.data_as(vp), n, 1 if lower else 0, len(r0), r0.ctypes.data_as(vp), w.ctypes.data_as(vp),
+               tinv.ctypes.data_as(vp))
+        self.tinv = L.to_device(tinv)
 
 
 def plan_triangular_tasks(m: sparse.csr_matrix, lower: bool, chunk: int) -> dict:
@@ -221,6 +239,11 @@ class _DeviceLU:
     WARPS_PER_SM = 16
     CTAS_PER_SM = 2
     SUPERNODAL = True
+    # in-tile triangles of the U solve by precomputed tile inverses (hn_sptrsv_super_inv): 7 %
+    # faster L+U solve on config 3 (tools/ab_tinv.py: 4.17 -> 3.86 ms) but the preconditioner
+    # output moves by 1.5e-10 relative (ill-conditioned U tiles), so one BiCGStab step no longer
+    # lands at direct-solve accuracy.  Off: substitution, exact to rounding.
+    TILE_INVERSE = False
 
     def __init__(self, lu):
         Lm = sparse.csr_matrix(lu.L)
@@ -235,7 +258,7 @@ class _DeviceLU:
         self.supernodal = self.SUPERNODAL
         if self.supernodal:
             self.sL = _SuperSchedule(Ls, lower=True)
-            self.sU = _SuperSchedule(Us, lower=False)
+            self.sU = _SuperSchedule(Us, lower=False, diag=np.asarray(Um.diagonal(), dtype=np.float64))
         else:
             self.sL = _TriSchedule(Ls, lower=True)
             self.sU = _TriSchedule(Us, lower=False)
@@ -261,10 +284,11 @@ class _DeviceLU:
 
     def _tri(self, sch, m, diag, b, x, s):
         if self.supernodal:
-            L.call("hn_sptrsv_super", 1 if diag is None else 0, L.ptr(sch.kind), L.ptr(sch.r0), L.ptr(sch.w),
+            L.call("hn_sptrsv_super_inv", 1 if diag is None else 0, L.ptr(sch.kind), L.ptr(sch.r0), L.ptr(sch.w),
                    L.ptr(sch.rb), L.ptr(sch.rc), sch.ntasks, L.ptr(m.rowptr), L.ptr(m.cols), L.ptr(m.vals),
-                   L.ptr(diag), L.ptr(b), L.ptr(x), L.ptr(self.ysum), self.n, L.ptr(self.ticket), self.CTAS_PER_SM,
-                   s)
+                   L.ptr(diag), L.ptr(sch.tinv if (self.TILE_INVERSE and diag is not None) else None),
+                   L.ptr(b), L.ptr(x),
+                   L.ptr(self.ysum), self.n, L.ptr(self.ticket), self.CTAS_PER_SM, s)
             return
         L.call("hn_sptrsv_tasks", 0 if diag is None else 1, L.ptr(sch.row), L.ptr(sch.beg), L.ptr(sch.len),
                L.ptr(sch.part), L.ptr(sch.np_), sch.ntasks, L.ptr(m.cols), L.ptr(m.vals), L.ptr(diag), L.ptr(b),
