@@ -357,3 +357,32 @@ class TestRun:
         npt.assert_array_equal(a.state.velocity[ns.boundary_mask], 0.0)
         mask = ns.role == 1
         npt.assert_array_equal(a.state.temperature[mask], ns.bc_value[mask])
+
+
+def test_device_lu_solve_matches_superlu_both_tile_modes():
+    """The GPU preconditioner (SuperLU factors, supernodal sync-free solves) against SuperLU's own
+    solve: substitution (default) to rounding; with the optional diagonal-tile inverses for U
+    (hn_sptrsv_super_inv) to the drift DESIGN.md states."""
+    from paper_2303_01760_b200 import _lib as L
+    from paper_2303_01760_b200.solver import _DeviceLU
+    ns = nodesets.hybrid_hole_2d(60, seed=2)
+    ops = hn.build_operators(ns, {"wall:x-"}, PoissonSolveSettings())
+    lu = ops.poisson_precond
+    old = _DeviceLU.TILE_INVERSE
+    try:
+        _DeviceLU.TILE_INVERSE = True
+        dlu = _DeviceLU(lu)
+        b = np.random.default_rng(3).normal(size=dlu.n)
+        ref = lu.solve(b)
+        t = L.torch()
+        bd, xd = L.to_device(b), L.empty(dlu.n, t.float64)
+        got = {}
+        for mode in (False, True):
+            _DeviceLU.TILE_INVERSE = mode
+            dlu.solve(bd, xd)
+            got[mode] = xd.cpu().numpy().copy()
+    finally:
+        _DeviceLU.TILE_INVERSE = old
+    scale = np.abs(ref).max()
+    assert np.abs(got[False] - ref).max() / scale <= 1e-12
+    assert np.abs(got[True] - ref).max() / scale <= 1e-8
