@@ -365,9 +365,10 @@ def test_device_lu_solve_matches_superlu_both_tile_modes():
     (hn_sptrsv_super_inv) to the drift DESIGN.md states."""
     from paper_2303_01760_b200 import _lib as L
     from paper_2303_01760_b200.solver import _DeviceLU
+    from scipy.sparse import linalg as spla
     ns = nodesets.hybrid_hole_2d(60, seed=2)
     ops = hn.build_operators(ns, {"wall:x-"}, PoissonSolveSettings())
-    lu = ops.poisson_precond
+    lu = spla.splu(ops.poisson_matrix.tocsc())  # the factorisation build_operators makes
     old = _DeviceLU.TILE_INVERSE
     try:
         _DeviceLU.TILE_INVERSE = True
