@@ -453,8 +453,10 @@ def _interior_native(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
     t = L.torch()
     g = dn.grid(dn.fine_cell) if dn.fine_cell is not None else dn.grid(dn.cell, exact=True)
     kind = np.asarray(nodeset.kind)
-    rbf_rows_h = np.flatnonzero(kind != KIND_BOUNDARY) if not np.any(kind == KIND_REGULAR) else None
-    k_rbf_host = len(rbf_rows_h) if rbf_rows_h is not None else -1
+    # no regular node: the RBF rows are the non-boundary nodes, ascending -- only their count
+    # and the chunk cut ids are needed, from the (few) boundary ids
+    bnd = np.flatnonzero(kind == KIND_BOUNDARY) if not np.any(kind == KIND_REGULAR) else None
+    k_rbf_host = n - len(bnd) if bnd is not None else -1
     has_lat = dn.lattice_grid is not None
     nmon = 2 * dim + 1
     cap_mon = n if k_rbf_host < 0 else 1  # no regular node -> no MON rows
@@ -480,9 +482,10 @@ def _interior_native(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
     # node-ordered RBF chunks: each chunk's table slice is copied back while the next computes
     chunks = NATIVE_CHUNKS if k_rbf_host != 0 else 1
     cut = None
-    if rbf_rows_h is not None and chunks > 1:
+    if bnd is not None and chunks > 1 and k_rbf_host > 0:
         kb = (k_rbf_host * np.arange(1, chunks)) // chunks
-        cut = L.host_i64(rbf_rows_h[kb])
+        # id of the kb-th non-boundary node = kb + #{boundary ids b_j with b_j - j <= kb}
+        cut = L.host_i64(kb + np.searchsorted(bnd - np.arange(len(bnd)), kb, side="right"))
     L.call("hn_weights_pipeline", L.ptr(dn.pos), dim, n, L.ptr(dn.kind), L.ptr(dn.lattice_idx if has_lat else None),
            L.ptr(dn.lattice_grid if has_lat else None), L.host_ints(dn.grid_dims if has_lat else [1, 1, 1]),
            L.host_dbls(dn.lo), g.cell, L.host_ints(g.dims), L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos),
