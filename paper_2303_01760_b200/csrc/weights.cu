@@ -288,16 +288,19 @@ __device__ __forceinline__ bool mon_static(const double* __restrict__ pos, const
   return true;
 }
 
-// Fast kernel: canonical lattice stencils (mon_static); any other row is flagged
-// (flag[k] = 1) for mon_general_kernel, which runs the general partial-pivoting path.
-// Two kernels, so the general path's register budget does not set the fast path's
-// occupancy (a called device function would).
 template <int D, int NOPS>
-__global__ void __launch_bounds__(128) mon_weights_kernel(const double* __restrict__ pos,
+__device__ __noinline__ void mon_general_call(const double* __restrict__ pos, const int* __restrict__ stencils,
+                                              int64_t K, int64_t k, const OpSpec& ops, int* __restrict__ out_idx,
+                                              double* __restrict__ out_w, int* __restrict__ info);
+
+// Fast kernel: canonical lattice stencils (mon_static); any other row runs the general
+// partial-pivoting path in a separately compiled (noinline) function, so its register budget
+// does not set the fast path's occupancy, and no second launch or flag array is needed.
+template <int D, int NOPS>
+__global__ void __launch_bounds__(128, D == 2 ? 7 : 5) mon_weights_kernel(const double* __restrict__ pos,
                                                           const int* __restrict__ stencils, int64_t K,
                                                           OpSpec ops, int* __restrict__ out_idx,
-                                                          double* __restrict__ out_w, int* __restrict__ info,
-                                                          int* __restrict__ flag) {
+                                                          double* __restrict__ out_w, int* __restrict__ info) {
   constexpr int N = 2 * D + 1;
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= K) return;
@@ -307,8 +310,11 @@ __global__ void __launch_bounds__(128) mon_weights_kernel(const double* __restri
   double c[D];
   load_point<D>(pos, sid[0], c);
   const bool done = mon_static<D, NOPS>(pos, sid, c, K, k, ops, out_idx, out_w);
-  flag[k] = done ? 0 : 1;
-  if (done && info) info[k] = 0;
+  if (done) {
+    if (info) info[k] = 0;
+  } else {
+    mon_general_call<D, NOPS>(pos, stencils, K, k, ops, out_idx, out_w, info);
+  }
 }
 
 template <int D, int NOPS>
@@ -317,13 +323,9 @@ __device__ __forceinline__ void mon_general(const double* __restrict__ pos, cons
                                             double* __restrict__ out_w, int* __restrict__ info);
 
 template <int D, int NOPS>
-__global__ void __launch_bounds__(128) mon_general_kernel(const double* __restrict__ pos,
-                                                          const int* __restrict__ stencils, int64_t K,
-                                                          OpSpec ops, int* __restrict__ out_idx,
-                                                          double* __restrict__ out_w, int* __restrict__ info,
-                                                          const int* __restrict__ flag) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= K || !flag[k]) return;
+__device__ __noinline__ void mon_general_call(const double* __restrict__ pos, const int* __restrict__ stencils,
+                                              int64_t K, int64_t k, const OpSpec& ops, int* __restrict__ out_idx,
+                                              double* __restrict__ out_w, int* __restrict__ info) {
   mon_general<D, NOPS>(pos, stencils, K, k, ops, out_idx, out_w, info);
 }
 
@@ -1385,12 +1387,10 @@ HN_EXPORT int hn_weights_mon(const double* pos, int d, const int* stencils, int6
   cudaStream_t s = as_stream(stream);
   const int th = 128;
   const int64_t bl = ceil_div(K, th);
-  int* flag = nullptr;
-  HN_TRY(stream_alloc(reinterpret_cast<void**>(&flag), sizeof(int) * K, s));
+
 #define HN_MON(DD, NO)                                                                                  \
   do {                                                                                                  \
-    mon_weights_kernel<DD, NO><<<bl, th, 0, s>>>(pos, stencils, K, ops, out_idx, out_w, info, flag);    \
-    mon_general_kernel<DD, NO><<<bl, th, 0, s>>>(pos, stencils, K, ops, out_idx, out_w, info, flag);    \
+    mon_weights_kernel<DD, NO><<<bl, th, 0, s>>>(pos, stencils, K, ops, out_idx, out_w, info);          \
   } while (0)
   if (d == 2) {
     switch (nops) { case 1: HN_MON(2, 1); break; case 2: HN_MON(2, 2); break; case 3: HN_MON(2, 3); break; default: HN_MON(2, 4); }
@@ -1398,7 +1398,6 @@ HN_EXPORT int hn_weights_mon(const double* pos, int d, const int* stencils, int6
     switch (nops) { case 1: HN_MON(3, 1); break; case 2: HN_MON(3, 2); break; case 3: HN_MON(3, 3); break; default: HN_MON(3, 4); }
   }
 #undef HN_MON
-  cudaFreeAsync(flag, s);
   HN_CHECK_LAUNCH();
   return 0;
 }
