@@ -188,7 +188,7 @@ class _SuperSchedule:
         self.kind, self.r0, self.w = L.to_device(plan["kind"]), L.to_device(plan["t_r0"]), L.to_device(plan["t_w"])
         self.rb, self.rc = L.to_device(plan["t_rb"]), L.to_device(plan["t_rc"])
         self.tinv = None
-        if lower or not _DeviceLU.TILE_INVERSE:
+        if not (_DeviceLU.TILE_INVERSE_L if lower else _DeviceLU.TILE_INVERSE):
             return
         # inverses of the 32-row diagonal tiles of every block (setup): the kernel's in-tile
         # triangles become matrix-vector products (hn_sptrsv_super_inv)
@@ -244,6 +244,7 @@ class _DeviceLU:
     # output moves by 1.5e-10 relative (ill-conditioned U tiles), so one BiCGStab step no longer
     # lands at direct-solve accuracy.  Off: substitution, exact to rounding.
     TILE_INVERSE = False
+    TILE_INVERSE_L = False  # the same for the unit-lower L solve
 
     def __init__(self, lu):
         Lm = sparse.csr_matrix(lu.L)
@@ -286,7 +287,8 @@ class _DeviceLU:
         if self.supernodal:
             L.call("hn_sptrsv_super_inv", 1 if diag is None else 0, L.ptr(sch.kind), L.ptr(sch.r0), L.ptr(sch.w),
                    L.ptr(sch.rb), L.ptr(sch.rc), sch.ntasks, L.ptr(m.rowptr), L.ptr(m.cols), L.ptr(m.vals),
-                   L.ptr(diag), L.ptr(sch.tinv if (self.TILE_INVERSE and diag is not None) else None),
+                   L.ptr(diag), L.ptr(sch.tinv if (self.TILE_INVERSE_L if diag is None else self.TILE_INVERSE)
+                                      else None),
                    L.ptr(b), L.ptr(x),
                    L.ptr(self.ysum), self.n, L.ptr(self.ticket), self.CTAS_PER_SM, s)
             return
