@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
     unsigned long long* ticket) {
   __shared__ double ys[kSnMaxW];
   __shared__ unsigned long long tk;
+  extern __shared__ double sn_nbuf[];  // [32][kSnThreads]: the next tile's entries (cp.async)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   while (true) {
     if (tid == 0) tk = atomicAdd(ticket, 1ull);
@@ -354,12 +355,33 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
                      : (ok ? __ldg(vals + (LOWER ? (rz - tid) + c : ra + (c - tid - 1))) : 0.0);
         }
       };
-      double cur[32], nxt[32];
+      // the next tile goes to shared memory by cp.async (thread tid only touches column tid,
+      // so no barrier guards it): no registers held for it across the tile
+      auto prefetch_tile = [&](int t0) {
+        const int tw = min(32, w - t0);
+        const bool own = tinv && has && tid >= t0 && tid < t0 + tw;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int c = t0 + k;
+          const bool ok = has && k < tw && (LOWER ? c < tid : c > tid);
+          double* dst = sn_nbuf + k * kSnThreads + tid;
+          const double* src = own ? (k < tw ? tinv + static_cast<int64_t>(i) * 32 + k : nullptr)
+                                  : (ok ? vals + (LOWER ? (rz - tid) + c : ra + (c - tid - 1)) : nullptr);
+          if (src) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(
+                             __cvta_generic_to_shared(dst))), "l"(src) : "memory");
+          } else {
+            *dst = 0.0;
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      double cur[32];
       load_tile(tile_t0(0), cur);
       for (int tt = 0; tt < ntiles; ++tt) {
         const int t0 = tile_t0(tt);
         const int tw = min(32, w - t0);
-        if (tt + 1 < ntiles) load_tile(tile_t0(tt + 1), nxt);
+        if (tt + 1 < ntiles) prefetch_tile(tile_t0(tt + 1));
         if (warp == t0 / 32 && tinv) {  // x = T^-1 y, no dependency chain
           const double yv = lane < tw ? ys[tid] : 0.0;
           double acc0 = 0.0, acc1 = 0.0;
@@ -404,8 +426,11 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
           ys[tid] -= acc;
         }
         __syncthreads();
+        if (tt + 1 < ntiles) {
+          asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
-        for (int k = 0; k < 32; ++k) cur[k] = nxt[k];
+          for (int k = 0; k < 32; ++k) cur[k] = sn_nbuf[k * kSnThreads + tid];
+        }
       }
       if (tr && tid == 0) tr[4 * t + 2] = gtime();
       continue;
@@ -637,11 +662,18 @@ HN_EXPORT int hn_sptrsv_super_inv(int lower, const int* blk_kind, const int* blk
   HN_TRY(cudaMemsetAsync(ysum, 0xFF, sizeof(double) * n, s));
   HN_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s));
   const int blocks = sm_count() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
+  constexpr int kNbuf = 32 * kSnThreads * static_cast<int>(sizeof(double));  // next-tile buffer
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sptrsv_super_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNbuf);
+    cudaFuncSetAttribute(sptrsv_super_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNbuf);
+    attr = true;
+  }
   if (lower)
-    sptrsv_super_kernel<true><<<blocks, kSnThreads, 0, s>>>(blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr, cols,
+    sptrsv_super_kernel<true><<<blocks, kSnThreads, kNbuf, s>>>(blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr, cols,
                                                             vals, diag, tinv, b, x, ysum, ticket);
   else
-    sptrsv_super_kernel<false><<<blocks, kSnThreads, 0, s>>>(blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr,
+    sptrsv_super_kernel<false><<<blocks, kSnThreads, kNbuf, s>>>(blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr,
                                                              cols, vals, diag, tinv, b, x, ysum, ticket);
   HN_CHECK_LAUNCH();
   return 0;
