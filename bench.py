@@ -1,15 +1,20 @@
 """Benchmark for the hybrid RBF-FD hot path on B200 (contract: see DESIGN.md §6).
 
-Default workload (BASELINE configs[1], the metric's first half): config 1, the 2D
-scattered set N = 99,856 -- one step = cell-list kNN stencils + batched RBF-FD
-PHS r^3 + degree-2 weight solves (18x18 fp64, Laplacian/d/dx/d/dy) for all 98,596
-interior rows, written into HBM ELL slabs.  `value` = stencil weights/s over the whole
-job; `e2e` = the same through the public API compute_weights() with host NodeSet in and
-host WeightTable out; `roofline` = the dominant kernel (weight solve) vs the live DFMA
-peak; `cpu_baseline` = the reference's algorithm (oracle port, 1 thread, the reference's
-protocol) on the same host.  --config 3 measures node-updates/s of explicit steps.
+Default workload: config 4, the largest single-GPU configuration of BASELINE.json (3D
+hybrid sphere set, N = 1,054,026, 22 % scattered) -- one step = cell list + classify + MON
+7-point stencils and solves + kNN n = 20 + RBF-FD PHS r^3 + degree-2 30x30 fp64 solves
+(Laplacian, d/dx, d/dy, d/dz) for every interior row, written into HBM ELL slabs.  `value`
+= stencil weights/s over the whole job; `e2e` = the same through the public API
+compute_weights() with host NodeSet in and host WeightTable out; `roofline` = the dominant
+kernel (the RBF-FD solve) vs the live DFMA peak; `cpu_baseline` = the reference's algorithm
+(oracle port, 1 thread, the reference's protocol) on the same host.  The metric's second
+half rides on the same line as `time_steps`: config 3 (the 2D hybrid set at full N = 243,955,
+explicit Boussinesq steps with the reference's LU-preconditioned BiCGStab pressure) in
+node-updates/s, its full-step and explicit-part HBM fractions, e2e with host fields in and
+out every step, and the oracle step on the same host (1 thread).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 0|1|2|3|4]
+                  [--no-steps] [--no-cpu-baseline]
 """
 
 from __future__ import annotations
@@ -58,8 +63,9 @@ def parse():
                     help="timed steps (default: 200 for weight configs, 50 for config 3)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=4, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-steps", action="store_true", help="weights line without the config-3 steps object")
     ap.add_argument("--phase", default=None, choices=["weights", "steps"],
                     help="config 4 has both: weight computation (default) or the Boussinesq steps")
     return ap.parse_args()
@@ -357,9 +363,7 @@ def run_weights_bench(args, rank, world):
         "metric": "stencil weights/sec", "value": value, "unit": "stencils/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded node sets, SURVEY Appendix B)",
-        "config": {"workload": config_name(cfg, ns), "N": len(ns), "interior_rows": n_int,
-                   "stencils": stencil_mix(dev), "ops": len(ops), "l2": "flushed between steps (256 MiB write + 256 MiB read: L2 left clean)",
-                   "parallelism": f"weak x{world} (independent node set per rank)"},
+        "config": weights_config(cfg, ns, world, pipe.k_mon, pipe.k_rbf, len(ops)),
         "e2e": {"value": world * n_int / e2e_s, "unit": "stencils/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "api": "paper_2303_01760_b200.compute_weights(NodeSet, ops)",
                 "samples_ms": [round(1e3 * x, 3) for x in e2e_t]},
@@ -416,6 +420,19 @@ def config_name(cfg, ns):
 
 def stencil_mix(dev):
     return {f"w{b.width}": int(b.K) for b in dev.bins if b.width}
+
+
+def weights_config(cfg, ns, world, k_mon, k_rbf, ops):
+    """The `config` object of a weights line -- identical for both arms (same_config)."""
+    dim = ns.dim
+    mix = {}
+    if k_mon:
+        mix[f"w{2 * dim + 1}"] = int(k_mon)
+    if k_rbf:
+        mix[f"w{20 if dim == 3 else 12}"] = int(k_rbf)
+    return {"workload": config_name(cfg, ns), "N": len(ns), "interior_rows": int(k_mon + k_rbf), "stencils": mix,
+            "ops": int(ops), "l2": "flushed between steps (256 MiB write + 256 MiB read: L2 left clean)",
+            "parallelism": f"weak x{world} (independent node set per rank)"}
 
 
 def cpu_baseline_weights(ns, ops, rbf_n):
@@ -490,18 +507,29 @@ def _explicit_roofline(L, stepper, ns, steps, flush):
             "frac_of_8tbs_nominal": nbytes / (ms * 1e-3) / 8e12}
 
 
-def run_steps_bench(args, rank, world):
+def pressure_bytes(ops) -> int:
+    """Algorithmic HBM bytes of one warm pressure solve (one BiCGStab half-step, SURVEY §8(a)
+    A17): 2 A-matvecs (12 B/nnz + int64 row pointer + x gather/y write), one preconditioner
+    application (L and U: 12 B/nnz, the U diagonal, the two permutations in and out) and the
+    BiCGStab vector algebra (~12 vector passes of 8 B/element)."""
+    n1 = ops.n + 1
+    a_nnz = int(ops._d_poisson.nnz)
+    lu = ops._d_lu
+    return 2 * (12 * a_nnz + 24 * n1) + 12 * (lu.L.nnz + lu.U.nnz) + 8 * n1 + 4 * 12 * n1 + 12 * 8 * n1
+
+
+def steps_measure(args, rank, world, cfg=3, flush=None, with_cpu=True):
     """Config 3 (2D, full N, reference pressure treatment) -> node-updates/s of full steps.
     Config 4 (3D): full steps (with the reference's SuperLU pressure) at a reduced-N twin of
     the same generator -- SuperLU at N = 1e6 is infeasible -- plus the explicit
-    part at the full N = 1.02e6."""
+    part at the full N = 1.05e6."""
     import paper_2303_01760_b200 as hn
     from paper_2303_01760_b200 import _lib as L, nodesets
     t = L.torch()
     counter = LaunchCounter(L)
-    flush = L2Flush(L)
+    flush = flush or L2Flush(L)
     off = shard_seed(0, rank) if world > 1 else 0
-    if args.config == 3:
+    if cfg == 3:
         ns, Ra = build_nodeset(3, off), 1e6
     else:
         ns, Ra = nodesets.hybrid_sphere_3d(24, seed=4 + off, refine=2.8), 1e5
@@ -509,7 +537,10 @@ def run_steps_bench(args, rank, world):
     # explicit scheme is unstable on this set -- |v| grows x1.2 per step and the run blows up
     # at step 42, in the CPU oracle of the reference algorithm exactly as on the GPU
     # (DESIGN.md §5); the explicit part at the full N below keeps n = 20.
-    stepper, ops, dt = _stepper(hn, ns, True, Ra, rbf_n=30 if args.config == 4 else None)
+    t_setup = time.perf_counter()
+    stepper, ops, dt = _stepper(hn, ns, True, Ra, rbf_n=30 if cfg == 4 else None)
+    t_setup = time.perf_counter() - t_setup
+    steps = args.steps_steps
     for _ in range(args.warmup):
         stepper.step()
     t.cuda.synchronize()
@@ -518,30 +549,97 @@ def run_steps_bench(args, rank, world):
     counter.enabled = True
     with ClockSampler() as clocks:
         e0.record()
-        for _ in range(args.steps):
+        for _ in range(steps):
             stepper.step()
         e1.record()
         t.cuda.synchronize()
     counter.enabled = False
-    stepper.check_finite(args.steps)
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
-    explicit = _explicit_roofline(L, stepper, ns, args.steps, flush)
-    line = {"metric": "node-updates/sec per step", "value": world * len(ns) / (ms * 1e-3), "unit": "node-updates/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": config_name(args.config, ns), "N": len(ns), "dt": dt, "Ra": Ra,
-                       "pressure": "LU-preconditioned BiCGStab (SuperLU factors in HBM, supernodal sync-free "
-                                   "trisolves)"},
-            "explicit": explicit,
-            "gpu_launches": counter.count // max(1, args.steps), "clocks": clocks.summary()}
-    if args.config == 4:
-        line["config"]["workload"] = line["config"]["workload"].replace("n=20 (30x30)", "n=30 (40x40)")
+    stepper.check_finite()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    explicit = _explicit_roofline(L, stepper, ns, steps, flush)
+    d, n = ns.dim, len(ns)
+    peak = load_peaks().get("hbm_gbs", 6526.8)
+    pb = pressure_bytes(ops)
+    full_bytes = explicit["bytes"] + pb
+
+    # ---- e2e: host fields in (pinned staging), one step, host fields out, every step ----
+    from paper_2303_01760_b200.operators import FieldState
+    host = stepper.state()
+    e2e_t = []
+    b0 = dict(L.TRAFFIC)
+    for k in range(3 + min(steps, 10)):
+        t.cuda.synchronize()
+        t0 = time.perf_counter()
+        stepper.load_state(host)
+        stepper.step()
+        host = stepper.state()
+        if k >= 3:
+            e2e_t.append(time.perf_counter() - t0)
+    stepper.check_finite()
+    e2e_ms = max_over_ranks(1e3 * float(np.mean(e2e_t)), world)
+    h2d = (L.TRAFFIC["h2d"] - b0["h2d"]) // (3 + min(steps, 10))
+    d2h = (d + 2) * 8 * n
+    out = {"metric": "node-updates/sec per step", "value": world * n / (ms * 1e-3), "unit": "node-updates/s",
+           "ms_per_step": ms, "steps": steps, "warmup": args.warmup,
+           "config": {"workload": config_name(cfg, ns), "N": n, "dt": dt, "Ra": Ra,
+                      "pressure": "LU-preconditioned BiCGStab (SuperLU factors in HBM, supernodal sync-free "
+                                  "trisolves)", "setup_s": round(t_setup, 2),
+                      "l2": "not flushed between full steps (each step moves > 1 GB); explicit part: flushed"},
+           "hbm_full_step": {"bytes": full_bytes, "explicit_bytes": explicit["bytes"], "pressure_bytes": pb,
+                             "bytes_formula": "explicit S(28+24d)+40N(d+1) + pressure (bench.pressure_bytes)",
+                             "achieved_gbs": full_bytes / (ms * 1e-3) / 1e9, "peak_gbs": peak,
+                             "frac": full_bytes / (ms * 1e-3) / 1e9 / peak},
+           "explicit": explicit,
+           "e2e": {"value": world * n / (e2e_ms * 1e-3), "unit": "node-updates/s", "ms_per_step": e2e_ms,
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                   "api": "DeviceStepper.load_state(host FieldState) + step() + state() -> host, every step"},
+           "gpu_launches": counter.count // max(1, steps), "clocks": clocks.summary()}
+    if cfg == 4:
+        out["config"]["workload"] = out["config"]["workload"].replace("n=20 (30x30)", "n=30 (40x40)")
         big = build_nodeset(4, off)
         st_big, _, _ = _stepper(hn, big, False, Ra)
-        line["explicit_full_N"] = dict(_explicit_roofline(L, st_big, big, args.steps, flush), N=len(big))
-        line["config"]["note"] = ("full steps at a reduced-N twin (hybrid_sphere_3d(24)) with interior n=30 "
-                                  "(n=20 diverges at step 42 in the reference algorithm too); the explicit part "
-                                  "at the full N=%d with n=20" % len(big))
+        out["explicit_full_N"] = dict(_explicit_roofline(L, st_big, big, steps, flush), N=len(big))
+        out["config"]["note"] = ("full steps at a reduced-N twin (hybrid_sphere_3d(24)) with interior n=30 "
+                                 "(n=20 diverges at step 42 in the reference algorithm too); the explicit part "
+                                 "at the full N=%d with n=20" % len(big))
+    if with_cpu and rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_steps(ns, Ra, rbf_n=30 if cfg == 4 else None)
+    return out
+
+
+def cpu_baseline_steps(ns, Ra, rbf_n=None, budget_s=8.0):
+    """The reference's run-loop body (oracle port of solver.py:439-452: scipy csr_matvec +
+    bicgstab with the SuperLU preconditioner) on the same host, 1 thread; build_operators
+    (splu) is setup, reported separately.  Bounded sample: as many steps as fit in ~8 s."""
+    from oracle import hn_oracle as O
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        o = O.build_operators(ns, {"wall:x-"}, rbf_n=rbf_n)
+        setup = time.perf_counter() - t0
+        dt = O.dt_rule(float(np.min(ns.spacing)), Ra)
+        T = O.temperature_bc(o, (ns.positions[:, 0] - 0.5) + 1e-3 * np.random.default_rng(3).normal(size=len(ns)))
+        state, p = (np.zeros((len(ns), ns.dim)), T), None
+        state, p = O.step(o, state, Ra, 0.71, 0.0, dt, p_prev=p)  # cold first step: not timed
+        k, t_steps = 0, 0.0
+        while t_steps < budget_s and k < 200:
+            t0 = time.perf_counter()
+            state, p = O.step(o, state, Ra, 0.71, 0.0, dt, p_prev=p)
+            t_steps += time.perf_counter() - t0
+            k += 1
+    return {"value": len(ns) * k / t_steps, "unit": "node-updates/s", "cores": 1, "kind": "port",
+            "ms_per_step": 1e3 * t_steps / k,
+            "sample": f"oracle run-loop body x{k} warm steps ({t_steps:.1f} s) on the same node set, after "
+                      f"build_operators (setup {setup:.1f} s, not timed), OPENBLAS_NUM_THREADS=1 (cli.py:7-10)",
+            "setup_s": round(setup, 2), "host_cpu": cpu_model()}
+
+
+def run_steps_bench(args, rank, world):
+    m = steps_measure(args, rank, world, cfg=args.config)
+    line = {"metric": m["metric"], "value": m["value"], "unit": m["unit"], "n_gpus": world,
+            "steps": m["steps"], "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic"}
+    line.update({k: v for k, v in m.items() if k not in line and k != "metric"})
     return line
 
 
@@ -629,7 +727,7 @@ def run_reference(args, rank, world):
     return {"impl": "reference", "metric": "stencil weights/sec", "value": v, "unit": "stencils/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": config_name(cfg, ns), "N": len(ns)},
+            "config": weights_config(cfg, ns, world, int((method == 0).sum()), int((method == 1).sum()), len(keys)),
             "cpu_baseline": {"value": v, "unit": "stencils/s", "cores": P, "kind": "port",
                              "sample": f"full workload per step, {args.steps} steps: numpy/scipy oracle port of the "
                                        f"reference (cKDTree + batched LAPACK dgesv) over {P} worker processes, "
@@ -641,9 +739,10 @@ def run_reference(args, rank, world):
 def main():
     args = parse()
     if args.steps is None:
-        args.steps = 50 if args.config == 3 else (3 if args.impl == "reference" else 200)
+        args.steps = 50 if args.config == 3 else (3 if args.impl == "reference" else 20)
     if args.phase is None:
         args.phase = "steps" if args.config == 3 else "weights"
+    args.steps_steps = args.steps if args.phase == "steps" else 50  # steps timed for the `steps` object
     rank, world = dist_init(args.gpus)
     if args.impl == "reference":
         line = run_reference(args, rank, world)
@@ -651,6 +750,9 @@ def main():
         line = run_steps_bench(args, rank, world)
     else:
         line = run_weights_bench(args, rank, world)
+        if args.config == 4 and not args.no_steps:
+            # the metric's second half (node-updates/s per step, % HBM) on BASELINE config 3
+            line["time_steps"] = steps_measure(args, rank, world, cfg=3)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -186,18 +186,33 @@ class DeviceNodes:
 _NODE_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
+def _node_key(nodeset):
+    """Identity of everything DeviceNodes snapshots (positions, kind, spacing, lattice map)
+    plus a strided fingerprint of the positions, so replaced arrays and most in-place edits
+    rebuild the device copy.  Node sets are treated as immutable inputs, as the reference's
+    per-call cKDTree implies; edit a copy (or a new NodeSet) to be sure."""
+    pos = nodeset.positions
+    lat = getattr(nodeset, "lattice", None)
+    arrays = (pos, getattr(nodeset, "kind", None), getattr(nodeset, "spacing", None),
+              getattr(nodeset, "lattice_idx", None), getattr(lat, "grid", None))
+    flat = np.asarray(pos).reshape(-1)
+    step = max(1, flat.size // 4096)
+    return (tuple(id(a) for a in arrays), tuple(getattr(a, "shape", None) for a in arrays),
+            flat[::step].tobytes())
+
+
 def device_nodes(nodeset) -> DeviceNodes:
-    """Cached DeviceNodes for a node set (rebuilt if its position array was replaced)."""
-    key_arr = nodeset.positions
+    """Cached DeviceNodes for a node set (rebuilt when _node_key changes)."""
+    key = _node_key(nodeset)
     try:
         ent = _NODE_CACHE.get(nodeset)
     except TypeError:
         ent = None
-    if ent is not None and ent[0] is key_arr and ent[1] == key_arr.shape:
+    if ent is not None and ent[0] == key:
         return ent[2]
     dn = DeviceNodes(nodeset)
     try:
-        _NODE_CACHE[nodeset] = (key_arr, key_arr.shape, dn)
+        _NODE_CACHE[nodeset] = (key, None, dn)
     except TypeError:
         pass
     return dn

@@ -663,12 +663,10 @@ HN_EXPORT int hn_sptrsv_super_inv(int lower, const int* blk_kind, const int* blk
   HN_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s));
   const int blocks = sm_count() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
   constexpr int kNbuf = 32 * kSnThreads * static_cast<int>(sizeof(double));  // next-tile buffer
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sptrsv_super_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNbuf);
-    cudaFuncSetAttribute(sptrsv_super_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNbuf);
-    attr = true;
-  }
+  // per-device function attribute: set on every call (cheap), so any device a process drives
+  // gets the opt-in
+  HN_TRY(cudaFuncSetAttribute(sptrsv_super_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNbuf));
+  HN_TRY(cudaFuncSetAttribute(sptrsv_super_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNbuf));
   if (lower)
     sptrsv_super_kernel<true><<<blocks, kSnThreads, kNbuf, s>>>(blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr, cols,
                                                             vals, diag, tinv, b, x, ysum, ticket);

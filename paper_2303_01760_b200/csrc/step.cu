@@ -400,13 +400,34 @@ __device__ __forceinline__ double csr_row_seq32_neu(const int* __restrict__ cols
 __global__ void neumann_kernel(const int64_t* __restrict__ rowptr, const int* __restrict__ cols,
                                const double* __restrict__ vals, const int* __restrict__ neu_idx,
                                const double* __restrict__ diag, const uint8_t* __restrict__ is_neu, int64_t nrows,
-                               double* __restrict__ T) {
+                               double* __restrict__ T, int* __restrict__ flags) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
   const int64_t e0 = __ldg(rowptr + r), e1 = __ldg(rowptr + r + 1);
   const double acc = e1 - e0 <= 32 ? csr_row_seq32_neu(cols, vals, T, is_neu, e0, static_cast<int>(e1 - e0))
                                    : csr_row_seq<true>(cols, vals, T, is_neu, e0, e1);
-  T[neu_idx[r]] = __ddiv_rn(-acc, diag[r]);
+  const double t = __ddiv_rn(-acc, diag[r]);
+  const int node = neu_idx[r];
+  T[node] = t;
+  if (flags && !isfinite(t)) {  // the reference probes T after its boundary conditions (solver.py:448-452)
+    atomicOr(flags, 1);
+    atomicMin(flags + 1, node);
+  }
+}
+
+// End of a step: latch the first step whose fields went non-finite (flags written by K10 and
+// the Neumann rows) with the lowest non-finite temperature node, as the reference's per-step
+// probe reports it (solver.py:448-452); then clear the per-step flags.
+// latch = [steps completed, first bad step (0: none), its node (INT_MAX: none in T)].
+__global__ void step_latch_kernel(int* __restrict__ flags, int* __restrict__ latch) {
+  const int s = latch[0] + 1;
+  latch[0] = s;
+  if (flags[0] && latch[1] == 0) {
+    latch[1] = s;
+    latch[2] = flags[1];
+  }
+  flags[0] = 0;
+  flags[1] = 0x7fffffff;
 }
 
 // ---- generic sequential CSR matvec (scipy csr_matvec order), thread per row ----
@@ -594,7 +615,7 @@ HN_EXPORT int hn_correct_temperature(int nbins, const int64_t* bin_K_host, const
 HN_EXPORT int hn_temperature_bc(const int* dir_idx, const double* dir_val, int64_t ndir, const int64_t* neu_rowptr,
                                 const int* neu_cols, const double* neu_vals, const int* neu_idx,
                                 const double* neu_diag, const uint8_t* is_neu, int64_t nneu, double* T,
-                                void* stream) {
+                                int* flags, void* stream) {
   cudaStream_t s = as_stream(stream);
   const int th = 256;
   if (ndir > 0) {
@@ -602,9 +623,16 @@ HN_EXPORT int hn_temperature_bc(const int* dir_idx, const double* dir_val, int64
     HN_CHECK_LAUNCH();
   }
   if (nneu > 0) {
-    neumann_kernel<<<ceil_div(nneu, th), th, 0, s>>>(neu_rowptr, neu_cols, neu_vals, neu_idx, neu_diag, is_neu, nneu, T);
+    neumann_kernel<<<ceil_div(nneu, th), th, 0, s>>>(neu_rowptr, neu_cols, neu_vals, neu_idx, neu_diag, is_neu, nneu, T,
+                                                     flags);
     HN_CHECK_LAUNCH();
   }
+  return 0;
+}
+
+HN_EXPORT int hn_step_latch(int* flags, int* latch, void* stream) {
+  step_latch_kernel<<<1, 1, 0, as_stream(stream)>>>(flags, latch);
+  HN_CHECK_LAUNCH();
   return 0;
 }
 

@@ -245,6 +245,7 @@ class _DeviceLU:
     # lands at direct-solve accuracy.  Off: substitution, exact to rounding.
     TILE_INVERSE = False
     TILE_INVERSE_L = False  # the same for the unit-lower L solve
+    PARITY_TOL = 1e-10  # max-norm relative distance to SuperLU's solve (tests): U is ill-conditioned (block kappa up to 7e7), two exact substitution orders differ by ~6e-11
 
     def __init__(self, lu):
         Lm = sparse.csr_matrix(lu.L)
@@ -517,15 +518,15 @@ def _correct_temp_dev(ops: OperatorSet, vstar_soa, p, T, dt: float, vout, Tout, 
            L.ptr(hc), L.ptr(l2), L.stream_handle())
 
 
-def _temperature_bc_dev(ops: OperatorSet, T):
+def _temperature_bc_dev(ops: OperatorSet, T, flags=None):
     nd = len(ops.dirichlet_idx)
     if ops._d_neu is not None:
         L.call("hn_temperature_bc", L.ptr(ops._d_dir_idx), L.ptr(ops._d_dir_val), nd, L.ptr(ops._d_neu.rowptr),
                L.ptr(ops._d_neu.cols), L.ptr(ops._d_neu.vals), L.ptr(ops._d_neu_idx), L.ptr(ops._d_neu_diag),
-               L.ptr(ops._d_is_neu), len(ops.neumann_idx), L.ptr(T), L.stream_handle())
+               L.ptr(ops._d_is_neu), len(ops.neumann_idx), L.ptr(T), L.ptr(flags), L.stream_handle())
     else:
         L.call("hn_temperature_bc", L.ptr(ops._d_dir_idx), L.ptr(ops._d_dir_val), nd, None, None, None, None, None,
-               None, 0, L.ptr(T), L.stream_handle())
+               None, 0, L.ptr(T), None, L.stream_handle())
     return T
 
 
@@ -565,6 +566,12 @@ class _BiCGStab:
     def solve(self, b, x0, rtol: float, maxiter: int):
         """Returns (x (device, n+1), info)."""
         bnrm2 = self._norm(b)
+        if not np.isfinite(bnrm2):
+            # non-finite right-hand side: the fields went non-finite in an earlier step, which
+            # the step latch reports as the reference's probe would (solver.py:448-452); the
+            # Krylov loop is skipped instead of running maxiter iterations on NaN
+            self.x.fill_(float("nan"))
+            return self.x, 0
         atol = max(0.0, float(rtol) * float(bnrm2))
         if bnrm2 == 0:
             return b.clone(), 0
@@ -617,17 +624,99 @@ class _BiCGStab:
         return x, maxiter
 
 
+class _GMRES:
+    """Retry solver after a BiCGStab failure, standing in for scipy's lgmres (reference
+    solver.py:306-312): restarted GMRES(m) with the same LU preconditioner (right
+    preconditioning, modified Gram-Schmidt) and the same stopping rule
+    ||b - A x|| <= rtol ||b||, on device vectors with libhn reductions and updates.  It only
+    runs when BiCGStab reports a failure, so its host-side Hessenberg algebra is off the
+    per-step path."""
+
+    RESTART = 30
+
+    def __init__(self, ops: OperatorSet):
+        self.ops = ops
+        self.n1 = ops.n + 1
+        t = L.torch()
+        m = self.RESTART
+        self.V = L.empty((m + 1, self.n1), t.float64)
+        self.Z = L.empty((m, self.n1), t.float64)
+        self.w = L.empty(self.n1, t.float64)
+
+    def _dot(self, a, b):
+        return self.ops.reduce(0, a, b, n=self.n1)
+
+    def _axpy(self, y, x, alpha):
+        L.call("hn_bicg_update", 1, L.ptr(y), L.ptr(x), None, float(alpha), 0.0, self.n1, L.stream_handle())
+
+    def solve(self, b, x0, rtol: float, maxiter: int):
+        ops, m = self.ops, self.RESTART
+        bnrm = float(np.sqrt(self._dot(b, b)))
+        if not np.isfinite(bnrm):
+            return x0, -1
+        atol = float(rtol) * bnrm
+        x = x0.clone() if x0 is not None else L.zeros(self.n1, L.torch().float64)
+        if bnrm == 0:
+            return x.zero_(), 0
+        V, Z, w = self.V, self.Z, self.w
+        for _ in range(max(1, maxiter)):
+            ops._d_poisson.residual(x, b, w)
+            beta = float(np.sqrt(self._dot(w, w)))
+            if beta <= atol:
+                return x, 0
+            V[0].zero_()
+            self._axpy(V[0], w, 1.0 / beta)
+            H = np.zeros((m + 1, m))
+            cs, sn = np.zeros(m), np.zeros(m)
+            g = np.zeros(m + 1)
+            g[0] = beta
+            k = 0
+            for j in range(m):
+                ops._d_lu.solve(V[j], Z[j])
+                ops._d_poisson.matvec(Z[j], w)
+                for i in range(j + 1):
+                    H[i, j] = self._dot(w, V[i])
+                    self._axpy(w, V[i], -H[i, j])
+                H[j + 1, j] = float(np.sqrt(self._dot(w, w)))
+                if H[j + 1, j] > 0:
+                    V[j + 1].zero_()
+                    self._axpy(V[j + 1], w, 1.0 / H[j + 1, j])
+                for i in range(j):  # apply the previous Givens rotations to column j
+                    a, c = H[i, j], H[i + 1, j]
+                    H[i, j], H[i + 1, j] = cs[i] * a + sn[i] * c, -sn[i] * a + cs[i] * c
+                r = np.hypot(H[j, j], H[j + 1, j])
+                cs[j], sn[j] = (H[j, j] / r, H[j + 1, j] / r) if r > 0 else (1.0, 0.0)
+                H[j, j], H[j + 1, j] = r, 0.0
+                g[j + 1] = -sn[j] * g[j]
+                g[j] = cs[j] * g[j]
+                k = j + 1
+                if abs(g[j + 1]) <= atol or H[j + 1, j] == 0 and r == 0:
+                    break
+            y = np.linalg.lstsq(np.triu(H[:k, :k]), g[:k], rcond=None)[0]
+            for i in range(k):
+                self._axpy(x, Z[i], y[i])
+        ops._d_poisson.residual(x, b, w)
+        return x, (0 if float(np.sqrt(self._dot(w, w))) <= atol else maxiter)
+
+
 def _pressure_dev(ops: OperatorSet, rhs, x0, settings: PoissonSolveSettings, solver: _BiCGStab):
     if ops._d_poisson is None or ops._d_lu is None:
         raise RuntimeError("operators were built with factorize=False: no pressure solve available")
     x, info = solver.solve(rhs, x0, settings.tol, settings.maxiter)
     if info != 0:
-        tt = L.torch()
-        res_vec = L.empty(ops.n + 1, tt.float64)
-        ops._d_poisson.residual(x, rhs, res_vec)
-        res = np.sqrt(ops.reduce(0, res_vec, res_vec)) / max(np.sqrt(ops.reduce(0, rhs, rhs)), 1e-300)
-        raise PoissonConvergenceError(f"pressure Poisson solve did not converge (info={info}); the GPU path "
-                                      "has no lgmres retry", residual=float(res))
+        # the reference retries with lgmres before giving up (solver.py:306-312)
+        retry = getattr(ops, "_gmres", None) or _GMRES(ops)
+        ops._gmres = retry
+        x, info = retry.solve(rhs, x0, settings.tol, settings.maxiter)
+        if info != 0:
+            tt = L.torch()
+            res_vec = L.empty(ops.n + 1, tt.float64)
+            ops._d_poisson.residual(x, rhs, res_vec)
+            res = np.sqrt(ops.reduce(0, res_vec, res_vec)) / max(np.sqrt(ops.reduce(0, rhs, rhs)), 1e-300)
+            raise PoissonConvergenceError(f"pressure Poisson solve did not converge (info={info})",
+                                          residual=float(res))
+        solver.x.copy_(x)
+        x = solver.x
     return x
 
 
@@ -755,6 +844,8 @@ class DeviceStepper:
         self.rhs = L.empty(n + 1, t.float64)
         self.x0 = L.empty(n + 1, t.float64)
         self.flags = L.to_device(np.array([0, INT32_MAX], dtype=np.int32))
+        # [steps done, first non-finite step (0: none), its lowest non-finite T node] (hn_step_latch)
+        self.latch = L.to_device(np.array([0, 0, INT32_MAX], dtype=np.int32))
         self.solver = _BiCGStab(ops)
         self.have_p = False
         self.steps = 0
@@ -774,7 +865,8 @@ class DeviceStepper:
         self.have_p = True
         _correct_temp_dev(ops, self.vstar, self.p, self.T, self.dt, self.v_next, self.T_next, self.flags,
                           self.params.dissipation)
-        _temperature_bc_dev(ops, self.T_next)
+        _temperature_bc_dev(ops, self.T_next, self.flags)
+        L.call("hn_step_latch", L.ptr(self.flags), L.ptr(self.latch), L.stream_handle())
         self.v, self.v_next = self.v_next, self.v
         self.T, self.T_next = self.T_next, self.T
         self.steps += 1
@@ -787,18 +879,33 @@ class DeviceStepper:
         _div_rhs_dev(ops, self.vstar, self.dt, self.rhs)
         _correct_temp_dev(ops, self.vstar, self.p, self.T, self.dt, self.v_next, self.T_next, self.flags,
                           self.params.dissipation)
-        _temperature_bc_dev(ops, self.T_next)
+        _temperature_bc_dev(ops, self.T_next, self.flags)
+        L.call("hn_step_latch", L.ptr(self.flags), L.ptr(self.latch), L.stream_handle())
         self.v, self.v_next = self.v_next, self.v
         self.T, self.T_next = self.T_next, self.T
 
-    def check_finite(self, step: int):
-        f = self.flags.cpu().numpy()
-        if f[0]:
-            node = int(f[1]) if f[1] != INT32_MAX else -1
-            raise SolverDivergenceError(f"non-finite field at step {step}", step=step, node=node)
+    def check_finite(self, step: int | None = None):
+        """Raise SolverDivergenceError for the first step whose fields went non-finite, with
+        the reference's step number (counted from this stepper's first step) and node (the
+        lowest non-finite temperature index, -1 if only the velocity was), solver.py:448-452.
+        The device latches it every step; this reads it (one 12-byte copy)."""
+        f = self.latch.cpu().numpy()
+        if f[1]:
+            bad = int(f[1])
+            node = int(f[2]) if f[2] != INT32_MAX else -1
+            raise SolverDivergenceError(f"non-finite field at step {bad}", step=bad, node=node)
 
     def state(self) -> FieldState:
         return FieldState(self.v.cpu().numpy().T.copy(), self.p.cpu().numpy(), self.T.cpu().numpy())
+
+    def load_state(self, state: FieldState):
+        """Replace the device fields with a host state (the pressure also warm-starts the next
+        solve, as p_prev does in the reference loop)."""
+        self.v.copy_(L.torch().from_numpy(np.ascontiguousarray(np.asarray(state.velocity, dtype=np.float64).T)))
+        self.T.copy_(L.torch().from_numpy(np.asarray(state.temperature, dtype=np.float64)))
+        self.p.copy_(L.torch().from_numpy(np.asarray(state.pressure, dtype=np.float64)))
+        L.TRAFFIC["h2d"] += self.v.nbytes + self.T.nbytes + self.p.nbytes
+        self.have_p = True
 
     def nusselt(self) -> float:
         return _nusselt_dev(self.ops, self.T) if self.ops._d_nu is not None else float("nan")
@@ -837,13 +944,19 @@ def run(config, spec=None, nodeset=None) -> RunResult:
     used only if it is importable."""
     timings: dict = {}
     t0 = time.perf_counter()
-    if nodeset is None:
+    if spec is None and callable(getattr(config, "cold_origins", None)):
+        # the reference always builds the domain first (solver.py:412-415): its
+        # CaseConfig.cold_origins(spec) reads spec.obstacles, even with a precomputed node set
         try:
             from hybridnodes.config import build_domain
+            spec = build_domain(config)
+        except ImportError:
+            pass
+    if nodeset is None:
+        try:
             from hybridnodes.nodegen import hybrid_discretize
         except ImportError as exc:  # pragma: no cover - depends on the environment
             raise ValueError("run() needs a nodeset: node generation is not part of the GPU path") from exc
-        spec = spec if spec is not None else build_domain(config)
         nodeset = hybrid_discretize(config, spec)
     timings["nodegen"] = time.perf_counter() - t0
     settings = PoissonSolveSettings(tol=config.poisson_tol, maxiter=config.poisson_maxiter)

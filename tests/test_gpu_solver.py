@@ -387,3 +387,66 @@ def test_device_lu_solve_matches_superlu_both_tile_modes():
     scale = np.abs(ref).max()
     assert np.abs(got[False] - ref).max() / scale <= 1e-12
     assert np.abs(got[True] - ref).max() / scale <= 1e-8
+
+
+# ---------------------------------------------------------------- run(): reference loop semantics
+def _run_config(g, **over):
+    Ra, Pr, t_cold, t_hot, t_init, t_end, stride = (float(v) for v in g["run_cfg"])
+    base = dict(case="dvd", discretization="hybrid", Ra=Ra, Pr=Pr, t_cold=t_cold, t_hot=t_hot, t_init=t_init,
+                t_end=t_end, poisson_tol=1e-8, poisson_maxiter=2000, steady_tol=1e-6, nu_window=40,
+                nu_stride=int(stride), cold_origins={"wall:x-"})
+    base.update(over)
+    return SimpleNamespace(**base)
+
+
+def test_run_matches_reference_golden(golden):
+    """run() against the reference's own solver.run on a tie-free node set (A22)."""
+    ns, g = golden("run_jittered")
+    res = run(_run_config(g), nodeset=ns)
+    assert res.steps == int(g["run_steps"])
+    assert res.dt == pytest.approx(float(g["run_dt"]), rel=0, abs=0)
+    npt.assert_array_equal(res.nu_steps, g["run_nu_steps"])
+    npt.assert_allclose(res.nu_values, g["run_nu_values"], rtol=1e-8)
+    for got, ref in ((res.state.velocity, g["run_v"]), (res.state.temperature, g["run_T"]),
+                     (res.state.pressure, g["run_p"])):
+        assert rel(got, ref) <= FIELD_TOL
+    div = np.asarray(res.diagnostics["divergence_samples"], dtype=float)
+    assert div.shape == g["run_div"].shape
+    npt.assert_array_equal(div[:, 0], g["run_div"][:, 0])
+    npt.assert_allclose(div[:, 1:], g["run_div"][:, 1:], rtol=1e-6)
+
+
+def test_run_divergence_reports_reference_step_and_node(golden):
+    """The finite probe fires at the reference's step with its node (solver.py:448-452),
+    although the host reads the device latch only every nu_stride steps."""
+    from paper_2303_01760_b200.errors import SolverDivergenceError
+    ns, g = golden("run_jittered")
+    Pr, t_end = (float(v) for v in g["div_cfg"])
+    with pytest.raises(SolverDivergenceError) as exc:
+        run(_run_config(g, Pr=Pr, t_end=t_end), nodeset=ns)
+    assert exc.value.step == int(g["div_step"])
+    assert exc.value.node == int(g["div_node"])
+
+
+def test_pressure_retry_after_bicgstab_failure(dvd_setup, monkeypatch):
+    """A failed BiCGStab is retried by the GMRES stand-in for lgmres (solver.py:306-312), which
+    reaches the direct solution; both failing raises PoissonConvergenceError with a residual."""
+    from paper_2303_01760_b200 import solver as S
+    from paper_2303_01760_b200.errors import PoissonConvergenceError
+    ns, ops, _, settings, _ = dvd_setup
+    vstar = np.random.default_rng(21).normal(size=(len(ns), 2))
+    apply_velocity_bc(vstar, ops)
+    n = len(ns)
+    rhs = np.zeros(n + 1)
+    rhs[:n] = (ops.partials[0].matrix @ vstar[:, 0] + ops.partials[1].matrix @ vstar[:, 1]) / 1e-5
+    rhs[ops.boundary_idx] = 0.0
+    direct = ops.poisson_precond @ rhs
+    orig = S._BiCGStab.solve
+    monkeypatch.setattr(S._BiCGStab, "solve", lambda self, b, x0, rtol, maxiter: (orig(self, b, x0, rtol, 0)[0], -10))
+    ops._poisson_lambda = 0.0
+    p = pressure_solve(vstar, ops, settings, 1e-5)
+    assert rel(p, direct[:n]) <= 1e-9
+    monkeypatch.setattr(S._GMRES, "solve", lambda self, b, x0, rtol, maxiter: (b.clone(), 7))
+    with pytest.raises(PoissonConvergenceError) as exc:
+        pressure_solve(vstar, ops, settings, 1e-5)
+    assert exc.value.residual > 0

@@ -198,3 +198,36 @@ def test_host_tile_inverse_inverts_every_diagonal_tile(lower):
             np.testing.assert_allclose(tinv[s, :tw] @ T, np.eye(tw), atol=1e-10)
             checked += 1
     assert checked > 10
+
+
+def test_run_builds_the_domain_spec_for_cold_origins(monkeypatch):
+    """run(config, nodeset=...) builds the reference's domain spec before cold_origins(spec)
+    (reference solver.py:412-415) when the reference config module is importable: obstacle
+    cases read spec.obstacles there."""
+    import sys
+    import types
+    from paper_2303_01760_b200 import solver as S
+
+    spec_obj = object()
+    fake_cfg = types.ModuleType("hybridnodes.config")
+    fake_cfg.build_domain = lambda config: spec_obj
+    fake_pkg = types.ModuleType("hybridnodes")
+    fake_pkg.config = fake_cfg
+    monkeypatch.setitem(sys.modules, "hybridnodes", fake_pkg)
+    monkeypatch.setitem(sys.modules, "hybridnodes.config", fake_cfg)
+
+    class Reached(Exception):
+        pass
+
+    seen = {}
+
+    class Cfg:
+        poisson_tol, poisson_maxiter = 1e-8, 2000
+
+        def cold_origins(self, spec):
+            seen["spec"] = spec
+            raise Reached
+
+    with pytest.raises(Reached):
+        S.run(Cfg(), nodeset=nodesets.jittered_box(8, seed=0))
+    assert seen["spec"] is spec_obj
