@@ -218,7 +218,7 @@ int hn_temperature_bc(const int* dir_idx, const double* dir_val, int64_t ndir, c
  * lowest non-finite temperature node of that step (INT_MAX = none)]; clears flags.  Lets the
  * host read the probe every nu_stride steps and still report the reference's step and node.
  * Replaces: the per-step probe of run() solver.py:448-452. */
-int hn_step_latch(int* flags, int* latch, void* stream);
+int hn_step_latch(int* flags, int* latch, const int* pstatus, void* stream);
 
 /* y = A x / y = b - A x for a CSR matrix (int64 rowptr), scipy csr_matvec order. */
 int hn_csr_matvec(const int64_t* rowptr, const int* cols, const double* vals, const double* x,
@@ -228,61 +228,71 @@ int hn_csr_residual(const int64_t* rowptr, const int* cols, const double* vals, 
 
 /* ---------------------------------------------------------------- pressure (K9, K12) */
 
-/* Sync-free triangular solve.  lower != 0: unit-lower L (strict part in CSR), rows 0..n-1;
- * lower == 0: strict-upper U in CSR + diag, rows n-1..0.  ticket: one device uint64.
- * Replaces: SuperLU lu.solve inside the bicgstab preconditioner, solver.py:213-214. */
-int hn_sptrsv(int lower, const int64_t* rowptr, const int* cols, const double* vals, const double* diag,
-              const double* b, double* x, int64_t n, unsigned long long* ticket, void* stream);
-
-/* Scheduled sync-free triangular solve over precomputed tasks (rows in dependency-level
- * order; rows longer than a chunk split into partial-sum tasks, task_np = -1, combined in
- * fixed order by the row's final task, task_np = #partials).  divide != 0 divides by diag.
- * x (n) and partial (npartial) are reset inside.  Deterministic. */
-int hn_sptrsv_tasks(int divide, const int* task_row, const int64_t* task_beg, const int* task_len,
-                    const int* task_part, const int* task_np, int64_t ntasks, const int* cols,
-                    const double* vals, const double* diag, const double* b, double* x, int64_t n,
-                    double* partial, int64_t npartial, unsigned long long* ticket, int warps_per_sm,
-                    void* stream);
-
-/* Supernodal sync-free triangular solve over tasks in dependency-level order.  A block
- * [r0, r0+w) has a dense in-block triangle (w <= 4096).  kind 0: one CTA pulls the block's
- * outside part (one global hop) and solves the dense triangle in 32-column tiles; kind 1:
- * helper computing the outside sums of block rows [rb, rb+rc) into ysum (heavy blocks);
- * kind 2: dense part of a heavy block, fed by its helpers (scheduled just before it).
+/* Supernodal sync-free triangular solve over tasks in dependency-level order (one
+ * preconditioner application = permute, this for L, this for U, permute).
+ * Replaces: SuperLU lu.solve inside the bicgstab preconditioner, solver.py:213-214,304-305.
+ * A block [r0, r0+w) (w <= 256) has a dense in-block triangle.  kind 0: one CTA pulls the
+ * block's outside part (one global hop) and solves the dense triangle in 32-column tiles
+ * read from `packed` (hn_host_pack_panels; next panel by bulk async copy); kind 1: helper
+ * computing the outside sums of block rows [rb, rb+rc) into ysum (heavy blocks); kind 2:
+ * dense part of a heavy block, fed by its helpers (scheduled just before it); kind 3: up to
+ * 8 small blocks (w <= 32) of one level, one warp each (members listed after the tasks).
+ * inv: the packed diagonal tiles are inverses (x = T^-1 y per tile instead of substitution).
  * lower: unit diagonal; upper: divides by diag.  Strict CSR, sorted columns.  x and ysum
  * (n each) are reset inside.  Deterministic. */
+/* One triangular factor's supernodal task list (all device pointers; see hn_sptrsv_super). */
+typedef struct hn_tri_plan {
+  int lower;             /* 1: unit-lower L, 0: upper U (divides by diag) */
+  int inv;               /* packed diagonal tiles are inverses */
+  int64_t ntasks;
+  const int* kind;
+  const int* r0;
+  const int* w;
+  const int* rb;
+  const int* rc;
+  const int64_t* off;
+  const int64_t* rowptr; /* strict triangle, CSR, sorted columns */
+  const int* cols;
+  const double* vals;
+  const double* diag;    /* U only */
+  const double* packed;
+} hn_tri_plan;
+
 int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
-                    const int* blk_rc, int64_t nblk, const int64_t* rowptr, const int* cols,
-                    const double* vals, const double* diag, const double* b, double* x, double* ysum,
-                    int64_t n, unsigned long long* ticket, int ctas_per_sm, void* stream);
-
-/* hn_sptrsv_super with tinv (n x 32 doubles, or NULL = substitution): every row's row of the
- * inverse of its 32-row diagonal tile (tiles start at each block's r0, r0+32, ..), from
- * hn_host_tile_inverse; the in-tile triangle is then one matrix-vector product per tile. */
-int hn_sptrsv_super_inv(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
-                        const int* blk_rc, int64_t nblk, const int64_t* rowptr, const int* cols,
-                        const double* vals, const double* diag, const double* tinv, const double* b, double* x,
-                        double* ysum, int64_t n, unsigned long long* ticket, int ctas_per_sm, void* stream);
-/* Host (setup): the tile inverses hn_sptrsv_super_inv reads, from the strict CSR (sorted
- * columns; lower: unit diagonal, upper: diag) and the block list (r0, w) of nb blocks. */
-int hn_host_tile_inverse(const int64_t* rowptr_host, const int* cols_host, const double* vals_host,
-                         const double* diag_host, int64_t n, int lower, int64_t nb, const int* r0_host,
-                         const int* w_host, double* tinv_host);
-
-/* Debug: per-task timeline of hn_sptrsv_super launches ([start, outside sums done, end]
- * in %globaltimer ns, SM id) written to trace (4 u64 per task); NULL switches it off. */
-int hn_debug_sptrsv_trace(unsigned long long* trace);
+                    const int* blk_rc, const int64_t* blk_off, int64_t nblk, const int64_t* rowptr,
+                    const int* cols, const double* vals, const double* diag, const double* packed, int inv,
+                    const double* b, double* x, double* ysum, int64_t n, unsigned long long* ticket,
+                    int ctas_per_sm, void* stream);
 
 /* Setup helpers on HOST arrays: dense-triangle row blocks (returns the count; blocks in row
- * order) and their dependency levels. */
+ * order, w <= cap <= 256), their dependency levels, and the packed dense triangles of the
+ * tasks of kind 0/2 (panels of 32 columns, column-major; off[t] in doubles, -1 for other
+ * kinds; packed == NULL computes offsets only; returns the total, -1 if a block's in-block
+ * triangle is not dense).  inverse != 0: every diagonal tile's rows hold that tile's inverse
+ * (diag_host = U's diagonal for upper) and hn_sptrsv_super must be called with inv = 1. */
 int64_t hn_host_supernodes(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower, int cap,
                            int* blk_r0_host, int* blk_w_host);
 int hn_host_block_levels(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower, int64_t nblk,
                          const int* blk_r0_host, const int* blk_w_host, int* levels_host);
+int64_t hn_host_pack_panels(const int64_t* rowptr_host, const int* cols_host, const double* vals_host,
+                            const double* diag_host, int lower, int inverse, int64_t ntasks, const int* kind_host,
+                            const int* r0_host, const int* w_host, int64_t* off_host, double* packed_host);
 
-/* Setup helper on HOST arrays: dependency level of each row of a triangular CSR
- * (rows swept increasing when lower != 0, decreasing otherwise). */
-int hn_host_levels(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower, int* levels_host);
+/* Device-driven pressure solve (K9 driver, csrc/bicgstab.cu).
+ * Replaces: pressure_solve's bicgstab call with the LU preconditioner, solver.py:304-305
+ * (scipy BiCGStab, rtol, atol = 0, maxiter), every scalar on the device; the loop is a
+ * CUDA-graph WHILE node, so no host round trip happens per solve.  setup: A = the bordered
+ * Poisson matrix (CSR, n rows), the L and U task lists (hn_tri_plan), SuperLU's perm_r /
+ * perm_c; all device pointers, kept (not copied) -> *handle_out.  solve: x0 NULL = zero
+ * start, x0 == x = start from x's contents; status (device int[2], may be NULL) = [scipy
+ * info, completed passes].  Inside a stream capture the solve is added to the caller's
+ * graph; otherwise a cached graph is launched on the stream. */
+int hn_pressure_setup(int64_t n, const int64_t* a_rowptr, const int* a_cols, const double* a_vals,
+                      const hn_tri_plan* lower, const hn_tri_plan* upper, const int* perm_r, const int* perm_c,
+                      int ctas_per_sm, int64_t* handle_out);
+int hn_pressure_solve(int64_t handle, const double* b, const double* x0, double* x, double rtol, int maxiter,
+                      int* status, void* stream);
+int hn_pressure_free(int64_t handle);
 
 /* direction 0: out[perm[i]] = in[i]; direction 1: out[i] = in[perm[i]]. */
 int hn_permute(int direction, const int* perm, const double* in, int64_t n, double* out, void* stream);

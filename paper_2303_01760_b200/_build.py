@@ -34,20 +34,24 @@ def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
 
-def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False) -> Path:
-    BUILD.mkdir(parents=True, exist_ok=True)
+def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False, trace: bool = False) -> Path:
+    """trace=True: a dev build (libhn_trace.so, -DHN_TRACE) with the trisolve task timeline
+    hook hn_debug_sptrsv_trace (tools/trace_sptrsv.py); the product library never has it."""
+    build_dir = BUILD.parent / "hn_trace" if trace else BUILD
+    lib_path = PKG / "libhn_trace.so" if trace else LIB
+    build_dir.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
     newest_header = max((h.stat().st_mtime for h in headers), default=0.0)
     objs = []
     nvcc = _nvcc()
     procs = []
     for src in sources():
-        obj = BUILD / (src.stem + ".o")
+        obj = build_dir / (src.stem + ".o")
         objs.append(obj)
         stale = force or not obj.exists() or obj.stat().st_mtime < max(src.stat().st_mtime, newest_header)
         if not stale:
             continue
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *(["-DHN_TRACE"] if trace else []), "-c", str(src), "-o", str(obj)]
         if ptxas_info:
             cmd += ["-Xptxas", "-v"]
         if verbose:
@@ -62,15 +66,15 @@ def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False) 
             failed.append(src.name)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    lib_stale = force or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs)
+    lib_stale = force or not lib_path.exists() or any(o.stat().st_mtime > lib_path.stat().st_mtime for o in objs)
     if lib_stale:
-        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"]
+        cmd = [nvcc, *ARCH, "-shared", "-o", str(lib_path), *map(str, objs), "-lcudart"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, ptxas_info="--ptxas" in sys.argv, force="-f" in sys.argv)
-    print(LIB)
+    print(build(verbose="-v" in sys.argv, ptxas_info="--ptxas" in sys.argv, force="-f" in sys.argv,
+                trace="--trace" in sys.argv))

@@ -24,6 +24,13 @@ _i = C.c_int
 _i64 = C.c_int64
 _d = C.c_double
 
+class TriPlan(C.Structure):
+    """hn_tri_plan (include/hn.h): one triangular factor's supernodal task list."""
+    _fields_ = [("lower", _i), ("inv", _i), ("ntasks", _i64), ("kind", _vp), ("r0", _vp), ("w", _vp), ("rb", _vp),
+                ("rc", _vp), ("off", _vp), ("rowptr", _vp), ("cols", _vp), ("vals", _vp), ("diag", _vp),
+                ("packed", _vp)]
+
+
 # name -> (restype, argtypes); mirrors include/hn.h exactly (tests check the export list)
 SIGNATURES: dict[str, tuple] = {
     "hn_version": (_i, []),
@@ -59,23 +66,19 @@ SIGNATURES: dict[str, tuple] = {
     "hn_correct_temperature": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i,
                                     _c_int_p, _i, _vp, _vp, _vp, _i64, _d, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hn_temperature_bc": (_i, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
-    "hn_step_latch": (_i, [_vp, _vp, _vp]),
+    "hn_step_latch": (_i, [_vp, _vp, _vp, _vp]),
     "hn_csr_matvec": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "hn_csr_residual": (_i, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
-    "hn_sptrsv": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
-    "hn_sptrsv_tasks": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _i,
-                             _vp]),
-    "hn_host_levels": (_i, [_vp, _vp, _i64, _i, _vp]),
-    "hn_sptrsv_super": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i,
-                             _vp]),
-    "hn_sptrsv_super_inv": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
-                                 _vp, _i, _vp]),
-    "hn_host_tile_inverse": (_i, [_vp, _vp, _vp, _vp, _i64, _i, _i64, _vp, _vp, _vp]),
-    "hn_debug_sptrsv_trace": (_i, [_vp]),
+    "hn_sptrsv_super": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp,
+                             _vp, _i64, _vp, _i, _vp]),
+    "hn_host_pack_panels": (_i64, [_vp, _vp, _vp, _vp, _i, _i, _i64, _vp, _vp, _vp, _vp, _vp]),
     "hn_host_supernodes": (_i64, [_vp, _vp, _i64, _i, _i, _vp, _vp]),
     "hn_host_block_levels": (_i, [_vp, _vp, _i64, _i, _i64, _vp, _vp, _vp]),
     "hn_partition_methods": (_i, [_vp, _i64, _vp, _vp, _vp, _vp]),
     "hn_permute": (_i, [_i, _vp, _vp, _i64, _vp, _vp]),
+    "hn_pressure_setup": (_i, [_i64, _vp, _vp, _vp, C.POINTER(TriPlan), C.POINTER(TriPlan), _vp, _vp, _i, _c_i64_p]),
+    "hn_pressure_solve": (_i, [_i64, _vp, _vp, _vp, _d, _i, _vp, _vp]),
+    "hn_pressure_free": (_i, [_i64]),
     "hn_reduce": (_i, [_i, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "hn_bicg_update": (_i, [_i, _vp, _vp, _vp, _d, _d, _i64, _vp]),
 }

@@ -17,7 +17,7 @@
 //
 // Reductions (dot, norm, max|.|, sums) use a fixed two-level tree (fixed grid of
 // partials, then one block) -> deterministic.
-#include "hn_common.cuh"
+#include "pressure.cuh"
 
 namespace hn {
 
@@ -41,42 +41,8 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// LOWER=true: rows 0..n-1, x_i = b_i - sum_j L_ij x_j (unit diagonal not stored)
-// LOWER=false: rows n-1..0, x_i = (b_i - sum_j U_ij x_j) / diag_i
-template <bool LOWER>
-__global__ void __launch_bounds__(256) sptrsv_kernel(const int64_t* __restrict__ rowptr, const int* __restrict__ cols,
-                                                     const double* __restrict__ vals, const double* __restrict__ diag,
-                                                     const double* __restrict__ b, double* x, int64_t n,
-                                                     unsigned long long* ticket) {
-  const int lane = threadIdx.x & 31;
-  while (true) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(ticket, 1ull);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= static_cast<unsigned long long>(n)) return;
-    const int64_t row = LOWER ? static_cast<int64_t>(t) : n - 1 - static_cast<int64_t>(t);
-    const int64_t e0 = __ldg(rowptr + row), e1 = __ldg(rowptr + row + 1);
-    double sum = 0.0;
-    for (int64_t e = e0 + lane; e < e1; e += 32) {
-      const int c = __ldg(cols + e);
-      const double v = __ldg(vals + e);
-      double xc = ld_acquire_dbl(x + c);
-      while (is_sentinel(xc)) xc = ld_acquire_dbl(x + c);
-      sum = fma(v, xc, sum);
-    }
-    sum = warp_sum(sum);
-    if (lane == 0) {
-      double r = __ldg(b + row) - sum;
-      if (!LOWER) r = r / __ldg(diag + row);
-      st_release_dbl(x + row, r);
-    }
-  }
-}
-
-// Scheduled variant: tasks in dependency-level order; a row longer than the chunk size is
-// split into partial-sum tasks (np = -1, written to partial[part]) followed by a final
-// task (np = number of partials) that adds them in fixed order -> deterministic.
-// Waiting uses exponential __nanosleep backoff so idle warps do not saturate L2.
+// Dependencies are spun on with exponential __nanosleep backoff so idle warps do not
+// saturate L2 with polling loads.
 __device__ __forceinline__ double wait_value(const double* p) {
   double v = ld_acquire_dbl(p);
   unsigned ns = 32;
@@ -88,71 +54,70 @@ __device__ __forceinline__ double wait_value(const double* p) {
   return v;
 }
 
-constexpr int kTaskChunk = 256;           // nnz per task (host planner uses the same)
+constexpr int kTaskChunk = 256;  // row entries a warp requests before it waits on any of them
 constexpr int kPerLane = kTaskChunk / 32;
 
-template <bool DIV>
-__global__ void __launch_bounds__(256) sptrsv_tasks_kernel(
-    const int* __restrict__ task_row, const int64_t* __restrict__ task_beg, const int* __restrict__ task_len,
-    const int* __restrict__ task_part, const int* __restrict__ task_np, int64_t ntasks, const int* __restrict__ cols,
-    const double* __restrict__ vals, const double* __restrict__ diag, const double* __restrict__ b, double* x,
-    double* partial, unsigned long long* ticket) {
-  const int lane = threadIdx.x & 31;
-  while (true) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(ticket, 1ull);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= static_cast<unsigned long long>(ntasks)) return;
-    const int row = __ldg(task_row + t);
-    const int64_t e0 = __ldg(task_beg + t);
-    const int len = __ldg(task_len + t);
-    // all of the lane's operands are requested before anything waits: one L2 round trip
-    // per task instead of one per element; then spin only on values not yet produced
-    int c[kPerLane];
-    double v[kPerLane], xv[kPerLane];
-#pragma unroll
-    for (int k = 0; k < kPerLane; ++k) {
-      const int e = lane + 32 * k;
-      c[k] = e < len ? __ldg(cols + e0 + e) : -1;
-      v[k] = e < len ? __ldg(vals + e0 + e) : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < kPerLane; ++k) xv[k] = c[k] >= 0 ? ld_acquire_dbl(x + c[k]) : 0.0;
-    double sum = 0.0;
-#pragma unroll
-    for (int k = 0; k < kPerLane; ++k) {
-      if (c[k] >= 0 && is_sentinel(xv[k])) xv[k] = wait_value(x + c[k]);
-      sum = fma(v[k], xv[k], sum);
-    }
-    sum = warp_sum(sum);
-    if (lane == 0) {
-      const int np = __ldg(task_np + t);
-      const int part = __ldg(task_part + t);
-      if (np < 0) {
-        st_release_dbl(partial + part, sum);
-      } else {
-        double tot = 0.0;
-        for (int k = 0; k < np; ++k) tot += wait_value(partial + part + k);
-        tot += sum;
-        double r = __ldg(b + row) - tot;
-        if (DIV) r = r / __ldg(diag + row);
-        st_release_dbl(x + row, r);
-      }
-    }
-  }
-}
-
-// ---- supernodal variant -------------------------------------------------------------
+// ---- supernodal sync-free triangular solve --------------------------------------------
 // Rows are grouped into blocks [r0, r0+w) whose in-block triangle is dense (SuperLU
-// supernodes).  One CTA per block: (1) every row's outside part is pulled (warp per row,
-// load-first + spin, one global hop per block), (2) the dense in-block triangle is solved
-// in 32-column tiles: one warp solves the diagonal tile with shuffles, then all warps
-// apply the tile to the remaining rows.  Row layout in the strict CSR (sorted columns):
+// supernodes, w <= 256).  One CTA per block: (1) every row's outside part is pulled (warp
+// per row, load-first + spin, one global hop per block; heavy blocks get helper tasks on
+// other SMs), (2) the dense in-block triangle is solved in 32-column tiles: the warp owning
+// the tile's rows solves it with shuffles, then every thread applies it to its own row.
+// Row layout in the strict CSR (sorted columns):
 //   lower: [outside cols < r0 | inside cols r0..i-1]   (inside count = i - r0)
 //   upper: [inside cols i+1..r1-1 | outside cols >= r1] (inside count = r1-1-i)
+// The dense triangle is read from a packed copy (hn_host_pack_panels): per 32-column tile
+// one panel, column-major over the rows the tile touches, so a warp's load of one column
+// is 32 consecutive doubles and the next panel arrives by ONE bulk async copy (TMA engine,
+// cp.async.bulk + mbarrier) while the current tile is solved.  The CSR copy of the same
+// entries is what the outside sums read; the panels are only the dense part.
 constexpr int kSnThreads = 256;
 constexpr int kSnWarps = kSnThreads / 32;
-constexpr int kSnMaxW = 4096;
+constexpr int kSnMaxW = kSnThreads;  // block width cap (one row per thread)
+constexpr int kSnMaxPairs = 512;     // (row, 256-entry chunk) pairs of one task's outside phase
+
+// Panel tt of a packed block of width w, in processing order (lower: tiles left to right,
+// upper: right to left).  Panel rows: lower [t0, w), upper [0, t0 + tw); stored column-
+// major with a row stride rp (rows rounded up to even: 16-byte aligned panels), always 32
+// columns (the last tile's missing columns are zero).  Entry (row, t0 + k) lives at
+// panel[k * rp + row - rbase]; entries on or across the diagonal are zero.
+__host__ __device__ __forceinline__ void panel_geom(bool lower, int w, int tt, int& t0, int& tw, int& rbase,
+                                                    int& rows, int& rp) {
+  const int ntiles = (w + 31) / 32;
+  t0 = lower ? 32 * tt : 32 * (ntiles - 1 - tt);
+  tw = w - t0 < 32 ? w - t0 : 32;
+  rbase = lower ? t0 : 0;
+  rows = lower ? w - t0 : t0 + tw;
+  rp = (rows + 1) & ~1;
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one thread: arm the barrier with the byte count, then the bulk copy completes it
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void l2_prefetch(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 
 __device__ __forceinline__ double row_outside_sum(const int* __restrict__ cols, const double* __restrict__ vals,
                                                   int64_t e0, int len, const double* x, int lane) {
@@ -177,14 +142,37 @@ __device__ __forceinline__ double row_outside_sum(const int* __restrict__ cols, 
   return warp_sum(sum);
 }
 
+// The 32-row diagonal tile of a block by one warp: lane = row - t0, yv = its right-hand
+// side with every earlier tile applied, lv[k] = its entry in column t0 + k (zero on and
+// across the diagonal).  Forward (lower, unit diagonal) or backward (upper) substitution
+// through the shuffle network; returns the lane's solution.
+template <bool LOWER>
+__device__ __forceinline__ double tile_substitute(const double (&lv)[32], double yv, double dg, int lane, int tw) {
+  const double rdg = 1.0 / dg;  // off the dependency chain (x * (1/d): <= 1 ulp from x / d)
+  if (LOWER) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double xk = __shfl_sync(0xffffffffu, yv, k);
+      if (lane > k) yv = fma(-lv[k], xk, yv);
+    }
+  } else {
+#pragma unroll
+    for (int k = 31; k >= 0; --k) {
+      if (lane == k && lane < tw) yv = yv * rdg;
+      const double xk = __shfl_sync(0xffffffffu, yv, k);
+      if (lane < k) yv = fma(-lv[k], xk, yv);
+    }
+  }
+  return yv;
+}
+
 // Small block (w <= 32) solved by one warp: lane r owns row r0+r -- its outside part by a
 // serial loop with 8 loads in flight (the planner only batches blocks whose rows are
 // short), then the dense triangle with shuffles.  No shared memory, no CTA barrier.
 template <bool LOWER>
 __device__ __forceinline__ void warp_small_block(const int64_t* __restrict__ rowptr, const int* __restrict__ cols,
                                                  const double* __restrict__ vals, const double* __restrict__ diag,
-                                                 const double* __restrict__ tinv, const double* __restrict__ b,
-                                                 double* x, int r0, int w, int lane) {
+                                                 const double* __restrict__ b, double* x, int r0, int w, int lane) {
   double yv = 0.0, dg = 1.0;
   double lv[32];
 #pragma unroll
@@ -215,9 +203,7 @@ __device__ __forceinline__ void warp_small_block(const int64_t* __restrict__ row
     yv = __ldg(b + i) - s;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
-      if (tinv) {
-        if (k < w) lv[k] = __ldg(tinv + static_cast<int64_t>(i) * 32 + k);  // row of the tile inverse
-      } else if (LOWER) {
+      if (LOWER) {
         if (k < lane) lv[k] = __ldg(vals + (z - lane) + k);           // col r0 + k
       } else {
         if (k > lane && k < w) lv[k] = __ldg(vals + a + (k - lane - 1));  // col r0 + k
@@ -225,40 +211,12 @@ __device__ __forceinline__ void warp_small_block(const int64_t* __restrict__ row
     }
     if (!LOWER) dg = __ldg(diag + i);
   }
-  if (tinv) {  // x = T^-1 y: 32 independent products, no dependency chain through the shuffles
-    double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < 32; k += 2) {
-      acc0 = fma(lv[k], __shfl_sync(0xffffffffu, yv, k), acc0);
-      acc1 = fma(lv[k + 1], __shfl_sync(0xffffffffu, yv, k + 1), acc1);
-    }
-    if (lane < w) st_release_dbl(x + r0 + lane, acc0 + acc1);
-    return;
-  }
-  const double rdg = 1.0 / dg;  // off the dependency chain below (x * (1/d): <= 1 ulp from x / d)
-  if (LOWER) {
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      const double xk = __shfl_sync(0xffffffffu, yv, k);
-      if (lane > k) yv = fma(-lv[k], xk, yv);
-    }
-  } else {
-#pragma unroll
-    for (int k = 31; k >= 0; --k) {
-      if (lane == k && lane < w) yv = yv * rdg;
-      const double xk = __shfl_sync(0xffffffffu, yv, k);
-      if (lane < k) yv = fma(-lv[k], xk, yv);
-    }
-  }
+  yv = tile_substitute<LOWER>(lv, yv, dg, lane, w);
   if (lane < w) st_release_dbl(x + r0 + lane, yv);
 }
 
-// Task kinds: 0 = whole block (outside + dense), 1 = helper (outside sums of rows
-// [rb, rb+rc) of a heavy block -> ysum, sentinel-flagged), 2 = dense part of a heavy block
-// whose outside sums come from its helpers (scheduled right before it), 3 = batch of up to
-// kSnWarps independent small blocks of one level, warp k solving member rb+k (member
-// entries live past the task list in the same arrays).
-// optional per-task timeline (hn_debug_sptrsv_trace): [start, outside-done, end] ns + SM id
+#ifdef HN_TRACE
+// dev builds only (libhn_trace.so): per-task timeline [start, outside-done, end] ns + SM id
 __device__ unsigned long long* g_sn_trace = nullptr;
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -270,236 +228,222 @@ __device__ __forceinline__ unsigned smid() {
   asm volatile("mov.u32 %0, %smid;" : "=r"(r));
   return r;
 }
+#define SN_TRACE(slot, value)                               \
+  do {                                                      \
+    if (g_sn_trace) g_sn_trace[4 * t + (slot)] = (value);   \
+  } while (0)
+#else
+#define SN_TRACE(slot, value) \
+  do {                        \
+  } while (0)
+#endif
 
+// Task kinds: 0 = whole block (outside + dense), 1 = helper (outside sums of rows
+// [rb, rb+rc) of a heavy block -> ysum, sentinel-flagged), 2 = dense part of a heavy block
+// whose outside sums come from its helpers (scheduled right before it), 3 = batch of up to
+// kSnWarps independent small blocks of one level, warp k solving member rb+k (member
+// entries live past the task list in the same arrays).  blk_off[t] = offset of task t's
+// packed panels (kinds 0 and 2).
 template <bool LOWER>
 __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
     const int* __restrict__ blk_kind, const int* __restrict__ blk_r0, const int* __restrict__ blk_w,
-    const int* __restrict__ blk_rb, const int* __restrict__ blk_rc, int64_t nblk, const int64_t* __restrict__ rowptr,
-    const int* __restrict__ cols, const double* __restrict__ vals, const double* __restrict__ diag,
-    const double* __restrict__ tinv, const double* __restrict__ b, double* x, double* ysum,
-    unsigned long long* ticket) {
+    const int* __restrict__ blk_rb, const int* __restrict__ blk_rc, const int64_t* __restrict__ blk_off,
+    int64_t nblk, const int64_t* __restrict__ rowptr, const int* __restrict__ cols, const double* __restrict__ vals,
+    const double* __restrict__ diag, const double* __restrict__ packed, int inv, const double* __restrict__ b,
+    double* x, double* ysum, unsigned long long* ticket, const int* __restrict__ skip) {
+  if (skip && *skip) return;
   __shared__ double ys[kSnMaxW];
+  __shared__ int s_cnt[kSnMaxW], s_off[kSnMaxW + 1];  // outside phase: chunks per row, their offsets
+  __shared__ short s_prow[kSnMaxPairs];                // pair -> row
+  __shared__ double s_part[kSnMaxPairs];               // pair partial sums
   __shared__ unsigned long long tk;
-  extern __shared__ double sn_nbuf[];  // [32][kSnThreads]: the next tile's entries (cp.async)
+  __shared__ alignas(8) unsigned long long mbar;
+  extern __shared__ __align__(128) double sn_nbuf[];  // the next panel: [32][rp] (bulk copy)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) mbar_init(&mbar);
+  __syncthreads();
+  unsigned phase = 0;
   while (true) {
     if (tid == 0) tk = atomicAdd(ticket, 1ull);
     __syncthreads();
     const unsigned long long t = tk;
     __syncthreads();
     if (t >= static_cast<unsigned long long>(nblk)) return;
-    unsigned long long* tr = g_sn_trace;
-    if (tr && tid == 0) {
-      tr[4 * t] = gtime();
-      tr[4 * t + 3] = smid();
+#ifdef HN_TRACE
+    if (tid == 0) {
+      SN_TRACE(0, gtime());
+      SN_TRACE(3, smid());
     }
+#endif
     const int kind = __ldg(blk_kind + t);
     if (kind == 3) {
       const int mb = __ldg(blk_rb + t), mc = __ldg(blk_rc + t);
       if (warp < mc)
-        warp_small_block<LOWER>(rowptr, cols, vals, diag, tinv, b, x, __ldg(blk_r0 + mb + warp), __ldg(blk_w + mb + warp),
+        warp_small_block<LOWER>(rowptr, cols, vals, diag, b, x, __ldg(blk_r0 + mb + warp), __ldg(blk_w + mb + warp),
                                 lane);
-      if (tr) {
-        __syncthreads();
-        if (tid == 0) tr[4 * t + 2] = gtime();
-      }
+#ifdef HN_TRACE
+      __syncthreads();
+      if (tid == 0) SN_TRACE(2, gtime());
+#endif
       continue;
     }
     const int r0 = __ldg(blk_r0 + t), w = __ldg(blk_w + t);
+    const double* P = kind == 1 ? nullptr : packed + __ldg(blk_off + t);
+    const int ntiles = (w + 31) / 32;
+    if (tid == 0 && P && ntiles > 1) {  // the whole packed triangle towards L2 while the outside sums run
+      int t0, tw, rbase, rows, rp;
+      unsigned bytes = 0;
+      for (int tt = 0; tt < ntiles; ++tt) {
+        panel_geom(LOWER, w, tt, t0, tw, rbase, rows, rp);
+        bytes += 32u * rp * 8u;
+      }
+      l2_prefetch(P, bytes);
+    }
     if (kind == 2) {
       for (int rr = tid; rr < w; rr += kSnThreads) ys[rr] = wait_value(ysum + r0 + rr);
     } else {
-      // (1) outside contributions, warp per row
+      // (1) outside contributions of rows [rb, re): every row is cut into 256-entry chunks
+      // and the (row, chunk) pairs are spread over the 8 warps, so a long row costs
+      // ceil(chunks / 8) dependent memory round trips instead of one per chunk; the chunk
+      // partials are then added per row in chunk order (deterministic)
       const int rb = kind == 1 ? __ldg(blk_rb + t) : 0;
-      const int re = kind == 1 ? rb + __ldg(blk_rc + t) : w;
-      for (int rr = rb + warp; rr < re; rr += kSnWarps) {
-        const int i = r0 + rr;
+      const int nr = (kind == 1 ? __ldg(blk_rc + t) : w);
+      for (int q = tid; q < nr; q += kSnThreads) {
+        const int rr = rb + q, i = r0 + rr;
+        const int len = static_cast<int>(__ldg(rowptr + i + 1) - __ldg(rowptr + i)) - (LOWER ? rr : (w - 1 - rr));
+        s_cnt[q] = len > 0 ? (len + kTaskChunk - 1) / kTaskChunk : 1;
+      }
+      __syncthreads();
+      if (warp == 0) {  // exclusive scan of the chunk counts (nr <= 256: 8 per lane)
+        int v[8], tot = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int q = lane * 8 + k;
+          v[k] = q < nr ? s_cnt[q] : 0;
+          tot += v[k];
+        }
+        int inc = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        int run = inc - tot;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int q = lane * 8 + k;
+          if (q < nr) s_off[q] = run;
+          run += v[k];
+        }
+        if (lane == 31) s_off[nr] = inc;
+      }
+      __syncthreads();
+      const int npairs = s_off[nr];  // the planner keeps this <= kSnMaxPairs
+      for (int q = tid; q < nr; q += kSnThreads)
+        for (int p = s_off[q]; p < s_off[q + 1]; ++p) s_prow[p] = static_cast<short>(q);
+      __syncthreads();
+      for (int p = warp; p < npairs; p += kSnWarps) {
+        const int q = s_prow[p], rr = rb + q, i = r0 + rr;
         const int64_t a = __ldg(rowptr + i), z = __ldg(rowptr + i + 1);
         const int inside = LOWER ? rr : (w - 1 - rr);
-        const int64_t e0 = LOWER ? a : a + inside;
         const int len = static_cast<int>(z - a) - inside;
-        const double s = row_outside_sum(cols, vals, e0, len, x, lane);
-        if (lane == 0) {
-          if (kind == 1) st_release_dbl(ysum + i, __ldg(b + i) - s);
-          else ys[rr] = __ldg(b + i) - s;
-        }
+        const int c0 = (p - s_off[q]) * kTaskChunk;
+        const int clen = len - c0 < kTaskChunk ? len - c0 : kTaskChunk;
+        const double sp = clen > 0 ? row_outside_sum(cols, vals, (LOWER ? a : a + inside) + c0, clen, x, lane) : 0.0;
+        if (lane == 0) s_part[p] = sp;
+      }
+      __syncthreads();
+      for (int q = tid; q < nr; q += kSnThreads) {
+        double sum = 0.0;
+        for (int p = s_off[q]; p < s_off[q + 1]; ++p) sum += s_part[p];
+        const int rr = rb + q, i = r0 + rr;
+        if (kind == 1) st_release_dbl(ysum + i, __ldg(b + i) - sum);
+        else ys[rr] = __ldg(b + i) - sum;
       }
       if (kind == 1) {
-        if (tr) {
-          __syncthreads();
-          if (tid == 0) tr[4 * t + 2] = gtime();
-        }
+#ifdef HN_TRACE
+        __syncthreads();
+        if (tid == 0) SN_TRACE(2, gtime());
+#endif
         continue;
       }
     }
+    if (tid >= w) ys[tid] = 0.0;  // the last tile's missing columns multiply zeros, never stale values
     __syncthreads();
-    if (tr && tid == 0) tr[4 * t + 1] = gtime();
-    // (2) dense in-block triangle, 32-column tiles
-    const int ntiles = (w + 31) / 32;
-    if (w <= kSnThreads) {
-      // thread tid owns block row tid: it loads its 32 entries of the next tile while the
-      // current tile is solved (the diagonal tile by the warp that owns its rows, lane =
-      // row - t0), so the apply of a tile never waits on memory; same arithmetic and order
-      const bool has = tid < w;
-      const int i = r0 + tid;
-      const int64_t ra = has ? __ldg(rowptr + i) : 0, rz = has ? __ldg(rowptr + i + 1) : 0;
-      auto tile_t0 = [&](int tt) { return LOWER ? 32 * tt : 32 * (ntiles - 1 - tt); };
-      auto load_tile = [&](int t0, double* v) {
-        const int tw = min(32, w - t0);
-        const bool own = tinv && has && tid >= t0 && tid < t0 + tw;  // my diagonal tile: its inverse
+#ifdef HN_TRACE
+    if (tid == 0) SN_TRACE(1, gtime());
+#endif
+    // (2) dense in-block triangle from the packed panels; thread tid owns block row tid
+    const bool has = tid < w;
+    const int i = r0 + tid;
+    const double dg = (!LOWER && has) ? __ldg(diag + i) : 1.0;
+    int t0, tw, rbase, rows, rp;
+    panel_geom(LOWER, w, 0, t0, tw, rbase, rows, rp);
+    const double* panel = P;
+    double cur[32];
+    {
+      const int rr = tid - rbase;
+      const bool in = has && rr >= 0 && rr < rows;
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const int c = t0 + k;
-          const bool ok = has && k < tw && (LOWER ? c < tid : c > tid);
-          v[k] = own ? (k < tw ? __ldg(tinv + static_cast<int64_t>(i) * 32 + k) : 0.0)
-                     : (ok ? __ldg(vals + (LOWER ? (rz - tid) + c : ra + (c - tid - 1))) : 0.0);
-        }
-      };
-      // the next tile goes to shared memory by cp.async (thread tid only touches column tid,
-      // so no barrier guards it): no registers held for it across the tile
-      auto prefetch_tile = [&](int t0) {
-        const int tw = min(32, w - t0);
-        const bool own = tinv && has && tid >= t0 && tid < t0 + tw;
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const int c = t0 + k;
-          const bool ok = has && k < tw && (LOWER ? c < tid : c > tid);
-          double* dst = sn_nbuf + k * kSnThreads + tid;
-          const double* src = own ? (k < tw ? tinv + static_cast<int64_t>(i) * 32 + k : nullptr)
-                                  : (ok ? vals + (LOWER ? (rz - tid) + c : ra + (c - tid - 1)) : nullptr);
-          if (src) {
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(
-                             __cvta_generic_to_shared(dst))), "l"(src) : "memory");
-          } else {
-            *dst = 0.0;
-          }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      };
-      double cur[32];
-      load_tile(tile_t0(0), cur);
-      for (int tt = 0; tt < ntiles; ++tt) {
-        const int t0 = tile_t0(tt);
-        const int tw = min(32, w - t0);
-        if (tt + 1 < ntiles) prefetch_tile(tile_t0(tt + 1));
-        if (warp == t0 / 32 && tinv) {  // x = T^-1 y, no dependency chain
-          const double yv = lane < tw ? ys[tid] : 0.0;
-          double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-          for (int k = 0; k < 32; k += 2) {
-            acc0 = fma(cur[k], __shfl_sync(0xffffffffu, yv, k), acc0);
-            acc1 = fma(cur[k + 1], __shfl_sync(0xffffffffu, yv, k + 1), acc1);
-          }
-          if (lane < tw) {
-            ys[tid] = acc0 + acc1;
-            st_release_dbl(x + i, acc0 + acc1);
-          }
-        } else if (warp == t0 / 32) {  // the diagonal tile's rows: lane = row - t0
-          double yv = lane < tw ? ys[tid] : 0.0;
-          const double dg = (!LOWER && lane < tw) ? __ldg(diag + i) : 1.0;
-          const double rdg = 1.0 / dg;
-          if (LOWER) {
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              const double xk = __shfl_sync(0xffffffffu, yv, k);
-              if (lane > k) yv = fma(-cur[k], xk, yv);
-            }
-          } else {
-#pragma unroll
-            for (int k = 31; k >= 0; --k) {
-              if (lane == k && lane < tw) yv = yv * rdg;
-              const double xk = __shfl_sync(0xffffffffu, yv, k);
-              if (lane < k) yv = fma(-cur[k], xk, yv);
-            }
-          }
-          if (lane < tw) {
-            ys[tid] = yv;
-            st_release_dbl(x + i, yv);
-          }
-        }
-        __syncthreads();
-        if (has && (LOWER ? tid >= t0 + tw : tid < t0)) {  // apply the solved tile to my row
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < 32; ++k)
-            if (k < tw) acc = fma(cur[k], ys[t0 + k], acc);
-          ys[tid] -= acc;
-        }
-        __syncthreads();
-        if (tt + 1 < ntiles) {
-          asm volatile("cp.async.wait_all;" ::: "memory");
-#pragma unroll
-          for (int k = 0; k < 32; ++k) cur[k] = sn_nbuf[k * kSnThreads + tid];
-        }
-      }
-      if (tr && tid == 0) tr[4 * t + 2] = gtime();
-      continue;
+      for (int k = 0; k < 32; ++k) cur[k] = in ? __ldg(panel + k * rp + rr) : 0.0;
     }
     for (int tt = 0; tt < ntiles; ++tt) {
-      const int t0 = LOWER ? 32 * tt : 32 * (ntiles - 1 - tt);  // first block row of the tile
-      const int tw = min(32, w - t0);
-      if (warp == (tt % kSnWarps)) {
-        const int rr = t0 + lane;
-        double yv = lane < tw ? ys[rr] : 0.0;
-        const int i = r0 + rr;
-        // this lane's row entries inside the diagonal tile
-        double lv[32];
-        if (lane < tw) {
-          const int64_t a = __ldg(rowptr + i), z = __ldg(rowptr + i + 1);
+      const bool more = tt + 1 < ntiles;
+      int n0, nw, nbase, nrows, nrp;
+      panel_geom(LOWER, w, more ? tt + 1 : tt, n0, nw, nbase, nrows, nrp);
+      if (more && tid == 0) bulk_load(sn_nbuf, panel + 32 * rp, 32u * nrp * 8u, &mbar);
+      if (warp == t0 / 32 && inv) {  // x = T^-1 y: 32 independent products, no chain
+        const double yv = lane < tw ? ys[tid] : 0.0;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            double val = 0.0;
-            if (LOWER) {
-              if (k < lane) val = __ldg(vals + (z - rr) + t0 + k);           // col r0 + t0 + k
-            } else {
-              if (k > lane && k < tw) val = __ldg(vals + a + (t0 + k - rr - 1));  // col r0 + t0 + k
-            }
-            lv[k] = val;
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 32; ++k) lv[k] = 0.0;
-        }
-        const double dg = (!LOWER && lane < tw) ? __ldg(diag + i) : 1.0;
-        const double rdg = 1.0 / dg;
-        if (LOWER) {
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const double xk = __shfl_sync(0xffffffffu, yv, k);
-            if (lane > k) yv = fma(-lv[k], xk, yv);
-          }
-        } else {
-#pragma unroll
-          for (int k = 31; k >= 0; --k) {
-            if (lane == k && lane < tw) yv = yv * rdg;
-            const double xk = __shfl_sync(0xffffffffu, yv, k);
-            if (lane < k) yv = fma(-lv[k], xk, yv);
-          }
+        for (int k = 0; k < 32; k += 4) {
+          a0 = fma(cur[k], __shfl_sync(0xffffffffu, yv, k), a0);
+          a1 = fma(cur[k + 1], __shfl_sync(0xffffffffu, yv, k + 1), a1);
+          a2 = fma(cur[k + 2], __shfl_sync(0xffffffffu, yv, k + 2), a2);
+          a3 = fma(cur[k + 3], __shfl_sync(0xffffffffu, yv, k + 3), a3);
         }
         if (lane < tw) {
-          ys[rr] = yv;
+          ys[tid] = (a0 + a1) + (a2 + a3);
+          st_release_dbl(x + i, ys[tid]);
+        }
+      } else if (warp == t0 / 32) {  // the diagonal tile's rows: lane = row - t0
+        const double yv = tile_substitute<LOWER>(cur, lane < tw ? ys[tid] : 0.0, dg, lane, tw);
+        if (lane < tw) {
+          ys[tid] = yv;
           st_release_dbl(x + i, yv);
         }
       }
       __syncthreads();
-      // apply the solved tile to the rows not yet solved
-      const int lo = LOWER ? t0 + tw : 0;
-      const int hi = LOWER ? w : t0;
-      for (int rr = lo + tid; rr < hi; rr += kSnThreads) {
-        const int i = r0 + rr;
-        double acc = 0.0;
-        if (LOWER) {
-          const double* rowv = vals + (__ldg(rowptr + i + 1) - rr) + t0;  // cols r0+t0 ..
-          for (int k = 0; k < tw; ++k) acc = fma(__ldg(rowv + k), ys[t0 + k], acc);
-        } else {
-          const double* rowv = vals + __ldg(rowptr + i) + (t0 - rr - 1);     // col r0+t0+k at +k
-          for (int k = 0; k < tw; ++k) acc = fma(__ldg(rowv + k), ys[t0 + k], acc);
+      if (has && (LOWER ? tid >= t0 + tw : tid < t0)) {  // apply the solved tile to my row
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          a0 = fma(cur[k], ys[t0 + k], a0);
+          a1 = fma(cur[k + 1], ys[t0 + k + 1], a1);
+          a2 = fma(cur[k + 2], ys[t0 + k + 2], a2);
+          a3 = fma(cur[k + 3], ys[t0 + k + 3], a3);
         }
-        ys[rr] -= acc;
+        ys[tid] -= (a0 + a1) + (a2 + a3);
+      }
+      if (more) {
+        mbar_wait(&mbar, phase);
+        phase ^= 1u;
+        const int rr = tid - nbase;
+        const bool in = has && rr >= 0 && rr < nrows;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) cur[k] = in ? sn_nbuf[k * nrp + rr] : 0.0;
+        panel += 32 * rp;
+        t0 = n0;
+        tw = nw;
+        rbase = nbase;
+        rows = nrows;
+        rp = nrp;
       }
       __syncthreads();
     }
-    if (tr && tid == 0) tr[4 * t + 2] = gtime();
+#ifdef HN_TRACE
+    if (tid == 0) SN_TRACE(2, gtime());
+#endif
   }
 }
 
@@ -591,135 +535,137 @@ __global__ void axpy_kernel(double* __restrict__ y, const double* __restrict__ x
 
 using namespace hn;
 
-HN_EXPORT int hn_sptrsv(int lower, const int64_t* rowptr, const int* cols, const double* vals, const double* diag,
-                        const double* b, double* x, int64_t n, unsigned long long* ticket, void* stream) {
-  if (n == 0) return 0;
-  cudaStream_t s = as_stream(stream);
-  HN_TRY(cudaMemsetAsync(x, 0xFF, sizeof(double) * n, s));
-  HN_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s));
-  const int blocks = sm_count() * 4;  // 8 warps per block -> 32 resident rows per SM
-  if (lower) sptrsv_kernel<true><<<blocks, 256, 0, s>>>(rowptr, cols, vals, diag, b, x, n, ticket);
-  else sptrsv_kernel<false><<<blocks, 256, 0, s>>>(rowptr, cols, vals, diag, b, x, n, ticket);
-  HN_CHECK_LAUNCH();
-  return 0;
-}
-
-// Scheduled sync-free solve (see sptrsv_tasks_kernel).  divide != 0: x_row /= diag[row].
-// x (n) and partial (npartial) are reset to the sentinel here; warps_per_sm resident warps.
-HN_EXPORT int hn_sptrsv_tasks(int divide, const int* task_row, const int64_t* task_beg, const int* task_len,
-                              const int* task_part, const int* task_np, int64_t ntasks, const int* cols,
-                              const double* vals, const double* diag, const double* b, double* x, int64_t n,
-                              double* partial, int64_t npartial, unsigned long long* ticket, int warps_per_sm,
-                              void* stream) {
-  if (ntasks == 0) return 0;
-  cudaStream_t s = as_stream(stream);
-  HN_TRY(cudaMemsetAsync(x, 0xFF, sizeof(double) * n, s));
-  if (npartial > 0) HN_TRY(cudaMemsetAsync(partial, 0xFF, sizeof(double) * npartial, s));
-  HN_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s));
-  const int wps = warps_per_sm > 0 ? warps_per_sm : 16;
-  const int blocks = sm_count() * ((wps + 7) / 8);
-  if (divide)
-    sptrsv_tasks_kernel<true><<<blocks, 256, 0, s>>>(task_row, task_beg, task_len, task_part, task_np, ntasks, cols,
-                                                     vals, diag, b, x, partial, ticket);
-  else
-    sptrsv_tasks_kernel<false><<<blocks, 256, 0, s>>>(task_row, task_beg, task_len, task_part, task_np, ntasks, cols,
-                                                      vals, diag, b, x, partial, ticket);
-  HN_CHECK_LAUNCH();
-  return 0;
-}
-
-// Debug timeline for hn_sptrsv_super: trace = 4 x ntasks u64 per launch (NULL = off).
+#ifdef HN_TRACE
+// Dev builds only (libhn_trace.so, tools/trace_sptrsv.py): per-task timeline of the
+// supernodal solves, trace = 4 x ntasks u64 per launch (NULL = off).
 HN_EXPORT int hn_debug_sptrsv_trace(unsigned long long* trace) {
   return cudaMemcpyToSymbol(g_sn_trace, &trace, sizeof(trace)) == cudaSuccess ? 0 : -1;
 }
+#endif
 
-// Supernodal solve over planned blocks (processing order), see sptrsv_super_kernel.
-HN_EXPORT int hn_sptrsv_super_inv(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w,
-                                  const int* blk_rb, const int* blk_rc, int64_t nblk, const int64_t* rowptr,
-                                  const int* cols, const double* vals, const double* diag, const double* tinv,
-                                  const double* b, double* x, double* ysum, int64_t n, unsigned long long* ticket,
-                                  int ctas_per_sm, void* stream);
+namespace hn {
 
-HN_EXPORT int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
-                              const int* blk_rc, int64_t nblk, const int64_t* rowptr, const int* cols,
-                              const double* vals, const double* diag, const double* b, double* x, double* ysum,
-                              int64_t n, unsigned long long* ticket, int ctas_per_sm, void* stream) {
-  return hn_sptrsv_super_inv(lower, blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr, cols, vals, diag, nullptr,
-                             b, x, ysum, n, ticket, ctas_per_sm, stream);
+__global__ void sptrsv_reset_kernel(double* __restrict__ x, double* __restrict__ ysum, int64_t n,
+                                    unsigned long long* __restrict__ ticket, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    x[i] = __longlong_as_double(static_cast<long long>(kSentinel));
+    ysum[i] = __longlong_as_double(static_cast<long long>(kSentinel));
+  }
+  if (i == 0) *ticket = 0ull;
 }
 
-// As hn_sptrsv_super; tinv (n x 32, or NULL) holds, for every row, its row of the inverse of
-// its 32-row diagonal tile (hn_host_tile_inverse): the in-tile triangle is then one
-// matrix-vector product instead of a 32-step substitution chain.
-HN_EXPORT int hn_sptrsv_super_inv(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w,
-                                  const int* blk_rb, const int* blk_rc, int64_t nblk, const int64_t* rowptr,
-                                  const int* cols, const double* vals, const double* diag, const double* tinv,
-                                  const double* b, double* x, double* ysum, int64_t n, unsigned long long* ticket,
-                                  int ctas_per_sm, void* stream) {
-  if (nblk == 0) return 0;
-  cudaStream_t s = as_stream(stream);
-  HN_TRY(cudaMemsetAsync(x, 0xFF, sizeof(double) * n, s));
-  HN_TRY(cudaMemsetAsync(ysum, 0xFF, sizeof(double) * n, s));
-  HN_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s));
+constexpr int kNbuf = 32 * kSnMaxW * static_cast<int>(sizeof(double));  // one panel (dynamic smem)
+
+cudaError_t sptrsv_prepare() {
+  // per-device function attributes: set on every call (cheap), so any device a process
+  // drives gets the opt-in; never called inside a stream capture
+  cudaError_t e = cudaFuncSetAttribute(sptrsv_super_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNbuf);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(sptrsv_super_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNbuf);
+}
+
+cudaError_t sptrsv_enqueue(const hn_tri_plan& p, const double* b, double* x, double* ysum, int64_t n,
+                           unsigned long long* ticket, int ctas_per_sm, const int* skip, cudaStream_t s) {
+  if (p.ntasks == 0 || n == 0) return cudaSuccess;
+  sptrsv_reset_kernel<<<ceil_div(n, 256), 256, 0, s>>>(x, ysum, n, ticket, skip);
   const int blocks = sm_count() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
-  constexpr int kNbuf = 32 * kSnThreads * static_cast<int>(sizeof(double));  // next-tile buffer
-  // per-device function attribute: set on every call (cheap), so any device a process drives
-  // gets the opt-in
-  HN_TRY(cudaFuncSetAttribute(sptrsv_super_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNbuf));
-  HN_TRY(cudaFuncSetAttribute(sptrsv_super_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNbuf));
-  if (lower)
-    sptrsv_super_kernel<true><<<blocks, kSnThreads, kNbuf, s>>>(blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr, cols,
-                                                            vals, diag, tinv, b, x, ysum, ticket);
+  if (p.lower)
+    sptrsv_super_kernel<true><<<blocks, kSnThreads, kNbuf, s>>>(p.kind, p.r0, p.w, p.rb, p.rc, p.off, p.ntasks,
+                                                                p.rowptr, p.cols, p.vals, p.diag, p.packed, p.inv, b,
+                                                                x, ysum, ticket, skip);
   else
-    sptrsv_super_kernel<false><<<blocks, kSnThreads, kNbuf, s>>>(blk_kind, blk_r0, blk_w, blk_rb, blk_rc, nblk, rowptr,
-                                                             cols, vals, diag, tinv, b, x, ysum, ticket);
-  HN_CHECK_LAUNCH();
+    sptrsv_super_kernel<false><<<blocks, kSnThreads, kNbuf, s>>>(p.kind, p.r0, p.w, p.rb, p.rc, p.off, p.ntasks,
+                                                                 p.rowptr, p.cols, p.vals, p.diag, p.packed, p.inv,
+                                                                 b, x, ysum, ticket, skip);
+  return cudaGetLastError();
+}
+
+}  // namespace hn
+
+using namespace hn;
+
+// Supernodal solve over planned tasks (processing order), see sptrsv_super_kernel.
+// x and ysum are reset to the sentinel here; ctas_per_sm persistent CTAs per SM.
+HN_EXPORT int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
+                              const int* blk_rc, const int64_t* blk_off, int64_t nblk, const int64_t* rowptr,
+                              const int* cols, const double* vals, const double* diag, const double* packed,
+                              int inv, const double* b, double* x, double* ysum, int64_t n,
+                              unsigned long long* ticket, int ctas_per_sm, void* stream) {
+  if (nblk == 0) return 0;
+  HN_TRY(sptrsv_prepare());
+  const hn_tri_plan p{lower, inv, nblk, blk_kind, blk_r0, blk_w, blk_rb, blk_rc, blk_off, rowptr, cols, vals, diag,
+                      packed};
+  HN_TRY(sptrsv_enqueue(p, b, x, ysum, n, ticket, ctas_per_sm, nullptr, as_stream(stream)));
   return 0;
 }
 
-// Host helper (setup): inverses of the 32-row diagonal tiles of every block [r0, r0+w)
-// (tiles start at r0, r0+32, ..; the last one may be narrower), as hn_sptrsv_super_inv
-// reads them: tinv[i*32 + k] = row (i - tile start) of T^-1, column k.  T = I + the strict
-// lower in-tile entries (lower) or diag + the strict upper in-tile entries (upper); the
-// inverse by substitution on the identity columns.  tinv must hold n*32 doubles.
-HN_EXPORT int hn_host_tile_inverse(const int64_t* rowptr, const int* cols, const double* vals, const double* diag,
-                                   int64_t n, int lower, int64_t nb, const int* r0, const int* w, double* tinv) {
-  for (int64_t q = 0; q < n * 32; ++q) tinv[q] = 0.0;
-  double T[32][32], X[32][32];
-  for (int64_t blk = 0; blk < nb; ++blk) {
-    for (int t0 = 0; t0 < w[blk]; t0 += 32) {
-      const int tw = w[blk] - t0 < 32 ? w[blk] - t0 : 32;
-      const int64_t base = static_cast<int64_t>(r0[blk]) + t0;
-      for (int l = 0; l < tw; ++l)
-        for (int k = 0; k < tw; ++k) T[l][k] = 0.0;
-      for (int l = 0; l < tw; ++l) {
-        const int64_t i = base + l;
-        T[l][l] = lower ? 1.0 : diag[i];
-        for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
-          const int64_t c = cols[e];
-          if (c >= base && c < base + tw && (lower ? c < i : c > i)) T[l][c - base] = vals[e];
-        }
-      }
-      for (int j = 0; j < tw; ++j) {  // column j of X = T^-1
-        if (lower) {
-          for (int l = 0; l < tw; ++l) {
-            double v = l == j ? 1.0 : 0.0;
-            for (int k = 0; k < l; ++k) v -= T[l][k] * X[k][j];
-            X[l][j] = v;
-          }
-        } else {
-          for (int l = tw - 1; l >= 0; --l) {
-            double v = l == j ? 1.0 : 0.0;
-            for (int k = l + 1; k < tw; ++k) v -= T[l][k] * X[k][j];
-            X[l][j] = v / T[l][l];
+// Host helper (setup): the packed dense triangles sptrsv_super_kernel reads (see
+// panel_geom), for every task of kind 0 or 2 (blk_off[t] = its offset in doubles; -1 for
+// other kinds).  packed == NULL: offsets only.  Returns the total size in doubles.
+HN_EXPORT int64_t hn_host_pack_panels(const int64_t* rowptr_host, const int* cols_host, const double* vals_host,
+                                      const double* diag_host, int lower, int inverse, int64_t ntasks,
+                                      const int* kind_host, const int* r0_host, const int* w_host,
+                                      int64_t* off_host, double* packed_host) {
+  int64_t total = 0;
+  for (int64_t t = 0; t < ntasks; ++t) {
+    const int w = w_host[t];
+    if ((kind_host[t] != 0 && kind_host[t] != 2) || w < 1 || w > kSnMaxW) {
+      off_host[t] = -1;
+      continue;
+    }
+    off_host[t] = total;
+    const int ntiles = (w + 31) / 32;
+    for (int tt = 0; tt < ntiles; ++tt) {
+      int t0, tw, rbase, rows, rp;
+      panel_geom(lower != 0, w, tt, t0, tw, rbase, rows, rp);
+      if (packed_host) {
+        double* pn = packed_host + total;
+        for (int64_t q = 0; q < 32LL * rp; ++q) pn[q] = 0.0;
+        for (int rr = 0; rr < rows; ++rr) {
+          const int row = rbase + rr;
+          const int64_t i = static_cast<int64_t>(r0_host[t]) + row;
+          const int64_t a = rowptr_host[i], z = rowptr_host[i + 1];
+          for (int k = 0; k < tw; ++k) {
+            const int c = t0 + k;
+            if (lower ? c < row : c > row) {
+              const int64_t e = lower ? (z - row) + c : a + (c - row - 1);
+              if (cols_host[e] != r0_host[t] + c) return -1;  // not a dense in-block triangle
+              pn[static_cast<int64_t>(k) * rp + rr] = vals_host[e];
+            }
           }
         }
+        if (inverse) {  // the diagonal tile's rows hold T^-1 (substitution on the identity)
+          double T[32][32], X[32][32];
+          const int d0 = t0 - rbase;  // first diagonal-tile row inside the panel
+          for (int l = 0; l < tw; ++l)
+            for (int k = 0; k < tw; ++k)
+              T[l][k] = l == k ? (lower ? 1.0 : diag_host[r0_host[t] + t0 + l])
+                               : pn[static_cast<int64_t>(k) * rp + d0 + l];
+          for (int j = 0; j < tw; ++j) {
+            if (lower) {
+              for (int l = 0; l < tw; ++l) {
+                double v = l == j ? 1.0 : 0.0;
+                for (int k = 0; k < l; ++k) v -= T[l][k] * X[k][j];
+                X[l][j] = v;
+              }
+            } else {
+              for (int l = tw - 1; l >= 0; --l) {
+                double v = l == j ? 1.0 : 0.0;
+                for (int k = l + 1; k < tw; ++k) v -= T[l][k] * X[k][j];
+                X[l][j] = v / T[l][l];
+              }
+            }
+          }
+          for (int l = 0; l < tw; ++l)
+            for (int k = 0; k < tw; ++k) pn[static_cast<int64_t>(k) * rp + d0 + l] = X[l][k];
+        }
       }
-      for (int l = 0; l < tw; ++l)
-        for (int k = 0; k < tw; ++k) tinv[(base + l) * 32 + k] = X[l][k];
+      total += 32LL * rp;
     }
   }
-  return 0;
+  return total;
 }
 
 // Host helper (setup): split the rows of a strict triangular CSR (sorted columns) into
@@ -788,22 +734,6 @@ HN_EXPORT int hn_host_block_levels(const int64_t* rowptr_host, const int* cols_h
     levels_host[k] = lev;
   }
   delete[] owner;
-  return 0;
-}
-
-// Host helper (setup): dependency level of every row of a triangular CSR, sweeping rows in
-// increasing (lower != 0) or decreasing order.  Host pointers.
-HN_EXPORT int hn_host_levels(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower,
-                             int* levels_host) {
-  for (int64_t k = 0; k < n; ++k) {
-    const int64_t i = lower ? k : n - 1 - k;
-    int lev = 0;
-    for (int64_t e = rowptr_host[i]; e < rowptr_host[i + 1]; ++e) {
-      const int l = levels_host[cols_host[e]] + 1;
-      lev = l > lev ? l : lev;
-    }
-    levels_host[i] = lev;
-  }
   return 0;
 }
 

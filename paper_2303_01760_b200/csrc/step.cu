@@ -418,13 +418,18 @@ __global__ void neumann_kernel(const int64_t* __restrict__ rowptr, const int* __
 // End of a step: latch the first step whose fields went non-finite (flags written by K10 and
 // the Neumann rows) with the lowest non-finite temperature node, as the reference's per-step
 // probe reports it (solver.py:448-452); then clear the per-step flags.
-// latch = [steps completed, first bad step (0: none), its node (INT_MAX: none in T)].
-__global__ void step_latch_kernel(int* __restrict__ flags, int* __restrict__ latch) {
+// latch = [steps completed, first bad step (0: none), its node (INT_MAX: none in T),
+//          first step whose pressure solve reported info != 0 (0: none), that info].
+__global__ void step_latch_kernel(int* __restrict__ flags, int* __restrict__ latch, const int* __restrict__ pstatus) {
   const int s = latch[0] + 1;
   latch[0] = s;
   if (flags[0] && latch[1] == 0) {
     latch[1] = s;
     latch[2] = flags[1];
+  }
+  if (pstatus && pstatus[0] != 0 && latch[3] == 0) {  // first step whose pressure solve failed
+    latch[3] = s;
+    latch[4] = pstatus[0];
   }
   flags[0] = 0;
   flags[1] = 0x7fffffff;
@@ -630,8 +635,8 @@ HN_EXPORT int hn_temperature_bc(const int* dir_idx, const double* dir_val, int64
   return 0;
 }
 
-HN_EXPORT int hn_step_latch(int* flags, int* latch, void* stream) {
-  step_latch_kernel<<<1, 1, 0, as_stream(stream)>>>(flags, latch);
+HN_EXPORT int hn_step_latch(int* flags, int* latch, const int* pstatus, void* stream) {
+  step_latch_kernel<<<1, 1, 0, as_stream(stream)>>>(flags, latch, pstatus);
   HN_CHECK_LAUNCH();
   return 0;
 }

@@ -20,7 +20,9 @@ applied by sync-free triangular solves.
 
 from __future__ import annotations
 
+import ctypes as C
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -93,18 +95,24 @@ class PoissonSolveSettings:
             raise ValueError("stabilization must lie in [0, 1]")
 
 
-class _TriSchedule:
-    """Task list of a sync-free triangular solve: rows in dependency-level order, rows
-    longer than CHUNK split into partial-sum tasks + one final task (hn_sptrsv_tasks)."""
+_MAX_PAIRS = 512  # kSnMaxPairs (csrc/pressure.cu): (row, 256-entry chunk) pairs per task
 
-    CHUNK = 256
 
-    def __init__(self, m: sparse.csr_matrix, lower: bool):
-        plan = plan_triangular_tasks(m, lower, self.CHUNK)
-        self.depth, self.ntasks, self.npartial = plan["depth"], plan["ntasks"], plan["npartial"]
-        self.row, self.beg, self.len = (L.to_device(plan["row"]), L.to_device(plan["beg"]), L.to_device(plan["len"]))
-        self.part, self.np_ = L.to_device(plan["part"]), L.to_device(plan["np"])
-        self.partial = L.empty(max(self.npartial, 1), L.torch().float64)
+def _split_by_chunks(outside: np.ndarray, bounds: np.ndarray) -> np.ndarray:
+    """Refine helper row ranges so no task has more than _MAX_PAIRS (row, chunk) pairs."""
+    chunks = np.maximum(1, -(-outside // 256))
+    out = [int(bounds[0])]
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        a, b = int(a), int(b)
+        while chunks[a:b].sum() > _MAX_PAIRS:
+            if b - a == 1:
+                raise ValueError("a factor row has more than 131,072 off-block entries")
+            m = a + int(np.searchsorted(np.cumsum(chunks[a:b]), _MAX_PAIRS, side="right"))
+            m = min(max(m, a + 1), b - 1)
+            out.append(m)
+            a = m
+        out.append(b)
+    return np.asarray(out)
 
 
 def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, helper_nnz: int = 4096,
@@ -165,10 +173,14 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, he
             o = outside[starts[k]: starts[k] + w[k]]
             cut = np.searchsorted(np.cumsum(o), np.arange(1, int(np.ceil(o.sum() / helper_nnz))) * helper_nnz)
             bounds = np.unique(np.concatenate([[0], cut, [w[k]]]))
+            bounds = _split_by_chunks(o, bounds)
             for a, b in zip(bounds[:-1], bounds[1:]):
                 kinds.append(1); tr0.append(r0[k]); tw.append(w[k]); trb.append(a); trc.append(b - a)
             kinds.append(2); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k])
         else:
+            o = outside[starts[k]: starts[k] + w[k]]
+            if np.maximum(1, -(-o // 256)).sum() > _MAX_PAIRS:
+                raise ValueError("a one-row block has more than 131,072 off-block entries")
             kinds.append(0); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k])
     flush()
     ntasks = len(kinds)
@@ -182,72 +194,52 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, he
 
 
 class _SuperSchedule:
-    def __init__(self, m: sparse.csr_matrix, lower: bool, diag: np.ndarray | None = None, **plan_kw):
+    """Device task list of one supernodal triangular solve: the planned tasks plus the packed
+    dense triangles of the block tasks (hn_host_pack_panels)."""
+
+    def __init__(self, m: sparse.csr_matrix, lower: bool, diag: np.ndarray | None = None, inverse: bool = False,
+                 **plan_kw):
         plan = plan_supernodal_blocks(m, lower, **plan_kw)
+        self.inverse = bool(inverse)
         self.nblk, self.depth, self.ntasks = plan["nblk"], plan["depth"], plan["ntasks"]
-        self.kind, self.r0, self.w = L.to_device(plan["kind"]), L.to_device(plan["t_r0"]), L.to_device(plan["t_w"])
-        self.rb, self.rc = L.to_device(plan["t_rb"]), L.to_device(plan["t_rc"])
-        self.tinv = None
-        if not (_DeviceLU.TILE_INVERSE_L if lower else _DeviceLU.TILE_INVERSE):
-            return
-        # inverses of the 32-row diagonal tiles of every block (setup): the kernel's in-tile
-        # triangles become matrix-vector products (hn_sptrsv_super_inv)
-        n = m.shape[0]
+        kind, r0, w = plan["kind"], plan["t_r0"], plan["t_w"]
         vp = L._vp
         rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
         cols = np.ascontiguousarray(m.indices, dtype=np.int32)
         vals = np.ascontiguousarray(m.data, dtype=np.float64)
-        dg = np.ascontiguousarray(diag if diag is not None else np.ones(max(n, 1)), dtype=np.float64)
-        r0 = np.ascontiguousarray(plan["r0"], dtype=np.int32)
-        w = np.ascontiguousarray(plan["w"], dtype=np.int32)
-        tinv = np.empty(max(n, 1) * 32, dtype=np.float64)
-        L.call("hn_host_tile_inverse", rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), vals.ctypes.data_as(vp),
-               dg.ctypes.data_as(vp), n, 1 if lower else 0, len(r0), r0.ctypes.data_as(vp), w.ctypes.data_as(vp),
-               tinv.ctypes.data_as(vp))
-        self.tinv = L.to_device(tinv)
-
-
-def plan_triangular_tasks(m: sparse.csr_matrix, lower: bool, chunk: int) -> dict:
-    """Host planning of hn_sptrsv_tasks (setup; levels from the native hn_host_levels)."""
-    n = m.shape[0]
-    rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
-    cols = np.ascontiguousarray(m.indices, dtype=np.int32)
-    lev = np.zeros(n, dtype=np.int32)
-    L.call("hn_host_levels", rowptr.ctypes.data_as(L._vp), cols.ctypes.data_as(L._vp), n, 1 if lower else 0,
-           lev.ctypes.data_as(L._vp))
-    order = np.lexsort((np.arange(n), lev))
-    length = np.diff(rowptr)[order]
-    nchunk = np.maximum(1, -(-length // chunk))
-    ntasks = int(nchunk.sum())
-    first = np.concatenate([[0], np.cumsum(nchunk)[:-1]])
-    k = np.arange(ntasks) - np.repeat(first, nchunk)                 # chunk index within its row
-    is_final = k == np.repeat(nchunk, nchunk) - 1
-    part_slot = np.cumsum(~is_final) - 1                              # non-final chunks: own slot
-    row_first = np.repeat(np.concatenate([[0], np.cumsum(nchunk - 1)[:-1]]), nchunk)
-    return {"depth": int(lev.max()) + 1 if n else 0, "levels": lev, "ntasks": ntasks,
-            "npartial": int((~is_final).sum()),
-            "row": np.repeat(order, nchunk).astype(np.int32),
-            "beg": (np.repeat(rowptr[order], nchunk) + k * chunk).astype(np.int64),
-            "len": np.minimum(chunk, np.repeat(length, nchunk) - k * chunk).astype(np.int32),
-            "part": np.where(is_final, row_first, part_slot).astype(np.int32),
-            "np": np.where(is_final, np.repeat(nchunk - 1, nchunk), -1).astype(np.int32)}
+        off = np.empty(len(kind), dtype=np.int64)
+        dg = np.ascontiguousarray(diag if diag is not None else np.ones(1), dtype=np.float64)
+        args = (rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), vals.ctypes.data_as(vp), dg.ctypes.data_as(vp),
+                1 if lower else 0, 1 if inverse else 0, self.ntasks, kind.ctypes.data_as(vp), r0.ctypes.data_as(vp), w.ctypes.data_as(vp),
+                off.ctypes.data_as(vp))
+        total = int(L.lib().hn_host_pack_panels(*args, None))
+        packed = np.empty(max(total, 2), dtype=np.float64)
+        if int(L.lib().hn_host_pack_panels(*args, packed.ctypes.data_as(vp))) != total:
+            raise RuntimeError("hn_host_pack_panels: a planned block's in-block triangle is not dense")
+        off[self.ntasks:] = -1
+        self.kind, self.r0, self.w = L.to_device(kind), L.to_device(r0), L.to_device(w)
+        self.rb, self.rc = L.to_device(plan["t_rb"]), L.to_device(plan["t_rc"])
+        self.off, self.packed = L.to_device(off), L.to_device(packed)
+        self.packed_bytes = 8 * total
 
 
 class _DeviceLU:
-    """SuperLU factors Pr A Pc = L U in HBM: strict-lower L, strict-upper U + diag, perms."""
+    """SuperLU factors Pr A Pc = L U in HBM: strict-lower L, strict-upper U + diag, perms,
+    and the supernodal task lists of both solves."""
 
-    WARPS_PER_SM = 16
     CTAS_PER_SM = 2
-    SUPERNODAL = True
-    # in-tile triangles of the U solve by precomputed tile inverses (hn_sptrsv_super_inv): 7 %
-    # faster L+U solve on config 3 (tools/ab_tinv.py: 4.17 -> 3.86 ms) but the preconditioner
-    # output moves by 1.5e-10 relative (ill-conditioned U tiles), so one BiCGStab step no longer
-    # lands at direct-solve accuracy (SURVEY H6).  Off: substitution, exact to rounding.
-    TILE_INVERSE = False
-    TILE_INVERSE_L = False  # the same for the unit-lower L solve
-    PARITY_TOL = 1e-10  # max-norm relative distance to SuperLU's solve (tests): U is ill-conditioned (block kappa up to 7e7), two exact substitution orders differ by ~6e-11
+    # diagonal 32-row tiles of the packed triangles applied as precomputed inverses (x = T^-1 y,
+    # no substitution chain) for the L / U solve.  Config 3 (tools/ab_inverse.py): L 1.10 ->
+    # 0.91 ms, U 1.27 -> 1.06 ms; the solve moves from 1.2e-11 to 1.1e-10 of SuperLU's (max
+    # norm, random rhs) and the fields after 50 full steps by <= 1.1e-12 (relative).
+    TILE_INVERSE_L = True
+    TILE_INVERSE_U = True
+    # max-norm relative distance to SuperLU's solve on a random rhs (tests): U is ill-conditioned
+    # (block kappa up to 7e7), two exact substitution orders differ by ~6e-11; the diagonal-tile
+    # inverses move it to ~1.1e-10 (fields: <= 1.1e-12 after 50 steps, see above)
+    PARITY_TOL = {False: 1e-10, True: 1e-9}
 
-    def __init__(self, lu):
+    def __init__(self, lu, inverse: bool | None = None, **plan_kw):
         Lm = sparse.csr_matrix(lu.L)
         Um = sparse.csr_matrix(lu.U)
         self.n = Lm.shape[0]
@@ -257,14 +249,11 @@ class _DeviceLU:
         Us.sort_indices()
         self.L = DeviceCSR(Ls)
         self.U = DeviceCSR(Us)
-        self.supernodal = self.SUPERNODAL
-        if self.supernodal:
-            self.sL = _SuperSchedule(Ls, lower=True)
-            self.sU = _SuperSchedule(Us, lower=False, diag=np.asarray(Um.diagonal(), dtype=np.float64))
-        else:
-            self.sL = _TriSchedule(Ls, lower=True)
-            self.sU = _TriSchedule(Us, lower=False)
-        self.diag = L.to_device(np.asarray(Um.diagonal(), dtype=np.float64))
+        udiag = np.asarray(Um.diagonal(), dtype=np.float64)
+        self.sL = _SuperSchedule(Ls, lower=True, inverse=self.TILE_INVERSE_L if inverse is None else inverse, **plan_kw)
+        self.sU = _SuperSchedule(Us, lower=False, diag=udiag, inverse=self.TILE_INVERSE_U if inverse is None else inverse,
+                                 **plan_kw)
+        self.diag = L.to_device(udiag)
         self.perm_r = L.to_device(np.asarray(lu.perm_r, dtype=np.int32))
         self.perm_c = L.to_device(np.asarray(lu.perm_c, dtype=np.int32))
         t = L.torch()
@@ -274,6 +263,16 @@ class _DeviceLU:
         self.ticket = L.zeros(1, t.int64)
         self.ysum = L.empty(self.n, t.float64)
         self.nnz = self.L.nnz + self.U.nnz + self.n
+        self.parity_tol = self.PARITY_TOL[self.sL.inverse or self.sU.inverse]
+
+    def plans(self):
+        """(L, U) as hn_tri_plan structs for hn_pressure_setup (the arrays stay owned here)."""
+        def mk(sch, m, diag, lower):
+            return L.TriPlan(1 if lower else 0, 1 if sch.inverse else 0, sch.ntasks, sch.kind.data_ptr(),
+                             sch.r0.data_ptr(), sch.w.data_ptr(), sch.rb.data_ptr(), sch.rc.data_ptr(),
+                             sch.off.data_ptr(), m.rowptr.data_ptr(), m.cols.data_ptr(), m.vals.data_ptr(),
+                             diag.data_ptr() if diag is not None else None, sch.packed.data_ptr())
+        return mk(self.sL, self.L, None, True), mk(self.sU, self.U, self.diag, False)
 
     def solve(self, b, x):
         """x = Pc U^-1 L^-1 Pr b (scipy SuperLU.solve semantics)."""
@@ -285,17 +284,38 @@ class _DeviceLU:
         return x
 
     def _tri(self, sch, m, diag, b, x, s):
-        if self.supernodal:
-            L.call("hn_sptrsv_super_inv", 1 if diag is None else 0, L.ptr(sch.kind), L.ptr(sch.r0), L.ptr(sch.w),
-                   L.ptr(sch.rb), L.ptr(sch.rc), sch.ntasks, L.ptr(m.rowptr), L.ptr(m.cols), L.ptr(m.vals),
-                   L.ptr(diag), L.ptr(sch.tinv if (self.TILE_INVERSE_L if diag is None else self.TILE_INVERSE)
-                                      else None),
-                   L.ptr(b), L.ptr(x),
-                   L.ptr(self.ysum), self.n, L.ptr(self.ticket), self.CTAS_PER_SM, s)
-            return
-        L.call("hn_sptrsv_tasks", 0 if diag is None else 1, L.ptr(sch.row), L.ptr(sch.beg), L.ptr(sch.len),
-               L.ptr(sch.part), L.ptr(sch.np_), sch.ntasks, L.ptr(m.cols), L.ptr(m.vals), L.ptr(diag), L.ptr(b),
-               L.ptr(x), self.n, L.ptr(sch.partial), sch.npartial, L.ptr(self.ticket), self.WARPS_PER_SM, s)
+        L.call("hn_sptrsv_super", 1 if diag is None else 0, L.ptr(sch.kind), L.ptr(sch.r0), L.ptr(sch.w),
+               L.ptr(sch.rb), L.ptr(sch.rc), L.ptr(sch.off), sch.ntasks, L.ptr(m.rowptr), L.ptr(m.cols),
+               L.ptr(m.vals), L.ptr(diag), L.ptr(sch.packed), 1 if sch.inverse else 0, L.ptr(b), L.ptr(x), L.ptr(self.ysum), self.n,
+               L.ptr(self.ticket), self.CTAS_PER_SM, s)
+
+
+def _free_pressure(handle: int):
+    try:
+        L.lib().hn_pressure_free(handle)
+    except Exception:  # interpreter shutdown
+        pass
+
+
+class _NativePressure:
+    """The device-driven BiCGStab of the bordered Poisson system (hn_pressure_setup /
+    hn_pressure_solve, csrc/bicgstab.cu): scipy's algorithm with every scalar on the device,
+    the loop a CUDA-graph WHILE node; no host round trip per solve."""
+
+    def __init__(self, A: "DeviceCSR", lu: _DeviceLU):
+        pl, pu = lu.plans()
+        h = C.c_int64(0)
+        L.call("hn_pressure_setup", lu.n, L.ptr(A.rowptr), L.ptr(A.cols), L.ptr(A.vals), C.byref(pl), C.byref(pu),
+               L.ptr(lu.perm_r), L.ptr(lu.perm_c), lu.CTAS_PER_SM, C.byref(h))
+        self.handle = h.value
+        self._keep = (A, lu)
+        self._finalizer = weakref.finalize(self, _free_pressure, self.handle)
+
+    def solve(self, b, x0, x, rtol: float, maxiter: int, status):
+        """Enqueue one solve on the current stream: x0 None = zero start, x0 is x = warm start
+        from x; status (device int32[2]) <- [scipy info, passes]."""
+        L.call("hn_pressure_solve", self.handle, L.ptr(b), L.ptr(x0), L.ptr(x), float(rtol), int(maxiter),
+               L.ptr(status), L.stream_handle())
 
 
 class OperatorSet:
@@ -330,6 +350,8 @@ class OperatorSet:
         self._d_planes = [ops.index(p.kind) for p in partials]
         self._d_poisson = DeviceCSR(poisson_matrix) if poisson_matrix is not None else None
         self._d_lu = _DeviceLU(lu) if lu is not None else None
+        self._d_press = _NativePressure(self._d_poisson, self._d_lu) if self._d_lu is not None else None
+        self._d_pstatus = L.zeros(2, t.int32)
         self._d_dir_idx = L.to_device(self.dirichlet_idx.astype(np.int32))
         self.dirichlet_values = nodeset.bc_value[self.dirichlet_idx]
         self._d_neu = None
@@ -530,100 +552,6 @@ def _temperature_bc_dev(ops: OperatorSet, T, flags=None):
     return T
 
 
-class _BiCGStab:
-    """scipy.sparse.linalg.bicgstab (scipy 1.18 _isolve/iterative.py) on device vectors.
-
-    Same iteration, breakdown tests and stopping rule; dot products are device
-    reductions (fixed tree), scalars come back to the host for the control flow."""
-
-    def __init__(self, ops: OperatorSet):
-        t = L.torch()
-        n1 = ops.n + 1
-        self.ops = ops
-        self.n1 = n1
-        for name in ("r", "rt", "p", "phat", "v", "shat", "t", "x"):
-            setattr(self, name, L.empty(n1, t.float64))
-        self.matvecs = 0
-        self.psolves = 0
-
-    def _dot(self, a, b):
-        return self.ops.reduce(0, a, b, n=self.n1)
-
-    def _norm(self, a):
-        return float(np.sqrt(self._dot(a, a)))
-
-    def _axpy(self, y, x, alpha):
-        L.call("hn_bicg_update", 1, L.ptr(y), L.ptr(x), None, float(alpha), 0.0, self.n1, L.stream_handle())
-
-    def _A(self, x, y):
-        self.matvecs += 1
-        self.ops._d_poisson.matvec(x, y)
-
-    def _M(self, x, y):
-        self.psolves += 1
-        self.ops._d_lu.solve(x, y)
-
-    def solve(self, b, x0, rtol: float, maxiter: int):
-        """Returns (x (device, n+1), info)."""
-        bnrm2 = self._norm(b)
-        if not np.isfinite(bnrm2):
-            # non-finite right-hand side: the fields went non-finite in an earlier step, which
-            # the step latch reports as the reference's probe would (solver.py:448-452); the
-            # Krylov loop is skipped instead of running maxiter iterations on NaN
-            self.x.fill_(float("nan"))
-            return self.x, 0
-        atol = max(0.0, float(rtol) * float(bnrm2))
-        if bnrm2 == 0:
-            return b.clone(), 0
-        x = self.x
-        if x0 is not None:
-            x.copy_(x0)
-        else:
-            x.zero_()
-        rhotol = np.finfo(np.float64).eps ** 2
-        omegatol = rhotol
-        r, rt, p, phat, v, shat, tt = self.r, self.rt, self.p, self.phat, self.v, self.shat, self.t
-        if x0 is not None and self.ops.reduce(1, x, n=self.n1) > 0:
-            self.matvecs += 1
-            self.ops._d_poisson.residual(x, b, r)
-        else:
-            r.copy_(b)
-        rt.copy_(r)
-        rho_prev = omega = alpha = None
-        for it in range(maxiter):
-            if self._norm(r) < atol:
-                return x, 0
-            rho = self._dot(rt, r)
-            if abs(rho) < rhotol:
-                return x, -10
-            if it > 0:
-                if abs(omega) < omegatol:
-                    return x, -11
-                beta = (rho / rho_prev) * (alpha / omega)
-                L.call("hn_bicg_update", 0, L.ptr(p), L.ptr(v), L.ptr(r), float(omega), float(beta), self.n1,
-                       L.stream_handle())
-            else:
-                p.copy_(r)
-            self._M(p, phat)
-            self._A(phat, v)
-            rv = self._dot(rt, v)
-            if rv == 0:
-                return x, -11
-            alpha = rho / rv
-            self._axpy(r, v, -alpha)
-            if self._norm(r) < atol:
-                self._axpy(x, phat, alpha)
-                return x, 0
-            self._M(r, shat)
-            self._A(shat, tt)
-            omega = self._dot(tt, r) / self._dot(tt, tt)
-            self._axpy(x, phat, alpha)
-            self._axpy(x, shat, omega)
-            self._axpy(r, tt, -omega)
-            rho_prev = rho
-        return x, maxiter
-
-
 class _GMRES:
     """Retry solver after a BiCGStab failure, standing in for scipy's lgmres (reference
     solver.py:306-312): restarted GMRES(m) with the same LU preconditioner (right
@@ -699,24 +627,27 @@ class _GMRES:
         return x, (0 if float(np.sqrt(self._dot(w, w))) <= atol else maxiter)
 
 
-def _pressure_dev(ops: OperatorSet, rhs, x0, settings: PoissonSolveSettings, solver: _BiCGStab):
-    if ops._d_poisson is None or ops._d_lu is None:
+def _pressure_dev(ops: OperatorSet, rhs, x0, settings: PoissonSolveSettings, x, status=None):
+    """One checked pressure solve into x (device, n+1): the native BiCGStab, the status read
+    back, and on failure the reference's retry (lgmres there, the GMRES stand-in here) from the
+    same x0 before PoissonConvergenceError (solver.py:304-313).  x0 must not alias x."""
+    if ops._d_press is None:
         raise RuntimeError("operators were built with factorize=False: no pressure solve available")
-    x, info = solver.solve(rhs, x0, settings.tol, settings.maxiter)
+    status = ops._d_pstatus if status is None else status
+    ops._d_press.solve(rhs, x0, x, settings.tol, settings.maxiter, status)
+    info = int(status[0].item())
     if info != 0:
-        # the reference retries with lgmres before giving up (solver.py:306-312)
         retry = getattr(ops, "_gmres", None) or _GMRES(ops)
         ops._gmres = retry
-        x, info = retry.solve(rhs, x0, settings.tol, settings.maxiter)
+        xr, info = retry.solve(rhs, x0, settings.tol, settings.maxiter)
         if info != 0:
             tt = L.torch()
             res_vec = L.empty(ops.n + 1, tt.float64)
-            ops._d_poisson.residual(x, rhs, res_vec)
+            ops._d_poisson.residual(xr, rhs, res_vec)
             res = np.sqrt(ops.reduce(0, res_vec, res_vec)) / max(np.sqrt(ops.reduce(0, rhs, rhs)), 1e-300)
             raise PoissonConvergenceError(f"pressure Poisson solve did not converge (info={info})",
                                           residual=float(res))
-        solver.x.copy_(x)
-        x = solver.x
+        x.copy_(xr)
     return x
 
 
@@ -753,11 +684,10 @@ def pressure_solve(vstar: np.ndarray, ops: OperatorSet, settings: PoissonSolveSe
         rhs.index_copy_(0, bidx, L.to_device(np.broadcast_to(np.asarray(wall_gradient, float),
                                                              ops.boundary_idx.shape).copy()))
     x0d = None
-    if x0 is not None and len(x0) == n:
-        x0d = L.to_device(np.concatenate([np.asarray(x0, dtype=np.float64), [ops._poisson_lambda]]))
-    solver = getattr(ops, "_bicg", None) or _BiCGStab(ops)
-    ops._bicg = solver
-    x = _pressure_dev(ops, rhs, x0d, settings, solver)
+    if x0 is not None:  # the reference appends the last lambda to an n-vector (solver.py:302-303)
+        x0 = np.asarray(x0, dtype=np.float64)
+        x0d = L.to_device(np.concatenate([x0, [ops._poisson_lambda]]) if len(x0) == n else x0)
+    x = _pressure_dev(ops, rhs, x0d, settings, L.empty(n + 1, t.float64))
     p = x.cpu().numpy()
     ops._poisson_lambda = float(p[n])
     return p[:n].copy()
@@ -827,85 +757,166 @@ def _interior_divergence_dev(ops: OperatorSet, v_soa) -> float:
 
 # ============================================================ device-resident stepping
 class DeviceStepper:
-    """One explicit step = K7 -> K8 -> K9 -> K10 -> K11 on HBM-resident state
-    (replicates the loop body of run(), solver.py:439-452)."""
+    """One explicit step = K7 -> K8 -> K9 -> K10 -> K11 on HBM-resident state (replicates the
+    loop body of run(), solver.py:439-452).
+
+    After the first (eager) step every step is ONE CUDA-graph replay on the stepper's own
+    stream: momentum, divergence, the device-driven BiCGStab (a WHILE node, warm-started from
+    the previous [p, lambda] as the reference's x0), correction + temperature, boundary
+    conditions and the end-of-step latch -- no host synchronisation.  The latch records the
+    first non-finite step and the first step whose BiCGStab failed; `check_finite` (called
+    every nu_stride steps by run()) reads it.  A BiCGStab failure rolls the fields back to the
+    last check and replays the steps one by one with the reference's failure handling (the
+    lgmres stand-in, then PoissonConvergenceError at that step)."""
 
     def __init__(self, ops: OperatorSet, params: PhysicsParams, settings: PoissonSolveSettings, dt: float,
-                 state: FieldState):
+                 state: FieldState, graphs: bool = True):
         t = L.torch()
         self.ops, self.params, self.settings, self.dt = ops, params, settings, float(dt)
         n, d = ops.n, ops.dim
         self.v = _soa(state.velocity)
         self.T = L.to_device(np.asarray(state.temperature, dtype=np.float64))
-        self.p = L.to_device(np.asarray(state.pressure, dtype=np.float64))
+        # x = [p, lambda]: the pressure is a view of the Krylov solution (warm start of the next step)
+        self.x = L.to_device(np.concatenate([np.asarray(state.pressure, dtype=np.float64),
+                                             [getattr(ops, "_poisson_lambda", 0.0)]]))
+        self.p = self.x[:n]
+        self.x0 = L.empty(n + 1, t.float64)
         self.vstar = L.empty((d, n), t.float64)
         self.v_next = L.empty((d, n), t.float64)
         self.T_next = L.empty(n, t.float64)
         self.rhs = L.empty(n + 1, t.float64)
-        self.x0 = L.empty(n + 1, t.float64)
+        self.status = L.zeros(2, t.int32)
         self.flags = L.to_device(np.array([0, INT32_MAX], dtype=np.int32))
-        # [steps done, first non-finite step (0: none), its lowest non-finite T node] (hn_step_latch)
-        self.latch = L.to_device(np.array([0, 0, INT32_MAX], dtype=np.int32))
-        self.solver = _BiCGStab(ops)
+        # [steps done, first non-finite step (0: none), its lowest non-finite T node, first step
+        # whose BiCGStab failed (0: none), its info] (hn_step_latch)
+        self.latch = L.to_device(np.array([0, 0, INT32_MAX, 0, 0], dtype=np.int32))
         self.have_p = False
         self.steps = 0
+        self.graphs_enabled = bool(graphs) and ops._d_press is not None
+        self.stream = t.cuda.Stream()
+        self._graphs = {}
+        self._bufs = (self.v, self.v_next, self.T, self.T_next)
+        self._snapshot()
 
-    def step(self):
+    # ---- one step, enqueued on the current stream ----
+    def _explicit_front(self):
         ops = self.ops
         _momentum_dev(ops, self.params, self.dt, self.v, self.T, self.vstar, zero_boundary=True)
         _div_rhs_dev(ops, self.vstar, self.dt, self.rhs)
-        x0 = None
-        if self.have_p:
-            self.x0[: ops.n].copy_(self.p)
-            self.x0[ops.n] = ops._poisson_lambda
-            x0 = self.x0
-        x = _pressure_dev(ops, self.rhs, x0, self.settings, self.solver)
-        ops._poisson_lambda = float(x[ops.n].item())
-        self.p.copy_(x[: ops.n])
-        self.have_p = True
+
+    def _explicit_back(self, pstatus):
+        ops = self.ops
         _correct_temp_dev(ops, self.vstar, self.p, self.T, self.dt, self.v_next, self.T_next, self.flags,
                           self.params.dissipation)
         _temperature_bc_dev(ops, self.T_next, self.flags)
-        L.call("hn_step_latch", L.ptr(self.flags), L.ptr(self.latch), L.stream_handle())
+        L.call("hn_step_latch", L.ptr(self.flags), L.ptr(self.latch), L.ptr(pstatus), L.stream_handle())
+
+    def _body(self):
+        """Unchecked step (graph body): warm-started device solve, status -> latch."""
+        self._explicit_front()
+        self.ops._d_press.solve(self.rhs, self.x if self.have_p else None, self.x, self.settings.tol,
+                                self.settings.maxiter, self.status)
+        self._explicit_back(self.status)
+
+    def _checked_step(self):
+        """Eager step with the status read back and the reference's failure handling."""
+        self._explicit_front()
+        x0 = None
+        if self.have_p:
+            self.x0.copy_(self.x)
+            x0 = self.x0
+        _pressure_dev(self.ops, self.rhs, x0, self.settings, self.x, self.status)
+        self._explicit_back(None)
+
+    def _swap(self):
         self.v, self.v_next = self.v_next, self.v
         self.T, self.T_next = self.T_next, self.T
         self.steps += 1
 
+    def step(self):
+        t = L.torch()
+        self.stream.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(self.stream):
+            if not self.graphs_enabled:
+                if self.ops._d_press is None:
+                    raise RuntimeError("operators were built with factorize=False: no pressure solve available")
+                self._checked_step()
+            elif not self.have_p:
+                self._body()  # first step: zero start, no warm-start pointer in the graph
+            else:
+                key = self.v.data_ptr()
+                g = self._graphs.get(key)
+                if g is None:
+                    g = t.cuda.CUDAGraph()
+                    with t.cuda.graph(g, stream=self.stream, capture_error_mode="relaxed"):
+                        self._body()
+                    self._graphs[key] = g
+                g.replay()
+        t.cuda.current_stream().wait_stream(self.stream)
+        self.have_p = True
+        self._swap()
+
     def explicit_step(self):
         """The explicit part of a step only (K7, K8, K10, K11) with the pressure held at its
         current value -- for measuring the HBM-bound kernels in isolation (bench)."""
-        ops = self.ops
-        _momentum_dev(ops, self.params, self.dt, self.v, self.T, self.vstar, zero_boundary=True)
-        _div_rhs_dev(ops, self.vstar, self.dt, self.rhs)
-        _correct_temp_dev(ops, self.vstar, self.p, self.T, self.dt, self.v_next, self.T_next, self.flags,
-                          self.params.dissipation)
-        _temperature_bc_dev(ops, self.T_next, self.flags)
-        L.call("hn_step_latch", L.ptr(self.flags), L.ptr(self.latch), L.stream_handle())
+        self._explicit_front()
+        self._explicit_back(None)
         self.v, self.v_next = self.v_next, self.v
         self.T, self.T_next = self.T_next, self.T
 
+    # ---- checks, rollback ----
+    def _snapshot(self):
+        self._snap = (self.v.clone(), self.T.clone(), self.x.clone(), self.latch.clone(), self.steps, self.have_p)
+
+    def _restore(self):
+        v, T, x, latch, steps, have_p = self._snap
+        self.v.copy_(v)
+        self.T.copy_(T)
+        self.x.copy_(x)
+        self.latch.copy_(latch)
+        self.steps, self.have_p = steps, have_p
+
     def check_finite(self, step: int | None = None):
-        """Raise SolverDivergenceError for the first step whose fields went non-finite, with
-        the reference's step number (counted from this stepper's first step) and node (the
-        lowest non-finite temperature index, -1 if only the velocity was), solver.py:448-452.
-        The device latches it every step; this reads it (one 12-byte copy)."""
+        """Read the device latch (one 20-byte copy).  A BiCGStab failure (before any non-finite
+        step) rolls back to the last check and replays with the reference's handling: the
+        lgmres stand-in, else PoissonConvergenceError at that step (solver.py:304-313).  Then
+        SolverDivergenceError for the first step whose fields went non-finite, with the
+        reference's step number (counted from this stepper's first step) and node (the lowest
+        non-finite temperature index, -1 if only the velocity was), solver.py:448-452."""
         f = self.latch.cpu().numpy()
+        if f[3] and (f[1] == 0 or f[3] <= f[1]):
+            target = self.steps
+            self._restore()
+            t = L.torch()
+            with t.cuda.stream(self.stream):
+                while self.steps < target:
+                    self._checked_step()
+                    self.have_p = True
+                    self._swap()
+            t.cuda.current_stream().wait_stream(self.stream)
+            f = self.latch.cpu().numpy()
         if f[1]:
             bad = int(f[1])
             node = int(f[2]) if f[2] != INT32_MAX else -1
             raise SolverDivergenceError(f"non-finite field at step {bad}", step=bad, node=node)
+        self._snapshot()
 
     def state(self) -> FieldState:
-        return FieldState(self.v.cpu().numpy().T.copy(), self.p.cpu().numpy(), self.T.cpu().numpy())
+        x = self.x.cpu().numpy()
+        self.ops._poisson_lambda = float(x[self.ops.n])
+        return FieldState(self.v.cpu().numpy().T.copy(), x[: self.ops.n].copy(), self.T.cpu().numpy())
 
     def load_state(self, state: FieldState):
         """Replace the device fields with a host state (the pressure also warm-starts the next
         solve, as p_prev does in the reference loop)."""
-        self.v.copy_(L.torch().from_numpy(np.ascontiguousarray(np.asarray(state.velocity, dtype=np.float64).T)))
-        self.T.copy_(L.torch().from_numpy(np.asarray(state.temperature, dtype=np.float64)))
-        self.p.copy_(L.torch().from_numpy(np.asarray(state.pressure, dtype=np.float64)))
+        t = L.torch()
+        self.v.copy_(t.from_numpy(np.ascontiguousarray(np.asarray(state.velocity, dtype=np.float64).T)))
+        self.T.copy_(t.from_numpy(np.asarray(state.temperature, dtype=np.float64)))
+        self.p.copy_(t.from_numpy(np.asarray(state.pressure, dtype=np.float64)))
+        self.x[self.ops.n] = float(getattr(self.ops, "_poisson_lambda", 0.0))
         L.TRAFFIC["h2d"] += self.v.nbytes + self.T.nbytes + self.p.nbytes
         self.have_p = True
+        self._snapshot()
 
     def nusselt(self) -> float:
         return _nusselt_dev(self.ops, self.T) if self.ops._d_nu is not None else float("nan")

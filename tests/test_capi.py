@@ -26,7 +26,7 @@ def lib_path():
 def test_header_declares_entry_points():
     syms = header_symbols()
     for must in ("hn_knn", "hn_weights_mon", "hn_weights_rbf", "hn_apply_ell", "hn_momentum", "hn_div_rhs",
-                 "hn_correct_temperature", "hn_temperature_bc", "hn_sptrsv", "hn_reduce"):
+                 "hn_correct_temperature", "hn_temperature_bc", "hn_sptrsv_super", "hn_reduce"):
         assert must in syms
 
 

@@ -160,7 +160,7 @@ def test_config3_full_n_preconditioner_matches_superlu(config3):
         ops._d_lu.solve(L.to_device(b), x)
         worst = max(worst, rel(x.cpu().numpy(), ref))
     record("config3_fullN_precond_vs_superlu", float(f"{worst:.3e}"))
-    assert worst <= ops._d_lu.PARITY_TOL
+    assert worst <= ops._d_lu.parity_tol
 
 
 def test_config3_tie_rows_own_choice_delta(config3):

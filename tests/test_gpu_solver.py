@@ -359,34 +359,49 @@ class TestRun:
         npt.assert_array_equal(a.state.temperature[mask], ns.bc_value[mask])
 
 
-def test_device_lu_solve_matches_superlu_both_tile_modes():
-    """The GPU preconditioner (SuperLU factors, supernodal sync-free solves) against SuperLU's own
-    solve: substitution (default) to rounding; with the optional diagonal-tile inverses for U
-    (hn_sptrsv_super_inv) to the drift DESIGN.md states."""
+@pytest.mark.parametrize("inverse,tol", [(False, 1e-12), (True, 1e-9)])
+def test_device_lu_solve_matches_superlu(inverse, tol):
+    """The GPU preconditioner (SuperLU factors, supernodal sync-free solves over packed dense
+    panels) against SuperLU's own solve: substitution to rounding, diagonal-tile inverses (the
+    default) to the drift DESIGN.md states; twice in a row: bitwise reproducible."""
     from paper_2303_01760_b200 import _lib as L
     from paper_2303_01760_b200.solver import _DeviceLU
     from scipy.sparse import linalg as spla
     ns = nodesets.hybrid_hole_2d(60, seed=2)
     ops = hn.build_operators(ns, {"wall:x-"}, PoissonSolveSettings())
     lu = spla.splu(ops.poisson_matrix.tocsc())  # the factorisation build_operators makes
-    old = _DeviceLU.TILE_INVERSE
-    try:
-        _DeviceLU.TILE_INVERSE = True
-        dlu = _DeviceLU(lu)
-        b = np.random.default_rng(3).normal(size=dlu.n)
-        ref = lu.solve(b)
-        t = L.torch()
-        bd, xd = L.to_device(b), L.empty(dlu.n, t.float64)
-        got = {}
-        for mode in (False, True):
-            _DeviceLU.TILE_INVERSE = mode
-            dlu.solve(bd, xd)
-            got[mode] = xd.cpu().numpy().copy()
-    finally:
-        _DeviceLU.TILE_INVERSE = old
-    scale = np.abs(ref).max()
-    assert np.abs(got[False] - ref).max() / scale <= 1e-12
-    assert np.abs(got[True] - ref).max() / scale <= 1e-8
+    dlu = _DeviceLU(lu, inverse=inverse)
+    assert int((dlu.sL.w.cpu().numpy() > 32).sum()) > 0  # multi-tile blocks exercised
+    b = np.random.default_rng(3).normal(size=dlu.n)
+    ref = lu.solve(b)
+    t = L.torch()
+    bd, xd = L.to_device(b), L.empty(dlu.n, t.float64)
+    dlu.solve(bd, xd)
+    got = xd.cpu().numpy().copy()
+    dlu.solve(bd, xd)
+    assert got.tobytes() == xd.cpu().numpy().tobytes()
+    assert np.abs(got - ref).max() / np.abs(ref).max() <= tol
+
+
+@pytest.mark.parametrize("cap,helper", [(32, 64), (96, 512), (256, 4096)])
+@pytest.mark.parametrize("inverse", [False, True])
+def test_device_lu_random_fill_all_block_shapes(cap, helper, inverse):
+    """Random sparse matrix with heavy fill: blocks of every width up to the cap (partial last
+    panels, upper and lower), helper-fed blocks and batched small blocks, vs SuperLU."""
+    from paper_2303_01760_b200 import _lib as L
+    from paper_2303_01760_b200.solver import _DeviceLU
+    from scipy import sparse
+    from scipy.sparse import linalg as spla
+    n = 3000
+    a = sparse.random(n, n, density=0.004, random_state=7, format="csc") + sparse.eye(n) * 2.0
+    lu = spla.splu(a.tocsc())
+    dlu = _DeviceLU(lu, inverse=inverse, cap=cap, helper_nnz=helper)
+    b = np.random.default_rng(5).normal(size=n)
+    t = L.torch()
+    xd = L.empty(n, t.float64)
+    dlu.solve(L.to_device(b), xd)
+    ref = lu.solve(b)
+    assert np.abs(xd.cpu().numpy() - ref).max() / np.abs(ref).max() <= (1e-9 if inverse else 1e-11)
 
 
 # ---------------------------------------------------------------- run(): reference loop semantics
@@ -441,8 +456,14 @@ def test_pressure_retry_after_bicgstab_failure(dvd_setup, monkeypatch):
     rhs[:n] = (ops.partials[0].matrix @ vstar[:, 0] + ops.partials[1].matrix @ vstar[:, 1]) / 1e-5
     rhs[ops.boundary_idx] = 0.0
     direct = ops.poisson_precond @ rhs
-    orig = S._BiCGStab.solve
-    monkeypatch.setattr(S._BiCGStab, "solve", lambda self, b, x0, rtol, maxiter: (orig(self, b, x0, rtol, 0)[0], -10))
+    orig = S._NativePressure.solve
+
+    def failing(self, b, x0, x, rtol, maxiter, status):  # the device solve reports a breakdown
+        orig(self, b, x0, x, rtol, maxiter, status)
+        status[0] = -10
+        x.zero_()
+
+    monkeypatch.setattr(S._NativePressure, "solve", failing)
     ops._poisson_lambda = 0.0
     p = pressure_solve(vstar, ops, settings, 1e-5)
     assert rel(p, direct[:n]) <= 1e-9
@@ -450,3 +471,45 @@ def test_pressure_retry_after_bicgstab_failure(dvd_setup, monkeypatch):
     with pytest.raises(PoissonConvergenceError) as exc:
         pressure_solve(vstar, ops, settings, 1e-5)
     assert exc.value.residual > 0
+
+
+def test_native_pressure_matches_direct_and_scipy_semantics(dvd_setup):
+    """hn_pressure_solve (device-driven BiCGStab, graph WHILE node): the direct solution from a
+    zero and from a warm start; b = 0 gives x = 0; tol = 0 runs maxiter passes (info = maxiter)."""
+    from paper_2303_01760_b200 import _lib as L
+    ns, ops, _, settings, _ = dvd_setup
+    t = L.torch()
+    n1 = ops.n + 1
+    b = np.random.default_rng(4).normal(size=n1)
+    b[ops.boundary_idx] = 0.0
+    b[-1] = 0.0
+    direct = ops.poisson_precond @ b
+    bd, x, st = L.to_device(b), L.empty(n1, t.float64), L.zeros(2, t.int32)
+    ops._d_press.solve(bd, None, x, 1e-8, 2000, st)
+    assert st.cpu().numpy()[0] == 0
+    assert rel(x.cpu().numpy(), direct) <= 1e-9
+    x0 = L.to_device(direct * (1 + 1e-3))
+    ops._d_press.solve(bd, x0, x, 1e-8, 2000, st)
+    assert st.cpu().numpy()[0] == 0 and rel(x.cpu().numpy(), direct) <= 1e-9
+    ops._d_press.solve(bd, x, x, 1e-8, 2000, st)  # warm start from x itself
+    assert st.cpu().numpy()[0] == 0 and rel(x.cpu().numpy(), direct) <= 1e-9
+    ops._d_press.solve(L.zeros(n1, t.float64), None, x, 1e-8, 2000, st)
+    assert st.cpu().numpy()[0] == 0 and not x.cpu().numpy().any()
+    ops._d_press.solve(bd, None, x, 0.0, 3, st)
+    assert st.cpu().numpy().tolist() == [3, 3]
+
+
+def test_stepper_rolls_back_and_raises_at_the_failing_step(dvd_setup):
+    """tol = 1e-300 makes every BiCGStab (and the retry) fail: the graph-mode stepper latches the
+    failure on the device, and check_finite rolls back, replays step 1 with the reference's
+    handling and raises PoissonConvergenceError there (solver.py:304-313)."""
+    from paper_2303_01760_b200.errors import PoissonConvergenceError
+    ns, ops, params, _, _ = dvd_setup
+    st = FieldState(np.zeros((len(ns), 2)), np.zeros(len(ns)), (ns.positions[:, 0] - 0.5).copy())
+    apply_temperature_bc(st.temperature, ops)
+    stepper = DeviceStepper(ops, params, PoissonSolveSettings(tol=1e-300, maxiter=2), 1e-5, st)
+    for _ in range(4):
+        stepper.step()
+    with pytest.raises(PoissonConvergenceError):
+        stepper.check_finite()
+    assert stepper.steps == 0  # rolled back to the start, failed again at step 1

@@ -1,6 +1,6 @@
-"""Host-side logic that needs no GPU: triangular-solve task planning (emulated task by
-task in ticket order, the order the kernel's atomic ticket hands them out), node-set
-generators, operator-code mapping."""
+"""Host-side logic that needs no GPU: supernodal triangular-solve planning (emulated task
+by task in ticket order, the order the kernel's atomic ticket hands them out) and the
+packed dense panels, node-set generators, operator-code mapping."""
 
 import numpy as np
 import pytest
@@ -9,47 +9,6 @@ from scipy.sparse.linalg import spsolve_triangular
 
 from paper_2303_01760_b200 import nodesets
 from paper_2303_01760_b200.approx import _op_code, Laplacian, NormalDerivative, Partial
-from paper_2303_01760_b200.solver import plan_triangular_tasks
-
-
-def emulate(plan, m, b, diag=None):
-    """Execute the task list sequentially in ticket order (a valid schedule)."""
-    x = np.full(m.shape[0], np.nan)
-    partial = np.full(max(plan["npartial"], 1), np.nan)
-    for t in range(plan["ntasks"]):
-        r, e0, ln = plan["row"][t], plan["beg"][t], plan["len"][t]
-        cols = m.indices[e0:e0 + ln]
-        assert not np.any(np.isnan(x[cols])), "task ran before a dependency"
-        s = float(np.dot(m.data[e0:e0 + ln], x[cols]))
-        if plan["np"][t] < 0:
-            partial[plan["part"][t]] = s
-        else:
-            p0, k = plan["part"][t], plan["np"][t]
-            assert not np.any(np.isnan(partial[p0:p0 + k]))
-            tot = float(np.sum(partial[p0:p0 + k])) + s
-            x[r] = (b[r] - tot) / (diag[r] if diag is not None else 1.0)
-    return x
-
-
-@pytest.mark.parametrize("lower", [True, False])
-@pytest.mark.parametrize("chunk", [4, 256])
-def test_task_plan_solves_triangular_systems(lower, chunk):
-    rng = np.random.default_rng(0)
-    n = 400
-    a = sp.random(n, n, density=0.05, random_state=1, format="csr")
-    a = a + sp.csr_matrix((np.ones(n), (np.full(n, n - 1 if lower else 0), np.arange(n))), shape=(n, n))
-    tri = sp.tril(a, k=-1, format="csr") if lower else sp.triu(a, k=1, format="csr")
-    tri.sort_indices()
-    b = rng.normal(size=n)
-    diag = rng.uniform(1, 2, size=n)
-    plan = plan_triangular_tasks(tri, lower, chunk)
-    x = emulate(plan, tri, b, None if lower else diag)
-    full = (tri + sp.eye(n)) if lower else (tri + sp.diags(diag))
-    want = spsolve_triangular(full.tocsr(), b, lower=lower)
-    np.testing.assert_allclose(x, want, rtol=1e-10, atol=1e-12)
-    assert plan["ntasks"] >= n
-    if chunk == 4:
-        assert plan["npartial"] > 0
 
 
 def test_generators_match_baseline_sizes():
@@ -163,41 +122,64 @@ def test_supernodal_plan_solves_triangular_systems(lower):
     np.testing.assert_allclose(x, spsolve_triangular(full.tocsr(), b, lower=lower), rtol=1e-9, atol=1e-11)
 
 
+def _panel_geom(lower, w, tt):
+    """Python restatement of panel_geom (csrc/pressure.cu)."""
+    ntiles = (w + 31) // 32
+    t0 = 32 * tt if lower else 32 * (ntiles - 1 - tt)
+    tw = min(32, w - t0)
+    rbase = t0 if lower else 0
+    rows = w - t0 if lower else t0 + tw
+    return t0, tw, rbase, rows, (rows + 1) & ~1
+
+
 @pytest.mark.parametrize("lower", [True, False])
-def test_host_tile_inverse_inverts_every_diagonal_tile(lower):
-    """hn_host_tile_inverse (host code, no GPU): row i of tinv is row (i - tile start) of the
-    inverse of its 32-row diagonal tile (unit lower / diag-upper), tiles from each block start."""
+def test_host_pack_panels_hold_every_dense_triangle(lower):
+    """hn_host_pack_panels (host code, no GPU): reading the packed panels back with the
+    kernel's geometry gives exactly the strict in-block triangle of every block task."""
     from scipy.sparse import linalg as spla
 
     from paper_2303_01760_b200 import _lib as L
     from paper_2303_01760_b200.solver import plan_supernodal_blocks
-    n = 400
+    n = 600
     a = sp.random(n, n, density=0.02, random_state=5, format="csc") + sp.eye(n) * 3
-    lu = spla.splu(a.tocsc(), permc_spec="NATURAL", diag_pivot_thresh=0.0)
+    lu = spla.splu(a.tocsc())
     tri = sp.tril(sp.csr_matrix(lu.L), k=-1, format="csr") if lower else sp.triu(sp.csr_matrix(lu.U), k=1, format="csr")
     tri.sort_indices()
-    diag = np.ascontiguousarray(sp.csr_matrix(lu.U).diagonal(), dtype=np.float64)
-    plan = plan_supernodal_blocks(tri, lower, cap=96)
-    r0, w = np.ascontiguousarray(plan["r0"], np.int32), np.ascontiguousarray(plan["w"], np.int32)
+    plan = plan_supernodal_blocks(tri, lower, cap=96, helper_nnz=200)
+    kind, r0, w = plan["kind"], plan["t_r0"], plan["t_w"]
     rowptr = np.ascontiguousarray(tri.indptr, np.int64)
     cols = np.ascontiguousarray(tri.indices, np.int32)
     vals = np.ascontiguousarray(tri.data, np.float64)
-    tinv = np.empty(n * 32)
+    off = np.empty(len(kind), np.int64)
     vp = L._vp
-    L.call("hn_host_tile_inverse", rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), vals.ctypes.data_as(vp),
-           diag.ctypes.data_as(vp), n, 1 if lower else 0, len(r0), r0.ctypes.data_as(vp), w.ctypes.data_as(vp),
-           tinv.ctypes.data_as(vp))
-    tinv = tinv.reshape(n, 32)
+    one = np.ones(1)
+    args = (rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), vals.ctypes.data_as(vp), one.ctypes.data_as(vp),
+            1 if lower else 0, 0, plan["ntasks"], kind.ctypes.data_as(vp), r0.ctypes.data_as(vp), w.ctypes.data_as(vp),
+            off.ctypes.data_as(vp))
+    lib = L.lib()
+    total = lib.hn_host_pack_panels(*args, None)
+    packed = np.full(total, np.nan)
+    assert lib.hn_host_pack_panels(*args, packed.ctypes.data_as(vp)) == total
+    assert not np.isnan(packed).any()
     dense = tri.toarray()
     checked = 0
-    for b0, bw in zip(r0, w):
-        for t0 in range(0, bw, 32):
-            tw = min(32, bw - t0)
-            s = slice(b0 + t0, b0 + t0 + tw)
-            T = dense[s, s] + (np.eye(tw) if lower else np.diag(diag[s]))
-            np.testing.assert_allclose(tinv[s, :tw] @ T, np.eye(tw), atol=1e-10)
-            checked += 1
-    assert checked > 10
+    for t in range(plan["ntasks"]):
+        if kind[t] not in (0, 2):
+            assert off[t] == -1
+            continue
+        b0, bw = int(r0[t]), int(w[t])
+        got = np.zeros((bw, bw))
+        pos = int(off[t])
+        for tt in range((bw + 31) // 32):
+            t0, tw, rbase, rows, rp = _panel_geom(lower, bw, tt)
+            panel = packed[pos:pos + 32 * rp].reshape(32, rp)
+            assert pos % 2 == 0 and not panel[tw:].any()  # 16-byte aligned, missing columns zero
+            got[rbase:rbase + rows, t0:t0 + tw] = panel[:tw, :rows].T
+            pos += 32 * rp
+        want = np.tril(dense[b0:b0 + bw, b0:b0 + bw], -1) if lower else np.triu(dense[b0:b0 + bw, b0:b0 + bw], 1)
+        np.testing.assert_array_equal(got, want)
+        checked += bw > 32
+    assert checked > 0
 
 
 def test_run_builds_the_domain_spec_for_cold_origins(monkeypatch):

@@ -1,11 +1,16 @@
 """Record the per-task timeline of the supernodal L and U solves on config 3 (dev tool);
 writes gpurun_out/trace_sptrsv.npz for offline analysis."""
+import ctypes as C
+import os
 import sys
 from pathlib import Path
 
 import numpy as np
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+# the trace hook only exists in the dev build (python -m paper_2303_01760_b200._build --trace)
+os.environ.setdefault("HN_LIB_PATH", str(ROOT / "paper_2303_01760_b200" / "libhn_trace.so"))
 import paper_2303_01760_b200 as hn  # noqa: E402
 from paper_2303_01760_b200 import _lib as L, nodesets  # noqa: E402
 
@@ -25,13 +30,13 @@ def main():
         tr = L.zeros(4 * sch.kind.numel(), t.int64)
         lu._tri(sch, m, dg, b, y, s)  # warm
         t.cuda.synchronize()
-        L.call("hn_debug_sptrsv_trace", L.ptr(tr))
+        L.lib().hn_debug_sptrsv_trace(L.ptr(tr))
         e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
         e0.record()
         lu._tri(sch, m, dg, b, y, s)
         e1.record()
         t.cuda.synchronize()
-        L.call("hn_debug_sptrsv_trace", None)
+        L.lib().hn_debug_sptrsv_trace(None)
         out[name + "_trace"] = tr.cpu().numpy().reshape(-1, 4)[: sch.ntasks]
         for k in ("kind", "r0", "w", "rb", "rc"):
             out[name + "_" + k] = getattr(sch, k).cpu().numpy()
