@@ -365,9 +365,16 @@ __global__ void __launch_bounds__(128, D == 2 ? 7 : 5) knn_box_kernel(Grid g, co
                                                       const double* __restrict__ qpos, int64_t nq, int n,
                                                       const uint8_t* __restrict__ exclude, double r0,
                                                       const double* __restrict__ qh, double rscale,
-                                                      int* __restrict__ out_idx, double* __restrict__ out_dist) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= nq) return;
+                                                      int* __restrict__ out_idx, double* __restrict__ out_dist,
+                                                      const int* __restrict__ nq_dev = nullptr,
+                                                      const int* __restrict__ out_rows = nullptr) {
+  // nq_dev / out_rows: the warp kernel's fallback list (count on the device, query t of the
+  // list is output row out_rows[t]); grid-stride so a fixed grid covers any count
+  const int64_t nq_eff = nq_dev ? static_cast<int64_t>(*nq_dev) : nq;
+  const double r_base = r0;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < nq_eff;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  r0 = r_base;
   double q[D];
   load_query<D>(pos, queries, qpos, t, q);
   if (qh) {  // radius from the query's own nominal spacing (graded node sets)
@@ -443,7 +450,166 @@ __global__ void __launch_bounds__(128, D == 2 ? 7 : 5) knn_box_kernel(Grid g, co
     topn_init<NMAX>(kd, ki, n);
     ring_scan<D, NMAX>(g, cell_start, cell_items, cell_pos, exclude, q, c0, kd, ki);
   }
-  topn_store<NMAX>(kd, ki, n, t, out_idx, out_dist);
+  topn_store<NMAX>(kd, ki, n, out_rows ? static_cast<int64_t>(__ldg(out_rows + t)) : t, out_idx, out_dist);
+  }
+}
+
+// ---- kNN query, one warp per query (n <= 32) ----------------------------------------
+// The candidates of the query's axis box (|p - q|_inf <= r, r from the query's own nominal
+// spacing) are enumerated as one flattened list over the box's cell runs (each lane owns
+// one run's bounds; a warp scan gives the offsets, a 5-step search maps a list slot to its
+// run), every lane takes list slots lane, lane + 32, .. and tests d^2 <= r^2; the accepted
+// (d, index) keys are compacted by ballot into a 32-slot warp list and sorted ONCE by a
+// 15-stage bitonic network across the lanes.  No per-candidate insertion network, no
+// divergence between queries.  The answer is exact when at most 32 keys were accepted and
+// the n-th lies within r (1 - 1e-12): every point with a smaller key is in the box and was
+// accepted.  Otherwise the query goes to a device list that knn_box_kernel finishes.
+constexpr int kWarpKnnWarps = 8;
+#ifdef HN_TRACE
+__device__ unsigned long long g_knn_fb_stats[4];  // dev builds: [fallbacks, >32 keys, < n keys, n-th beyond r]
+#endif
+
+template <int D>
+__global__ void __launch_bounds__(kWarpKnnWarps * 32) knn_warp_kernel(
+    Grid g, const double* __restrict__ pos, const int* __restrict__ cell_start, const int* __restrict__ cell_items,
+    const double* __restrict__ cell_pos, const int* __restrict__ queries, int64_t nq, int n,
+    const uint8_t* __restrict__ exclude, double r0, const double* __restrict__ qh, double rscale,
+    int* __restrict__ out_idx, double* __restrict__ out_dist, int* __restrict__ fb_count, int* __restrict__ fb_node,
+    int* __restrict__ fb_row) {
+  __shared__ int s_off[kWarpKnnWarps][33];
+  __shared__ int s_beg[kWarpKnnWarps][32];
+  __shared__ double s_kd[kWarpKnnWarps][32];
+  __shared__ int s_ki[kWarpKnnWarps][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpKnnWarps + wib;
+  if (t >= nq) return;
+  const int node = queries ? __ldg(queries + t) : static_cast<int>(t);
+  double q[D];
+  load_point<D>(pos, node, q);
+  double r = r0;
+  if (qh) {
+    const double h = __ldg(qh + node);
+    if (h > 0.0 && h < CUDART_INF) r = rscale * h;
+  }
+  // (rescanning with a radius rescaled by the count when more than 32 or fewer than n keys
+  // were accepted cut the fallbacks from 24 % to 5 % on config 4 but cost more than the
+  // fallback path saves: 577 -> 699 us)
+  const double thr2 = __dmul_rn(__dmul_rn(r, r), 1.0 + 1e-9);
+  const double rm = r * (1.0 + 1e-9);
+  int blo[D], bhi[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    blo[a] = min(max(static_cast<int>(floor((q[a] - rm - g.lo[a]) * g.inv_cell)), 0), g.dims[a] - 1);
+    bhi[a] = min(max(static_cast<int>(floor((q[a] + rm - g.lo[a]) * g.inv_cell)), 0), g.dims[a] - 1);
+  }
+  constexpr int L = D - 1;  // contiguous axis of the cell numbering
+  auto gap = [&](int a, int c) {
+    const double cl = g.lo[a] + c * g.cell;
+    const double gp = fmax(fmax(cl - q[a], q[a] - (cl + g.cell)), 0.0);
+    return fmax(gp - 1e-9 * g.cell, 0.0);
+  };
+  const int nx = bhi[0] - blo[0] + 1;
+  const int nrows = D == 2 ? nx : nx * (bhi[1] - blo[1] + 1);
+  bool fb = nrows > 32;
+  int accepted = 0;
+  if (!fb) {
+    // lane -> one run of cells along the contiguous axis, clipped to the ball
+    int beg = 0, cnt = 0;
+    if (lane < nrows) {
+      const int x = blo[0] + (D == 2 ? lane : lane % nx);
+      double rem2 = thr2;
+      const double gx = gap(0, x);
+      rem2 -= gx * gx;
+      int64_t cl = x;
+      if constexpr (D == 3) {
+        const int y = blo[1] + lane / nx;
+        const double gy = gap(1, y);
+        rem2 -= gy * gy;
+        cl = static_cast<int64_t>(x) * g.dims[1] + y;
+      }
+      if (rem2 >= 0.0) {
+        const double hw = sqrt(rem2) * (1.0 + 1e-9) + 1e-12 * g.cell;
+        const int c_lo = min(max(static_cast<int>(floor((q[L] - hw - g.lo[L]) * g.inv_cell)), blo[L]), bhi[L]);
+        const int c_hi = min(max(static_cast<int>(floor((q[L] + hw - g.lo[L]) * g.inv_cell)), blo[L]), bhi[L]);
+        const int64_t c0 = cl * g.dims[L] + c_lo;
+        beg = __ldg(cell_start + c0);
+        cnt = __ldg(cell_start + c0 + (c_hi - c_lo + 1)) - beg;
+      }
+    }
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, inc, 31);
+    s_off[wib][lane] = inc - cnt;
+    s_beg[wib][lane] = beg;
+    if (lane == 31) s_off[wib][32] = total;
+    __syncwarp();
+    for (int base = 0; base < total; base += 32) {
+      const int m = base + lane;
+      bool acc = false;
+      double d2 = 0.0;
+      int j = 0;
+      if (m < total) {
+        int lo = 0, hi = 31;  // last run with offset <= m (runs past nrows have offset == total)
+#pragma unroll
+        for (int step = 0; step < 5; ++step) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_off[wib][mid] <= m) lo = mid;
+          else hi = mid - 1;
+        }
+        const int sidx = s_beg[wib][lo] + (m - s_off[wib][lo]);
+        double p[D];
+        load_cand<D>(cell_pos, cell_items, sidx, j, p);
+        if (!(exclude && __ldg(exclude + j))) {
+          d2 = exact_dist2<D>(p, q);
+          acc = d2 <= thr2;
+        }
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, acc);
+      const int slot = accepted + __popc(mask & ((1u << lane) - 1u));
+      if (acc && slot < 32) {
+        s_kd[wib][slot] = __dsqrt_rn(d2);
+        s_ki[wib][slot] = j;
+      }
+      accepted += __popc(mask);
+    }
+    fb = accepted > 32 || accepted < n;
+  }
+  if (!fb) {
+    __syncwarp();
+    double kd = lane < accepted ? s_kd[wib][lane] : CUDART_INF;
+    int ki = lane < accepted ? s_ki[wib][lane] : INT_MAX;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, kd, j);
+        const int oi = __shfl_xor_sync(0xffffffffu, ki, j);
+        const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+        const bool take = keep_min ? key_less(od, oi, kd, ki) : key_less(kd, ki, od, oi);
+        kd = take ? od : kd;
+        ki = take ? oi : ki;
+      }
+    }
+    const double kth = __shfl_sync(0xffffffffu, kd, n - 1);
+    fb = !(kth <= r * (1.0 - 1e-12));
+    if (!fb && lane < n) {
+      out_idx[t * n + lane] = ki;
+      if (out_dist) out_dist[t * n + lane] = kd;
+    }
+  }
+  if (fb && lane == 0) {
+#ifdef HN_TRACE
+    atomicAdd(&g_knn_fb_stats[0], 1ull);
+    atomicAdd(&g_knn_fb_stats[accepted > 32 ? 1 : (accepted < n ? 2 : 3)], 1ull);
+#endif
+    const int k = atomicAdd(fb_count, 1);
+    fb_node[k] = node;
+    fb_row[k] = static_cast<int>(t);
+  }
 }
 
 // ---- classification + lattice stencils ------------------------------------------
@@ -610,7 +776,7 @@ HN_EXPORT int hn_partition_methods(const int8_t* method, int64_t n, int* rows_ou
   return e == cudaSuccess ? 0 : -static_cast<int>(e);
 }
 
-static int g_knn_variant = 0;  // 0/2/3: box pass (alpha 1.3/1.0/1.6) + ring fallback; 1: ring traversal only
+static int g_knn_variant = 0;  // 0: warp kernel (3D) / box pass (2D); 1: ring only; 2/3: box pass alpha; 5: box pass only
 HN_EXPORT void hn_knn_set_variant(int v) { g_knn_variant = v; }
 
 static Grid make_grid(const double* lo_host, double cell, const int* dims_host, int d) {
@@ -768,11 +934,39 @@ static void knn_launch_one(int variant, const Grid& g, const double* pos, const 
                                             radius_per_spacing(D, n, alpha), oi, od);
 }
 
+// warp kernel + fallback list finished by the box kernel (see knn_warp_kernel)
+template <int D, int NMAX>
+static int knn_warp_launch(const Grid& g, const double* pos, const int* cs, const int* ci, const double* cp,
+                           const int* queries, int64_t nq, int n, const uint8_t* excl, const double* qh, int* oi,
+                           double* od, cudaStream_t s) {
+  int* fb = nullptr;  // [count | nodes (nq) | rows (nq)]
+  HN_TRY(stream_alloc(reinterpret_cast<void**>(&fb), sizeof(int) * (1 + 2 * nq), s));
+  HN_TRY(cudaMemsetAsync(fb, 0, sizeof(int), s));
+  const double rs = radius_per_spacing(D, n + 4, 1.0);  // expected ~n + 4 keys inside r
+  knn_warp_kernel<D><<<ceil_div(nq, kWarpKnnWarps), kWarpKnnWarps * 32, 0, s>>>(
+      g, pos, cs, ci, cp, queries, nq, n, excl, rs * (D == 2 ? g.cell : g.cell / 1.25), qh, rs, oi, od, fb, fb + 1,
+      fb + 1 + nq);
+  const double alpha = D == 2 ? 1.4 : 1.15;
+  knn_box_kernel<D, NMAX><<<sm_count() * 4, 128, 0, s>>>(g, pos, cs, ci, cp, fb + 1, nullptr, nq, n, excl,
+                                                         box_radius(D, n, g.cell, alpha), qh,
+                                                         radius_per_spacing(D, n, alpha), oi, od, fb, fb + 1 + nq);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(fb, s);
+  return e == cudaSuccess ? 0 : -static_cast<int>(e);
+}
+
 template <int D>
 static int launch_knn(const Grid& g, const double* pos, const int* cs, const int* ci, const double* cp,
                       const int* queries, const double* qpos, int64_t nq, int n, const uint8_t* excl,
                       const double* qh, int* oi, double* od, cudaStream_t s) {
   const int v = g_knn_variant;
+  // 3D node queries: the warp kernel (config 4: 674 -> 577 us, 24 % of the queries finished
+  // by the box kernel).  In 2D (n = 12, ~25 box points) one thread per query is cheaper
+  // (config 1: 58 us vs 157 us for the warp kernel).
+  if (v == 0 && D == 3 && !qpos && n <= 32) {
+    if (n <= 20) return knn_warp_launch<D, 20>(g, pos, cs, ci, cp, queries, nq, n, excl, qh, oi, od, s);
+    return knn_warp_launch<D, 32>(g, pos, cs, ci, cp, queries, nq, n, excl, qh, oi, od, s);
+  }
 #define HN_KNN(NM) knn_launch_one<D, NM>(v, g, pos, cs, ci, cp, queries, qpos, nq, n, excl, qh, oi, od, s)
   if (n <= 5) HN_KNN(5);
   else if (n <= 8) HN_KNN(8);
@@ -848,3 +1042,12 @@ HN_EXPORT int hn_mon_stencils(const int* rows, int64_t nrows, const double* pos,
   HN_CHECK_LAUNCH();
   return 0;
 }
+
+#ifdef HN_TRACE
+// Dev builds only: read and reset the warp-kNN fallback counters (tools/tune_knn.py).
+HN_EXPORT int hn_debug_knn_fallbacks(unsigned long long* out_host) {
+  if (cudaMemcpyFromSymbol(out_host, g_knn_fb_stats, sizeof(unsigned long long) * 4) != cudaSuccess) return -1;
+  unsigned long long z[4] = {0, 0, 0, 0};
+  return cudaMemcpyToSymbol(g_knn_fb_stats, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif
