@@ -106,6 +106,15 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void mbar_expect(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -245,7 +254,7 @@ __device__ __forceinline__ unsigned smid() {
 // entries live past the task list in the same arrays).  blk_off[t] = offset of task t's
 // packed panels (kinds 0 and 2).
 template <bool LOWER>
-__global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
+__global__ void __launch_bounds__(kSnThreads, 2) sptrsv_super_kernel(
     const int* __restrict__ blk_kind, const int* __restrict__ blk_r0, const int* __restrict__ blk_w,
     const int* __restrict__ blk_rb, const int* __restrict__ blk_rc, const int64_t* __restrict__ blk_off,
     int64_t nblk, const int64_t* __restrict__ rowptr, const int* __restrict__ cols, const double* __restrict__ vals,
@@ -254,6 +263,8 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
   if (skip && *skip) return;
   __shared__ double ys[kSnMaxW];
   __shared__ int s_cnt[kSnMaxW], s_off[kSnMaxW + 1];  // outside phase: chunks per row, their offsets
+  __shared__ long long s_e0[kSnMaxW];                  // ... first outside entry of each row
+  __shared__ int s_len[kSnMaxW];                       // ... and the number of outside entries
   __shared__ short s_prow[kSnMaxPairs];                // pair -> row
   __shared__ double s_part[kSnMaxPairs];               // pair partial sums
   __shared__ unsigned long long tk;
@@ -310,8 +321,12 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
       const int nr = (kind == 1 ? __ldg(blk_rc + t) : w);
       for (int q = tid; q < nr; q += kSnThreads) {
         const int rr = rb + q, i = r0 + rr;
-        const int len = static_cast<int>(__ldg(rowptr + i + 1) - __ldg(rowptr + i)) - (LOWER ? rr : (w - 1 - rr));
+        const int64_t a = __ldg(rowptr + i);
+        const int inside = LOWER ? rr : (w - 1 - rr);
+        const int len = static_cast<int>(__ldg(rowptr + i + 1) - a) - inside;
         s_cnt[q] = len > 0 ? (len + kTaskChunk - 1) / kTaskChunk : 1;
+        s_e0[q] = LOWER ? a : a + inside;  // the row's outside entries: [s_e0, s_e0 + s_len)
+        s_len[q] = len;
       }
       __syncthreads();
       if (warp == 0) {  // exclusive scan of the chunk counts (nr <= 256: 8 per lane)
@@ -343,13 +358,10 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
         for (int p = s_off[q]; p < s_off[q + 1]; ++p) s_prow[p] = static_cast<short>(q);
       __syncthreads();
       for (int p = warp; p < npairs; p += kSnWarps) {
-        const int q = s_prow[p], rr = rb + q, i = r0 + rr;
-        const int64_t a = __ldg(rowptr + i), z = __ldg(rowptr + i + 1);
-        const int inside = LOWER ? rr : (w - 1 - rr);
-        const int len = static_cast<int>(z - a) - inside;
+        const int q = s_prow[p];
         const int c0 = (p - s_off[q]) * kTaskChunk;
-        const int clen = len - c0 < kTaskChunk ? len - c0 : kTaskChunk;
-        const double sp = clen > 0 ? row_outside_sum(cols, vals, (LOWER ? a : a + inside) + c0, clen, x, lane) : 0.0;
+        const int clen = s_len[q] - c0 < kTaskChunk ? s_len[q] - c0 : kTaskChunk;
+        const double sp = clen > 0 ? row_outside_sum(cols, vals, s_e0[q] + c0, clen, x, lane) : 0.0;
         if (lane == 0) s_part[p] = sp;
       }
       __syncthreads();
@@ -374,6 +386,9 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
     if (tid == 0) SN_TRACE(1, gtime());
 #endif
     // (2) dense in-block triangle from the packed panels; thread tid owns block row tid
+#ifdef HN_TRACE
+    unsigned long long wait_ns = 0;
+#endif
     const bool has = tid < w;
     const int i = r0 + tid;
     const double dg = (!LOWER && has) ? __ldg(diag + i) : 1.0;
@@ -391,7 +406,12 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
       const bool more = tt + 1 < ntiles;
       int n0, nw, nbase, nrows, nrp;
       panel_geom(LOWER, w, more ? tt + 1 : tt, n0, nw, nbase, nrows, nrp);
-      if (more && tid == 0) bulk_load(sn_nbuf, panel + 32 * rp, 32u * nrp * 8u, &mbar);
+      if (more && tid == 0) {  // the next panel as 4 bulk copies of 8 columns (one mbarrier phase)
+        const unsigned part = 8u * nrp * 8u;
+        mbar_expect(&mbar, 4u * part);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bulk_copy(sn_nbuf + k * 8 * nrp, panel + 32 * rp + k * 8 * nrp, part, &mbar);
+      }
       if (warp == t0 / 32 && inv) {  // x = T^-1 y: 32 independent products, no chain
         const double yv = lane < tw ? ys[tid] : 0.0;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -426,7 +446,13 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
         ys[tid] -= (a0 + a1) + (a2 + a3);
       }
       if (more) {
+#ifdef HN_TRACE
+        const unsigned long long tw0 = gtime();
         mbar_wait(&mbar, phase);
+        if (tid == 0) wait_ns += gtime() - tw0;
+#else
+        mbar_wait(&mbar, phase);
+#endif
         phase ^= 1u;
         const int rr = tid - nbase;
         const bool in = has && rr >= 0 && rr < nrows;
@@ -442,7 +468,10 @@ __global__ void __launch_bounds__(kSnThreads) sptrsv_super_kernel(
       __syncthreads();
     }
 #ifdef HN_TRACE
-    if (tid == 0) SN_TRACE(2, gtime());
+    if (tid == 0) {
+      SN_TRACE(2, gtime());
+      SN_TRACE(3, wait_ns);  // dense tasks: ns spent waiting for panel copies (instead of the SM id)
+    }
 #endif
   }
 }

@@ -756,6 +756,17 @@ def _interior_divergence_dev(ops: OperatorSet, v_soa) -> float:
 
 
 # ============================================================ device-resident stepping
+def _pinned_view(t, a: np.ndarray):
+    """A torch view of a host array for an async DMA: the array itself when it lives in pinned
+    memory, else a pinned staging copy (torch's caching host allocator)."""
+    src = t.from_numpy(a)
+    if src.is_pinned():
+        return src
+    stage = t.empty(src.shape, dtype=src.dtype, pin_memory=True)
+    stage.copy_(src)
+    return stage
+
+
 class DeviceStepper:
     """One explicit step = K7 -> K8 -> K9 -> K10 -> K11 on HBM-resident state (replicates the
     loop body of run(), solver.py:439-452).
@@ -902,21 +913,42 @@ class DeviceStepper:
         self._snapshot()
 
     def state(self) -> FieldState:
-        x = self.x.cpu().numpy()
-        self.ops._poisson_lambda = float(x[self.ops.n])
-        return FieldState(self.v.cpu().numpy().T.copy(), x[: self.ops.n].copy(), self.T.cpu().numpy())
+        """The fields on the host: one device pass puts [v (n x d) | p, lambda | T] into one
+        contiguous buffer, one DMA into pinned memory (torch's caching host allocator), one
+        synchronisation; the returned arrays are views of that pinned block, so a later
+        load_state() of them is a direct DMA again."""
+        t = L.torch()
+        n, d = self.ops.n, self.ops.dim
+        dev = L.empty(n * d + (n + 1) + n, t.float64)
+        dev[: n * d].view(n, d).copy_(self.v.t())
+        dev[n * d: n * d + n + 1].copy_(self.x)
+        dev[n * d + n + 1:].copy_(self.T)
+        host = t.empty(dev.shape, dtype=t.float64, pin_memory=True)
+        host.copy_(dev, non_blocking=True)
+        t.cuda.current_stream().synchronize()
+        L.TRAFFIC["d2h"] += host.nbytes
+        h = host.numpy()
+        self.ops._poisson_lambda = float(h[n * d + n])
+        return FieldState(h[: n * d].reshape(n, d), h[n * d: n * d + n], h[n * d + n + 1:])
 
     def load_state(self, state: FieldState):
         """Replace the device fields with a host state (the pressure also warm-starts the next
-        solve, as p_prev does in the reference loop)."""
+        solve, as p_prev does in the reference loop).  Pinned host arrays (e.g. from state())
+        go by direct DMA; others through a pinned staging block."""
         t = L.torch()
-        self.v.copy_(t.from_numpy(np.ascontiguousarray(np.asarray(state.velocity, dtype=np.float64).T)))
-        self.T.copy_(t.from_numpy(np.asarray(state.temperature, dtype=np.float64)))
-        self.p.copy_(t.from_numpy(np.asarray(state.pressure, dtype=np.float64)))
+        n, d = self.ops.n, self.ops.dim
+        for dst, src, shape in ((self.T, state.temperature, (n,)), (self.p, state.pressure, (n,))):
+            a = np.ascontiguousarray(np.asarray(src, dtype=np.float64).reshape(shape))
+            dst.copy_(_pinned_view(t, a), non_blocking=True)
+        v = np.ascontiguousarray(np.asarray(state.velocity, dtype=np.float64).reshape(n, d))
+        tmp = L.empty((n, d), t.float64)
+        tmp.copy_(_pinned_view(t, v), non_blocking=True)
+        self.v.copy_(tmp.t())
         self.x[self.ops.n] = float(getattr(self.ops, "_poisson_lambda", 0.0))
         L.TRAFFIC["h2d"] += self.v.nbytes + self.T.nbytes + self.p.nbytes
         self.have_p = True
         self._snapshot()
+        t.cuda.current_stream().synchronize()  # the caller may reuse its host arrays at once
 
     def nusselt(self) -> float:
         return _nusselt_dev(self.ops, self.T) if self.ops._d_nu is not None else float("nan")
