@@ -1450,11 +1450,8 @@ static cudaError_t launch_rbf_static(const double* pos, const int* st, int64_t K
   const size_t smem = sizeof(RbfStaticSmem<D, NST, NOPS>) * WARPS * SPW;
   auto go = [&](auto kc) {
     constexpr auto kern = decltype(kc)::value;
-    static bool attr = false;  // one attribute call per kernel (dynamic smem may exceed 48 KB)
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      attr = true;
-    }
+    // dynamic smem may exceed 48 KB; function attributes are per device, so set every call (cheap)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<grid, WARPS * 32, smem, s>>>(pos, st, K, ops, rn, oi, ow, info, buf ? buf + 1 : nullptr, buf, force);
   };
   using KT = decltype(&rbf_static_kernel<D, NST, NOPS, false, LPS, RPL, WARPS, MINB, ILV, SHB, LA>);
@@ -1473,10 +1470,10 @@ static cudaError_t launch_rbf_static(const double* pos, const int* st, int64_t K
   return cudaFreeAsync(buf, s);
 }
 
-// Kernel choice (tuning/tests; 0 = default static order + flagged fallback):
-// 100 = searching kernel for every stencil; 101 = static kernel with every stencil flagged
-// (exercises the fallback: in-kernel for 2D, list mode for 3D); 10..14 = launch shapes of
-// the static kernel.
+// Kernel choice (tests; 0 = default static order + flagged fallback): 100 = searching
+// kernel for every stencil; 101 = static kernel with every stencil flagged (exercises the
+// fallback: in-kernel for 2D, list mode for 3D).  The launch shapes tried while tuning are
+// recorded in DESIGN.md section 4.
 static int g_rbf_variant = 0;
 HN_EXPORT void hn_weights_rbf_set_variant(int v) { g_rbf_variant = v; }
 
@@ -1485,23 +1482,10 @@ static cudaError_t launch_rbf(const double* pos, const int* st, int64_t K, const
                               int* oi, double* ow, int* info, cudaStream_t s) {
   const int v = g_rbf_variant;
   const int force = v == 101 ? 1 : 0;
-  constexpr bool tune = NOPS == D + 1;  // launch-shape variants only for the standard op count
   if constexpr (D == 2) {
     if (v == 100) {
       launch_rbf_v<2, 12, NOPS, 6, 3, 4, 3>(pos, st, K, ops, rn, oi, ow, info, s);
       return cudaSuccess;
-    }
-    if constexpr (tune) {
-      switch (v) {
-        case 10: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 2, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        case 11: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 3, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        case 14: return launch_rbf_static<2, 12, NOPS, 3, 6, 4, 2, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        case 15: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        case 16: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 3, 6, 3, false, true>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        case 17: return launch_rbf_static<2, 12, NOPS, 3, 6, 4, 2, 6, 3, false, true>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        case 18: return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3, false, true, false>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        default: break;
-      }
     }
     // 2D default: pivot rows broadcast by shuffles (3D rows are 34 wide: shared memory wins)
     return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3, false, true>(pos, st, K, ops, rn, oi, ow, info, s, force);
@@ -1510,15 +1494,6 @@ static cudaError_t launch_rbf(const double* pos, const int* st, int64_t K, const
       launch_rbf_v<3, 20, NOPS, 15, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s);
       return cudaSuccess;
     }
-    if constexpr (tune) {
-      switch (v) {
-        case 11: return launch_rbf_static<3, 20, NOPS, 10, 3, 2, 2, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        case 12: return launch_rbf_static<3, 20, NOPS, 15, 2, 4, 2, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        case 13: return launch_rbf_static<3, 20, NOPS, 10, 3, 4, 1, 15, 2, false, true>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        case 14: return launch_rbf_static<3, 20, NOPS, 10, 3, 4, 1, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        default: break;
-      }
-    }
     // 3D: no look-ahead (the 34/40-wide pivot row would be a second live register row;
     // measured 2.3% (n=20) and 4.5% (n=30) faster than staging the next row early)
     return launch_rbf_static<3, 20, NOPS, 10, 3, 4, 2, 15, 2, false, false, false>(pos, st, K, ops, rn, oi, ow, info, s, force);
@@ -1526,12 +1501,6 @@ static cudaError_t launch_rbf(const double* pos, const int* st, int64_t K, const
     if (v == 100) {
       launch_rbf_v<3, 30, NOPS, 20, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s);
       return cudaSuccess;
-    }
-    if constexpr (tune) {
-      switch (v) {
-        case 14: return launch_rbf_static<3, 30, NOPS, 20, 2, 4, 1, 20, 2>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-        default: break;
-      }
     }
     return launch_rbf_static<3, 30, NOPS, 20, 2, 4, 1, 20, 2, false, false, false>(pos, st, K, ops, rn, oi, ow, info, s, force);
   }

@@ -398,7 +398,7 @@ def test_knn_box_pass_equals_ring_traversal(dim):
     k = 12 if dim == 2 else 20
     out = {}
     try:
-        for v in (1, 0, 2, 3):
+        for v in (1, 0, 2, 3, 5):  # 3D: 0 = warp kernel + box fallback, 5 = box pass only
             L.lib().hn_knn_set_variant(v)
             a, da = dn.knn(k, rows=rows, with_dist=True)
             b = dn.knn(k, rows=rows, exclude=excl)
@@ -406,7 +406,7 @@ def test_knn_box_pass_equals_ring_traversal(dim):
             out[v] = (a.cpu().numpy(), da.cpu().numpy(), b.cpu().numpy(), c.cpu().numpy())
     finally:
         L.lib().hn_knn_set_variant(0)
-    for v in (0, 2, 3):
+    for v in (0, 2, 3, 5):
         for x, y in zip(out[v], out[1]):
             npt.assert_array_equal(x, y)
     # and the ring answer is the brute-force (distance, index) order
