@@ -1290,6 +1290,404 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
   }
 }
 
+// ===================== null-space kernel (default for the tuned sizes) ======================
+// The same static null-space elimination order as rbf_static_kernel (step A: partial-
+// pivoting LU of P picks the unisolvent nodes I, nodes renumbered [I, J]), but the saddle
+// system is reduced algebraically instead of by a Gauss-Jordan sweep over all n+q rows:
+//   P^T w = c          ->  w_I = g - M^T w_J,      M^T = P_I^-T P_J^T,  g = P_I^-T c
+//   A w + P lambda = f ->  S w_J = h - B_I g,      B = A_J: - M A_I:,   h = f_J - M f_I,
+//                          S = B_J - B_I M^T       (= Z^T A Z, SPD for r^3 on a unisolvent set)
+// (1) M^T and g by a Gauss-Jordan sweep of the q x (n + ops) block [P^T | c] with step A's
+// pivots, (2) B and h from the I rows of A (staged in shared memory), (3) S and its right-
+// hand side, (4) a q'-step Gauss-Jordan of [S | rhs] (q' = n - q, pivots on the diagonal,
+// S is SPD), (5) w_I.  One segment of q lanes per system: lane s owns node row I_s, the J
+// rows s, s + q, .. (n - q = q or 2q), monomial row s of (1) and J row(s) of (3)-(4).  The
+// fp64 work is ~7.6K lane-FMAs per 3D n = 20 system instead of the sweep's ~16.7K, every
+// matrix row lives in registers only while it is being used (no 34-wide rows per slot), and
+// stencils with a small pivot are flagged for the searching kernel as in the sweep.
+template <int D, int NST, int NOPS>
+struct RbfNsCore {
+  static constexpr int NQ = poly_count<D>();
+  static constexpr int NJ = NST - NQ;
+  static constexpr int YS = D == 2 ? 2 : 4;
+  static constexpr int NQP = (NQ + 1) & ~1;
+  double prow[2][NQP];         // step A pivot rows (P only)
+  double inv_hist[NQP];        // step A 1/pivots
+  double yp[NST][YS];          // local coordinates, renumbered [I, J]
+  double ai[NQ][NST];          // A rows of the I nodes (renumbered columns); w, wj alias it later
+  double fi[NQ][NOPS];         // f rows of the I nodes
+  double mt[NQ][NJ];           // M^T
+  double g[NQ][NOPS];          // P_I^-T c
+  int sidp[NST];               // node ids, renumbered
+};
+template <int D, int NST, int NOPS>
+struct __align__(16) RbfNsSmem : RbfNsCore<D, NST, NOPS> {
+  static constexpr int kCore = static_cast<int>(sizeof(RbfNsCore<D, NST, NOPS>));
+  static constexpr int kPad = ((16 - kCore % 128) % 128 + 128) % 128;
+  char pad[kPad == 0 ? 128 : kPad];
+};
+
+template <int D, int NST, int NOPS, bool STD, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
+    const double* __restrict__ pos, const int* __restrict__ stencils, int64_t K, OpSpec ops,
+    const double* __restrict__ row_normals, int* __restrict__ out_idx, double* __restrict__ out_w,
+    int* __restrict__ info, int* __restrict__ flag_list, int* __restrict__ flag_count, int force_flag) {
+  constexpr int NQ = poly_count<D>();
+  constexpr int NJ = NST - NQ;
+  constexpr int LPS = NQ;              // lanes per system
+  constexpr int JPL = NJ / LPS;        // J rows per lane
+  constexpr int SPW = 32 / LPS;
+  constexpr int PA = (NST + LPS - 1) / LPS;  // step-A slots
+  constexpr int NQC = NST + NOPS;            // columns of [P^T | c]
+  static_assert(NJ % LPS == 0, "J rows spread evenly over the segment");
+  static_assert(NST <= 31, "node bitmask");
+  using Sm = RbfNsSmem<D, NST, NOPS>;
+  static_assert(sizeof(double) * NQ * NST >= sizeof(double) * NST * NOPS + sizeof(double) * NJ * NOPS,
+                "w and wj alias ai");
+  extern __shared__ __align__(16) unsigned char rbf_ns_smem[];
+  Sm* smem_all = reinterpret_cast<Sm*>(rbf_ns_smem);
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const bool lane_live = lane < SPW * LPS;
+  const int s = lane_live ? lane % LPS : 0;
+  const int sys_w = lane_live ? lane / LPS : 0;
+  const int64_t k_raw = (static_cast<int64_t>(blockIdx.x) * WARPS + warp) * SPW + sys_w;
+  const bool sys_live = lane_live && k_raw < K;
+  const int64_t k = k_raw < K ? k_raw : K - 1;
+  Sm& sm = smem_all[warp * SPW + sys_w];
+  double* wsm = &sm.ai[0][0];          // w[NST][NOPS] (renumbered), valid after (3)
+  double* wjs = wsm + NST * NOPS;      // w_J[NJ][NOPS]
+  auto seg_lane = [&](int t) { return lane_live ? sys_w * LPS + t : lane; };
+  auto seg_xor = [&](int off) {
+    int t = s ^ off;
+    t = t < LPS ? t : LPS - 1;
+    return seg_lane(t);
+  };
+
+  const bool use_rn = !STD && row_normals != nullptr;
+  double rn[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) rn[a] = use_rn ? __ldg(row_normals + k * D + a) : 0.0;
+
+  // ---- gather, shift to the centre, scale by the stencil radius (approx.py:245-250) ----
+  double c[D];
+  load_point<D>(pos, __ldg(stencils + k * NST), c);
+  double yo[PA][D];
+  int sido[PA];
+  double d2max = 0.0;
+#pragma unroll
+  for (int r = 0; r < PA; ++r) {
+    const int j = s + r * LPS;
+    sido[r] = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) yo[r][a] = 0.0;
+    if (j < NST) {
+      sido[r] = __ldg(stencils + k * NST + j);
+      double p[D];
+      load_point<D>(pos, sido[r], p);
+      double d2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        yo[r][a] = p[a] - c[a];
+        d2 = fma(yo[r][a], yo[r][a], d2);
+      }
+      d2max = fmax(d2max, d2);
+    }
+  }
+#pragma unroll
+  for (int off = 1; off < LPS; off <<= 1) d2max = fmax(d2max, __shfl_sync(0xffffffffu, d2max, seg_xor(off)));
+  const double s1 = fast_rcp(fast_sqrt(d2max));
+#pragma unroll
+  for (int r = 0; r < PA; ++r)
+#pragma unroll
+    for (int a = 0; a < D; ++a) yo[r][a] *= s1;
+
+  const unsigned pb0 = smem_addr(&sm.prow[0][0]);
+  const unsigned pb1 = smem_addr(&sm.prow[1][0]);
+  const unsigned hist = smem_addr(&sm.inv_hist[0]);
+  bool bad = force_flag != 0;
+
+  // ---- step A: LU of P with partial pivoting over the nodes -> I (as rbf_static_kernel) ----
+  {
+    double pp[PA][NQ];
+    unsigned vm[PA];
+#pragma unroll
+    for (int r = 0; r < PA; ++r) {
+      const int j = s + r * LPS;
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) pp[r][m] = mono_val<D>(m, yo[r]);
+      vm[r] = (lane_live && j < NST) ? (0x7fffffc0u | static_cast<unsigned>(63 - j)) : 0u;
+    }
+    unsigned chosen = 1u;
+    vm[0] = s == 0 ? 0u : vm[0];
+    if (lane_live && s == 0) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) sm.yp[0][a] = yo[0][a];
+      sm.sidp[0] = sido[0];
+      sm.inv_hist[0] = 1.0;
+    }
+    static_for<NQ - 1>([&](auto mc) {
+      constexpr int m = decltype(mc)::value + 1;
+      unsigned key = 0;
+#pragma unroll
+      for (int r = 0; r < PA; ++r)
+        key = max(key, (static_cast<unsigned>(__double2hiint(pp[r][m])) | 63u) & vm[r]);
+#pragma unroll
+      for (int off = 1; off < LPS; off <<= 1) key = max(key, __shfl_sync(0xffffffffu, key, seg_xor(off)));
+      const unsigned ptag = key & 63u;
+      const unsigned pbase = (m & 1) ? pb1 : pb0;
+      bool isp[PA];
+#pragma unroll
+      for (int r = 0; r < PA; ++r) {
+        isp[r] = ((vm[r] & 63u) == ptag) && vm[r] != 0u;
+        constexpr int j0 = m & ~1;
+#pragma unroll
+        for (int jj = j0; jj < NQ; jj += 2) {
+          if (jj + 1 < NQ) st_pred2(isp[r], pbase + 8u * jj, pp[r][jj], pp[r][jj + 1]);
+          else st_pred1(isp[r], pbase + 8u * jj, pp[r][jj]);
+        }
+        if (isp[r]) {
+#pragma unroll
+          for (int a = 0; a < D; ++a) sm.yp[m][a] = yo[r][a];
+          sm.sidp[m] = sido[r];
+        }
+      }
+      __syncwarp();
+      const double* prow = sm.prow[m & 1];
+      const double piv = prow[m];
+      bad = bad || !(fabs(piv) >= kStaticPivMin);
+      const double inv = fast_rcp(piv);
+      st_pred1(lane_live && s == 0, hist + 8u * m, inv);
+#pragma unroll
+      for (int r = 0; r < PA; ++r) {
+        const double l = isp[r] ? 0.0 : pp[r][m] * inv;
+        vm[r] = isp[r] ? 0u : vm[r];
+#pragma unroll
+        for (int cc = m + 1; cc < NQ; ++cc) pp[r][cc] = fma(-l, prow[cc], pp[r][cc]);
+      }
+      chosen |= 1u << (63u - ptag);
+    });
+#pragma unroll
+    for (int r = 0; r < PA; ++r) {
+      const int j = s + r * LPS;
+      if (lane_live && j < NST && !((chosen >> j) & 1u)) {
+        const int ni = NQ + __popc(~chosen & ((1u << j) - 1u));
+#pragma unroll
+        for (int a = 0; a < D; ++a) sm.yp[ni][a] = yo[r][a];
+        sm.sidp[ni] = sido[r];
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---- the I row of A and f (node I_s) -> shared memory ----
+  double yI[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) yI[a] = sm.yp[s][a];
+  {
+    const double rI = norm_fast<D>(yI);
+#pragma unroll
+    for (int o = 0; o < NOPS; ++o) {
+      double f;
+      if constexpr (STD) f = o == 0 ? 3.0 * (D + 1) * rI : -3.0 * rI * yI[o - 1];
+      else f = phs_rhs<D>(ops, o, yI, rI, use_rn, rn);
+      if (lane_live) sm.fi[s][o] = f;
+    }
+#pragma unroll
+    for (int cc = 0; cc < NST; cc += 2) {
+      double v[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        v[h] = 0.0;
+        if (cc + h < NST) {
+          double d2 = 0.0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const double t = yI[a] - sm.yp[cc + h][a];
+            d2 = fma(t, t, d2);
+          }
+          v[h] = cube_from_sq(d2);
+        }
+      }
+      if (cc + 1 < NST) st_pred2(lane_live, smem_addr(&sm.ai[s][cc]), v[0], v[1]);
+      else st_pred1(lane_live, smem_addr(&sm.ai[s][cc]), v[0]);
+    }
+  }
+
+  // ---- (1) [P^T | c] -> [diag | M^T | g] by Gauss-Jordan with step A's pivot order ----
+  {
+    double q[NQC];
+#pragma unroll
+    for (int cc = 0; cc < NST; ++cc) {
+      double y[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) y[a] = sm.yp[cc][a];
+      q[cc] = mono_val_sel<D>(s, y);
+    }
+#pragma unroll
+    for (int o = 0; o < NOPS; ++o) q[NST + o] = STD ? std_poly_rhs<D>(o, s) : poly_rhs<D>(ops, o, s, use_rn, rn);
+    static_for<NQ>([&](auto kc) {
+      constexpr int kk = decltype(kc)::value;
+      const int src = seg_lane(kk);
+      const double piv = __shfl_sync(0xffffffffu, q[kk], src);
+      bad = bad || !(fabs(piv) >= 0.5 * kStaticPivMin);
+      const double l = s == kk ? 0.0 : q[kk] * fast_rcp(piv);
+#pragma unroll
+      for (int cc = kk + 1; cc < NQC; ++cc) {
+        const double pv = __shfl_sync(0xffffffffu, q[cc], src);
+        q[cc] = fma(-l, pv, q[cc]);
+      }
+      if (s != kk) q[kk] = 0.0;
+    });
+    double own = 0.0;
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) own = s == m ? q[m] : own;
+    const double inv = fast_rcp(own);
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+      if (lane_live) sm.mt[s][j] = q[NQ + j] * inv;
+#pragma unroll
+    for (int o = 0; o < NOPS; ++o)
+      if (lane_live) sm.g[s][o] = q[NST + o] * inv;
+  }
+  __syncwarp();
+
+  // ---- (2)-(3) B row, h, then S row and its right-hand side, for each of my J rows ----
+  double S[JPL][NJ], R[JPL][NOPS];
+#pragma unroll
+  for (int r = 0; r < JPL; ++r) {
+    const int jr = s + r * LPS;  // J index
+    double yJ[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) yJ[a] = sm.yp[NQ + jr][a];
+    double b[NST], h[NOPS];
+    const double rJ = norm_fast<D>(yJ);
+#pragma unroll
+    for (int o = 0; o < NOPS; ++o) {
+      if constexpr (STD) h[o] = o == 0 ? 3.0 * (D + 1) * rJ : -3.0 * rJ * yJ[o - 1];
+      else h[o] = phs_rhs<D>(ops, o, yJ, rJ, use_rn, rn);
+    }
+#pragma unroll
+    for (int cc = 0; cc < NST; ++cc) {
+      double d2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double t = yJ[a] - sm.yp[cc][a];
+        d2 = fma(t, t, d2);
+      }
+      b[cc] = cube_from_sq(d2);
+    }
+    // B row = A_J row - sum_i M[j][i] A_I row i;  h = f_J - sum_i M[j][i] f_I row i
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) {
+      const double mji = sm.mt[i][jr];
+#pragma unroll
+      for (int cc = 0; cc < NST; cc += 2) {
+        if (cc + 1 < NST) {
+          const double2 av = *reinterpret_cast<const double2*>(&sm.ai[i][cc]);
+          b[cc] = fma(-mji, av.x, b[cc]);
+          b[cc + 1] = fma(-mji, av.y, b[cc + 1]);
+        } else {
+          b[cc] = fma(-mji, sm.ai[i][cc], b[cc]);
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < NOPS; ++o) h[o] = fma(-mji, sm.fi[i][o], h[o]);
+    }
+    // S row = B_J - B_I M^T;  rhs = h - B_I g
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) S[r][jj] = b[NQ + jj];
+#pragma unroll
+    for (int o = 0; o < NOPS; ++o) R[r][o] = h[o];
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) {
+      const double bi = b[i];
+#pragma unroll
+      for (int jj = 0; jj < NJ; ++jj) S[r][jj] = fma(-bi, sm.mt[i][jj], S[r][jj]);
+#pragma unroll
+      for (int o = 0; o < NOPS; ++o) R[r][o] = fma(-bi, sm.g[i][o], R[r][o]);
+    }
+  }
+  __syncwarp();  // ai is dead from here on: w / wj alias it
+
+  // ---- (4) Gauss-Jordan on [S | rhs], diagonal pivots (S is SPD) ----
+  static_for<NJ>([&](auto kc) {
+    constexpr int kk = decltype(kc)::value;
+    constexpr int ko = kk % LPS, kr = kk / LPS;  // owner lane and slot of pivot row kk
+    const int src = seg_lane(ko);
+    const double piv = __shfl_sync(0xffffffffu, S[kr][kk], src);
+    bad = bad || !(piv >= kStaticSchurMin);
+    const double inv = fast_rcp(piv);
+    double pr[NJ + NOPS];
+#pragma unroll
+    for (int cc = kk + 1; cc < NJ; ++cc) pr[cc] = __shfl_sync(0xffffffffu, S[kr][cc], src);
+#pragma unroll
+    for (int o = 0; o < NOPS; ++o) pr[NJ + o] = __shfl_sync(0xffffffffu, R[kr][o], src);
+#pragma unroll
+    for (int r = 0; r < JPL; ++r) {
+      const bool mine = (r == kr) && (s == ko);
+      const double l = mine ? 0.0 : S[r][kk] * inv;
+#pragma unroll
+      for (int cc = kk + 1; cc < NJ; ++cc) S[r][cc] = fma(-l, pr[cc], S[r][cc]);
+#pragma unroll
+      for (int o = 0; o < NOPS; ++o) R[r][o] = fma(-l, pr[NJ + o], R[r][o]);
+    }
+  });
+#pragma unroll
+  for (int r = 0; r < JPL; ++r) {
+    const int jr = s + r * LPS;
+    double dg = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) dg = jj == jr ? S[r][jj] : dg;
+    const double inv = fast_rcp(dg);
+#pragma unroll
+    for (int o = 0; o < NOPS; ++o) {
+      const double wv = R[r][o] * inv;
+      if (lane_live) {
+        wjs[jr * NOPS + o] = wv;
+        wsm[(NQ + jr) * NOPS + o] = wv;
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---- (5) w_I = g - M^T w_J ----
+#pragma unroll
+  for (int o = 0; o < NOPS; ++o) {
+    double v = sm.g[s][o];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) v = fma(-sm.mt[s][j], wjs[j * NOPS + o], v);
+    if (lane_live) wsm[s * NOPS + o] = v;
+  }
+  __syncwarp();
+
+  if (!sys_live) return;
+  if (bad) {
+    if (s == 0) flag_list[atomicAdd(flag_count, 1)] = static_cast<int>(k);
+    return;
+  }
+  if (info && s == 0) info[k] = 0;
+  // ---- epilogue: ascending node-index order, un-scale (approx.py:283-284, 407-410) ----
+  const double s2 = s1 * s1;
+#pragma unroll
+  for (int r = 0; r < PA; ++r) {
+    const int j = s + r * LPS;
+    if (j < NST) {
+      const int id = sm.sidp[j];
+      int rank = 0;
+#pragma unroll
+      for (int i = 0; i < NST; ++i) rank += sm.sidp[i] < id;
+      out_idx[static_cast<int64_t>(rank) * K + k] = id;
+#pragma unroll
+      for (int o = 0; o < NOPS; ++o) {
+        const double f = (STD ? o == 0 : ops.order[o] == 2) ? s2 : s1;
+        out_w[(static_cast<int64_t>(o) * NST + rank) * K + k] = wsm[j * NOPS + o] * f;
+      }
+    }
+  }
+}
+
 // ===================== generic fallback (any n, any op count): thread per stencil ==========
 // Used for stencil sizes without a tuned instantiation (per-stencil API calls in tests).
 // Matrix lives in a caller-provided global workspace; LU with partial pivoting + row swaps.
@@ -1470,9 +1868,40 @@ static cudaError_t launch_rbf_static(const double* pos, const int* st, int64_t K
   return cudaFreeAsync(buf, s);
 }
 
-// Kernel choice (tests; 0 = default static order + flagged fallback): 100 = searching
-// kernel for every stencil; 101 = static kernel with every stencil flagged (exercises the
-// fallback: in-kernel for 2D, list mode for 3D).  The launch shapes tried while tuning are
+// Null-space kernel, then the searching kernel over the stencils it flagged (list mode).
+template <int D, int NST, int NOPS, int WARPS, int MINB, int FLPS, int FRPL>
+static cudaError_t launch_rbf_ns(const double* pos, const int* st, int64_t K, const OpSpec& ops, const double* rn,
+                                 int* oi, double* ow, int* info, cudaStream_t s, int force) {
+  bool std_ops = rn == nullptr && NOPS == D + 1 && ops.kind[0] == kOpLaplacian;
+  for (int o = 1; o < NOPS && std_ops; ++o) std_ops = ops.kind[o] == kOpPartial && ops.axis[o] == o - 1;
+  int* buf = nullptr;  // [count, list...] of flagged stencils
+  cudaError_t e = stream_alloc(reinterpret_cast<void**>(&buf), sizeof(int) * (K + 1), s);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(buf, 0, sizeof(int), s);
+  constexpr int SPW = 32 / poly_count<D>();
+  const int64_t grid = ceil_div(K, static_cast<int64_t>(WARPS) * SPW);
+  const size_t smem = sizeof(RbfNsSmem<D, NST, NOPS>) * WARPS * SPW;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<grid, WARPS * 32, smem, s>>>(pos, st, K, ops, rn, oi, ow, info, buf + 1, buf, force);
+  };
+  if constexpr (NOPS == D + 1) {
+    if (std_ops) go(rbf_ns_kernel<D, NST, NOPS, true, WARPS, MINB>);
+    else go(rbf_ns_kernel<D, NST, NOPS, false, WARPS, MINB>);
+  } else {
+    go(rbf_ns_kernel<D, NST, NOPS, false, WARPS, MINB>);
+  }
+  constexpr int FSPW = 32 / FLPS;
+  const int64_t groups = ceil_div(K, static_cast<int64_t>(4) * FSPW);
+  const int64_t cap = static_cast<int64_t>(sm_count()) * 2;
+  rbf_weights_kernel<D, NST, NOPS, FLPS, FRPL, 4, 1><<<static_cast<int>(groups < cap ? groups : cap), 128, 0, s>>>(
+      pos, st, K, ops, rn, oi, ow, info, buf + 1, buf);
+  return cudaFreeAsync(buf, s);
+}
+
+// Kernel choice (tests; 0 = default: null-space kernel + flagged fallback): 100 = searching
+// kernel for every stencil; 101 = null-space kernel with every stencil flagged (exercises
+// the list-mode fallback); 102 = the Gauss-Jordan sweep kernel (rbf_static_kernel).  The launch shapes tried while tuning are
 // recorded in DESIGN.md section 4.
 static int g_rbf_variant = 0;
 HN_EXPORT void hn_weights_rbf_set_variant(int v) { g_rbf_variant = v; }
@@ -1487,8 +1916,9 @@ static cudaError_t launch_rbf(const double* pos, const int* st, int64_t K, const
       launch_rbf_v<2, 12, NOPS, 6, 3, 4, 3>(pos, st, K, ops, rn, oi, ow, info, s);
       return cudaSuccess;
     }
-    // 2D default: pivot rows broadcast by shuffles (3D rows are 34 wide: shared memory wins)
-    return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3, false, true>(pos, st, K, ops, rn, oi, ow, info, s, force);
+    if (v == 102)  // the Gauss-Jordan sweep (pivot rows broadcast by shuffles)
+      return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3, false, true>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+    return launch_rbf_ns<2, 12, NOPS, 4, 4, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, force);
   } else if constexpr (NST == 20) {
     if (v == 100) {
       launch_rbf_v<3, 20, NOPS, 15, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s);
@@ -1496,13 +1926,17 @@ static cudaError_t launch_rbf(const double* pos, const int* st, int64_t K, const
     }
     // 3D: no look-ahead (the 34/40-wide pivot row would be a second live register row;
     // measured 2.3% (n=20) and 4.5% (n=30) faster than staging the next row early)
-    return launch_rbf_static<3, 20, NOPS, 10, 3, 4, 2, 15, 2, false, false, false>(pos, st, K, ops, rn, oi, ow, info, s, force);
+    if (v == 102)
+      return launch_rbf_static<3, 20, NOPS, 10, 3, 4, 2, 15, 2, false, false, false>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+    return launch_rbf_ns<3, 20, NOPS, 4, 4, 15, 2>(pos, st, K, ops, rn, oi, ow, info, s, force);
   } else {
     if (v == 100) {
       launch_rbf_v<3, 30, NOPS, 20, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s);
       return cudaSuccess;
     }
-    return launch_rbf_static<3, 30, NOPS, 20, 2, 4, 1, 20, 2, false, false, false>(pos, st, K, ops, rn, oi, ow, info, s, force);
+    if (v == 102)
+      return launch_rbf_static<3, 30, NOPS, 20, 2, 4, 1, 20, 2, false, false, false>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+    return launch_rbf_ns<3, 30, NOPS, 4, 2, 20, 2>(pos, st, K, ops, rn, oi, ow, info, s, force);
   }
 }
 

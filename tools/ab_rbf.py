@@ -83,7 +83,7 @@ def main():
         rows = np.nonzero(ns.kind == 1)[0]
         for n in (20, 30):
             print(f"config 4 scattered rows: K = {len(rows)} (3D n={n})", flush=True)
-            run(ns, 3, n, rows, [v for v in variants if v in (100, 0, 101)], fine=True)
+            run(ns, 3, n, rows, variants, fine=True)
 
 
 if __name__ == "__main__":
