@@ -369,7 +369,7 @@ def run_weights_bench(args, rank, world):
         "e2e": {"value": world * n_int / e2e_s, "unit": "stencils/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "api": "paper_2303_01760_b200.compute_weights(NodeSet, ops)",
                 "samples_ms": [round(1e3 * x, 3) for x in e2e_t]},
-        "roofline": ({"bound": "fp64", "kernel": f"rbf_static_kernel<{dim},{nst}>", "achieved": achieved,
+        "roofline": ({"bound": "fp64", "kernel": (f"rbf_ns_kernel<{dim},{nst}>" if dim == 3 else f"rbf_static_kernel<{dim},{nst}>"), "achieved": achieved,
                       "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                       "algorithmic": f"{fps} flop/stencil (LAPACK getrf+getrs count, SURVEY §8(d)) x {K} stencils",
                       "kernel_ms": k_ms,

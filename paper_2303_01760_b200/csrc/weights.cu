@@ -1290,34 +1290,37 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
   }
 }
 
-// ===================== null-space kernel (default for the tuned sizes) ======================
+// ===================== null-space kernel (default for the tuned 3D sizes) ======================
 // The same static null-space elimination order as rbf_static_kernel (step A: partial-
 // pivoting LU of P picks the unisolvent nodes I, nodes renumbered [I, J]), but the saddle
 // system is reduced algebraically instead of by a Gauss-Jordan sweep over all n+q rows:
-//   P^T w = c          ->  w_I = g - M^T w_J,      M^T = P_I^-T P_J^T,  g = P_I^-T c
+//   P^T w = c          ->  w_I = g - M^T w_J,      M = P_J P_I^-1 = L_J L_I^-1,  g = P_I^-T c
 //   A w + P lambda = f ->  S w_J = h - B_I g,      B = A_J: - M A_I:,   h = f_J - M f_I,
 //                          S = B_J - B_I M^T       (= Z^T A Z, SPD for r^3 on a unisolvent set)
-// (1) M^T and g by a Gauss-Jordan sweep of the q x (n + ops) block [P^T | c] with step A's
-// pivots, (2) B and h from the I rows of A (staged in shared memory), (3) S and its right-
-// hand side, (4) a q'-step Gauss-Jordan of [S | rhs] (q' = n - q, pivots on the diagonal,
-// S is SPD), (5) w_I.  One segment of q lanes per system: lane s owns node row I_s, the J
-// rows s, s + q, .. (n - q = q or 2q), monomial row s of (1) and J row(s) of (3)-(4).  The
-// fp64 work is ~7.6K lane-FMAs per 3D n = 20 system instead of the sweep's ~16.7K, every
-// matrix row lives in registers only while it is being used (no 34-wide rows per slot), and
-// stencils with a small pivot are flagged for the searching kernel as in the sweep.
+// where step A's LU of P (Pi P = L U, L = [L_I; L_J]) gives M without another elimination:
+// (1) every lane keeps its rows' step-A multipliers; M's rows by a back substitution with
+// L_I, g = L_I^-T U^-T c by two tiny substitutions, (2) B and h from the I rows of A (staged
+// in shared memory; A is symmetric, so a J row's I part is read from there too), (3) S and
+// its right-hand side, (4) a (n - q)-step Gauss-Jordan of [S | rhs] (diagonal pivots, S is
+// SPD), (5) w_I.  One segment of q lanes per system: lane s owns node row I_s and the J rows
+// s, s + q, .. (n - q = q or 2q).  Stencils with a small pivot are flagged for the searching
+// kernel as in the sweep.
 template <int D, int NST, int NOPS>
 struct RbfNsCore {
   static constexpr int NQ = poly_count<D>();
   static constexpr int NJ = NST - NQ;
   static constexpr int YS = D == 2 ? 2 : 4;
   static constexpr int NQP = (NQ + 1) & ~1;
-  double prow[2][NQP];         // step A pivot rows (P only)
+  static constexpr int NLU = NQ * NQP + NJ * NQ + NQ * NQP;  // u, lj, li
+  static constexpr int NAI = NQ * NST;                       // ai, later w and w_J
   double inv_hist[NQP];        // step A 1/pivots
   double yp[NST][YS];          // local coordinates, renumbered [I, J]
-  double ai[NQ][NST];          // A rows of the I nodes (renumbered columns); w, wj alias it later
-  double fi[NQ][NOPS];         // f rows of the I nodes
+  static constexpr int NOP2 = (NOPS + 1) & ~1;
+  double fi[NQ][NOP2];         // f rows of the I nodes (16-B rows)
   double mt[NQ][NJ];           // M^T
-  double g[NQ][NOPS];          // P_I^-T c
+  double g[NQ][NOP2];          // P_I^-T c
+  // step A's U rows | L_J rows | L_I rows, then (aliased) the I rows of A, then w and w_J
+  double work[NLU > NAI ? NLU : NAI];
   int sidp[NST];               // node ids, renumbered
 };
 template <int D, int NST, int NOPS>
@@ -1338,12 +1341,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
   constexpr int JPL = NJ / LPS;        // J rows per lane
   constexpr int SPW = 32 / LPS;
   constexpr int PA = (NST + LPS - 1) / LPS;  // step-A slots
-  constexpr int NQC = NST + NOPS;            // columns of [P^T | c]
+  constexpr int NQP = (NQ + 1) & ~1;
   static_assert(NJ % LPS == 0, "J rows spread evenly over the segment");
+  static_assert(NJ % 2 == 0 && NST % 2 == 0, "16-B shared-memory rows");
   static_assert(NST <= 31, "node bitmask");
+  static_assert(NQ * NST >= NST * NOPS + NJ * NOPS, "w and w_J alias the I rows of A");
   using Sm = RbfNsSmem<D, NST, NOPS>;
-  static_assert(sizeof(double) * NQ * NST >= sizeof(double) * NST * NOPS + sizeof(double) * NJ * NOPS,
-                "w and wj alias ai");
   extern __shared__ __align__(16) unsigned char rbf_ns_smem[];
   Sm* smem_all = reinterpret_cast<Sm*>(rbf_ns_smem);
 
@@ -1356,8 +1359,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
   const bool sys_live = lane_live && k_raw < K;
   const int64_t k = k_raw < K ? k_raw : K - 1;
   Sm& sm = smem_all[warp * SPW + sys_w];
-  double* wsm = &sm.ai[0][0];          // w[NST][NOPS] (renumbered), valid after (3)
-  double* wjs = wsm + NST * NOPS;      // w_J[NJ][NOPS]
+  double* su = sm.work;                  // U[NQ][NQP]
+  double* slj = su + NQ * NQP;           // L_J[NJ][NQ]
+  double* sli = slj + NJ * NQ;           // L_I[NQ][NQP]
+  double* sai = sm.work;                 // A_I[NQ][NST]   (after (1))
+  double* wsm = sm.work;                 // w[NST][NOPS]   (after (3))
+  double* wjs = wsm + NST * NOPS;        // w_J[NJ][NOPS]
   auto seg_lane = [&](int t) { return lane_live ? sys_w * LPS + t : lane; };
   auto seg_xor = [&](int off) {
     int t = s ^ off;
@@ -1403,29 +1410,38 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
 #pragma unroll
     for (int a = 0; a < D; ++a) yo[r][a] *= s1;
 
-  const unsigned pb0 = smem_addr(&sm.prow[0][0]);
-  const unsigned pb1 = smem_addr(&sm.prow[1][0]);
+  const unsigned ub = smem_addr(su);
   const unsigned hist = smem_addr(&sm.inv_hist[0]);
   bool bad = force_flag != 0;
 
-  // ---- step A: LU of P with partial pivoting over the nodes -> I (as rbf_static_kernel) ----
+  // ---- step A: LU of P with partial pivoting over the nodes -> I; U rows to shared memory,
+  // every row's multipliers kept (L) ----
   {
-    double pp[PA][NQ];
+    double pp[PA][NQ], lm[PA][NQ];
     unsigned vm[PA];
+    int step_of[PA];  // step that chose the slot's node (I index), -1: a J node
 #pragma unroll
     for (int r = 0; r < PA; ++r) {
       const int j = s + r * LPS;
 #pragma unroll
-      for (int m = 0; m < NQ; ++m) pp[r][m] = mono_val<D>(m, yo[r]);
+      for (int m = 0; m < NQ; ++m) {
+        pp[r][m] = mono_val<D>(m, yo[r]);
+        lm[r][m] = 0.0;
+      }
+      lm[r][0] = 1.0;  // column 0 is all ones: every row's step-0 multiplier is 1
       vm[r] = (lane_live && j < NST) ? (0x7fffffc0u | static_cast<unsigned>(63 - j)) : 0u;
+      step_of[r] = -1;
     }
     unsigned chosen = 1u;
     vm[0] = s == 0 ? 0u : vm[0];
+    if (s == 0) step_of[0] = 0;
     if (lane_live && s == 0) {
 #pragma unroll
       for (int a = 0; a < D; ++a) sm.yp[0][a] = yo[0][a];
       sm.sidp[0] = sido[0];
       sm.inv_hist[0] = 1.0;
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) su[m] = pp[0][m];  // the centre's row: [1, 0, ..] (y = 0)
     }
     static_for<NQ - 1>([&](auto mc) {
       constexpr int m = decltype(mc)::value + 1;
@@ -1436,7 +1452,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
 #pragma unroll
       for (int off = 1; off < LPS; off <<= 1) key = max(key, __shfl_sync(0xffffffffu, key, seg_xor(off)));
       const unsigned ptag = key & 63u;
-      const unsigned pbase = (m & 1) ? pb1 : pb0;
+      const unsigned pbase = ub + 8u * m * NQP;
       bool isp[PA];
 #pragma unroll
       for (int r = 0; r < PA; ++r) {
@@ -1451,41 +1467,99 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
 #pragma unroll
           for (int a = 0; a < D; ++a) sm.yp[m][a] = yo[r][a];
           sm.sidp[m] = sido[r];
+          step_of[r] = m;
         }
       }
       __syncwarp();
-      const double* prow = sm.prow[m & 1];
+      const double* prow = su + m * NQP;
       const double piv = prow[m];
       bad = bad || !(fabs(piv) >= kStaticPivMin);
       const double inv = fast_rcp(piv);
       st_pred1(lane_live && s == 0, hist + 8u * m, inv);
 #pragma unroll
       for (int r = 0; r < PA; ++r) {
-        const double l = isp[r] ? 0.0 : pp[r][m] * inv;
+        const double l = (vm[r] == 0u) ? 0.0 : pp[r][m] * inv;  // rows still unpivoted
+        if (vm[r] != 0u && !isp[r]) lm[r][m] = l;
+        const double le = isp[r] ? 0.0 : l;
         vm[r] = isp[r] ? 0u : vm[r];
 #pragma unroll
-        for (int cc = m + 1; cc < NQ; ++cc) pp[r][cc] = fma(-l, prow[cc], pp[r][cc]);
+        for (int cc = m + 1; cc < NQ; ++cc) pp[r][cc] = fma(-le, prow[cc], pp[r][cc]);
       }
       chosen |= 1u << (63u - ptag);
     });
+    // renumbered coordinates and ids of J; multiplier rows by renumbered index
 #pragma unroll
     for (int r = 0; r < PA; ++r) {
       const int j = s + r * LPS;
-      if (lane_live && j < NST && !((chosen >> j) & 1u)) {
-        const int ni = NQ + __popc(~chosen & ((1u << j) - 1u));
+      if (!(lane_live && j < NST)) continue;
+      if (!((chosen >> j) & 1u)) {
+        const int jr = __popc(~chosen & ((1u << j) - 1u));
 #pragma unroll
-        for (int a = 0; a < D; ++a) sm.yp[ni][a] = yo[r][a];
-        sm.sidp[ni] = sido[r];
+        for (int a = 0; a < D; ++a) sm.yp[NQ + jr][a] = yo[r][a];
+        sm.sidp[NQ + jr] = sido[r];
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) slj[jr * NQ + m] = lm[r][m];
+      } else {
+        const int i = step_of[r];
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) sli[i * NQP + m] = m < i ? lm[r][m] : (m == i ? 1.0 : 0.0);
       }
     }
   }
   __syncwarp();
 
-  // ---- the I row of A and f (node I_s) -> shared memory ----
-  double yI[D];
+  // ---- (1) M rows (J rows of mine) by back substitution with L_I; g = L_I^-T U^-T c ----
+  // (right-looking: a finished unknown updates every pending one at once, so the dependent
+  // chain is q FMAs deep instead of q(q-1)/2)
+  double mj[JPL][NQ];
 #pragma unroll
-  for (int a = 0; a < D; ++a) yI[a] = sm.yp[s][a];
+  for (int r = 0; r < JPL; ++r) {
+    const int jr = s + r * LPS;
+#pragma unroll
+    for (int i = 0; i < NQ; i += 2) {
+      const double2 lv = *reinterpret_cast<const double2*>(slj + jr * NQ + i);
+      mj[r][i] = lv.x;
+      if (i + 1 < NQ) mj[r][i + 1] = lv.y;
+    }
+#pragma unroll
+    for (int i = NQ - 1; i > 0; --i)
+#pragma unroll
+      for (int i2 = 0; i2 < i; ++i2) mj[r][i2] = fma(-mj[r][i], sli[i * NQP + i2], mj[r][i2]);
+#pragma unroll
+    for (int i = 0; i < NQ; ++i)
+      if (lane_live) sm.mt[i][jr] = mj[r][i];
+  }
+  if (s < NOPS) {  // lane s: column o = s of g, U^T z = c forward then L_I^T g = z backward
+    double z[NQ];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) {
+      double cv = 0.0;
+#pragma unroll
+      for (int o = 0; o < NOPS; ++o)
+        if (o == s) cv = STD ? std_poly_rhs<D>(o, m) : poly_rhs<D>(ops, o, m, use_rn, rn);
+      z[m] = cv;
+    }
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) {  // right-looking: z[m] final, update the pending ones
+      z[m] *= sm.inv_hist[m];
+#pragma unroll
+      for (int m2 = m + 1; m2 < NQ; ++m2) z[m2] = fma(-su[m * NQP + m2], z[m], z[m2]);
+    }
+#pragma unroll
+    for (int i = NQ - 1; i > 0; --i)
+#pragma unroll
+      for (int m = 0; m < i; ++m) z[m] = fma(-sli[i * NQP + m], z[i], z[m]);
+#pragma unroll
+    for (int m = 0; m < NQ; ++m)
+      if (lane_live) sm.g[m][s] = z[m];
+  }
+  __syncwarp();  // U and L are dead: the I rows of A take their place
+
+  // ---- the I row of A and f (node I_s) -> shared memory ----
   {
+    double yI[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) yI[a] = sm.yp[s][a];
     const double rI = norm_fast<D>(yI);
 #pragma unroll
     for (int o = 0; o < NOPS; ++o) {
@@ -1510,46 +1584,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
           v[h] = cube_from_sq(d2);
         }
       }
-      if (cc + 1 < NST) st_pred2(lane_live, smem_addr(&sm.ai[s][cc]), v[0], v[1]);
-      else st_pred1(lane_live, smem_addr(&sm.ai[s][cc]), v[0]);
+      if (cc + 1 < NST) st_pred2(lane_live, smem_addr(sai + s * NST + cc), v[0], v[1]);
+      else st_pred1(lane_live, smem_addr(sai + s * NST + cc), v[0]);
     }
-  }
-
-  // ---- (1) [P^T | c] -> [diag | M^T | g] by Gauss-Jordan with step A's pivot order ----
-  {
-    double q[NQC];
-#pragma unroll
-    for (int cc = 0; cc < NST; ++cc) {
-      double y[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) y[a] = sm.yp[cc][a];
-      q[cc] = mono_val_sel<D>(s, y);
-    }
-#pragma unroll
-    for (int o = 0; o < NOPS; ++o) q[NST + o] = STD ? std_poly_rhs<D>(o, s) : poly_rhs<D>(ops, o, s, use_rn, rn);
-    static_for<NQ>([&](auto kc) {
-      constexpr int kk = decltype(kc)::value;
-      const int src = seg_lane(kk);
-      const double piv = __shfl_sync(0xffffffffu, q[kk], src);
-      bad = bad || !(fabs(piv) >= 0.5 * kStaticPivMin);
-      const double l = s == kk ? 0.0 : q[kk] * fast_rcp(piv);
-#pragma unroll
-      for (int cc = kk + 1; cc < NQC; ++cc) {
-        const double pv = __shfl_sync(0xffffffffu, q[cc], src);
-        q[cc] = fma(-l, pv, q[cc]);
-      }
-      if (s != kk) q[kk] = 0.0;
-    });
-    double own = 0.0;
-#pragma unroll
-    for (int m = 0; m < NQ; ++m) own = s == m ? q[m] : own;
-    const double inv = fast_rcp(own);
-#pragma unroll
-    for (int j = 0; j < NJ; ++j)
-      if (lane_live) sm.mt[s][j] = q[NQ + j] * inv;
-#pragma unroll
-    for (int o = 0; o < NOPS; ++o)
-      if (lane_live) sm.g[s][o] = q[NST + o] * inv;
   }
   __syncwarp();
 
@@ -1569,7 +1606,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
       else h[o] = phs_rhs<D>(ops, o, yJ, rJ, use_rn, rn);
     }
 #pragma unroll
-    for (int cc = 0; cc < NST; ++cc) {
+    for (int i = 0; i < NQ; ++i) b[i] = sai[i * NST + NQ + jr];  // A symmetric: A[J][I_i] = A[I_i][J]
+#pragma unroll
+    for (int cc = NQ; cc < NST; ++cc) {
       double d2 = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
@@ -1581,19 +1620,27 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
     // B row = A_J row - sum_i M[j][i] A_I row i;  h = f_J - sum_i M[j][i] f_I row i
 #pragma unroll
     for (int i = 0; i < NQ; ++i) {
-      const double mji = sm.mt[i][jr];
+      const double mji = mj[r][i];
 #pragma unroll
       for (int cc = 0; cc < NST; cc += 2) {
         if (cc + 1 < NST) {
-          const double2 av = *reinterpret_cast<const double2*>(&sm.ai[i][cc]);
+          const double2 av = *reinterpret_cast<const double2*>(sai + i * NST + cc);
           b[cc] = fma(-mji, av.x, b[cc]);
           b[cc + 1] = fma(-mji, av.y, b[cc + 1]);
         } else {
-          b[cc] = fma(-mji, sm.ai[i][cc], b[cc]);
+          b[cc] = fma(-mji, sai[i * NST + cc], b[cc]);
         }
       }
 #pragma unroll
-      for (int o = 0; o < NOPS; ++o) h[o] = fma(-mji, sm.fi[i][o], h[o]);
+      for (int o = 0; o < NOPS; o += 2) {
+        if (o + 1 < NOPS) {
+          const double2 fv = *reinterpret_cast<const double2*>(&sm.fi[i][o]);
+          h[o] = fma(-mji, fv.x, h[o]);
+          h[o + 1] = fma(-mji, fv.y, h[o + 1]);
+        } else {
+          h[o] = fma(-mji, sm.fi[i][o], h[o]);
+        }
+      }
     }
     // S row = B_J - B_I M^T;  rhs = h - B_I g
 #pragma unroll
@@ -1604,12 +1651,24 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
     for (int i = 0; i < NQ; ++i) {
       const double bi = b[i];
 #pragma unroll
-      for (int jj = 0; jj < NJ; ++jj) S[r][jj] = fma(-bi, sm.mt[i][jj], S[r][jj]);
+      for (int jj = 0; jj < NJ; jj += 2) {
+        const double2 mv = *reinterpret_cast<const double2*>(&sm.mt[i][jj]);
+        S[r][jj] = fma(-bi, mv.x, S[r][jj]);
+        S[r][jj + 1] = fma(-bi, mv.y, S[r][jj + 1]);
+      }
 #pragma unroll
-      for (int o = 0; o < NOPS; ++o) R[r][o] = fma(-bi, sm.g[i][o], R[r][o]);
+      for (int o = 0; o < NOPS; o += 2) {
+        if (o + 1 < NOPS) {
+          const double2 gv = *reinterpret_cast<const double2*>(&sm.g[i][o]);
+          R[r][o] = fma(-bi, gv.x, R[r][o]);
+          R[r][o + 1] = fma(-bi, gv.y, R[r][o + 1]);
+        } else {
+          R[r][o] = fma(-bi, sm.g[i][o], R[r][o]);
+        }
+      }
     }
   }
-  __syncwarp();  // ai is dead from here on: w / wj alias it
+  __syncwarp();  // the I rows of A are dead from here on: w / w_J take their place
 
   // ---- (4) Gauss-Jordan on [S | rhs], diagonal pivots (S is SPD) ----
   static_for<NJ>([&](auto kc) {
@@ -1900,8 +1959,9 @@ static cudaError_t launch_rbf_ns(const double* pos, const int* st, int64_t K, co
 }
 
 // Kernel choice (tests; 0 = default: null-space kernel + flagged fallback): 100 = searching
-// kernel for every stencil; 101 = null-space kernel with every stencil flagged (exercises
-// the list-mode fallback); 102 = the Gauss-Jordan sweep kernel (rbf_static_kernel).  The launch shapes tried while tuning are
+// kernel for every stencil; 101 = default kernel with every stencil flagged (exercises the
+// fallback); 102 = the Gauss-Jordan sweep kernel (rbf_static_kernel) in 3D; 103 = the
+// null-space kernel in 2D.  The launch shapes tried while tuning are
 // recorded in DESIGN.md section 4.
 static int g_rbf_variant = 0;
 HN_EXPORT void hn_weights_rbf_set_variant(int v) { g_rbf_variant = v; }
@@ -1916,9 +1976,10 @@ static cudaError_t launch_rbf(const double* pos, const int* st, int64_t K, const
       launch_rbf_v<2, 12, NOPS, 6, 3, 4, 3>(pos, st, K, ops, rn, oi, ow, info, s);
       return cudaSuccess;
     }
-    if (v == 102)  // the Gauss-Jordan sweep (pivot rows broadcast by shuffles)
-      return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3, false, true>(pos, st, K, ops, rn, oi, ow, info, s, 0);
-    return launch_rbf_ns<2, 12, NOPS, 4, 4, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, force);
+    // 2D: the Gauss-Jordan sweep with pivot rows broadcast by shuffles (config 1: 86 us; the
+    // null-space kernel, variant 103, is 6 % slower at this size: 6 lanes per system)
+    if (v == 103) return launch_rbf_ns<2, 12, NOPS, 4, 4, 6, 3>(pos, st, K, ops, rn, oi, ow, info, s, 0);
+    return launch_rbf_static<2, 12, NOPS, 6, 3, 4, 4, 6, 3, false, true>(pos, st, K, ops, rn, oi, ow, info, s, force);
   } else if constexpr (NST == 20) {
     if (v == 100) {
       launch_rbf_v<3, 20, NOPS, 15, 2, 4, 1>(pos, st, K, ops, rn, oi, ow, info, s);

@@ -501,10 +501,11 @@ def test_all_boundary_node_set_gives_empty_rows():
 # ---------------------------------------------------------------- RBF kernel variants
 @pytest.mark.parametrize("dim,n", [(2, 12), (3, 20), (3, 30)])
 def test_rbf_static_order_and_fallbacks_match_dgesv(dim, n):
-    """The static null-space elimination (default), the partial-pivoting searching kernel
-    (variant 100) and the static kernel with every stencil flagged (variant 101: in-kernel
-    fallback in 2D, list-mode second launch in 3D) all match dgesv; the flagged path is
-    bit-identical to the searching kernel."""
+    """The default kernel (2D: static-order Gauss-Jordan sweep; 3D: null-space reduction to
+    Z^T A Z), the partial-pivoting searching kernel (variant 100), the default kernel with
+    every stencil flagged (variant 101: in-kernel fallback in 2D, list-mode second launch in
+    3D), the 3D sweep (102) and the 2D null-space kernel (103) all match dgesv; the flagged
+    path is bit-identical to the searching kernel."""
     from paper_2303_01760_b200 import _lib as L
     from paper_2303_01760_b200._device import DeviceNodes
 
@@ -528,7 +529,7 @@ def test_rbf_static_order_and_fallbacks_match_dgesv(dim, n):
     want = np.take_along_axis(want, order[:, :, None], 1)
     res = {}
     try:
-        for v in (0, 100, 101):
+        for v in (0, 100, 101, 102, 103):
             L.lib().hn_weights_rbf_set_variant(v)
             oi = L.empty((n, K), t.int32)
             ow = L.empty((nops, n, K), t.float64)
