@@ -198,7 +198,7 @@ class LaunchCounter:
     KERNELS = {"hn_celllist_build": 5, "hn_partition_methods": 6, "hn_sptrsv_super": 2,
                "hn_knn": 1, "hn_knn_spacing": 1, "hn_classify": 1, "hn_mon_stencils": 1, "hn_weights_mon": 2,
                "hn_weights_rbf": 1, "hn_apply_ell": 1, "hn_momentum": 1, "hn_div_rhs": 1,
-               "hn_correct_temperature": 1, "hn_temperature_bc": 2, "hn_csr_matvec": 1, "hn_csr_residual": 1,
+               "hn_correct_temperature": 1, "hn_temperature_bc": 1, "hn_csr_matvec": 1, "hn_csr_residual": 1,
                "hn_pressure_solve": 31, "hn_permute": 1, "hn_reduce": 2, "hn_bicg_update": 1, "hn_bench_dfma": 1}
 
     def __init__(self, L):

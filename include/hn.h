@@ -206,19 +206,20 @@ int hn_correct_temperature(int nbins, const int64_t* bin_K_host, const int* bin_
                            const double* hyper_lap2, void* stream);
 
 /* T[dir_idx] = dir_val; T[neu_idx[r]] = -(W_r . t0) / neu_diag[r], t0 = T with Neumann
- * entries zeroed (is_neu mask).  flags (nullable, the K10 pair): a non-finite Neumann value
- * sets flags[0] and lowers flags[1] to its node.  Replaces: apply_temperature_bc
- * solver.py:334-342. */
+ * entries zeroed (is_neu mask); one launch.  flags (nullable, the K10 words + a block
+ * counter, int[3]): a non-finite Neumann value sets flags[0] and lowers flags[1] to its
+ * node.  latch (nullable): the last block to finish also applies hn_step_latch (then flags
+ * is required).  Replaces: apply_temperature_bc solver.py:334-342 (+ the per-step probe). */
 int hn_temperature_bc(const int* dir_idx, const double* dir_val, int64_t ndir, const int64_t* neu_rowptr,
                       const int* neu_cols, const double* neu_vals, const int* neu_idx,
                       const double* neu_diag, const uint8_t* is_neu, int64_t nneu, double* T,
-                      int* flags, void* stream);
+                      int* flags, int* latch, const int* pstatus, void* stream);
 
-/* End-of-step latch of the finite probe: latch = [steps done, first non-finite step (0 = none),
- * lowest non-finite temperature node of that step (INT_MAX = none)]; clears flags.  Lets the
- * host read the probe every nu_stride steps and still report the reference's step and node.
- * Replaces: the per-step probe of run() solver.py:448-452. */
-int hn_step_latch(int* flags, int* latch, const int* pstatus, void* stream);
+/* (The end-of-step latch of the finite probe rides on hn_temperature_bc: latch = [steps done,
+ * first non-finite step (0 = none), lowest non-finite temperature node of that step (INT_MAX =
+ * none), first step whose pressure solve reported info != 0, that info]; flags cleared.  Lets
+ * the host read the probe every nu_stride steps and still report the reference's step and
+ * node.  Replaces: the per-step probe of run() solver.py:448-452.) */
 
 /* y = A x / y = b - A x for a CSR matrix (int64 rowptr), scipy csr_matvec order. */
 int hn_csr_matvec(const int64_t* rowptr, const int* cols, const double* vals, const double* x,

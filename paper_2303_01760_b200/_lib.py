@@ -65,8 +65,7 @@ SIGNATURES: dict[str, tuple] = {
                         _vp, _i64, _d, _vp, _vp]),
     "hn_correct_temperature": (_i, [_i, _c_i64_p, _c_int_p, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i,
                                     _c_int_p, _i, _vp, _vp, _vp, _i64, _d, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "hn_temperature_bc": (_i, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
-    "hn_step_latch": (_i, [_vp, _vp, _vp, _vp]),
+    "hn_temperature_bc": (_i, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "hn_csr_matvec": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "hn_csr_residual": (_i, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "hn_sptrsv_super": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp,

@@ -338,12 +338,6 @@ static bool fused_pair(const StepBins& b, int d, int* wa, int* wb) {
 }
 
 // ---- K11: temperature boundary conditions (solver.py:334-342) ----
-__global__ void dirichlet_kernel(const int* __restrict__ idx, const double* __restrict__ val, int64_t n,
-                                 double* __restrict__ T) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) T[idx[i]] = val[i];
-}
-
 // Insulated rows: T[b] = -(sum_j W_bj t0_j) / W_bb with t0 = T, Neumann entries zeroed.
 // The Neumann block W[:, neu] is diagonal (boundary stencils exclude every other
 // boundary node), so SuperLU's solve of it is an elementwise division.
@@ -397,21 +391,45 @@ __device__ __forceinline__ double csr_row_seq32_neu(const int* __restrict__ cols
   return acc;
 }
 
-__global__ void neumann_kernel(const int64_t* __restrict__ rowptr, const int* __restrict__ cols,
-                               const double* __restrict__ vals, const int* __restrict__ neu_idx,
-                               const double* __restrict__ diag, const uint8_t* __restrict__ is_neu, int64_t nrows,
-                               double* __restrict__ T, int* __restrict__ flags) {
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= nrows) return;
-  const int64_t e0 = __ldg(rowptr + r), e1 = __ldg(rowptr + r + 1);
-  const double acc = e1 - e0 <= 32 ? csr_row_seq32_neu(cols, vals, T, is_neu, e0, static_cast<int>(e1 - e0))
-                                   : csr_row_seq<true>(cols, vals, T, is_neu, e0, e1);
-  const double t = __ddiv_rn(-acc, diag[r]);
-  const int node = neu_idx[r];
-  T[node] = t;
-  if (flags && !isfinite(t)) {  // the reference probes T after its boundary conditions (solver.py:448-452)
-    atomicOr(flags, 1);
-    atomicMin(flags + 1, node);
+// Dirichlet rows (threads [0, ndir)) and Neumann rows (threads [ndir, ndir + nneu)) in one
+// launch -- they are independent: boundary stencils exclude every other boundary node, so a
+// Neumann row never reads a Dirichlet value -- and, with a latch, the end-of-step latch by
+// the last block to finish (flags[2] counts finished blocks, reset by that block).
+__device__ __forceinline__ void latch_apply(int* __restrict__ flags, int* __restrict__ latch,
+                                            const int* __restrict__ pstatus);
+
+__global__ void temperature_bc_kernel(const int* __restrict__ dir_idx, const double* __restrict__ dir_val,
+                                      int64_t ndir, const int64_t* __restrict__ rowptr, const int* __restrict__ cols,
+                                      const double* __restrict__ vals, const int* __restrict__ neu_idx,
+                                      const double* __restrict__ diag, const uint8_t* __restrict__ is_neu,
+                                      int64_t nneu, double* __restrict__ T, int* __restrict__ flags,
+                                      int* __restrict__ latch, const int* __restrict__ pstatus) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < ndir) {
+    T[dir_idx[i]] = dir_val[i];
+  } else if (i < ndir + nneu) {
+    const int64_t r = i - ndir;
+    const int64_t e0 = __ldg(rowptr + r), e1 = __ldg(rowptr + r + 1);
+    const double acc = e1 - e0 <= 32 ? csr_row_seq32_neu(cols, vals, T, is_neu, e0, static_cast<int>(e1 - e0))
+                                     : csr_row_seq<true>(cols, vals, T, is_neu, e0, e1);
+    const double t = __ddiv_rn(-acc, diag[r]);
+    const int node = neu_idx[r];
+    T[node] = t;
+    if (flags && !isfinite(t)) {  // the reference probes T after its boundary conditions (solver.py:448-452)
+      atomicOr(flags, 1);
+      atomicMin(flags + 1, node);
+    }
+  }
+  if (!latch) return;
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(flags + 2, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    latch_apply(flags, latch, pstatus);
+    flags[2] = 0;
   }
 }
 
@@ -420,7 +438,8 @@ __global__ void neumann_kernel(const int64_t* __restrict__ rowptr, const int* __
 // probe reports it (solver.py:448-452); then clear the per-step flags.
 // latch = [steps completed, first bad step (0: none), its node (INT_MAX: none in T),
 //          first step whose pressure solve reported info != 0 (0: none), that info].
-__global__ void step_latch_kernel(int* __restrict__ flags, int* __restrict__ latch, const int* __restrict__ pstatus) {
+__device__ __forceinline__ void latch_apply(int* __restrict__ flags, int* __restrict__ latch,
+                                            const int* __restrict__ pstatus) {
   const int s = latch[0] + 1;
   latch[0] = s;
   if (flags[0] && latch[1] == 0) {
@@ -620,26 +639,18 @@ HN_EXPORT int hn_correct_temperature(int nbins, const int64_t* bin_K_host, const
 HN_EXPORT int hn_temperature_bc(const int* dir_idx, const double* dir_val, int64_t ndir, const int64_t* neu_rowptr,
                                 const int* neu_cols, const double* neu_vals, const int* neu_idx,
                                 const double* neu_diag, const uint8_t* is_neu, int64_t nneu, double* T,
-                                int* flags, void* stream) {
-  cudaStream_t s = as_stream(stream);
-  const int th = 256;
-  if (ndir > 0) {
-    dirichlet_kernel<<<ceil_div(ndir, th), th, 0, s>>>(dir_idx, dir_val, ndir, T);
-    HN_CHECK_LAUNCH();
-  }
-  if (nneu > 0) {
-    neumann_kernel<<<ceil_div(nneu, th), th, 0, s>>>(neu_rowptr, neu_cols, neu_vals, neu_idx, neu_diag, is_neu, nneu, T,
-                                                     flags);
-    HN_CHECK_LAUNCH();
-  }
-  return 0;
-}
-
-HN_EXPORT int hn_step_latch(int* flags, int* latch, const int* pstatus, void* stream) {
-  step_latch_kernel<<<1, 1, 0, as_stream(stream)>>>(flags, latch, pstatus);
+                                int* flags, int* latch, const int* pstatus, void* stream) {
+  if (latch && !flags) return 1;
+  const int64_t n = ndir + nneu;
+  if (n == 0 && !latch) return 0;
+  const int th = 128;
+  temperature_bc_kernel<<<n > 0 ? ceil_div(n, th) : 1, th, 0, as_stream(stream)>>>(
+      dir_idx, dir_val, ndir, neu_rowptr, neu_cols, neu_vals, neu_idx, neu_diag, is_neu, nneu, T, flags, latch,
+      pstatus);
   HN_CHECK_LAUNCH();
   return 0;
 }
+
 
 HN_EXPORT int hn_csr_matvec(const int64_t* rowptr, const int* cols, const double* vals, const double* x,
                             int64_t nrows, double* y, void* stream) {

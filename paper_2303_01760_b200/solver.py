@@ -540,15 +540,15 @@ def _correct_temp_dev(ops: OperatorSet, vstar_soa, p, T, dt: float, vout, Tout, 
            L.ptr(hc), L.ptr(l2), L.stream_handle())
 
 
-def _temperature_bc_dev(ops: OperatorSet, T, flags=None):
+def _temperature_bc_dev(ops: OperatorSet, T, flags=None, latch=None, pstatus=None):
+    """K11 in one launch; with `latch` (and int32[3] flags) the end-of-step latch rides along."""
     nd = len(ops.dirichlet_idx)
-    if ops._d_neu is not None:
-        L.call("hn_temperature_bc", L.ptr(ops._d_dir_idx), L.ptr(ops._d_dir_val), nd, L.ptr(ops._d_neu.rowptr),
-               L.ptr(ops._d_neu.cols), L.ptr(ops._d_neu.vals), L.ptr(ops._d_neu_idx), L.ptr(ops._d_neu_diag),
-               L.ptr(ops._d_is_neu), len(ops.neumann_idx), L.ptr(T), L.ptr(flags), L.stream_handle())
-    else:
-        L.call("hn_temperature_bc", L.ptr(ops._d_dir_idx), L.ptr(ops._d_dir_val), nd, None, None, None, None, None,
-               None, 0, L.ptr(T), None, L.stream_handle())
+    neu = ops._d_neu
+    L.call("hn_temperature_bc", L.ptr(ops._d_dir_idx), L.ptr(ops._d_dir_val), nd,
+           L.ptr(neu.rowptr if neu else None), L.ptr(neu.cols if neu else None), L.ptr(neu.vals if neu else None),
+           L.ptr(ops._d_neu_idx if neu else None), L.ptr(ops._d_neu_diag if neu else None),
+           L.ptr(ops._d_is_neu if neu else None), len(ops.neumann_idx) if neu else 0, L.ptr(T), L.ptr(flags),
+           L.ptr(latch), L.ptr(pstatus), L.stream_handle())
     return T
 
 
@@ -797,7 +797,7 @@ class DeviceStepper:
         self.T_next = L.empty(n, t.float64)
         self.rhs = L.empty(n + 1, t.float64)
         self.status = L.zeros(2, t.int32)
-        self.flags = L.to_device(np.array([0, INT32_MAX], dtype=np.int32))
+        self.flags = L.to_device(np.array([0, INT32_MAX, 0], dtype=np.int32))  # [bad, node, blocks done]
         # [steps done, first non-finite step (0: none), its lowest non-finite T node, first step
         # whose BiCGStab failed (0: none), its info] (hn_step_latch)
         self.latch = L.to_device(np.array([0, 0, INT32_MAX, 0, 0], dtype=np.int32))
@@ -819,8 +819,7 @@ class DeviceStepper:
         ops = self.ops
         _correct_temp_dev(ops, self.vstar, self.p, self.T, self.dt, self.v_next, self.T_next, self.flags,
                           self.params.dissipation)
-        _temperature_bc_dev(ops, self.T_next, self.flags)
-        L.call("hn_step_latch", L.ptr(self.flags), L.ptr(self.latch), L.ptr(pstatus), L.stream_handle())
+        _temperature_bc_dev(ops, self.T_next, self.flags, self.latch, pstatus)  # + end-of-step latch
 
     def _body(self):
         """Unchecked step (graph body): warm-started device solve, status -> latch."""
@@ -869,9 +868,23 @@ class DeviceStepper:
 
     def explicit_step(self):
         """The explicit part of a step only (K7, K8, K10, K11) with the pressure held at its
-        current value -- for measuring the HBM-bound kernels in isolation (bench)."""
-        self._explicit_front()
-        self._explicit_back(None)
+        current value -- for measuring the HBM-bound kernels in isolation (bench).  Replayed
+        as a CUDA graph like the full step, so host launch latency does not enter."""
+        t = L.torch()
+        self.stream.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(self.stream):
+            key = ("explicit", self.v.data_ptr())
+            g = self._graphs.get(key)
+            if g is None:
+                self._explicit_front()  # eager once (lazy caches, e.g. hyper-dissipation)
+                self._explicit_back(None)
+                g = t.cuda.CUDAGraph()
+                with t.cuda.graph(g, stream=self.stream, capture_error_mode="relaxed"):
+                    self._explicit_front()
+                    self._explicit_back(None)
+                self._graphs[key] = g
+            g.replay()
+        t.cuda.current_stream().wait_stream(self.stream)
         self.v, self.v_next = self.v_next, self.v
         self.T, self.T_next = self.T_next, self.T
 
