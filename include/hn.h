@@ -70,15 +70,17 @@ int hn_knn_spacing(const double* pos, int d, const double* lo_host, double cell,
                    const int* queries, const double* qpos, int64_t nq, int n, const uint8_t* exclude,
                    const double* spacing, int* out_idx, double* out_dist, void* stream);
 
-/* kNN kernel variant (tuning knob, identical results): 0 box pass + exact ring fallback
- * (default), 1 ring traversal only, 2/3 box pass with a smaller/larger first radius. */
+/* kNN kernel variant (tuning knob, identical results): 0 default (3D: warp-per-query kernel +
+ * box-pass fallback list; 2D: box pass + exact ring fallback), 1 ring traversal only, 2/3 box
+ * pass with a smaller/larger first radius, 5 box pass only. */
 void hn_knn_set_variant(int v);
 
 /* compute_weights' whole device sequence in one call: classify -> partition [MON | RBF |
- * NONE] -> (class sizes: k_rbf_host >= 0 when the caller knows them -- no regular node --
+ * NONE] -> (class sizes: k_mon_host / k_rbf_host when the caller knows them, k_rbf_host >= 0
+ * -- no regular node, or a frozen replay; the call is then capturable in a CUDA graph --
  * else one read-back) -> MON stencils + solves -> kNN (spacing-sized, on the given grid) +
- * RBF-FD solves -> WeightTable layout (tab_*) -> async copy into pinned host memory (h_*,
- * skipped when h_idx is NULL).  Bins are written with stride K into capacity buffers;
+ * RBF-FD solves -> WeightTable layout (tab_*, skipped when tab_idx is NULL: the caller keeps
+ * the ELL bins) -> async copy into pinned host memory (h_*, skipped when h_idx is NULL).  Bins are written with stride K into capacity buffers;
  * counts_host (host, 3) receives (K_mon, K_rbf, K_none); summary (device, 4 int) and its
  * copy h_summary (pinned, may be NULL) = [MON singular count, first MON row, RBF count,
  * first RBF row].  chunks > 1 splits the RBF rows into node-ordered chunks whose table
@@ -91,7 +93,7 @@ int hn_weights_pipeline(const double* pos, int d, int64_t n, const int8_t* kind,
                         const int* lattice_grid, const int* grid_dims_host, const double* lo_host, double cell,
                         const int* dims_host, const int* cell_start, const int* cell_items, const double* cell_pos,
                         const double* spacing, int nops, const int* op_kind_host, const int* op_axis_host,
-                        const double* op_normal_host, int n_rbf, int64_t k_rbf_host, int8_t* method, int* rows,
+                        const double* op_normal_host, int n_rbf, int64_t k_mon_host, int64_t k_rbf_host, int8_t* method, int* rows,
                         int* counts, int* part_scratch, int* mon_st, int* mon_idx, double* mon_w, int* mon_info,
                         int* rbf_st, int* rbf_idx, double* rbf_w, int* rbf_info, int64_t* tab_idx,
                         int64_t* tab_sizes, double* tab_w, int64_t* h_idx, int64_t* h_sizes, double* h_w,

@@ -42,7 +42,7 @@ SIGNATURES: dict[str, tuple] = {
     "hn_knn_spacing": (_i, [_vp, _i, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp, _vp, _vp, _i64, _i, _vp, _vp, _vp, _vp,
                             _vp]),
     "hn_weights_pipeline": (_i, [_vp, _i, _i64, _vp, _vp, _vp, _c_int_p, _c_dbl_p, _d, _c_int_p, _vp, _vp, _vp,
-                                 _vp, _i, _c_int_p, _c_int_p, _c_dbl_p, _i, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                 _vp, _i, _c_int_p, _c_int_p, _c_dbl_p, _i, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64_p, _vp,
                                  _vp, _i, _c_i64_p, _vp]),
     "hn_classify": (_i, [_vp, _vp, _vp, _c_int_p, _i64, _i, _vp, _vp]),

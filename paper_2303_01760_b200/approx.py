@@ -442,9 +442,11 @@ def _native_ok(nodeset, ops, n_rbf: int | None = None) -> bool:
         L.lib().hn_weights_rbf_is_tuned(dim, n_rbf, len(list(ops))) == 0
 
 
-def _interior_native(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
-    """_interior_device_table(host_copy=True) as one native call (hn_weights_pipeline): the
-    same library kernels in the same order, without the per-stage Python host work."""
+def _interior_native(nodeset, ops, n_rbf: int | None = None, host_copy: bool = True) -> DeviceTable:
+    """The public orchestration as one native call (hn_weights_pipeline): classify ->
+    partition -> MON stencils + solves -> kNN + RBF-FD solves, plus (host_copy) the padded
+    WeightTable layout and its overlapped copy into pinned host memory.  host_copy=False
+    keeps the ELL bins in HBM (operator assembly)."""
     dim = nodeset.dim
     n = len(nodeset)
     n_rbf = RBF_SIZE[dim] if n_rbf is None else n_rbf
@@ -467,20 +469,23 @@ def _interior_native(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
     pool_i = L.empty(sum(i32_sizes), t.int32)
     rows, counts, scratch, mon_st, mon_idx, mon_info, rbf_st, rbf_idx, rbf_info, summary = \
         t.split(pool_i, i32_sizes)
-    pool_f = L.empty(nops * nmon * cap_mon + nops * n_rbf * cap_rbf + nops * max(n, 1) * n_rbf, t.float64)
-    mon_w, rbf_w, d_w = t.split(pool_f, [nops * nmon * cap_mon, nops * n_rbf * cap_rbf, nops * max(n, 1) * n_rbf])
-    pool_l = L.empty(max(n, 1) * (n_rbf + 1), t.int64)
-    d_idx, d_sizes = pool_l[: max(n, 1) * n_rbf], pool_l[max(n, 1) * n_rbf:]
+    tab = nops * max(n, 1) * n_rbf if host_copy else 0
+    pool_f = L.empty(nops * nmon * cap_mon + nops * n_rbf * cap_rbf + tab, t.float64)
+    mon_w, rbf_w, d_w = t.split(pool_f, [nops * nmon * cap_mon, nops * n_rbf * cap_rbf, tab])
     method = L.empty(max(n, 1), t.int8)
-    h_l = t.empty(max(n, 1) * (n_rbf + 1), dtype=t.int64, pin_memory=True)
-    h_w = t.empty((nops, max(n, 1), n_rbf), dtype=t.float64, pin_memory=True)
     h_small = t.empty(16 + max(n, 1), dtype=t.int8, pin_memory=True)  # 4 int32 summary + method
-    h_idx, h_sizes = h_l[: max(n, 1) * n_rbf].view(max(n, 1), n_rbf), h_l[max(n, 1) * n_rbf:]
     h_sum, h_m = h_small[:16].view(t.int32), h_small[16:]
+    d_idx = d_sizes = h_idx = h_sizes = h_w = None
+    if host_copy:
+        pool_l = L.empty(max(n, 1) * (n_rbf + 1), t.int64)
+        d_idx, d_sizes = pool_l[: max(n, 1) * n_rbf], pool_l[max(n, 1) * n_rbf:]
+        h_l = t.empty(max(n, 1) * (n_rbf + 1), dtype=t.int64, pin_memory=True)
+        h_w = t.empty((nops, max(n, 1), n_rbf), dtype=t.float64, pin_memory=True)
+        h_idx, h_sizes = h_l[: max(n, 1) * n_rbf].view(max(n, 1), n_rbf), h_l[max(n, 1) * n_rbf:]
     kinds, axes, normals = _op_args(ops, dim)
     cnt = (L.C.c_int64 * 3)()
     # node-ordered RBF chunks: each chunk's table slice is copied back while the next computes
-    chunks = NATIVE_CHUNKS if k_rbf_host != 0 else 1
+    chunks = NATIVE_CHUNKS if (k_rbf_host != 0 and host_copy) else 1
     cut = None
     if bnd is not None and chunks > 1 and k_rbf_host > 0:
         kb = (k_rbf_host * np.arange(1, chunks)) // chunks
@@ -489,7 +494,7 @@ def _interior_native(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
     L.call("hn_weights_pipeline", L.ptr(dn.pos), dim, n, L.ptr(dn.kind), L.ptr(dn.lattice_idx if has_lat else None),
            L.ptr(dn.lattice_grid if has_lat else None), L.host_ints(dn.grid_dims if has_lat else [1, 1, 1]),
            L.host_dbls(dn.lo), g.cell, L.host_ints(g.dims), L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos),
-           L.ptr(dn.spacing), nops, kinds, axes, normals, n_rbf, k_rbf_host, L.ptr(method), L.ptr(rows),
+           L.ptr(dn.spacing), nops, kinds, axes, normals, n_rbf, 0, k_rbf_host, L.ptr(method), L.ptr(rows),
            L.ptr(counts), L.ptr(scratch), L.ptr(mon_st), L.ptr(mon_idx), L.ptr(mon_w), L.ptr(mon_info),
            L.ptr(rbf_st), L.ptr(rbf_idx), L.ptr(rbf_w), L.ptr(rbf_info), L.ptr(d_idx), L.ptr(d_sizes), L.ptr(d_w),
            L.ptr(h_idx), L.ptr(h_sizes), L.ptr(h_w), L.ptr(h_m), cnt, L.ptr(summary), L.ptr(h_sum),
@@ -497,7 +502,8 @@ def _interior_native(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
     k_mon, k_rbf, k_none = int(cnt[0]), int(cnt[1]), int(cnt[2])
     chunks = max(1, min(chunks, k_rbf, 64)) if k_rbf else 1
     kb = [(k_rbf * c) // chunks for c in range(chunks + 1)]
-    L.TRAFFIC["d2h"] += h_idx.nbytes + h_sizes.nbytes + h_w.nbytes + n + 16
+    if host_copy:
+        L.TRAFFIC["d2h"] += h_idx.nbytes + h_sizes.nbytes + h_w.nbytes + n + 16
     bins = []
     if k_mon:
         b = Bin(None, nmon, mon_idx[: nmon * k_mon].view(nmon, k_mon),
@@ -517,8 +523,8 @@ def _interior_native(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
         bins.append(Bin(None, 0, L.empty((0, k_none), t.int32), L.empty((nops, 0, k_none), t.float64),
                         d_rows=rows[k_mon + k_rbf:n], K=k_none))
     dev = DeviceTable(n, dim, list(ops), bins, n_rbf, method[:n])
-    d_w3 = d_w.view(nops, max(n, 1), n_rbf)
-    dev._pending = (h_idx, h_sizes, h_w, h_m, (d_idx, d_sizes, d_w3))
+    if host_copy:
+        dev._pending = (h_idx, h_sizes, h_w, h_m, (d_idx, d_sizes, d_w.view(nops, max(n, 1), n_rbf)))
     t.cuda.current_stream().synchronize()  # the one synchronisation (flags + table copies)
     hs = h_sum.numpy()
     for cnt_, first, kind_, off in ((hs[0], hs[1], "MON", 0), (hs[2], hs[3], "RBF-FD saddle", k_mon)):
@@ -529,115 +535,12 @@ def _interior_native(nodeset, ops, n_rbf: int | None = None) -> DeviceTable:
     return dev
 
 
-def _copyback_chunks(nodeset, ops, n_rbf: int | None = None) -> int:
-    """Chunks for the overlapped copy-back: one per ~96 MB of padded host table (each chunk
-    costs ~0.15 ms of host launch work, which a small table's copy cannot hide)."""
-    n_rbf = RBF_SIZE[nodeset.dim] if n_rbf is None else n_rbf
-    table_bytes = len(nodeset) * n_rbf * 8 * (len(list(ops)) + 1)
-    return int(min(8, max(1, table_bytes // (96 << 20))))
-
-
-def _interior_host_table(nodeset, ops, n_rbf: int | None = None, chunks: int | None = None) -> DeviceTable:
-    """_interior_device_table for the public compute_weights: the RBF rows are solved in
-    node-ordered chunks and every chunk's slice of the host WeightTable is copied back on a
-    second stream while the next chunk computes (the D2H of the padded table is the
-    largest cost of the call).  Same arithmetic, same results; one synchronisation."""
-    dim = nodeset.dim
-    n = len(nodeset)
-    n_rbf = RBF_SIZE[dim] if n_rbf is None else n_rbf
-    dn = device_nodes(nodeset)
-    t = L.torch()
-    s = t.cuda.current_stream()
-    has_lattice = getattr(nodeset, "lattice", None) is not None and getattr(nodeset, "lattice_idx", None) is not None
-    if has_lattice or not np.any(np.asarray(nodeset.kind) == KIND_REGULAR):
-        method_d = dn.classify()
-    else:  # probe path without a lattice map (approx.py:352-356)
-        method_d = L.to_device(classify_methods(nodeset))
-    rows_d = L.empty(max(n, 1), t.int32)
-    counts_d = L.empty(3, t.int32)
-    scratch = L.empty(3 * (n // 256 + 1) + 1, t.int32)
-    L.call("hn_partition_methods", L.ptr(method_d), n, L.ptr(rows_d), L.ptr(counts_d), L.ptr(scratch),
-           L.stream_handle())
-    kind = np.asarray(nodeset.kind)
-    rbf_rows_h = None
-    if not np.any(kind == KIND_REGULAR):
-        rbf_rows_h = np.nonzero(kind != KIND_BOUNDARY)[0]  # = the device partition's RBF segment
-        k_rbf = len(rbf_rows_h)
-        k_mon, k_none = 0, n - k_rbf
-    else:
-        k_mon, k_rbf, k_none = (int(v) for v in counts_d.cpu().numpy())
-    if k_rbf and n_rbf > n:
-        raise ValueError(f"stencil size {n_rbf} exceeds node count {n}")
-    nops, m = len(ops), n_rbf
-    if chunks is None:
-        chunks = _copyback_chunks(nodeset, ops, n_rbf)
-    chunks = int(max(1, min(chunks, k_rbf))) if k_rbf else 1
-    bounds = np.linspace(0, k_rbf, chunks + 1).astype(np.int64) if k_rbf else np.zeros(1, np.int64)
-    # node id where each chunk's slice of the table starts (rows are ascending node ids)
-    if k_rbf and chunks > 1:
-        if rbf_rows_h is not None:
-            cut = rbf_rows_h[bounds[1:-1]]
-        else:
-            cut = rows_d[k_mon + L.to_device(bounds[1:-1])].cpu().numpy()
-        starts = np.concatenate([[0], cut, [n]]).astype(np.int64)
-    else:
-        starts = np.array([0, n], dtype=np.int64)
-    d_idx = L.empty((max(n, 1), m), t.int64)
-    d_sizes = L.zeros(max(n, 1), t.int64)
-    d_w = L.empty((nops, max(n, 1), m), t.float64)
-    h_idx = t.empty(d_idx.shape, dtype=t.int64, pin_memory=True)
-    h_sizes = t.empty(d_sizes.shape, dtype=t.int64, pin_memory=True)
-    h_w = t.empty(d_w.shape, dtype=t.float64, pin_memory=True)
-    h_m = t.empty(max(n, 1), dtype=t.int8, pin_memory=True)
-
-    def to_table(bb):
-        nb, K, W, R, I, Wt, live = bins_args(bb)
-        if nb:
-            L.call("hn_ell_to_table", nb, K, W, R, I, Wt, nops, m, n, L.ptr(d_idx), L.ptr(d_sizes), L.ptr(d_w),
-                   L.stream_handle())
-
-    bins, pending = [], []
-    if k_mon:
-        d_rows = rows_d[:k_mon]
-        st = dn.mon_stencils(d_rows) if has_lattice else dn.knn(MON_SIZE[dim], rows=d_rows)
-        pending.append(_solve_bin(dn, st, d_rows, ops, True))
-        bins.append(pending[-1][0])
-    if k_none:
-        bins.append(Bin(None, 0, L.empty((0, k_none), t.int32), L.empty((nops, 0, k_none), t.float64),
-                        d_rows=rows_d[k_mon + k_rbf:n], K=k_none))
-    to_table(bins)  # MON and empty rows first: every chunk slice below is then complete
-    cs = _copy_stream()
-    for c in range(len(starts) - 1):
-        if k_rbf:
-            d_rows = rows_d[k_mon + bounds[c]: k_mon + bounds[c + 1]]
-            pending.append(_solve_bin(dn, dn.knn(n_rbf, rows=d_rows, fine=True), d_rows, ops, False))
-            bins.append(pending[-1][0])
-            to_table([pending[-1][0]])
-        lo, hi = int(starts[c]), int(starts[c + 1])
-        cs.wait_stream(s)
-        with t.cuda.stream(cs):
-            h_idx[lo:hi].copy_(d_idx[lo:hi], non_blocking=True)
-            h_sizes[lo:hi].copy_(d_sizes[lo:hi], non_blocking=True)
-            for o in range(nops):
-                h_w[o, lo:hi].copy_(d_w[o, lo:hi], non_blocking=True)
-    cs.wait_stream(s)
-    with t.cuda.stream(cs):
-        h_m[:n].copy_(method_d[:n], non_blocking=True)
-    for x in (d_idx, d_sizes, d_w, method_d):  # keep the sources alive until the copies ran
-        x.record_stream(cs)
-    s.wait_stream(cs)
-    L.TRAFFIC["d2h"] += h_idx.nbytes + h_sizes.nbytes + h_w.nbytes + n
-    dev = DeviceTable(n, dim, list(ops), bins, n_rbf, method_d[:n])
-    dev._pending = (h_idx, h_sizes, h_w, h_m, (d_idx, d_sizes, d_w))
-    _check_info(pending)  # the one synchronisation: flags, after every copy on s's timeline
-    return dev
-
-
 class WeightsPipeline:
-    """compute_weights for a fixed node set as one host-sync-free launch sequence
-    (cell list -> classify -> partition -> MON stencils + solves -> kNN + RBF-FD solves),
-    with launch sizes frozen from one eager pass, so it can be replayed as a CUDA graph.
-    `check()` verifies the frozen sizes and the singular flags after replays."""
+    """The public orchestration (hn_weights_pipeline, as compute_weights calls it) for a fixed
+    node set with the class sizes frozen from one eager pass: no read-back, no host copy, the
+    bins stay in HBM -- so one step is host-sync-free and can be replayed as a CUDA graph
+    (bench.py's device-resident `value`).  `check()` verifies the frozen sizes and the
+    singular flags after replays."""
 
     def __init__(self, nodeset, ops, rbf_n: int | None = None):
         from ._device import DeviceNodes
@@ -646,65 +549,52 @@ class WeightsPipeline:
         self.dim = dim = nodeset.dim
         self.n = n = len(nodeset)
         self.n_rbf = RBF_SIZE[dim] if rbf_n is None else rbf_n
+        if not _native_ok(nodeset, self.ops, self.n_rbf):
+            raise NotImplementedError("WeightsPipeline needs the native orchestration (lattice map or no regular "
+                                      "node, tuned RBF size)")
         self.dn = dn = DeviceNodes(nodeset)
-        self.has_lattice = getattr(nodeset, "lattice", None) is not None and \
-            getattr(nodeset, "lattice_idx", None) is not None
-        if not self.has_lattice and np.any(np.asarray(nodeset.kind) == KIND_REGULAR):
-            raise NotImplementedError("WeightsPipeline needs the lattice map for regular nodes")
         self.method = L.empty(max(n, 1), t.int8)
         self.rows = L.empty(max(n, 1), t.int32)
         self.counts = L.empty(3, t.int32)
         self.part_scratch = L.empty(3 * (n // 256 + 1) + 1, t.int32)
+        self.summary = L.empty(4, t.int32)
         self.gq = dn.grid(dn.fine_cell) if dn.fine_cell is not None else dn.grid(dn.cell, exact=True)
-        self._classify_partition()
+        s = L.stream_handle()  # eager classification: the frozen class sizes
+        L.call("hn_classify", L.ptr(dn.kind), L.ptr(dn.lattice_idx), L.ptr(dn.lattice_grid),
+               L.host_ints(dn.grid_dims if dn.lattice_grid is not None else [1, 1, 1]), n, dim, L.ptr(self.method),
+               s)
+        L.call("hn_partition_methods", L.ptr(self.method), n, L.ptr(self.rows), L.ptr(self.counts),
+               L.ptr(self.part_scratch), s)
         self.k_mon, self.k_rbf, self.k_none = (int(v) for v in self.counts.cpu().numpy())
         if self.k_rbf and self.n_rbf > n:
             raise ValueError(f"stencil size {self.n_rbf} exceeds node count {n}")
         nops = len(self.ops)
         km, kr = max(self.k_mon, 1), max(self.k_rbf, 1)
-        self.mon_st = L.empty((km, 2 * dim + 1), t.int32)
+        nmon = 2 * dim + 1
+        self.mon_st = L.empty((km, nmon), t.int32)
         self.rbf_st = L.empty((kr, self.n_rbf), t.int32)
-        self.mon_idx, self.mon_w = L.empty((2 * dim + 1, km), t.int32), L.empty((nops, 2 * dim + 1, km), t.float64)
+        self.mon_idx, self.mon_w = L.empty((nmon, km), t.int32), L.empty((nops, nmon, km), t.float64)
         self.rbf_idx, self.rbf_w = L.empty((self.n_rbf, kr), t.int32), L.empty((nops, self.n_rbf, kr), t.float64)
         self.mon_info, self.rbf_info = L.zeros(km, t.int32), L.zeros(kr, t.int32)
         self._args = _op_args(self.ops, dim)
+        self._cnt = (L.C.c_int64 * 3)()
         self.graph = None
-
-    def _classify_partition(self):
-        s = L.stream_handle()
-        dn = self.dn
-        L.call("hn_classify", L.ptr(dn.kind), L.ptr(dn.lattice_idx), L.ptr(dn.lattice_grid),
-               L.host_ints(dn.grid_dims if dn.lattice_grid is not None else [1, 1, 1]), self.n, self.dim,
-               L.ptr(self.method), s)
-        L.call("hn_partition_methods", L.ptr(self.method), self.n, L.ptr(self.rows), L.ptr(self.counts),
-               L.ptr(self.part_scratch), s)
 
     def run(self):
         """The whole step, launched on the current stream, no host synchronisation."""
-        s = L.stream_handle()
-        dn = self.dn
-        dn.build_grid(self.gq)  # the cell list the RBF-FD queries search (K1)
-        self._classify_partition()
+        dn, g = self.dn, self.gq
+        dn.build_grid(g)  # the cell list the RBF-FD queries search (K1)
+        has_lat = dn.lattice_grid is not None
         kinds, axes, normals = self._args
-        nops, dim = len(self.ops), self.dim
-        if self.k_mon:
-            L.call("hn_mon_stencils", L.ptr(self.rows), self.k_mon, L.ptr(dn.pos), L.ptr(dn.lattice_idx),
-                   L.ptr(dn.lattice_grid), L.host_ints(dn.grid_dims), dim, L.ptr(self.mon_st), s)
-            L.call("hn_weights_mon", L.ptr(dn.pos), dim, L.ptr(self.mon_st), self.k_mon, nops, kinds, axes, normals,
-                   L.ptr(self.mon_idx), L.ptr(self.mon_w), L.ptr(self.mon_info), s)
-        if self.k_rbf:
-            q = self.rows[self.k_mon:]
-            g = self.gq
-            if dn.spacing is not None:
-                L.call("hn_knn_spacing", L.ptr(dn.pos), dim, L.host_dbls(dn.lo), g.cell, L.host_ints(g.dims),
-                       L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos), L.ptr(q), None, self.k_rbf,
-                       self.n_rbf, None, L.ptr(dn.spacing), L.ptr(self.rbf_st), None, s)
-            else:
-                L.call("hn_knn", L.ptr(dn.pos), dim, L.host_dbls(dn.lo), g.cell, L.host_ints(g.dims),
-                       L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos), L.ptr(q), None, self.k_rbf,
-                       self.n_rbf, None, L.ptr(self.rbf_st), None, s)
-            L.call("hn_weights_rbf", L.ptr(dn.pos), dim, L.ptr(self.rbf_st), self.k_rbf, self.n_rbf, nops, kinds,
-                   axes, normals, None, None, L.ptr(self.rbf_idx), L.ptr(self.rbf_w), L.ptr(self.rbf_info), s)
+        L.call("hn_weights_pipeline", L.ptr(dn.pos), self.dim, self.n, L.ptr(dn.kind),
+               L.ptr(dn.lattice_idx if has_lat else None), L.ptr(dn.lattice_grid if has_lat else None),
+               L.host_ints(dn.grid_dims if has_lat else [1, 1, 1]), L.host_dbls(dn.lo), g.cell, L.host_ints(g.dims),
+               L.ptr(g.start), L.ptr(g.items), L.ptr(g.pos), L.ptr(dn.spacing), len(self.ops), kinds, axes, normals,
+               self.n_rbf, self.k_mon, self.k_rbf, L.ptr(self.method), L.ptr(self.rows), L.ptr(self.counts),
+               L.ptr(self.part_scratch), L.ptr(self.mon_st), L.ptr(self.mon_idx), L.ptr(self.mon_w),
+               L.ptr(self.mon_info), L.ptr(self.rbf_st), L.ptr(self.rbf_idx), L.ptr(self.rbf_w),
+               L.ptr(self.rbf_info), None, None, None, None, None, None, None, self._cnt, L.ptr(self.summary), None,
+               1, None, L.stream_handle())
 
     def capture(self):
         t = L.torch()
@@ -721,9 +611,8 @@ class WeightsPipeline:
     def check(self):
         """Frozen sizes still hold and no stencil was singular (one read-back)."""
         t = L.torch()
-        flags = t.stack([self.counts.to(t.int64)[0], self.counts.to(t.int64)[1],
-                         t.count_nonzero(self.mon_info[: self.k_mon]), t.count_nonzero(self.rbf_info[: self.k_rbf])])
-        k_mon, k_rbf, bad_mon, bad_rbf = (int(v) for v in flags.cpu().numpy())
+        flags = t.cat([self.counts[:2], self.summary[0::2]]).cpu().numpy()
+        k_mon, k_rbf, bad_mon, bad_rbf = (int(v) for v in flags)
         if (k_mon, k_rbf) != (self.k_mon, self.k_rbf):
             raise RuntimeError("node classification changed under a frozen WeightsPipeline")
         if bad_mon or bad_rbf:
@@ -732,10 +621,10 @@ class WeightsPipeline:
     def table(self) -> DeviceTable:
         t = L.torch()
         bins = []
+        nmon = 2 * self.dim + 1
         if self.k_mon:
-            b = Bin(None, 2 * self.dim + 1, self.mon_idx[:, : self.k_mon], self.mon_w[:, :, : self.k_mon],
-                    d_rows=self.rows[: self.k_mon], K=self.k_mon)
-            bins.append(b)
+            bins.append(Bin(None, nmon, self.mon_idx[:, : self.k_mon], self.mon_w[:, :, : self.k_mon],
+                            d_rows=self.rows[: self.k_mon], K=self.k_mon))
         if self.k_rbf:
             bins.append(Bin(None, self.n_rbf, self.rbf_idx[:, : self.k_rbf], self.rbf_w[:, :, : self.k_rbf],
                             d_rows=self.rows[self.k_mon: self.k_mon + self.k_rbf], K=self.k_rbf))
@@ -762,11 +651,9 @@ def _compute_weights(nodeset, ops, with_kappa: bool = False, rbf_n: int | None =
     ops = list(ops)
     for op in ops:
         _op_code(op, nodeset.dim)
-    if host_copy and _native_ok(nodeset, ops, rbf_n):
-        dev = _interior_native(nodeset, ops, rbf_n)
-    elif host_copy and _copyback_chunks(nodeset, ops, rbf_n) > 1:
-        dev = _interior_host_table(nodeset, ops, rbf_n)
-    else:
+    if _native_ok(nodeset, ops, rbf_n):  # the native orchestration (lattice or no regular node, tuned size)
+        dev = _interior_native(nodeset, ops, rbf_n, host_copy=host_copy)
+    else:  # the same library calls driven stage by stage (host-probed classes, untuned sizes)
         dev = _interior_device_table(nodeset, ops, rbf_n, host_copy=host_copy)
     table = WeightTable(_device=dev)
     if with_kappa:

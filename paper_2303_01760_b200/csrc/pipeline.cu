@@ -61,7 +61,7 @@ HN_EXPORT int hn_weights_pipeline(
     const double* pos, int d, int64_t n, const int8_t* kind, const int* lattice_idx, const int* lattice_grid,
     const int* grid_dims_host, const double* lo_host, double cell, const int* dims_host, const int* cell_start,
     const int* cell_items, const double* cell_pos, const double* spacing, int nops, const int* op_kind_host,
-    const int* op_axis_host, const double* op_normal_host, int n_rbf, int64_t k_rbf_host, int8_t* method,
+    const int* op_axis_host, const double* op_normal_host, int n_rbf, int64_t k_mon_host, int64_t k_rbf_host, int8_t* method,
     int* rows, int* counts, int* part_scratch, int* mon_st, int* mon_idx, double* mon_w, int* mon_info,
     int* rbf_st, int* rbf_idx, double* rbf_w, int* rbf_info, int64_t* tab_idx, int64_t* tab_sizes,
     double* tab_w, int64_t* h_idx, int64_t* h_sizes, double* h_w, int8_t* h_method, int64_t* counts_host,
@@ -74,10 +74,10 @@ HN_EXPORT int hn_weights_pipeline(
                     stream));
   HN_RC(hn_partition_methods(method, n, rows, counts, part_scratch, stream));
   int64_t k_mon, k_rbf, k_none;
-  if (k_rbf_host >= 0) {  // no regular node: class sizes known to the caller, no read-back
-    k_mon = 0;
+  if (k_rbf_host >= 0) {  // class sizes known to the caller (no regular node, or a frozen
+    k_mon = k_mon_host;    // replay): no read-back, the call is capturable in a CUDA graph
     k_rbf = k_rbf_host;
-    k_none = n - k_rbf;
+    k_none = n - k_mon - k_rbf;
   } else {
     int c3[3];
     HN_TRY(cudaMemcpyAsync(c3, counts, sizeof(c3), cudaMemcpyDeviceToHost, s));
@@ -120,16 +120,20 @@ HN_EXPORT int hn_weights_pipeline(
   };
   add(k_mon, nmon, rows, mon_idx, mon_w);
   add(k_none, 0, rows + k_mon + k_rbf, mon_idx, mon_w);
-  HN_TRY(cudaMemsetAsync(tab_sizes, 0, sizeof(int64_t) * n, s));
-  if (nb) HN_RC(hn_ell_to_table(nb, bK, bW, bR, bI, bWt, nops, n_rbf, n, tab_idx, tab_sizes, tab_w, stream));
-  if (chunks < 1 || k_rbf == 0) chunks = 1;
+  if (tab_idx) {  // NULL: the caller keeps the ELL bins (operator assembly, device-resident runs)
+    HN_TRY(cudaMemsetAsync(tab_sizes, 0, sizeof(int64_t) * n, s));
+    if (nb) HN_RC(hn_ell_to_table(nb, bK, bW, bR, bI, bWt, nops, n_rbf, n, tab_idx, tab_sizes, tab_w, stream));
+  } else if (h_idx) {
+    return 4;  // a host copy needs the table
+  }
+  if (chunks < 1 || k_rbf == 0 || !h_idx) chunks = 1;
   if (chunks > k_rbf && k_rbf > 0) chunks = static_cast<int>(k_rbf);
   if (chunks > 64) chunks = 64;
   int64_t bounds[65], cut[65];  // chunk c = RBF rows [bounds[c], bounds[c+1]); its table rows [cut[c], cut[c+1])
   for (int c = 0; c <= chunks; ++c) bounds[c] = k_rbf * c / chunks;
   cut[0] = 0;
   cut[chunks] = n;
-  if (chunks > 1) {
+  if (chunks > 1 && h_idx) {
     if (cut_host) {
       for (int c = 1; c < chunks; ++c) cut[c] = cut_host[c - 1];
     } else {  // node id of each chunk's first row (rows are ascending within the RBF segment)
@@ -158,7 +162,7 @@ HN_EXPORT int hn_weights_pipeline(
       const int* R1[1] = {rows_c};
       const int* I1[1] = {idx_c};
       const double* Wt1[1] = {w_c};
-      HN_RC(hn_ell_to_table(1, K1, W1, R1, I1, Wt1, nops, n_rbf, n, tab_idx, tab_sizes, tab_w, stream));
+      if (tab_idx) HN_RC(hn_ell_to_table(1, K1, W1, R1, I1, Wt1, nops, n_rbf, n, tab_idx, tab_sizes, tab_w, stream));
     }
     if (h_idx && cut[c + 1] > cut[c]) {  // this chunk's slice of the host table, on the side stream
       const int64_t lo = cut[c], m = cut[c + 1] - cut[c];

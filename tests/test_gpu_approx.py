@@ -485,6 +485,18 @@ def test_native_pipeline_equals_stepwise_path(case):
         npt.assert_array_equal(wa[op], wb[op])
     npt.assert_array_equal(a.method, b.method)
     assert a.ell_ok  # chunk bins merge back into one slab per width for device applies
+    # the device-resident variants of the same native call: bins only (operator assembly) and
+    # the frozen, graph-replayed WeightsPipeline that bench.py times
+    c = approx._interior_native(ns, ops, rbf_n, host_copy=False)
+    pipe = approx.WeightsPipeline(ns, ops, rbf_n).capture()
+    pipe.replay()
+    pipe.check()
+    for dev in (c, pipe.table()):
+        ic, sc, wc = dev.host_arrays()
+        npt.assert_array_equal(ic, ia)
+        npt.assert_array_equal(sc, sa)
+        for op in ops:
+            npt.assert_array_equal(wc[op], wa[op])
 
 
 def test_all_boundary_node_set_gives_empty_rows():
