@@ -17,6 +17,8 @@
 // Status (device int[2]): [info, iterations] with scipy's info convention (0 converged,
 // maxiter = not converged, -10 / -11 breakdowns).  The caller decides what a failure means
 // (the reference retries with lgmres, solver.py:306-312).
+#include <cstdlib>
+
 #include "pressure.cuh"
 
 namespace hn {
@@ -305,7 +307,9 @@ __global__ void __launch_bounds__(kThr) ctrl_kernel(const double* __restrict__ p
   }
 }
 
-// end of one loop pass: iteration count, maxiter, the WHILE condition
+// end of one loop pass: iteration count, maxiter, the WHILE condition (GRAPH = false: the
+// dev-only eager mode, a fixed number of passes enqueued on the stream for profilers)
+template <bool GRAPH>
 __global__ void end_pass_kernel(double* __restrict__ sc, int* __restrict__ st, int maxiter,
                                 cudaGraphConditionalHandle cond) {
   if (threadIdx.x != 0) return;
@@ -318,7 +322,7 @@ __global__ void end_pass_kernel(double* __restrict__ sc, int* __restrict__ st, i
       st[kInfo] = maxiter;
     }
   }
-  cudaGraphSetConditional(cond, st[kDone] ? 0u : 1u);
+  if constexpr (GRAPH) cudaGraphSetConditional(cond, st[kDone] ? 0u : 1u);
 }
 
 // after the loop: special right-hand sides, status out
@@ -330,7 +334,7 @@ __global__ void finish_kernel(double* __restrict__ x, const double* __restrict__
     GRID_LOOP(i, n) x[i] = special == 1 ? nan : b[i];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && status) {
-    status[0] = st[kInfo];
+    status[0] = st[kDone] ? st[kInfo] : -99;  // -99: the eager dev mode ran out of passes
     status[1] = st[kIter];  // completed passes (a solve that stops at the first half-step: 0)
   }
 }
@@ -375,10 +379,13 @@ cudaError_t precond(PressureSolver& S, const double* in, double* out, cudaStream
   return cudaGetLastError();
 }
 
+template <bool GRAPH>
+cudaError_t enqueue_pass(PressureSolver& S, double* x, double rtol, int maxiter, cudaGraphConditionalHandle cond,
+                         cudaStream_t c);
+
 // Enqueue one solve on s, which must be capturing: set-up nodes, the WHILE node whose body
 // is one BiCGStab pass (captured on the private stream into the node's body graph), finish.
-cudaError_t enqueue_captured(PressureSolver& S, const double* b, const double* x0, double* x, double rtol,
-                             int maxiter, int* status, cudaStream_t s) {
+void enqueue_init(PressureSolver& S, const double* b, const double* x0, double* x, double rtol, cudaStream_t s) {
   const int64_t n = S.n;
   init_state_kernel<<<1, 32, 0, s>>>(S.st);
   bnorm_partial_kernel<<<kParts, kThr, 0, s>>>(b, n, S.part);
@@ -386,6 +393,27 @@ cudaError_t enqueue_captured(PressureSolver& S, const double* b, const double* x
   init_x_kernel<<<kParts, kThr, 0, s>>>(x0, x, n, S.part, S.st);
   if (x0) ctrl_kernel<kCtrlUseRes><<<1, kThr, 0, s>>>(S.part, S.sc, S.st, rtol);
   init_r_kernel<<<kParts, kThr, 0, s>>>(S.a_rowptr, S.a_cols, S.a_vals, x, b, n, S.r, S.rt, S.part, S.st);
+}
+
+// Dev-only eager mode (HN_PRESSURE_EAGER=k in the environment): the set-up kernels, k
+// passes and the finish kernel enqueued directly on the stream (no graph), so profilers
+// that do not descend into conditional graph nodes see every kernel.  A solve that needs
+// more than k passes reports info = -99.
+cudaError_t enqueue_eager(PressureSolver& S, const double* b, const double* x0, double* x, double rtol, int maxiter,
+                          int* status, int passes, cudaStream_t s) {
+  enqueue_init(S, b, x0, x, rtol, s);
+  for (int k = 0; k < passes; ++k) {
+    cudaError_t e = enqueue_pass<false>(S, x, rtol, maxiter, cudaGraphConditionalHandle{}, s);
+    if (e != cudaSuccess) return e;
+  }
+  finish_kernel<<<kParts, kThr, 0, s>>>(x, b, S.n, S.st, status);
+  return cudaGetLastError();
+}
+
+cudaError_t enqueue_captured(PressureSolver& S, const double* b, const double* x0, double* x, double rtol,
+                             int maxiter, int* status, cudaStream_t s) {
+  const int64_t n = S.n;
+  enqueue_init(S, b, x0, x, rtol, s);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
 
@@ -409,6 +437,22 @@ cudaError_t enqueue_captured(PressureSolver& S, const double* b, const double* x
   cudaStream_t c = S.cap;
   if ((e = cudaStreamBeginCaptureToGraph(c, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
     return e;
+  e = enqueue_pass<true>(S, x, rtol, maxiter, cond, c);
+  cudaError_t e2 = cudaStreamEndCapture(c, &body);
+  if (e != cudaSuccess) return e;
+  if (e2 != cudaSuccess) return e2;
+  if ((e = cudaStreamUpdateCaptureDependencies(s, &loop, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
+    return e;
+  finish_kernel<<<kParts, kThr, 0, s>>>(x, b, n, S.st, status);
+  return cudaGetLastError();
+}
+
+// one BiCGStab pass (the WHILE body)
+template <bool GRAPH>
+cudaError_t enqueue_pass(PressureSolver& S, double* x, double rtol, int maxiter, cudaGraphConditionalHandle cond,
+                         cudaStream_t c) {
+  const int64_t n = S.n;
+  cudaError_t e;
   ctrl_kernel<kCtrlTop><<<1, kThr, 0, c>>>(S.part, S.sc, S.st, rtol);
   p_update_kernel<<<kParts, kThr, 0, c>>>(S.p, S.v, S.r, n, S.sc, S.st);
   e = precond(S, S.p, S.phat, c);
@@ -422,14 +466,8 @@ cudaError_t enqueue_captured(PressureSolver& S, const double* b, const double* x
   matvec_dot_kernel<<<kParts, kThr, 0, c>>>(S.a_rowptr, S.a_cols, S.a_vals, S.shat, n, S.t, S.r, S.t, S.part, S.st);
   ctrl_kernel<kCtrlOmega><<<1, kThr, 0, c>>>(S.part, S.sc, S.st, rtol);
   xr_update_kernel<<<kParts, kThr, 0, c>>>(x, S.phat, S.shat, S.r, S.t, S.rt, n, S.sc, S.part, S.st);
-  end_pass_kernel<<<1, 32, 0, c>>>(S.sc, S.st, maxiter, cond);
-  cudaError_t e2 = cudaStreamEndCapture(c, &body);
+  end_pass_kernel<GRAPH><<<1, 32, 0, c>>>(S.sc, S.st, maxiter, cond);
   if (e != cudaSuccess) return e;
-  if (e2 != cudaSuccess) return e2;
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if ((e = cudaStreamUpdateCaptureDependencies(s, &loop, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
-    return e;
-  finish_kernel<<<kParts, kThr, 0, s>>>(x, b, n, S.st, status);
   return cudaGetLastError();
 }
 
@@ -490,6 +528,11 @@ HN_EXPORT int hn_pressure_solve(int64_t handle, const double* b, const double* x
   HN_TRY(cudaStreamIsCapturing(s, &cs));
   if (cs == cudaStreamCaptureStatusActive) {
     HN_TRY(enqueue_captured(*S, b, x0, x, rtol, maxiter, status, s));
+    return 0;
+  }
+  if (const char* ev = getenv("HN_PRESSURE_EAGER")) {
+    const int passes = atoi(ev) > 0 ? atoi(ev) : 1;
+    HN_TRY(enqueue_eager(*S, b, x0, x, rtol, maxiter, status, passes, s));
     return 0;
   }
   const bool hit = S->exec && S->kb == b && S->kx0 == x0 && S->kx == x && S->kstatus == status && S->krtol == rtol &&
