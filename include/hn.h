@@ -241,6 +241,10 @@ int hn_csr_residual(const int64_t* rowptr, const int* cols, const double* vals, 
  * dense part of a heavy block, fed by its helpers (scheduled just before it); kind 3: up to
  * 8 small blocks (w <= 32) of one level, one warp each (members listed after the tasks).
  * inv: the packed diagonal tiles are inverses (x = T^-1 y per tile instead of substitution).
+ * blk_rw (may be NULL): per task, the width of the dense rectangle coupling the block to its
+ * adjacent predecessor (lower: the rw rows before r0, upper: after r0 + w); those columns are
+ * left out of the off-block sums and applied from packed rectangle panels as the
+ * predecessor's tiles are solved.
  * lower: unit diagonal; upper: divides by diag.  Strict CSR, sorted columns.  x and ysum
  * (n each) are reset inside.  Deterministic. */
 /* One triangular factor's supernodal task list (all device pointers; see hn_sptrsv_super). */
@@ -254,6 +258,7 @@ typedef struct hn_tri_plan {
   const int* rb;
   const int* rc;
   const int64_t* off;
+  const int* rw;         /* per task: width of the dense rectangle to the adjacent predecessor block (may be NULL) */
   const int64_t* rowptr; /* strict triangle, CSR, sorted columns */
   const int* cols;
   const double* vals;
@@ -262,7 +267,7 @@ typedef struct hn_tri_plan {
 } hn_tri_plan;
 
 int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
-                    const int* blk_rc, const int64_t* blk_off, int64_t nblk, const int64_t* rowptr,
+                    const int* blk_rc, const int64_t* blk_off, const int* blk_rw, int64_t nblk, const int64_t* rowptr,
                     const int* cols, const double* vals, const double* diag, const double* packed, int inv,
                     const double* b, double* x, double* ysum, int64_t n, unsigned long long* ticket,
                     int ctas_per_sm, void* stream);
@@ -271,7 +276,9 @@ int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int
  * order, w <= cap <= 256), their dependency levels, and the packed dense triangles of the
  * tasks of kind 0/2 (panels of 32 columns, column-major; off[t] in doubles, -1 for other
  * kinds; packed == NULL computes offsets only; returns the total, -1 if a block's in-block
- * triangle is not dense).  inverse != 0: every diagonal tile's rows hold that tile's inverse
+ * triangle or rectangle is not dense; rw_host may be NULL).  Rectangle panels (rw_host[t] > 0)
+ * come first: the predecessor's columns in its tile order, all w rows.  inverse != 0: every
+ * diagonal tile's rows hold that tile's inverse
  * (diag_host = U's diagonal for upper) and hn_sptrsv_super must be called with inv = 1. */
 int64_t hn_host_supernodes(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower, int cap,
                            int* blk_r0_host, int* blk_w_host);
@@ -279,7 +286,8 @@ int hn_host_block_levels(const int64_t* rowptr_host, const int* cols_host, int64
                          const int* blk_r0_host, const int* blk_w_host, int* levels_host);
 int64_t hn_host_pack_panels(const int64_t* rowptr_host, const int* cols_host, const double* vals_host,
                             const double* diag_host, int lower, int inverse, int64_t ntasks, const int* kind_host,
-                            const int* r0_host, const int* w_host, int64_t* off_host, double* packed_host);
+                            const int* r0_host, const int* w_host, const int* rw_host, int64_t* off_host,
+                            double* packed_host);
 
 /* Device-driven pressure solve (K9 driver, csrc/bicgstab.cu).
  * Replaces: pressure_solve's bicgstab call with the LU preconditioner, solver.py:304-305

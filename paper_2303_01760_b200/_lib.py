@@ -27,7 +27,7 @@ _d = C.c_double
 class TriPlan(C.Structure):
     """hn_tri_plan (include/hn.h): one triangular factor's supernodal task list."""
     _fields_ = [("lower", _i), ("inv", _i), ("ntasks", _i64), ("kind", _vp), ("r0", _vp), ("w", _vp), ("rb", _vp),
-                ("rc", _vp), ("off", _vp), ("rowptr", _vp), ("cols", _vp), ("vals", _vp), ("diag", _vp),
+                ("rc", _vp), ("off", _vp), ("rw", _vp), ("rowptr", _vp), ("cols", _vp), ("vals", _vp), ("diag", _vp),
                 ("packed", _vp)]
 
 
@@ -68,9 +68,9 @@ SIGNATURES: dict[str, tuple] = {
     "hn_temperature_bc": (_i, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "hn_csr_matvec": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "hn_csr_residual": (_i, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
-    "hn_sptrsv_super": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp,
-                             _vp, _i64, _vp, _i, _vp]),
-    "hn_host_pack_panels": (_i64, [_vp, _vp, _vp, _vp, _i, _i, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "hn_sptrsv_super": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i, _vp,
+                             _vp, _vp, _i64, _vp, _i, _vp]),
+    "hn_host_pack_panels": (_i64, [_vp, _vp, _vp, _vp, _i, _i, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hn_host_supernodes": (_i64, [_vp, _vp, _i64, _i, _i, _vp, _vp]),
     "hn_host_block_levels": (_i, [_vp, _vp, _i64, _i, _i64, _vp, _vp, _vp]),
     "hn_partition_methods": (_i, [_vp, _i64, _vp, _vp, _vp, _vp]),

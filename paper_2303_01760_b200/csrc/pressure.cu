@@ -91,6 +91,27 @@ __host__ __device__ __forceinline__ void panel_geom(bool lower, int w, int tt, i
   rp = (rows + 1) & ~1;
 }
 
+// The panel sequence of a block task whose adjacent predecessor block P (the rw rows just
+// before it in processing order: lower [r0 - rw, r0), upper [r0 + w, r0 + w + rw)) couples
+// densely into every row: first ceil(rw / 32) "rectangle" panels -- P's columns in P's own
+// tile order, all w rows, column-major -- then the triangle panels of panel_geom.  The
+// rectangle tiles are applied as P's tiles are solved (the task polls their x values), so
+// the hop from P to this block no longer waits for helper sums over P's columns.
+__host__ __device__ __forceinline__ void seq_geom(bool lower, int w, int rw, int pi, bool& rect, int& t0, int& tw,
+                                                  int& rbase, int& rows, int& rp) {
+  const int nrect = (rw + 31) / 32;
+  rect = pi < nrect;
+  if (rect) {
+    t0 = lower ? 32 * pi : 32 * (nrect - 1 - pi);  // column offset inside P
+    tw = rw - t0 < 32 ? rw - t0 : 32;
+    rbase = 0;
+    rows = w;
+    rp = (w + 1) & ~1;
+  } else {
+    panel_geom(lower, w, pi - nrect, t0, tw, rbase, rows, rp);
+  }
+}
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -257,11 +278,12 @@ template <bool LOWER>
 __global__ void __launch_bounds__(kSnThreads, 2) sptrsv_super_kernel(
     const int* __restrict__ blk_kind, const int* __restrict__ blk_r0, const int* __restrict__ blk_w,
     const int* __restrict__ blk_rb, const int* __restrict__ blk_rc, const int64_t* __restrict__ blk_off,
-    int64_t nblk, const int64_t* __restrict__ rowptr, const int* __restrict__ cols, const double* __restrict__ vals,
+    const int* __restrict__ blk_rw, int64_t nblk, const int64_t* __restrict__ rowptr, const int* __restrict__ cols, const double* __restrict__ vals,
     const double* __restrict__ diag, const double* __restrict__ packed, int inv, const double* __restrict__ b,
     double* x, double* ysum, unsigned long long* ticket, const int* __restrict__ skip) {
   if (skip && *skip) return;
   __shared__ double ys[kSnMaxW];
+  __shared__ double s_xr[32];                          // a rectangle tile's x values
   __shared__ int s_cnt[kSnMaxW], s_off[kSnMaxW + 1];  // outside phase: chunks per row, their offsets
   __shared__ long long s_e0[kSnMaxW];                  // ... first outside entry of each row
   __shared__ int s_len[kSnMaxW];                       // ... and the number of outside entries
@@ -299,13 +321,15 @@ __global__ void __launch_bounds__(kSnThreads, 2) sptrsv_super_kernel(
       continue;
     }
     const int r0 = __ldg(blk_r0 + t), w = __ldg(blk_w + t);
+    const int rw = blk_rw ? __ldg(blk_rw + t) : 0;  // dense predecessor columns (rectangle panels)
     const double* P = kind == 1 ? nullptr : packed + __ldg(blk_off + t);
-    const int ntiles = (w + 31) / 32;
-    if (tid == 0 && P && ntiles > 1) {  // the whole packed triangle towards L2 while the outside sums run
+    const int npanels = (rw + 31) / 32 + (w + 31) / 32;
+    if (tid == 0 && P && npanels > 1) {  // the whole packed block towards L2 while the outside sums run
+      bool rect;
       int t0, tw, rbase, rows, rp;
       unsigned bytes = 0;
-      for (int tt = 0; tt < ntiles; ++tt) {
-        panel_geom(LOWER, w, tt, t0, tw, rbase, rows, rp);
+      for (int pi = 0; pi < npanels; ++pi) {
+        seq_geom(LOWER, w, rw, pi, rect, t0, tw, rbase, rows, rp);
         bytes += 32u * rp * 8u;
       }
       l2_prefetch(P, bytes);
@@ -323,9 +347,10 @@ __global__ void __launch_bounds__(kSnThreads, 2) sptrsv_super_kernel(
         const int rr = rb + q, i = r0 + rr;
         const int64_t a = __ldg(rowptr + i);
         const int inside = LOWER ? rr : (w - 1 - rr);
-        const int len = static_cast<int>(__ldg(rowptr + i + 1) - a) - inside;
+        const int len = static_cast<int>(__ldg(rowptr + i + 1) - a) - inside - rw;
         s_cnt[q] = len > 0 ? (len + kTaskChunk - 1) / kTaskChunk : 1;
-        s_e0[q] = LOWER ? a : a + inside;  // the row's outside entries: [s_e0, s_e0 + s_len)
+        // the row's outside entries minus the rectangle's: [s_e0, s_e0 + s_len)
+        s_e0[q] = LOWER ? a : a + inside + rw;
         s_len[q] = len;
       }
       __syncthreads();
@@ -392,8 +417,10 @@ __global__ void __launch_bounds__(kSnThreads, 2) sptrsv_super_kernel(
     const bool has = tid < w;
     const int i = r0 + tid;
     const double dg = (!LOWER && has) ? __ldg(diag + i) : 1.0;
+    const int pbase = LOWER ? r0 - rw : r0 + w;  // first row of the rectangle's predecessor
+    bool rect;
     int t0, tw, rbase, rows, rp;
-    panel_geom(LOWER, w, 0, t0, tw, rbase, rows, rp);
+    seq_geom(LOWER, w, rw, 0, rect, t0, tw, rbase, rows, rp);
     const double* panel = P;
     double cur[32];
     {
@@ -402,48 +429,65 @@ __global__ void __launch_bounds__(kSnThreads, 2) sptrsv_super_kernel(
 #pragma unroll
       for (int k = 0; k < 32; ++k) cur[k] = in ? __ldg(panel + k * rp + rr) : 0.0;
     }
-    for (int tt = 0; tt < ntiles; ++tt) {
-      const bool more = tt + 1 < ntiles;
+    for (int pi = 0; pi < npanels; ++pi) {
+      const bool more = pi + 1 < npanels;
+      bool nrect;
       int n0, nw, nbase, nrows, nrp;
-      panel_geom(LOWER, w, more ? tt + 1 : tt, n0, nw, nbase, nrows, nrp);
+      seq_geom(LOWER, w, rw, more ? pi + 1 : pi, nrect, n0, nw, nbase, nrows, nrp);
       if (more && tid == 0) {  // the next panel as 4 bulk copies of 8 columns (one mbarrier phase)
         const unsigned part = 8u * nrp * 8u;
         mbar_expect(&mbar, 4u * part);
 #pragma unroll
         for (int k = 0; k < 4; ++k) bulk_copy(sn_nbuf + k * 8 * nrp, panel + 32 * rp + k * 8 * nrp, part, &mbar);
       }
-      if (warp == t0 / 32 && inv) {  // x = T^-1 y: 32 independent products, no chain
-        const double yv = lane < tw ? ys[tid] : 0.0;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (rect) {  // predecessor columns [pbase + t0, + tw): wait for their x, apply to every row
+        if (warp == 0) s_xr[lane] = lane < tw ? wait_value(x + pbase + t0 + lane) : 0.0;
+        __syncthreads();
+        if (has) {
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-        for (int k = 0; k < 32; k += 4) {
-          a0 = fma(cur[k], __shfl_sync(0xffffffffu, yv, k), a0);
-          a1 = fma(cur[k + 1], __shfl_sync(0xffffffffu, yv, k + 1), a1);
-          a2 = fma(cur[k + 2], __shfl_sync(0xffffffffu, yv, k + 2), a2);
-          a3 = fma(cur[k + 3], __shfl_sync(0xffffffffu, yv, k + 3), a3);
+          for (int k = 0; k < 32; k += 4) {
+            a0 = fma(cur[k], s_xr[k], a0);
+            a1 = fma(cur[k + 1], s_xr[k + 1], a1);
+            a2 = fma(cur[k + 2], s_xr[k + 2], a2);
+            a3 = fma(cur[k + 3], s_xr[k + 3], a3);
+          }
+          ys[tid] -= (a0 + a1) + (a2 + a3);
         }
-        if (lane < tw) {
-          ys[tid] = (a0 + a1) + (a2 + a3);
-          st_release_dbl(x + i, ys[tid]);
-        }
-      } else if (warp == t0 / 32) {  // the diagonal tile's rows: lane = row - t0
-        const double yv = tile_substitute<LOWER>(cur, lane < tw ? ys[tid] : 0.0, dg, lane, tw);
-        if (lane < tw) {
-          ys[tid] = yv;
-          st_release_dbl(x + i, yv);
-        }
-      }
-      __syncthreads();
-      if (has && (LOWER ? tid >= t0 + tw : tid < t0)) {  // apply the solved tile to my row
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      } else {
+        if (warp == t0 / 32 && inv) {  // x = T^-1 y: 32 independent products, no chain
+          const double yv = lane < tw ? ys[tid] : 0.0;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-        for (int k = 0; k < 32; k += 4) {
-          a0 = fma(cur[k], ys[t0 + k], a0);
-          a1 = fma(cur[k + 1], ys[t0 + k + 1], a1);
-          a2 = fma(cur[k + 2], ys[t0 + k + 2], a2);
-          a3 = fma(cur[k + 3], ys[t0 + k + 3], a3);
+          for (int k = 0; k < 32; k += 4) {
+            a0 = fma(cur[k], __shfl_sync(0xffffffffu, yv, k), a0);
+            a1 = fma(cur[k + 1], __shfl_sync(0xffffffffu, yv, k + 1), a1);
+            a2 = fma(cur[k + 2], __shfl_sync(0xffffffffu, yv, k + 2), a2);
+            a3 = fma(cur[k + 3], __shfl_sync(0xffffffffu, yv, k + 3), a3);
+          }
+          if (lane < tw) {
+            ys[tid] = (a0 + a1) + (a2 + a3);
+            st_release_dbl(x + i, ys[tid]);
+          }
+        } else if (warp == t0 / 32) {  // the diagonal tile's rows: lane = row - t0
+          const double yv = tile_substitute<LOWER>(cur, lane < tw ? ys[tid] : 0.0, dg, lane, tw);
+          if (lane < tw) {
+            ys[tid] = yv;
+            st_release_dbl(x + i, yv);
+          }
         }
-        ys[tid] -= (a0 + a1) + (a2 + a3);
+        __syncthreads();
+        if (has && (LOWER ? tid >= t0 + tw : tid < t0)) {  // apply the solved tile to my row
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) {
+            a0 = fma(cur[k], ys[t0 + k], a0);
+            a1 = fma(cur[k + 1], ys[t0 + k + 1], a1);
+            a2 = fma(cur[k + 2], ys[t0 + k + 2], a2);
+            a3 = fma(cur[k + 3], ys[t0 + k + 3], a3);
+          }
+          ys[tid] -= (a0 + a1) + (a2 + a3);
+        }
       }
       if (more) {
 #ifdef HN_TRACE
@@ -459,6 +503,7 @@ __global__ void __launch_bounds__(kSnThreads, 2) sptrsv_super_kernel(
 #pragma unroll
         for (int k = 0; k < 32; ++k) cur[k] = in ? sn_nbuf[k * nrp + rr] : 0.0;
         panel += 32 * rp;
+        rect = nrect;
         t0 = n0;
         tw = nw;
         rbase = nbase;
@@ -601,11 +646,11 @@ cudaError_t sptrsv_enqueue(const hn_tri_plan& p, const double* b, double* x, dou
   sptrsv_reset_kernel<<<ceil_div(n, 256), 256, 0, s>>>(x, ysum, n, ticket, skip);
   const int blocks = sm_count() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
   if (p.lower)
-    sptrsv_super_kernel<true><<<blocks, kSnThreads, kNbuf, s>>>(p.kind, p.r0, p.w, p.rb, p.rc, p.off, p.ntasks,
+    sptrsv_super_kernel<true><<<blocks, kSnThreads, kNbuf, s>>>(p.kind, p.r0, p.w, p.rb, p.rc, p.off, p.rw, p.ntasks,
                                                                 p.rowptr, p.cols, p.vals, p.diag, p.packed, p.inv, b,
                                                                 x, ysum, ticket, skip);
   else
-    sptrsv_super_kernel<false><<<blocks, kSnThreads, kNbuf, s>>>(p.kind, p.r0, p.w, p.rb, p.rc, p.off, p.ntasks,
+    sptrsv_super_kernel<false><<<blocks, kSnThreads, kNbuf, s>>>(p.kind, p.r0, p.w, p.rb, p.rc, p.off, p.rw, p.ntasks,
                                                                  p.rowptr, p.cols, p.vals, p.diag, p.packed, p.inv,
                                                                  b, x, ysum, ticket, skip);
   return cudaGetLastError();
@@ -618,14 +663,15 @@ using namespace hn;
 // Supernodal solve over planned tasks (processing order), see sptrsv_super_kernel.
 // x and ysum are reset to the sentinel here; ctas_per_sm persistent CTAs per SM.
 HN_EXPORT int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
-                              const int* blk_rc, const int64_t* blk_off, int64_t nblk, const int64_t* rowptr,
+                              const int* blk_rc, const int64_t* blk_off, const int* blk_rw, int64_t nblk,
+                              const int64_t* rowptr,
                               const int* cols, const double* vals, const double* diag, const double* packed,
                               int inv, const double* b, double* x, double* ysum, int64_t n,
                               unsigned long long* ticket, int ctas_per_sm, void* stream) {
   if (nblk == 0) return 0;
   HN_TRY(sptrsv_prepare());
-  const hn_tri_plan p{lower, inv, nblk, blk_kind, blk_r0, blk_w, blk_rb, blk_rc, blk_off, rowptr, cols, vals, diag,
-                      packed};
+  const hn_tri_plan p{lower, inv, nblk, blk_kind, blk_r0, blk_w, blk_rb, blk_rc, blk_off, blk_rw, rowptr, cols, vals,
+                      diag, packed};
   HN_TRY(sptrsv_enqueue(p, b, x, ysum, n, ticket, ctas_per_sm, nullptr, as_stream(stream)));
   return 0;
 }
@@ -636,41 +682,53 @@ HN_EXPORT int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0,
 HN_EXPORT int64_t hn_host_pack_panels(const int64_t* rowptr_host, const int* cols_host, const double* vals_host,
                                       const double* diag_host, int lower, int inverse, int64_t ntasks,
                                       const int* kind_host, const int* r0_host, const int* w_host,
-                                      int64_t* off_host, double* packed_host) {
+                                      const int* rw_host, int64_t* off_host, double* packed_host) {
   int64_t total = 0;
   for (int64_t t = 0; t < ntasks; ++t) {
     const int w = w_host[t];
-    if ((kind_host[t] != 0 && kind_host[t] != 2) || w < 1 || w > kSnMaxW) {
+    const int rw = rw_host ? rw_host[t] : 0;
+    if ((kind_host[t] != 0 && kind_host[t] != 2) || w < 1 || w > kSnMaxW || rw < 0 || rw > kSnMaxW) {
       off_host[t] = -1;
       continue;
     }
     off_host[t] = total;
-    const int ntiles = (w + 31) / 32;
-    for (int tt = 0; tt < ntiles; ++tt) {
+    const int64_t r0 = r0_host[t];
+    const int64_t pr0 = lower ? r0 - rw : r0 + w;  // the rectangle's predecessor rows
+    const int npanels = (rw + 31) / 32 + (w + 31) / 32;
+    for (int pi = 0; pi < npanels; ++pi) {
+      bool rect;
       int t0, tw, rbase, rows, rp;
-      panel_geom(lower != 0, w, tt, t0, tw, rbase, rows, rp);
+      seq_geom(lower != 0, w, rw, pi, rect, t0, tw, rbase, rows, rp);
       if (packed_host) {
         double* pn = packed_host + total;
         for (int64_t q = 0; q < 32LL * rp; ++q) pn[q] = 0.0;
         for (int rr = 0; rr < rows; ++rr) {
           const int row = rbase + rr;
-          const int64_t i = static_cast<int64_t>(r0_host[t]) + row;
+          const int64_t i = r0 + row;
           const int64_t a = rowptr_host[i], z = rowptr_host[i + 1];
+          const int inside = lower ? row : w - 1 - row;
           for (int k = 0; k < tw; ++k) {
             const int c = t0 + k;
-            if (lower ? c < row : c > row) {
-              const int64_t e = lower ? (z - row) + c : a + (c - row - 1);
-              if (cols_host[e] != r0_host[t] + c) return -1;  // not a dense in-block triangle
-              pn[static_cast<int64_t>(k) * rp + rr] = vals_host[e];
+            int64_t e;
+            int64_t want;
+            if (rect) {  // predecessor column pr0 + c: the last rw outside entries (lower) / the first (upper)
+              e = lower ? (z - inside - rw) + c : a + inside + c;
+              want = pr0 + c;
+            } else {
+              if (!(lower ? c < row : c > row)) continue;
+              e = lower ? (z - row) + c : a + (c - row - 1);
+              want = r0 + c;
             }
+            if (e < a || e >= z || cols_host[e] != want) return -1;  // not dense
+            pn[static_cast<int64_t>(k) * rp + rr] = vals_host[e];
           }
         }
-        if (inverse) {  // the diagonal tile's rows hold T^-1 (substitution on the identity)
+        if (inverse && !rect) {  // the diagonal tile's rows hold T^-1 (substitution on the identity)
           double T[32][32], X[32][32];
           const int d0 = t0 - rbase;  // first diagonal-tile row inside the panel
           for (int l = 0; l < tw; ++l)
             for (int k = 0; k < tw; ++k)
-              T[l][k] = l == k ? (lower ? 1.0 : diag_host[r0_host[t] + t0 + l])
+              T[l][k] = l == k ? (lower ? 1.0 : diag_host[r0 + t0 + l])
                                : pn[static_cast<int64_t>(k) * rp + d0 + l];
           for (int j = 0; j < tw; ++j) {
             if (lower) {

@@ -116,11 +116,14 @@ def _split_by_chunks(outside: np.ndarray, bounds: np.ndarray) -> np.ndarray:
 
 
 def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, helper_nnz: int = 4096,
-                           batch: int = 8, batch_row_nnz: int = 32) -> dict:
+                           batch: int = 8, batch_row_nnz: int = 32, rect: bool = True) -> dict:
     """Host planning of hn_sptrsv_super: dense-triangle row blocks in dependency-level order.
     Consecutive small blocks (w <= 32, every row's outside part <= batch_row_nnz) of one
     level are grouped `batch` to a task (kind 3, one warp each); heavy blocks get helper
-    tasks (kind 1) for their outside sums."""
+    tasks (kind 1) for their outside sums.  rect: a block task whose rows all couple densely
+    to the adjacent predecessor block (the pieces of one supernode cut at `cap`) takes those
+    columns off its off-block sums and applies them itself from packed rectangle panels, tile
+    by tile as the predecessor solves them (t_rw = the rectangle's width)."""
     n = m.shape[0]
     rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
     cols = np.ascontiguousarray(m.indices, dtype=np.int32)
@@ -145,20 +148,41 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, he
     inside = rr if lower else owner_w - 1 - rr
     outside = rowlen[rows] - inside
     starts = np.concatenate([[0], np.cumsum(w)[:-1]]) if nb else np.empty(0, np.int64)
-    block_out = np.add.reduceat(outside, starts) if nb else np.empty(0)
-    kinds, tr0, tw, trb, trc = [], [], [], [], []
-    members = []  # (r0, w) of batched small blocks, appended after the task list (kind 3)
-    heavy = set(np.nonzero((block_out > helper_nnz) & (w > 1))[0].tolist())
     block_maxout = np.maximum.reduceat(outside, starts) if nb else np.empty(0)
     small = (w <= 32) & (block_maxout <= batch_row_nnz) if batch else np.zeros(nb, bool)
+    rect_w = np.zeros(nb, dtype=np.int64)
+    if rect and nb:
+        by_r0 = {int(a): k for k, a in enumerate(r0)}
+        by_end = {int(a) + int(b): k for k, (a, b) in enumerate(zip(r0, w))}
+        for k in np.nonzero(~small)[0]:
+            pk = by_end.get(int(r0[k])) if lower else by_r0.get(int(r0[k]) + int(w[k]))
+            if pk is None:
+                continue
+            pw = int(w[pk])
+            sl = slice(starts[k], starts[k] + w[k])
+            rk, ins, outk = rows[sl], inside[sl], outside[sl]
+            if (outk < pw).any():
+                continue
+            if lower:
+                e_first, e_last, c_first = rowptr[rk + 1] - ins - pw, rowptr[rk + 1] - ins - 1, int(r0[pk])
+            else:
+                e_first, e_last, c_first = rowptr[rk] + ins, rowptr[rk] + ins + pw - 1, int(r0[k] + w[k])
+            if (cols[e_first] == c_first).all() and (cols[e_last] == c_first + pw - 1).all():
+                rect_w[k] = pw
+                outside[sl] -= pw
+    block_out = np.add.reduceat(outside, starts) if nb else np.empty(0)
+    kinds, tr0, tw, trb, trc, trw = [], [], [], [], [], []
+    members = []  # (r0, w) of batched small blocks, appended after the task list (kind 3)
+    heavy = set(np.nonzero((block_out > helper_nnz) & (w > 1))[0].tolist())
     pending = []  # consecutive small blocks of one level -> one warp each
 
     def flush():
         if len(pending) == 1:
             k = pending[0]
-            kinds.append(0); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k])
+            kinds.append(0); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k]); trw.append(0)
         elif pending:
             kinds.append(3); tr0.append(0); tw.append(0); trb.append(len(members)); trc.append(len(pending))
+            trw.append(0)
             members.extend((int(r0[k]), int(w[k])) for k in pending)
         pending.clear()
 
@@ -176,21 +200,23 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, he
             bounds = _split_by_chunks(o, bounds)
             for a, b in zip(bounds[:-1], bounds[1:]):
                 kinds.append(1); tr0.append(r0[k]); tw.append(w[k]); trb.append(a); trc.append(b - a)
-            kinds.append(2); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k])
+                trw.append(rect_w[k])
+            kinds.append(2); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k]); trw.append(rect_w[k])
         else:
             o = outside[starts[k]: starts[k] + w[k]]
             if np.maximum(1, -(-o // 256)).sum() > _MAX_PAIRS:
                 raise ValueError("a one-row block has more than 131,072 off-block entries")
-            kinds.append(0); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k])
+            kinds.append(0); tr0.append(r0[k]); tw.append(w[k]); trb.append(0); trc.append(w[k]); trw.append(rect_w[k])
     flush()
     ntasks = len(kinds)
     for idx, (a, b) in enumerate(members):  # member entries: the kernel never tickets past ntasks
-        kinds.append(4); tr0.append(a); tw.append(b); trb.append(0); trc.append(b)
+        kinds.append(4); tr0.append(a); tw.append(b); trb.append(0); trc.append(b); trw.append(0)
     trb = [v + ntasks if kd == 3 else v for kd, v in zip(kinds, trb)]
     as32 = lambda v: np.asarray(v, dtype=np.int32)  # noqa: E731
     return {"nblk": nb, "r0": r0, "w": w, "levels": lev, "depth": int(lev.max()) + 1 if nb else 0,
             "ntasks": ntasks, "kind": as32(kinds), "t_r0": as32(tr0), "t_w": as32(tw), "t_rb": as32(trb),
-            "t_rc": as32(trc), "heavy": len(heavy), "batched": len(members)}
+            "t_rc": as32(trc), "t_rw": as32(trw), "heavy": len(heavy), "batched": len(members),
+            "rects": int((rect_w > 0).sum())}
 
 
 class _SuperSchedule:
@@ -202,7 +228,7 @@ class _SuperSchedule:
         plan = plan_supernodal_blocks(m, lower, **plan_kw)
         self.inverse = bool(inverse)
         self.nblk, self.depth, self.ntasks = plan["nblk"], plan["depth"], plan["ntasks"]
-        kind, r0, w = plan["kind"], plan["t_r0"], plan["t_w"]
+        kind, r0, w, rw = plan["kind"], plan["t_r0"], plan["t_w"], plan["t_rw"]
         vp = L._vp
         rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
         cols = np.ascontiguousarray(m.indices, dtype=np.int32)
@@ -210,8 +236,8 @@ class _SuperSchedule:
         off = np.empty(len(kind), dtype=np.int64)
         dg = np.ascontiguousarray(diag if diag is not None else np.ones(1), dtype=np.float64)
         args = (rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), vals.ctypes.data_as(vp), dg.ctypes.data_as(vp),
-                1 if lower else 0, 1 if inverse else 0, self.ntasks, kind.ctypes.data_as(vp), r0.ctypes.data_as(vp), w.ctypes.data_as(vp),
-                off.ctypes.data_as(vp))
+                1 if lower else 0, 1 if inverse else 0, self.ntasks, kind.ctypes.data_as(vp), r0.ctypes.data_as(vp),
+                w.ctypes.data_as(vp), rw.ctypes.data_as(vp), off.ctypes.data_as(vp))
         total = int(L.lib().hn_host_pack_panels(*args, None))
         packed = np.empty(max(total, 2), dtype=np.float64)
         if int(L.lib().hn_host_pack_panels(*args, packed.ctypes.data_as(vp))) != total:
@@ -220,6 +246,8 @@ class _SuperSchedule:
         self.kind, self.r0, self.w = L.to_device(kind), L.to_device(r0), L.to_device(w)
         self.rb, self.rc = L.to_device(plan["t_rb"]), L.to_device(plan["t_rc"])
         self.off, self.packed = L.to_device(off), L.to_device(packed)
+        self.rw = L.to_device(rw)
+        self.rects = plan["rects"]
         self.packed_bytes = 8 * total
 
 
@@ -270,7 +298,8 @@ class _DeviceLU:
         def mk(sch, m, diag, lower):
             return L.TriPlan(1 if lower else 0, 1 if sch.inverse else 0, sch.ntasks, sch.kind.data_ptr(),
                              sch.r0.data_ptr(), sch.w.data_ptr(), sch.rb.data_ptr(), sch.rc.data_ptr(),
-                             sch.off.data_ptr(), m.rowptr.data_ptr(), m.cols.data_ptr(), m.vals.data_ptr(),
+                             sch.off.data_ptr(), sch.rw.data_ptr(), m.rowptr.data_ptr(), m.cols.data_ptr(),
+                             m.vals.data_ptr(),
                              diag.data_ptr() if diag is not None else None, sch.packed.data_ptr())
         return mk(self.sL, self.L, None, True), mk(self.sU, self.U, self.diag, False)
 
@@ -285,7 +314,7 @@ class _DeviceLU:
 
     def _tri(self, sch, m, diag, b, x, s):
         L.call("hn_sptrsv_super", 1 if diag is None else 0, L.ptr(sch.kind), L.ptr(sch.r0), L.ptr(sch.w),
-               L.ptr(sch.rb), L.ptr(sch.rc), L.ptr(sch.off), sch.ntasks, L.ptr(m.rowptr), L.ptr(m.cols),
+               L.ptr(sch.rb), L.ptr(sch.rc), L.ptr(sch.off), L.ptr(sch.rw), sch.ntasks, L.ptr(m.rowptr), L.ptr(m.cols),
                L.ptr(m.vals), L.ptr(diag), L.ptr(sch.packed), 1 if sch.inverse else 0, L.ptr(b), L.ptr(x), L.ptr(self.ysum), self.n,
                L.ptr(self.ticket), self.CTAS_PER_SM, s)
 

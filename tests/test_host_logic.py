@@ -133,9 +133,11 @@ def _panel_geom(lower, w, tt):
 
 
 @pytest.mark.parametrize("lower", [True, False])
-def test_host_pack_panels_hold_every_dense_triangle(lower):
+@pytest.mark.parametrize("cap", [96, 40])
+def test_host_pack_panels_hold_every_dense_block(lower, cap):
     """hn_host_pack_panels (host code, no GPU): reading the packed panels back with the
-    kernel's geometry gives exactly the strict in-block triangle of every block task."""
+    kernel's geometry gives exactly the strict in-block triangle of every block task and, for
+    tasks with a predecessor rectangle (t_rw > 0), the block rows x predecessor columns."""
     from scipy.sparse import linalg as spla
 
     from paper_2303_01760_b200 import _lib as L
@@ -145,8 +147,10 @@ def test_host_pack_panels_hold_every_dense_triangle(lower):
     lu = spla.splu(a.tocsc())
     tri = sp.tril(sp.csr_matrix(lu.L), k=-1, format="csr") if lower else sp.triu(sp.csr_matrix(lu.U), k=1, format="csr")
     tri.sort_indices()
-    plan = plan_supernodal_blocks(tri, lower, cap=96, helper_nnz=200)
-    kind, r0, w = plan["kind"], plan["t_r0"], plan["t_w"]
+    plan = plan_supernodal_blocks(tri, lower, cap=cap, helper_nnz=200)
+    kind, r0, w, rw = plan["kind"], plan["t_r0"], plan["t_w"], plan["t_rw"]
+    if cap == 40:
+        assert plan["rects"] > 0  # supernodes wider than the cap come in dense-coupled pieces
     rowptr = np.ascontiguousarray(tri.indptr, np.int64)
     cols = np.ascontiguousarray(tri.indices, np.int32)
     vals = np.ascontiguousarray(tri.data, np.float64)
@@ -154,8 +158,8 @@ def test_host_pack_panels_hold_every_dense_triangle(lower):
     vp = L._vp
     one = np.ones(1)
     args = (rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), vals.ctypes.data_as(vp), one.ctypes.data_as(vp),
-            1 if lower else 0, 0, plan["ntasks"], kind.ctypes.data_as(vp), r0.ctypes.data_as(vp), w.ctypes.data_as(vp),
-            off.ctypes.data_as(vp))
+            1 if lower else 0, 0, plan["ntasks"], kind.ctypes.data_as(vp), r0.ctypes.data_as(vp),
+            w.ctypes.data_as(vp), rw.ctypes.data_as(vp), off.ctypes.data_as(vp))
     lib = L.lib()
     total = lib.hn_host_pack_panels(*args, None)
     packed = np.full(total, np.nan)
@@ -167,9 +171,22 @@ def test_host_pack_panels_hold_every_dense_triangle(lower):
         if kind[t] not in (0, 2):
             assert off[t] == -1
             continue
-        b0, bw = int(r0[t]), int(w[t])
-        got = np.zeros((bw, bw))
+        b0, bw, pw = int(r0[t]), int(w[t]), int(rw[t])
         pos = int(off[t])
+        nrect = (pw + 31) // 32
+        if pw:  # rectangle panels first: predecessor columns in its tile order, all rows
+            p0 = b0 - pw if lower else b0 + bw
+            got = np.zeros((bw, pw))
+            for q in range(nrect):
+                c0 = 32 * q if lower else 32 * (nrect - 1 - q)
+                tw = min(32, pw - c0)
+                rp = (bw + 1) & ~1
+                panel = packed[pos:pos + 32 * rp].reshape(32, rp)
+                got[:, c0:c0 + tw] = panel[:tw, :bw].T
+                pos += 32 * rp
+            np.testing.assert_array_equal(got, dense[b0:b0 + bw, p0:p0 + pw])
+            assert (got != 0).all()  # dense coupling
+        got = np.zeros((bw, bw))
         for tt in range((bw + 31) // 32):
             t0, tw, rbase, rows, rp = _panel_geom(lower, bw, tt)
             panel = packed[pos:pos + 32 * rp].reshape(32, rp)
