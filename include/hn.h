@@ -305,6 +305,16 @@ int hn_pressure_solve(int64_t handle, const double* b, const double* x0, double*
                       int* status, void* stream);
 int hn_pressure_free(int64_t handle);
 
+/* Condition numbers (2-norm, s_max / s_min as numpy's SVD; inf when singular) of K local
+ * weight systems, one warp each: the RBF-FD saddle matrix is symmetric (|eigenvalues|), the
+ * MON matrix via M M^T; Householder tridiagonalisation + Sturm multisection.  pos: node
+ * coordinates, row stride ps; stencil node j of system k at idx[k*rs + j*cs]; centers (may be
+ * NULL: node 0) the centre ids; out K fp64.  Supported: MON n = 2d+1, RBF-FD (d, n) in
+ * {(2,12), (3,20), (3,30)} (else returns 2).
+ * Replaces: the with_kappa SVDs of approx.py:229-233, 285-289. */
+int hn_condition_numbers(const double* pos, int ps, int d, const int* idx, int64_t rs, int64_t cs,
+                         const int* centers, int64_t K, int n, int mon, double* out, void* stream);
+
 /* direction 0: out[perm[i]] = in[i]; direction 1: out[i] = in[perm[i]]. */
 int hn_permute(int direction, const int* perm, const double* in, int64_t n, double* out, void* stream);
 

@@ -10,8 +10,9 @@ arithmetic runs in libhn.so:
   compute_weights                   -> all of the above, results kept in HBM as ELL bins
 
 `tree` arguments (scipy cKDTree in the reference) are accepted and ignored: the device
-cell list replaces them.  Condition numbers (with_kappa / WeightRow.kappa) are a host
-diagnostic computed with numpy SVD, as in the reference (approx.py:100-105, 229-233).
+cell list replaces them.  Condition numbers (with_kappa / WeightRow.kappa) -- the reference's
+numpy SVD diagnostic (approx.py:100-105, 229-233, 285-289) -- run on the GPU
+(hn_condition_numbers) for the stencil sizes the library has kernels for, else on the host.
 """
 
 from __future__ import annotations
@@ -150,6 +151,43 @@ def _kappa_host(positions: np.ndarray, stencils: np.ndarray, mon: bool) -> np.nd
         return np.where(s[:, -1] > 0, s[:, 0] / s[:, -1], np.inf)
 
 
+_KAPPA_SIZES = {(2, 5, True), (3, 7, True), (2, 12, False), (3, 20, False), (3, 30, False)}
+
+
+def _kappa_bin(dn, d_idx, rs: int, cs: int, d_centers, K: int, n: int, mon: bool):
+    """kappa of K device stencils (hn_condition_numbers) -> device fp64 (K,)."""
+    t = L.torch()
+    out = L.empty(max(K, 1), t.float64)
+    if K:
+        L.call("hn_condition_numbers", L.ptr(dn.pos), dn.stride, dn.dim, L.ptr(d_idx), rs, cs, L.ptr(d_centers), K, n,
+               1 if mon else 0, L.ptr(out), L.stream_handle())
+    return out[:K]
+
+
+def _kappa(nodeset_or_positions, stencils: np.ndarray, mon: bool) -> np.ndarray:
+    """kappa of host stencils (K, n), centre first: GPU for the library's sizes, else host SVD."""
+    positions = np.asarray(getattr(nodeset_or_positions, "positions", nodeset_or_positions), float)
+    stencils = np.atleast_2d(np.asarray(stencils, dtype=np.int64))
+    k, n = stencils.shape
+    if (positions.shape[1], n, bool(mon)) not in _KAPPA_SIZES:
+        return _kappa_host(positions, stencils, mon)
+    from ._device import DeviceNodes
+    dn = device_nodes(nodeset_or_positions) if hasattr(nodeset_or_positions, "positions") else None
+    if dn is None:
+        dn = _PosOnly(positions)
+    st = L.to_device(np.ascontiguousarray(stencils, dtype=np.int32))
+    return _kappa_bin(dn, st, n, 1, None, k, n, mon).cpu().numpy()
+
+
+class _PosOnly:
+    """Device copy of bare coordinates for hn_condition_numbers (per-stencil API calls)."""
+
+    def __init__(self, positions: np.ndarray):
+        self.dim = positions.shape[1]
+        self.stride = self.dim
+        self.pos = L.to_device(np.ascontiguousarray(positions, dtype=np.float64))
+
+
 # ---------------------------------------------------------------- device solves
 def _solve_bin(dn, stencils_dev, d_rows, ops, mon: bool, row_normals=None):
     """Weights for a batch of stencils straight into an ELL bin (ascending node order).
@@ -249,7 +287,7 @@ def find_stencil(center: int, nodeset, n: int, tree=None) -> StencilSpec:
 def _single(stencil, positions, op, mon: bool) -> WeightRow:
     nb = np.asarray(stencil.neighbors, dtype=np.int64)
     pts = np.asarray(positions, float)[nb][None]
-    kappa = float(_kappa_host(np.asarray(positions, float), nb[None], mon)[0])
+    kappa = float(_kappa(np.asarray(positions, float), nb[None], mon)[0])
     if not np.isfinite(kappa):
         kind = "MON" if mon else "RBF-FD"
         raise SingularSystemError(f"singular {kind} system (duplicate nodes?)", kappa)
@@ -658,13 +696,17 @@ def _compute_weights(nodeset, ops, with_kappa: bool = False, rbf_n: int | None =
     table = WeightTable(_device=dev)
     if with_kappa:
         kappa = np.full(len(nodeset), np.nan)
+        dn = device_nodes(nodeset)
         for b in dev.bins:
             if b.width == 0 or b.K == 0:
                 continue
-            idx = table.indices[b.rows_host, : b.width]
-            kappa[b.rows_host] = _kappa_host(np.asarray(nodeset.positions, float), _stencil_order(b.rows_host, idx),
-                                             b.width == MON_SIZE[nodeset.dim] and
-                                             np.all(dev.method[b.rows_host] == METHOD_MON))
+            mon = b.width == MON_SIZE[nodeset.dim] and bool(np.all(dev.method[b.rows_host] == METHOD_MON))
+            if (nodeset.dim, b.width, mon) in _KAPPA_SIZES:  # on the device, straight from the ELL bin
+                kappa[b.rows_host] = _kappa_bin(dn, b.d_idx, 1, b.K, b.d_rows, b.K, b.width, mon).cpu().numpy()
+            else:
+                idx = table.indices[b.rows_host, : b.width]
+                kappa[b.rows_host] = _kappa_host(np.asarray(nodeset.positions, float),
+                                                 _stencil_order(b.rows_host, idx), mon)
         table.kappa = kappa
     return table
 

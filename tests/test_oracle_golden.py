@@ -6,7 +6,7 @@ CPU-model dependent) and are bit-exact on the host that made the gold
 import numpy as np
 import pytest
 
-from conftest import GOLDEN_CASES
+from conftest import GOLDEN, GOLDEN_CASES
 from oracle import hn_oracle as O
 
 OPS2 = [("lap",), ("d", 0), ("d", 1)]
@@ -121,3 +121,27 @@ def test_oracle_classic_fd():
     w = O.mon_solve(lat, st, [("lap",), ("d", 0)])[0]
     np.testing.assert_allclose(w[:, 0], [-4 / h ** 2, 1 / h ** 2, 1 / h ** 2, 1 / h ** 2, 1 / h ** 2], rtol=1e-12)
     np.testing.assert_allclose(w[[1, 4], 1], [-1 / (2 * h), 1 / (2 * h)], rtol=1e-12)
+
+
+@pytest.mark.parametrize("case", ["dvd_coarse", "config1_small", "config2_small", "config4_small"])
+def test_host_kappa_matches_reference_golden(golden, case):
+    """The host restatement of the with_kappa diagnostic (approx._kappa_host, numpy SVD of the
+    local systems) against the reference's own compute_weights(with_kappa=True) output
+    (tests/golden/kappa_*.npz, oracle/make_golden_kappa.py)."""
+    from paper_2303_01760_b200.approx import _kappa_host
+    ns, g = golden(case)
+    pre = "n30_" if case == "config4_small" else ""
+    idx, sizes, method = g[pre + "indices"], g[pre + "sizes"], g[pre + "method"]
+    with np.load(GOLDEN / f"kappa_{case}.npz") as z:
+        want = z["kappa"]
+    got = np.full(len(ns), np.nan)
+    for mon in (True, False):
+        rows = np.nonzero((sizes > 0) & ((method == 0) == mon))[0]
+        if not len(rows):
+            continue
+        w = int(sizes[rows[0]])
+        st = np.array([np.concatenate([[r], [j for j in idx[r, :w] if j != r]]) for r in rows])
+        got[rows] = _kappa_host(ns.positions, st, mon)
+    np.testing.assert_array_equal(np.isnan(got), np.isnan(want))
+    fin = np.isfinite(want)
+    np.testing.assert_allclose(got[fin], want[fin], rtol=1e-10)
