@@ -20,7 +20,7 @@ from .operators import FieldState, SparseOperator, apply, assemble, divergence
 from .solver import (DeviceStepper, OperatorSet, PhysicsParams, PoissonSolveSettings, RunResult,
                      TimeControls, apply_temperature_bc, apply_velocity_bc, build_operators,
                      interior_divergence, momentum_predict, nusselt_average, pressure_solve, run,
-                     temperature_step, velocity_correct)
+                     temperature_step, velocity_correct, write_outputs)
 
 __all__ = [name for name in dir() if not name.startswith("_")]
 __version__ = "0.1.0"

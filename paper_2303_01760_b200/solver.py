@@ -1092,3 +1092,30 @@ def run(config, spec=None, nodeset=None) -> RunResult:
                                   "temperature_range": (float(final.temperature.min()),
                                                         float(final.temperature.max()))},
                      state=final, nodeset=nodeset)
+
+
+def write_outputs(result: RunResult, out_dir) -> None:
+    """The run artifacts the reference's bench layer writes (pkg/src/hybridnodes/bench.py:28-44),
+    same files and columns: nu_series.csv (step, t, Nu), timings.csv (phase, seconds, sorted)
+    and, with a final state, fields_<t>.csv (coordinates, velocity, p, T, h; t with '.' -> 'p')."""
+    import csv
+    from pathlib import Path
+
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+
+    def dump(name, header, rows):
+        with open(out / name, "w", newline="") as fh:
+            wr = csv.writer(fh)
+            wr.writerow(header)
+            wr.writerows(rows)
+
+    dump("nu_series.csv", ["step", "t", "Nu"], zip(result.nu_steps, result.nu_times, result.nu_values))
+    dump("timings.csv", ["phase", "seconds"], sorted(result.timings.items()))
+    if result.state is None or result.nodeset is None:
+        return
+    ns, st = result.nodeset, result.state
+    dim = ns.positions.shape[1]
+    header = [*"xyz"[:dim], *"uvw"[:dim], "p", "T", "h"]
+    table = np.column_stack([ns.positions, st.velocity, st.pressure, st.temperature, ns.spacing])
+    dump("fields_%s.csv" % ("%g" % result.t_final).replace(".", "p"), header, table)

@@ -230,3 +230,28 @@ def test_run_builds_the_domain_spec_for_cold_origins(monkeypatch):
     with pytest.raises(Reached):
         S.run(Cfg(), nodeset=nodesets.jittered_box(8, seed=0))
     assert seen["spec"] is spec_obj
+
+
+def test_write_outputs_matches_reference_artifacts(tmp_path):
+    """solver.write_outputs writes the reference bench layer's files and columns
+    (pkg/src/hybridnodes/bench.py:28-44) from a RunResult (no GPU needed)."""
+    import csv
+
+    from paper_2303_01760_b200 import nodesets
+    from paper_2303_01760_b200.operators import FieldState
+    from paper_2303_01760_b200.solver import RunResult, write_outputs
+    ns = nodesets.jittered_box(8, seed=1)
+    n = len(ns)
+    st = FieldState(np.ones((n, 2)), np.arange(n, dtype=float), np.full(n, 0.5))
+    res = RunResult(case="dvd", discretization="hybrid", final_nu=1.2, nu_steps=np.array([10, 20]),
+                    nu_times=np.array([0.1, 0.2]), nu_values=np.array([1.1, 1.2]), counts=(0, n, 0), n_total=n,
+                    timings={"stepping": 2.0, "nodegen": 0.5}, dt=0.01, steps=20, t_final=0.25, state=st,
+                    nodeset=ns)
+    write_outputs(res, tmp_path / "out")
+    rows = list(csv.reader(open(tmp_path / "out" / "nu_series.csv")))
+    assert rows[0] == ["step", "t", "Nu"] and rows[2] == ["20", "0.2", "1.2"]
+    rows = list(csv.reader(open(tmp_path / "out" / "timings.csv")))
+    assert rows == [["phase", "seconds"], ["nodegen", "0.5"], ["stepping", "2.0"]]
+    rows = list(csv.reader(open(tmp_path / "out" / "fields_0p25.csv")))
+    assert rows[0] == ["x", "y", "u", "v", "p", "T", "h"] and len(rows) == n + 1
+    np.testing.assert_allclose(np.array(rows[1:], dtype=float)[:, :2], ns.positions)
