@@ -232,10 +232,10 @@ def run_weights_bench(args, rank, world):
     # ---- device-resident step: positions in HBM; the whole pipeline (cell list ->
     # classify -> partition -> stencils -> solves) replayed as one CUDA graph ----
     pipe = approx.WeightsPipeline(ns, ops, rbf_n)
-    # hn_weights_pipeline's kernels: classify 1, partition 6, MON stencils 1 + solve 2, kNN
-    # (3D: warp kernel + box fallback), RBF-FD (3D: null-space + searching fallback; 2D: one
-    # launch, in-kernel fallback), 2 singular-flag summaries
-    counter.KERNELS["hn_weights_pipeline"] = 16 if dim == 3 else 14
+    # hn_weights_pipeline's kernels (no table, no summary): classify 1, partition 6, MON
+    # stencils 1 + solve 2, kNN (3D: warp kernel + box fallback), RBF-FD (3D: null-space +
+    # searching fallback; 2D: one launch, in-kernel fallback)
+    counter.KERNELS["hn_weights_pipeline"] = 14 if dim == 3 else 12
     counter.enabled = True
     pipe.run()
     launches = counter.count  # kernels per step (counted from one eager pass)

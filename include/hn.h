@@ -81,9 +81,9 @@ void hn_knn_set_variant(int v);
  * else one read-back) -> MON stencils + solves -> kNN (spacing-sized, on the given grid) +
  * RBF-FD solves -> WeightTable layout (tab_*, skipped when tab_idx is NULL: the caller keeps
  * the ELL bins) -> async copy into pinned host memory (h_*, skipped when h_idx is NULL).  Bins are written with stride K into capacity buffers;
- * counts_host (host, 3) receives (K_mon, K_rbf, K_none); summary (device, 4 int) and its
- * copy h_summary (pinned, may be NULL) = [MON singular count, first MON row, RBF count,
- * first RBF row].  chunks > 1 splits the RBF rows into node-ordered chunks whose table
+ * counts_host (host, 3) receives (K_mon, K_rbf, K_none); summary (device, 4 int, may be
+ * NULL: no summary) and its copy h_summary (pinned, may be NULL) = [MON singular count, first
+ * MON row, RBF count, first RBF row].  chunks > 1 splits the RBF rows into node-ordered chunks whose table
  * slices are copied back on a side stream while the next chunk computes; cut_host (host,
  * chunks-1 node ids where chunks 1.. start) or NULL (read back).  Returns without synchronising
  * (unless sizes were read back); info arrays flag singular stencils as in hn_weights_*.

@@ -595,7 +595,6 @@ class WeightsPipeline:
         self.rows = L.empty(max(n, 1), t.int32)
         self.counts = L.empty(3, t.int32)
         self.part_scratch = L.empty(3 * (n // 256 + 1) + 1, t.int32)
-        self.summary = L.empty(4, t.int32)
         self.gq = dn.grid(dn.fine_cell) if dn.fine_cell is not None else dn.grid(dn.cell, exact=True)
         s = L.stream_handle()  # eager classification: the frozen class sizes
         L.call("hn_classify", L.ptr(dn.kind), L.ptr(dn.lattice_idx), L.ptr(dn.lattice_grid),
@@ -631,7 +630,7 @@ class WeightsPipeline:
                self.n_rbf, self.k_mon, self.k_rbf, L.ptr(self.method), L.ptr(self.rows), L.ptr(self.counts),
                L.ptr(self.part_scratch), L.ptr(self.mon_st), L.ptr(self.mon_idx), L.ptr(self.mon_w),
                L.ptr(self.mon_info), L.ptr(self.rbf_st), L.ptr(self.rbf_idx), L.ptr(self.rbf_w),
-               L.ptr(self.rbf_info), None, None, None, None, None, None, None, self._cnt, L.ptr(self.summary), None,
+               L.ptr(self.rbf_info), None, None, None, None, None, None, None, self._cnt, None, None,
                1, None, L.stream_handle())
 
     def capture(self):
@@ -649,8 +648,9 @@ class WeightsPipeline:
     def check(self):
         """Frozen sizes still hold and no stencil was singular (one read-back)."""
         t = L.torch()
-        flags = t.cat([self.counts[:2], self.summary[0::2]]).cpu().numpy()
-        k_mon, k_rbf, bad_mon, bad_rbf = (int(v) for v in flags)
+        flags = t.stack([self.counts.to(t.int64)[0], self.counts.to(t.int64)[1],
+                         t.count_nonzero(self.mon_info[: self.k_mon]), t.count_nonzero(self.rbf_info[: self.k_rbf])])
+        k_mon, k_rbf, bad_mon, bad_rbf = (int(v) for v in flags.cpu().numpy())
         if (k_mon, k_rbf) != (self.k_mon, self.k_rbf):
             raise RuntimeError("node classification changed under a frozen WeightsPipeline")
         if bad_mon or bad_rbf:

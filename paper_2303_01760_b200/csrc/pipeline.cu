@@ -182,6 +182,8 @@ HN_EXPORT int hn_weights_pipeline(
     HN_TRY(cudaStreamWaitEvent(s, fj.done[0], 0));
   }
   // singular flags of both bins in 4 ints: [MON count, MON first, RBF count, RBF first]
+  // (summary == NULL: the caller inspects mon_info / rbf_info itself)
+  if (!summary) return 0;
   HN_TRY(cudaMemsetAsync(summary, 0, 4 * sizeof(int), s));
   HN_TRY(cudaMemsetAsync(summary + 1, 0x7f, sizeof(int), s));
   HN_TRY(cudaMemsetAsync(summary + 3, 0x7f, sizeof(int), s));
