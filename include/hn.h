@@ -328,6 +328,92 @@ int hn_reduce(int op, const double* a, const double* b, const int* idx, int64_t 
 int hn_bicg_update(int kind, double* y, const double* x, const double* r, double alpha, double beta,
                    int64_t n, void* stream);
 
+/* ------------------------------------------------------- node-set generation (K12) */
+
+/* Domain + spacing + scattered-region description shared by the node-generation calls
+ * (passed by pointer, read on the host; the arrays it points to are device memory).
+ * Box: [lo, hi]; obstacles: kind 0 circle/sphere (par = centre[d], radius), 1 star
+ * (cx, cy, mean radius, amplitude, lobes, phase), 2 ellipse (cx, cy, a, b, cos angle,
+ * sin angle); curves (kinds 1, 2) carry a 1024-point parameter table (curve_t) and its
+ * points (curve_tab + 2048*j for obstacle j).
+ * Spacing (SpacingFunction nodegen.py:33-60): graded = 0 -> h_r everywhere, else
+ * h_s + (h_r - h_s)*clip(obstacle_distance/width, 0, 1).
+ * Region (_scattered_region nodegen.py:384-433): 0 none, 1 everywhere, 2 dvd quarters
+ * (rc = box centre), 3 axis split (axis, p[axis] < rt[0]; near: < rt[1]), 4 obstacle
+ * layer (obstacle_distance < rt[0]; near: < rt[1]); quarters' near test: seam < rt[1]. */
+typedef struct hn_geom {
+  int dim;
+  int n_obs;
+  double lo[3], hi[3];
+  int graded;
+  double h_r, h_s, width;
+  const int* obs_kind;
+  const double* obs_par; /* n_obs x 8 */
+  const double* curve_t; /* 1024 */
+  const double* curve_tab; /* n_obs x 1024 x 2 */
+  int region;
+  int axis;
+  double rc[2];
+  double rt[2];
+} hn_geom;
+
+/* Point queries (pts: n x dim fp64, unpadded): mode 0 signed distance to the fluid
+ * region, 1 obstacle distance (+inf without obstacles), 2 target spacing, 3 box signed
+ * distance, 4 region predicate (0/1), 5 near-region predicate (0/1).
+ * Replaces: DomainSpec.signed_distance / obstacle_distance / box_signed_distance
+ * geometry.py:279-312, SpacingFunction.__call__ nodegen.py:53-60, the region predicates
+ * nodegen.py:384-433. */
+int hn_geom_eval(const hn_geom* g, const double* pts, int64_t n, int mode, double* out, void* stream);
+
+/* Interior lattice: every key k (1 <= k_a < cells_a) at lo + k*step, kept when
+ * signed_distance <= thr and, with drop_region, outside the scattered region; when
+ * carve > 0 also obstacle_distance >= carve.  Writes the kept nodes in C (ij) order:
+ * out_pos (K x dim), out_key (K x dim int64); *out_count_host = K (synchronises).
+ * out_* must hold prod(cells-1) rows.
+ * Replaces: regular_fill nodegen.py:196-216, carve_transition :219-227, the region cut
+ * of hybrid_discretize :457-461. */
+int hn_lattice_fill(const hn_geom* g, const int64_t* cells_host, const double* step_host, double thr,
+                    int drop_region, double carve, double* out_pos, int64_t* out_key, int64_t* out_count_host,
+                    void* stream);
+
+/* One advancing-front wave, part 1: the candidates of k parents (parent ids `front`, or
+ * front_lo + 0..k-1 when front is NULL) from the caller's random draws rnd (k x (d+1) x d
+ * standard normals) and u (k x (3d+1) uniforms): 2d axis + d+1 random unit directions in
+ * argsort(u) order, radius by the 3-step spacing fixed point; ok = inside the domain by
+ * half a spacing (and in the region when use_region).  cand ((3d+1)k x d), hcand, ok.
+ * Replaces: _wave_candidates nodegen.py:270-294 and the ok mask of scattered_fill :346-349. */
+int hn_front_candidates(const hn_geom* g, const double* pts, const double* hs, const int64_t* front,
+                        int64_t front_lo, int64_t k, const double* rnd, const double* u, int use_region,
+                        double* cand, double* hcand, uint8_t* ok, void* stream);
+
+/* Part 2: first-fit acceptance of the m candidates in order, exactly as the sequential
+ * loop of scattered_fill nodegen.py:350-374 (reject when any node -- existing or accepted
+ * earlier in this wave -- lies closer than 0.995*h_c, or a regular seed closer than seam;
+ * seam <= 0: no seam rule), decided in parallel (pre-test against the existing nodes, then
+ * an in-order sync-free resolution of the in-wave conflicts).  Accepted candidates are
+ * appended in order at pts[count..], hs[count..]; *new_count_host receives the new count
+ * (synchronises).  Needs capacity >= count + m.  cell >= every acceptance radius.
+ * seed_regular: n_seeds bytes (NULL = none regular). */
+int hn_front_accept(int d, double* pts, double* hs, int64_t count, int64_t capacity, const uint8_t* seed_regular,
+                    int64_t n_seeds, const double* cand, const double* hcand, const uint8_t* ok, int64_t m,
+                    double seam, const double* lo_host, const double* hi_host, double cell,
+                    int64_t* new_count_host, void* stream);
+
+/* Lattice index map (hybrid_discretize nodegen.py:503-516): grid ((cells_a+1) per axis,
+ * int64) = -1, then grid[key_i] = i for the n_reg regular nodes (keys: n_reg x d), then
+ * every boundary node (positions bpos, n_b x d; node id = b0 + i) whose position lies on
+ * a lattice point within tol takes a vacant key (lowest id first) and gets its key in
+ * out_bkey (n_b x d int64; LATTICE_NONE = INT64_MIN otherwise). */
+int hn_lattice_map(int d, const int64_t* cells_host, const double* origin_host, const double* step_host,
+                   double tol, const int64_t* keys, int64_t n_reg, const double* bpos, int64_t n_b, int64_t b0,
+                   int64_t* grid, int64_t* out_bkey, void* stream);
+
+/* Pairs i < j closer than 0.5*min(h_i, h_j) - 1e-12 (pts n x d, h n); cell >= 0.5*max h
+ * and the points inside [lo, hi] (a window of 3^d cells is then exact); synchronises.
+ * Replaces: NodeSet.min_distance_violations nodegen.py:139-148 (cKDTree.query_pairs). */
+int hn_close_pairs(int d, const double* pts, const double* h, int64_t n, const double* lo_host,
+                   const double* hi_host, double cell, int64_t* out_count_host, void* stream);
+
 /* ----------------------------------------------------------- diagnostics / peaks */
 
 /* DFMA throughput probe: `blocks` x 256 threads, `iters` x 16 independent DFMA chains

@@ -3,19 +3,25 @@
 Drop-in for the hot-path API of the reference package `hybridnodes`
 (pkg/src/hybridnodes/__init__.py:3-17): stencils and weights (approx), operator
 assembly/application (operators) and the explicit natural-convection step driver
-(solver), all computed by hand-written sm_100a kernels in libhn.so.  Node-set
-generation, geometry, CLI, benchmarking and plotting are not part of this package
-(SURVEY §2); `nodesets` provides seeded synthetic inputs for the BASELINE configs.
+(solver), and node-set generation (generate: lattice fill, advancing front, lattice map;
+geometry / config: the domains it fills), all computed by hand-written sm_100a kernels in
+libhn.so.  CLI, config-file parsing and plotting are not part of this package (SURVEY §2);
+`nodesets` provides the seeded Appendix-B inputs for the BASELINE configs.
 """
 
 from .approx import (METHOD_MON, METHOD_NONE, METHOD_RBFFD, MON_SIZE, POLY_COUNT, RBF_SIZE, Laplacian,
                      NormalDerivative, Partial, StencilSpec, WeightRow, WeightTable, boundary_partial_table,
                      classify_methods, compute_weights, condition_number, find_stencil, mon_weights,
                      normal_derivative_table, rbf_fd_weights, select_method)
+from .config import CaseConfig, build_domain
 from .errors import (ConfigurationError, PoissonConvergenceError, SingularSystemError,
                      SolverDivergenceError)
+from .generate import (RegularFill, SpacingFunction, carve_transition, hybrid_discretize, regular_fill,
+                       scattered_fill)
+from .geometry import (BoundarySet, Circle, DomainSpec, Ellipse, Obstacle, Star, discretize_boundary,
+                       signed_distance)
 from .nodegen import (KIND_BOUNDARY, KIND_REGULAR, KIND_SCATTERED, ROLE_DIRICHLET, ROLE_INTERIOR,
-                      ROLE_NEUMANN, LatticeInfo, NodeSet)
+                      ROLE_NEUMANN, LatticeInfo, Node, NodeSet)
 from .operators import FieldState, SparseOperator, apply, assemble, divergence
 from .solver import (DeviceStepper, OperatorSet, PhysicsParams, PoissonSolveSettings, RunResult,
                      TimeControls, apply_temperature_bc, apply_velocity_bc, build_operators,

@@ -81,6 +81,13 @@ SIGNATURES: dict[str, tuple] = {
     "hn_pressure_free": (_i, [_i64]),
     "hn_reduce": (_i, [_i, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "hn_bicg_update": (_i, [_i, _vp, _vp, _vp, _d, _d, _i64, _vp]),
+    "hn_geom_eval": (_i, [_vp, _vp, _i64, _i, _vp, _vp]),
+    "hn_lattice_fill": (_i, [_vp, _c_i64_p, _c_dbl_p, _d, _i, _d, _vp, _vp, _c_i64_p, _vp]),
+    "hn_front_candidates": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
+    "hn_front_accept": (_i, [_i, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _d, _c_dbl_p, _c_dbl_p,
+                             _d, _c_i64_p, _vp]),
+    "hn_lattice_map": (_i, [_i, _c_i64_p, _c_dbl_p, _c_dbl_p, _d, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "hn_close_pairs": (_i, [_i, _vp, _vp, _i64, _c_dbl_p, _c_dbl_p, _d, _c_i64_p, _vp]),
 }
 
 _LIB = None

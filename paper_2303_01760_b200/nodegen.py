@@ -1,16 +1,17 @@
 """Node-set container consumed by the hot path (mirror of the reference container).
 
 Reference: pkg/src/hybridnodes/nodegen.py:22-23 (KIND_*/ROLE_*), :73-87 (LatticeInfo),
-:90-179 (NodeSet).  The reference's node *generators* (advancing-front fill, geometry)
-are out of scope; every API here accepts any object with the NodeSet
-attributes, so a `hybridnodes.nodegen.NodeSet` built by the reference drops in
-unchanged.  Seeded synthetic generators for the benchmark configs live in
+:90-179 (NodeSet).  Every API here accepts any object with the NodeSet attributes, so a
+`hybridnodes.nodegen.NodeSet` built by the reference drops in unchanged.  The node
+generators (regular fill, advancing front, hybrid_discretize) run on the
+device: `generate.py`.  Seeded Appendix-B generators for the benchmark configs live in
 `nodesets.py`.
 """
 
 from __future__ import annotations
 
 import csv
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -128,3 +129,35 @@ class NodeSet:
             lattice_idx = np.asarray(a["lattice_idx"])
         return NodeSet(a["positions"], a["spacing"], a["kind"], a["role"], a["bc_value"], a["normals"],
                        [str(s) for s in a["origin"]], lattice, lattice_idx)
+
+    # ---- reference NodeSet helpers (nodegen.py:135-148) ----
+    def node(self, i: int) -> "Node":
+        normal = self.normals[i] if self.kind[i] == KIND_BOUNDARY else None
+        return Node(self.positions[i], float(self.spacing[i]), int(self.kind[i]), int(self.role[i]),
+                    float(self.bc_value[i]), normal)
+
+    def min_distance_violations(self) -> int:
+        """Pairs closer than 0.5*min(h_i, h_j) - 1e-12, counted on the device (hn_close_pairs)."""
+        from . import _lib
+        if len(self) < 2:
+            return 0
+        pos = np.ascontiguousarray(self.positions)
+        lo, hi = pos.min(axis=0), pos.max(axis=0)
+        dp, dh = _lib.to_device_many([pos, np.ascontiguousarray(self.spacing)])
+        out = C.c_int64(0)
+        _lib.call("hn_close_pairs", self.dim, _lib.ptr(dp), _lib.ptr(dh), len(self), _lib.host_dbls(lo),
+                  _lib.host_dbls(hi), 0.5 * float(np.max(self.spacing)) * (1 + 1e-9), C.byref(out),
+                  _lib.stream_handle())
+        return int(out.value)
+
+
+@dataclass(frozen=True)
+class Node:
+    """Single-node view into a NodeSet (reference nodegen.py:63-70)."""
+
+    position: np.ndarray
+    h: float
+    kind: int
+    role: int
+    bc_value: float
+    normal: np.ndarray | None
