@@ -459,14 +459,19 @@ __global__ void __launch_bounds__(128, D == 2 ? 7 : 5) knn_box_kernel(Grid g, co
 // spacing) are enumerated as one flattened list over the box's cell runs (each lane owns
 // one run's bounds; a warp scan gives the offsets, a 5-step search maps a list slot to its
 // run), every lane takes list slots lane, lane + 32, .. and tests d^2 <= r^2; the accepted
-// (d, index) keys are compacted by ballot into a 32-slot warp list and sorted ONCE by a
-// 15-stage bitonic network across the lanes.  No per-candidate insertion network, no
-// divergence between queries.  The answer is exact when at most 32 keys were accepted and
-// the n-th lies within r (1 - 1e-12): every point with a smaller key is in the box and was
-// accepted.  Otherwise the query goes to a device list that knn_box_kernel finishes.
+// (d^2, index) keys are compacted by ballot into a 64-slot warp list, square-rooted once and
+// sorted ONCE by a bitonic network across the lanes: 15 stages for up to 32 keys; for 33..64
+// keys the two 32-key halves are sorted in opposite directions, merged in-lane (the smaller
+// of each pair is one of the 32 smallest) and finished by a 5-stage bitonic merge.  No
+// per-candidate insertion network, no divergence between queries.  The answer is exact when
+// at most 64 keys were accepted and the n-th lies within r (1 - 1e-12): every point with a
+// smaller key is in the box and was accepted.  Otherwise the query goes to a device list
+// that knn_box_kernel finishes (none on config 4 at the default radius).
 constexpr int kWarpKnnWarps = 8;
+constexpr int kWarpKnnCap = 64;   // accepted keys a warp can sort
+constexpr int kWarpKnnRuns = 64;  // cell runs of the query's box (two per lane)
 #ifdef HN_TRACE
-__device__ unsigned long long g_knn_fb_stats[4];  // dev builds: [fallbacks, >32 keys, < n keys, n-th beyond r]
+__device__ unsigned long long g_knn_fb_stats[4];  // dev builds: [fallbacks, > cap keys, < n keys, n-th beyond r]
 #endif
 
 template <int D>
@@ -476,10 +481,10 @@ __global__ void __launch_bounds__(kWarpKnnWarps * 32) knn_warp_kernel(
     const uint8_t* __restrict__ exclude, double r0, const double* __restrict__ qh, double rscale,
     int* __restrict__ out_idx, double* __restrict__ out_dist, int* __restrict__ fb_count, int* __restrict__ fb_node,
     int* __restrict__ fb_row) {
-  __shared__ int s_off[kWarpKnnWarps][33];
-  __shared__ int s_beg[kWarpKnnWarps][32];
-  __shared__ double s_kd[kWarpKnnWarps][32];
-  __shared__ int s_ki[kWarpKnnWarps][32];
+  __shared__ int s_off[kWarpKnnWarps][kWarpKnnRuns + 1];
+  __shared__ int s_beg[kWarpKnnWarps][kWarpKnnRuns];
+  __shared__ double s_kd[kWarpKnnWarps][kWarpKnnCap];
+  __shared__ int s_ki[kWarpKnnWarps][kWarpKnnCap];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpKnnWarps + wib;
   if (t >= nq) return;
@@ -491,62 +496,96 @@ __global__ void __launch_bounds__(kWarpKnnWarps * 32) knn_warp_kernel(
     const double h = __ldg(qh + node);
     if (h > 0.0 && h < CUDART_INF) r = rscale * h;
   }
-  // (rescanning with a radius rescaled by the count when more than 32 or fewer than n keys
-  // were accepted cut the fallbacks from 24 % to 5 % on config 4 but cost more than the
-  // fallback path saves: 577 -> 699 us)
-  const double thr2 = __dmul_rn(__dmul_rn(r, r), 1.0 + 1e-9);
-  const double rm = r * (1.0 + 1e-9);
-  int blo[D], bhi[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    blo[a] = min(max(static_cast<int>(floor((q[a] - rm - g.lo[a]) * g.inv_cell)), 0), g.dims[a] - 1);
-    bhi[a] = min(max(static_cast<int>(floor((q[a] + rm - g.lo[a]) * g.inv_cell)), 0), g.dims[a] - 1);
-  }
   constexpr int L = D - 1;  // contiguous axis of the cell numbering
   auto gap = [&](int a, int c) {
     const double cl = g.lo[a] + c * g.cell;
     const double gp = fmax(fmax(cl - q[a], q[a] - (cl + g.cell)), 0.0);
     return fmax(gp - 1e-9 * g.cell, 0.0);
   };
-  const int nx = bhi[0] - blo[0] + 1;
-  const int nrows = D == 2 ? nx : nx * (bhi[1] - blo[1] + 1);
-  bool fb = nrows > 32;
-  int accepted = 0;
-  if (!fb) {
-    // lane -> one run of cells along the contiguous axis, clipped to the ball
-    int beg = 0, cnt = 0;
-    if (lane < nrows) {
-      const int x = blo[0] + (D == 2 ? lane : lane % nx);
-      double rem2 = thr2;
-      const double gx = gap(0, x);
-      rem2 -= gx * gx;
-      int64_t cl = x;
-      if constexpr (D == 3) {
-        const int y = blo[1] + lane / nx;
-        const double gy = gap(1, y);
-        rem2 -= gy * gy;
-        cl = static_cast<int64_t>(x) * g.dims[1] + y;
-      }
-      if (rem2 >= 0.0) {
-        const double hw = sqrt(rem2) * (1.0 + 1e-9) + 1e-12 * g.cell;
-        const int c_lo = min(max(static_cast<int>(floor((q[L] - hw - g.lo[L]) * g.inv_cell)), blo[L]), bhi[L]);
-        const int c_hi = min(max(static_cast<int>(floor((q[L] + hw - g.lo[L]) * g.inv_cell)), blo[L]), bhi[L]);
-        const int64_t c0 = cl * g.dims[L] + c_lo;
-        beg = __ldg(cell_start + c0);
-        cnt = __ldg(cell_start + c0 + (c_hi - c_lo + 1)) - beg;
+  // A query whose ball holds fewer than n or more than 64 keys (next to a surface, where half
+  // the ball is empty; a locally denser patch) rescans with a wider / narrower radius, up to
+  // three times, bracketing: a handful of queries per million, which the thread-per-query fallback kernel
+  // would otherwise serialise (4 such queries cost config 4 ~130 us).
+  bool done = false;
+  int why = 2;
+  double r_few = 0.0, r_many = 0.0;  // bracket: radii seen with too few / too many keys
+  auto shrink = [&]() {
+    r_many = r;
+    r = r_few > 0.0 ? sqrt(r_few * r_many) : 0.8 * r;
+  };
+  auto grow = [&]() {
+    r_few = r;
+    r = r_many > 0.0 ? sqrt(r_few * r_many) : 1.35 * r;
+  };
+  for (int attempt = 0; attempt < 4 && !done; ++attempt) {
+    __syncwarp();
+    const double thr2 = __dmul_rn(__dmul_rn(r, r), 1.0 + 1e-9);
+    const double rm = r * (1.0 + 1e-9);
+    int blo[D], bhi[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      blo[a] = min(max(static_cast<int>(floor((q[a] - rm - g.lo[a]) * g.inv_cell)), 0), g.dims[a] - 1);
+      bhi[a] = min(max(static_cast<int>(floor((q[a] + rm - g.lo[a]) * g.inv_cell)), 0), g.dims[a] - 1);
+    }
+    const int nx = bhi[0] - blo[0] + 1;
+    const int nrows = D == 2 ? nx : nx * (bhi[1] - blo[1] + 1);
+    if (nrows > kWarpKnnRuns) {
+      why = 1;
+      shrink();
+      continue;
+    }
+    // lane -> up to two runs of cells along the contiguous axis (rows lane and lane + 32 of
+    // the box), each clipped to the ball
+    int beg[2] = {0, 0}, cnt[2] = {0, 0};
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int row = lane + 32 * b;
+      if (row < nrows) {
+        const int x = blo[0] + (D == 2 ? row : row % nx);
+        double rem2 = thr2;
+        const double gx = gap(0, x);
+        rem2 -= gx * gx;
+        int64_t cl = x;
+        if constexpr (D == 3) {
+          const int y = blo[1] + row / nx;
+          const double gy = gap(1, y);
+          rem2 -= gy * gy;
+          cl = static_cast<int64_t>(x) * g.dims[1] + y;
+        }
+        if (rem2 >= 0.0) {
+          const double hw = sqrt(rem2) * (1.0 + 1e-9) + 1e-12 * g.cell;
+          const int c_lo = min(max(static_cast<int>(floor((q[L] - hw - g.lo[L]) * g.inv_cell)), blo[L]), bhi[L]);
+          const int c_hi = min(max(static_cast<int>(floor((q[L] + hw - g.lo[L]) * g.inv_cell)), blo[L]), bhi[L]);
+          const int64_t c0 = cl * g.dims[L] + c_lo;
+          beg[b] = __ldg(cell_start + c0);
+          cnt[b] = __ldg(cell_start + c0 + (c_hi - c_lo + 1)) - beg[b];
+        }
       }
     }
-    int inc = cnt;
+    const bool wide = nrows > 32;  // warp-uniform
+    int inc0 = cnt[0], inc1 = cnt[1];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
+      const int y = __shfl_up_sync(0xffffffffu, inc0, o);
+      if (lane >= o) inc0 += y;
     }
-    const int total = __shfl_sync(0xffffffffu, inc, 31);
-    s_off[wib][lane] = inc - cnt;
-    s_beg[wib][lane] = beg;
-    if (lane == 31) s_off[wib][32] = total;
+    const int total0 = __shfl_sync(0xffffffffu, inc0, 31);
+    int total = total0;
+    if (wide) {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc1, o);
+        if (lane >= o) inc1 += y;
+      }
+      total += __shfl_sync(0xffffffffu, inc1, 31);
+    }
+    s_off[wib][lane] = inc0 - cnt[0];
+    s_beg[wib][lane] = beg[0];
+    s_off[wib][32 + lane] = wide ? total0 + inc1 - cnt[1] : total;
+    s_beg[wib][32 + lane] = beg[1];
+    if (lane == 31) s_off[wib][kWarpKnnRuns] = total;
     __syncwarp();
+    int accepted = 0;
     for (int base = 0; base < total; base += 32) {
       const int m = base + lane;
       bool acc = false;
@@ -554,6 +593,9 @@ __global__ void __launch_bounds__(kWarpKnnWarps * 32) knn_warp_kernel(
       int j = 0;
       if (m < total) {
         int lo = 0, hi = 31;  // last run with offset <= m (runs past nrows have offset == total)
+        if (wide) {
+          if (s_off[wib][32] <= m) lo = 32, hi = 63;
+        }
 #pragma unroll
         for (int step = 0; step < 5; ++step) {
           const int mid = (lo + hi + 1) >> 1;
@@ -570,41 +612,77 @@ __global__ void __launch_bounds__(kWarpKnnWarps * 32) knn_warp_kernel(
       }
       const unsigned mask = __ballot_sync(0xffffffffu, acc);
       const int slot = accepted + __popc(mask & ((1u << lane) - 1u));
-      if (acc && slot < 32) {
-        s_kd[wib][slot] = __dsqrt_rn(d2);
+      if (acc && slot < kWarpKnnCap) {
+        s_kd[wib][slot] = d2;
         s_ki[wib][slot] = j;
       }
       accepted += __popc(mask);
     }
-    fb = accepted > 32 || accepted < n;
-  }
-  if (!fb) {
+    if (accepted > kWarpKnnCap) {
+      why = 1;
+      shrink();
+      continue;
+    }
+    if (accepted < n) {
+      why = 2;
+      grow();
+      continue;
+    }
     __syncwarp();
-    double kd = lane < accepted ? s_kd[wib][lane] : CUDART_INF;
+    double kd = lane < accepted ? __dsqrt_rn(s_kd[wib][lane]) : CUDART_INF;
     int ki = lane < accepted ? s_ki[wib][lane] : INT_MAX;
+    auto exchange = [&](double& d, int& i, int j, bool keep_min) {
+      const double od = __shfl_xor_sync(0xffffffffu, d, j);
+      const int oi = __shfl_xor_sync(0xffffffffu, i, j);
+      // branch-free: keys are distinct (or identical padding, where either choice is the
+      // same value), so "the other key is larger" is the negation of "it is smaller"
+      const bool other_less = (od < d) | ((od == d) & (oi < i));
+      const bool take = other_less == keep_min;
+      d = take ? od : d;
+      i = take ? oi : i;
+    };
+    if (accepted <= 32) {
 #pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
+      for (int k = 2; k <= 32; k <<= 1)
 #pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        const double od = __shfl_xor_sync(0xffffffffu, kd, j);
-        const int oi = __shfl_xor_sync(0xffffffffu, ki, j);
-        const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
-        const bool take = keep_min ? key_less(od, oi, kd, ki) : key_less(kd, ki, od, oi);
-        kd = take ? od : kd;
-        ki = take ? oi : ki;
-      }
+        for (int j = k >> 1; j > 0; j >>= 1) exchange(kd, ki, j, ((lane & j) == 0) == ((lane & k) == 0));
+    } else {
+      // keys 32..63 in a second register pair, sorted descending while keys 0..31 sort
+      // ascending (the k = 32 stage of a 64-key network), then the in-lane j = 32 exchange
+      // of the k = 64 stage keeps the smaller key of each pair: a bitonic sequence of the 32
+      // smallest keys, finished by the five ascending merge stages
+      double kd2 = lane + 32 < accepted ? __dsqrt_rn(s_kd[wib][lane + 32]) : CUDART_INF;
+      int ki2 = lane + 32 < accepted ? s_ki[wib][lane + 32] : INT_MAX;
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          const bool up = k == 32 ? true : (lane & k) == 0;
+          exchange(kd, ki, j, ((lane & j) == 0) == up);
+          exchange(kd2, ki2, j, ((lane & j) == 0) != up);
+        }
+      const bool take2 = (kd2 < kd) | ((kd2 == kd) & (ki2 < ki));
+      kd = take2 ? kd2 : kd;
+      ki = take2 ? ki2 : ki;
+#pragma unroll
+      for (int j = 16; j > 0; j >>= 1) exchange(kd, ki, j, (lane & j) == 0);
     }
     const double kth = __shfl_sync(0xffffffffu, kd, n - 1);
-    fb = !(kth <= r * (1.0 - 1e-12));
-    if (!fb && lane < n) {
+    if (!(kth <= r * (1.0 - 1e-12))) {  // the n-th key sits in the last 1e-12 of the ball
+      why = 3;
+      grow();
+      continue;
+    }
+    if (lane < n) {
       out_idx[t * n + lane] = ki;
       if (out_dist) out_dist[t * n + lane] = kd;
     }
+    done = true;
   }
-  if (fb && lane == 0) {
+  if (!done && lane == 0) {
 #ifdef HN_TRACE
     atomicAdd(&g_knn_fb_stats[0], 1ull);
-    atomicAdd(&g_knn_fb_stats[accepted > 32 ? 1 : (accepted < n ? 2 : 3)], 1ull);
+    atomicAdd(&g_knn_fb_stats[why], 1ull);
 #endif
     const int k = atomicAdd(fb_count, 1);
     fb_node[k] = node;
@@ -776,7 +854,8 @@ HN_EXPORT int hn_partition_methods(const int8_t* method, int64_t n, int* rows_ou
   return e == cudaSuccess ? 0 : -static_cast<int>(e);
 }
 
-static int g_knn_variant = 0;  // 0: warp kernel (3D) / box pass (2D); 1: ring only; 2/3: box pass alpha; 5: box pass only
+static int g_knn_variant = 0;  // 0: warp kernel (3D) / box pass (2D); 1: ring only; 2/3: box pass alpha; 5: box pass only;
+                               // 100 + e: warp kernel sized for n + e expected keys
 HN_EXPORT void hn_knn_set_variant(int v) { g_knn_variant = v; }
 
 static Grid make_grid(const double* lo_host, double cell, const int* dims_host, int d) {
@@ -942,7 +1021,11 @@ static int knn_warp_launch(const Grid& g, const double* pos, const int* cs, cons
   int* fb = nullptr;  // [count | nodes (nq) | rows (nq)]
   HN_TRY(stream_alloc(reinterpret_cast<void**>(&fb), sizeof(int) * (1 + 2 * nq), s));
   HN_TRY(cudaMemsetAsync(fb, 0, sizeof(int), s));
-  const double rs = radius_per_spacing(D, n + 4, 1.0);  // expected ~n + 4 keys inside r
+  // expected ~n + 4 keys inside r at density 1/h^d (config 4's graded band is ~20 % denser
+  // than its nominal spacing: ~29 accepted on average; queries short of n or above 64 rescan
+  // inside the kernel)
+  const int extra = g_knn_variant >= 100 ? g_knn_variant - 100 : 4;
+  const double rs = radius_per_spacing(D, n + extra, 1.0);
   knn_warp_kernel<D><<<ceil_div(nq, kWarpKnnWarps), kWarpKnnWarps * 32, 0, s>>>(
       g, pos, cs, ci, cp, queries, nq, n, excl, rs * (D == 2 ? g.cell : g.cell / 1.25), qh, rs, oi, od, fb, fb + 1,
       fb + 1 + nq);
@@ -959,7 +1042,7 @@ template <int D>
 static int launch_knn(const Grid& g, const double* pos, const int* cs, const int* ci, const double* cp,
                       const int* queries, const double* qpos, int64_t nq, int n, const uint8_t* excl,
                       const double* qh, int* oi, double* od, cudaStream_t s) {
-  const int v = g_knn_variant;
+  const int v = g_knn_variant >= 100 ? 0 : g_knn_variant;  // >= 100: warp-kernel radius tuning (dev)
   // 3D node queries: the warp kernel (config 4: 674 -> 577 us, 24 % of the queries finished
   // by the box kernel).  In 2D (n = 12, ~25 box points) one thread per query is cheaper
   // (config 1: 58 us vs 157 us for the warp kernel).

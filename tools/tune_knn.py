@@ -19,9 +19,13 @@ def main():
     variants = [int(v) for v in (args[0] if args else "1,0,2,3").split(",")]
     e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
     flush = L.empty(32 << 20, t.float64)
-    for name, ns, n in (("config1", nodesets.jittered_box(315, seed=1), 12),
-                        ("config2", nodesets.hybrid_hole_2d(500, seed=2), 12),
-                        ("config4", nodesets.hybrid_sphere_3d(94, seed=4, refine=2.8), 20)):
+    cases = [("config4", nodesets.hybrid_sphere_3d(94, seed=4, refine=2.8), 20)]
+    if "--c4" in sys.argv:  # 3D only, also the reference-default n = 30
+        cases.append(("config4", cases[0][1], 30))
+    else:
+        cases = [("config1", nodesets.jittered_box(315, seed=1), 12),
+                 ("config2", nodesets.hybrid_hole_2d(500, seed=2), 12)] + cases
+    for name, ns, n in cases:
         dn = DeviceNodes(ns)
         rows = L.to_device(np.nonzero(ns.kind == 1)[0].astype(np.int32))
         ref = None
