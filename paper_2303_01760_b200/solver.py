@@ -1024,24 +1024,17 @@ def run(config, spec=None, nodeset=None) -> RunResult:
 
     `config` needs the CaseConfig fields run() reads (Ra, Pr, t_cold, t_hot, t_init, t_end,
     poisson_tol, poisson_maxiter, steady_tol, nu_window, nu_stride, case, discretization)
-    and a `cold_origins(spec)` method or attribute.  Node generation is outside the hot
-    path: pass `nodeset` (any NodeSet-like object); the reference's hybrid_discretize is
-    used only if it is importable."""
+    and a `cold_origins(spec)` method or attribute.  Without a `nodeset` the case's node set
+    is generated on the device (generate.hybrid_discretize, reference nodegen.py:436-518)."""
     timings: dict = {}
     t0 = time.perf_counter()
     if spec is None and callable(getattr(config, "cold_origins", None)):
         # the reference always builds the domain first (solver.py:412-415): its
         # CaseConfig.cold_origins(spec) reads spec.obstacles, even with a precomputed node set
-        try:
-            from hybridnodes.config import build_domain
-            spec = build_domain(config)
-        except ImportError:
-            pass
+        from .config import build_domain
+        spec = build_domain(config)
     if nodeset is None:
-        try:
-            from hybridnodes.nodegen import hybrid_discretize
-        except ImportError as exc:  # pragma: no cover - depends on the environment
-            raise ValueError("run() needs a nodeset: node generation is not part of the GPU path") from exc
+        from .generate import hybrid_discretize
         nodeset = hybrid_discretize(config, spec)
     timings["nodegen"] = time.perf_counter() - t0
     settings = PoissonSolveSettings(tol=config.poisson_tol, maxiter=config.poisson_maxiter)

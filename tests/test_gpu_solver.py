@@ -513,3 +513,28 @@ def test_stepper_rolls_back_and_raises_at_the_failing_step(dvd_setup):
     with pytest.raises(PoissonConvergenceError):
         stepper.check_finite()
     assert stepper.steps == 0  # rolled back to the start, failed again at step 1
+
+
+def test_run_generates_its_node_set_on_the_device():
+    """run(CaseConfig) with no nodeset: domain, device node generation, operators and the loop
+    (reference solver.py:412-419); the same call with the generated set passed in is bitwise equal."""
+    import paper_2303_01760_b200 as hn
+    cfg = hn.CaseConfig(case="dvd", h_r=0.05, t_end=2e-4)
+    a = run(cfg)
+    ns = hn.hybrid_discretize(cfg)
+    assert len(a.nodeset) == len(ns) and np.array_equal(a.nodeset.positions, ns.positions)
+    b = run(cfg, nodeset=ns)
+    assert a.steps == b.steps >= 1
+    assert a.state.temperature.tobytes() == b.state.temperature.tobytes()
+    assert np.isfinite(a.final_nu)
+
+
+def test_run_obstacle_case_with_precomputed_node_set():
+    """CaseConfig.cold_origins(spec) reads spec.obstacles: run() builds the domain even when
+    the node set is given (reference solver.py:412-415)."""
+    import paper_2303_01760_b200 as hn
+    cfg = hn.CaseConfig(case="obstacles2d", h_r=0.04, t_end=1e-4)
+    ns = hn.hybrid_discretize(cfg)
+    res = run(cfg, nodeset=ns)
+    assert res.steps >= 1 and np.isfinite(res.final_nu)
+    assert np.isfinite(res.state.velocity).all()
