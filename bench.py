@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--config", type=int, default=4, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-steps", action="store_true", help="weights line without the config-3 steps object")
+    ap.add_argument("--sharded", action="store_true",
+                    help="--phase steps with --gpus N > 1: ONE node set row-sharded over the ranks (halo "
+                         "exchange per gather pass, replicated pressure; strong scaling) instead of replicas")
     ap.add_argument("--phase", default=None, choices=["weights", "steps"],
                     help="config 4 has both: weight computation (default) or the Boussinesq steps")
     return ap.parse_args()
@@ -645,12 +648,53 @@ def cpu_baseline_steps(ns, Ra, rbf_n=None, budget_s=8.0):
             "setup_s": round(setup, 2), "host_cpu": cpu_model()}
 
 
+def sharded_steps_measure(args, rank, world, cfg=3):
+    """Strong scaling of the config-3 step: one node set, rows sharded over the ranks
+    (paper_2303_01760_b200.sharded: halo exchange of v*, (v, T) and T per step over NCCL, the
+    right-hand side all-gathered, the pressure solve replicated).  Time = max over ranks."""
+    import paper_2303_01760_b200 as hn
+    from paper_2303_01760_b200 import _lib as L, nodesets, sharded as S
+    t = L.torch()
+    if cfg == 3:
+        ns, Ra, rbf_n = build_nodeset(3, 0), 1e6, None
+    else:
+        ns, Ra, rbf_n = nodesets.hybrid_sphere_3d(24, seed=4, refine=2.8), 1e5, 30
+    single, ops, dt = _stepper(hn, ns, True, Ra, rbf_n=rbf_n)
+    st0 = single.state()
+    tr = S.TorchDistTransport() if world > 1 else S.LocalTransport(1)
+    stepper = S.ShardedStepper(ops, single.params, single.settings, dt, st0, rank, world, transport=tr)
+    for _ in range(args.warmup):
+        stepper.step()
+    t.cuda.synchronize()
+    barrier(world)
+    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    steps = args.steps_steps
+    with ClockSampler() as clocks:
+        e0.record()
+        for _ in range(steps):
+            stepper.step()
+        e1.record()
+        t.cuda.synchronize()
+    stepper.check_finite()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    n, d, pl = len(ns), ns.dim, stepper.plan
+    return {"metric": "node-updates/sec per step", "value": n / (ms * 1e-3), "unit": "node-updates/s",
+            "ms_per_step": ms, "steps": steps, "warmup": args.warmup, "scaling": "strong",
+            "config": {"workload": config_name(cfg, ns), "N": n, "dt": dt, "Ra": Ra,
+                       "parallelism": f"rows sharded x{world} (slabs), replicated pressure solve",
+                       "rows_this_rank": pl.n_own, "halo_this_rank": pl.n_halo,
+                       "exchange_bytes_per_step": int(8 * (2 * d + 2) * (pl.n_halo + len(pl.send_loc)) + 8 * n)},
+            "clocks": clocks.summary()}
+
+
 def run_steps_bench(args, rank, world):
-    m = steps_measure(args, rank, world, cfg=args.config)
+    m = (sharded_steps_measure if getattr(args, "sharded", False) else steps_measure)(args, rank, world,
+                                                                                     cfg=args.config)
     line = {"metric": m["metric"], "value": m["value"], "unit": m["unit"], "n_gpus": world,
             "steps": m["steps"], "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic"}
     line.update({k: v for k, v in m.items() if k not in line and k != "metric"})
+    line["scaling"] = m.get("scaling", "weak")
     return line
 
 

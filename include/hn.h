@@ -315,6 +315,20 @@ int hn_pressure_free(int64_t handle);
 int hn_condition_numbers(const double* pos, int ps, int d, const int* idx, int64_t rs, int64_t cs,
                          const int* centers, int64_t K, int n, int mon, double* out, void* stream);
 
+/* ------------------------------------------------------ row-sharded explicit step (§8(e), F4) */
+
+/* One rank's view of the step: its owned rows first, then the halo nodes its stencils reach
+ * (grouped by owner).  The reference loop body (solver.py:439-452) has no distributed form;
+ * these three calls are the device side of the 1-hop halo exchange SURVEY §8(e) specifies
+ * (the transfer itself is NCCL send/recv on the same stream).
+ * hn_halo_gather: out[i] = src[map[i]] (pack a send buffer, or take the local part of a
+ * replicated vector).  hn_halo_scatter: dst[map[i]] = in[i] (received values into the halo
+ * tail; a rank's rows into a replicated vector).  hn_remap_indices: out[i] = map[in[i]]
+ * (stencil column ids to local numbering); *bad counts entries that map to < 0. */
+int hn_halo_gather(const double* src, const int64_t* map, int64_t n, double* out, void* stream);
+int hn_halo_scatter(const double* in, const int64_t* map, int64_t n, double* dst, void* stream);
+int hn_remap_indices(const int* in, const int* map, int64_t n, int* out, int* bad, void* stream);
+
 /* direction 0: out[perm[i]] = in[i]; direction 1: out[i] = in[perm[i]]. */
 int hn_permute(int direction, const int* perm, const double* in, int64_t n, double* out, void* stream);
 

@@ -5,7 +5,8 @@ Drop-in for the hot-path API of the reference package `hybridnodes`
 assembly/application (operators) and the explicit natural-convection step driver
 (solver), and node-set generation (generate: lattice fill, advancing front, lattice map;
 geometry / config: the domains it fills), all computed by hand-written sm_100a kernels in
-libhn.so.  CLI, config-file parsing and plotting are not part of this package (SURVEY §2);
+libhn.so; `sharded` is the one-process-per-GPU form of the step and of compute_weights
+(SURVEY §8(e)).  CLI, config-file parsing and plotting are not part of this package (SURVEY §2);
 `nodesets` provides the seeded Appendix-B inputs for the BASELINE configs.
 """
 
@@ -23,6 +24,8 @@ from .geometry import (BoundarySet, Circle, DomainSpec, Ellipse, Obstacle, Star,
 from .nodegen import (KIND_BOUNDARY, KIND_REGULAR, KIND_SCATTERED, ROLE_DIRICHLET, ROLE_INTERIOR,
                       ROLE_NEUMANN, LatticeInfo, Node, NodeSet)
 from .operators import FieldState, SparseOperator, apply, assemble, divergence
+from .sharded import (HaloPlan, LocalTransport, ShardedStepper, TorchDistTransport, build_halo_plan,
+                      compute_weights_sharded, partition_nodes)
 from .solver import (DeviceStepper, OperatorSet, PhysicsParams, PoissonSolveSettings, RunResult,
                      TimeControls, apply_temperature_bc, apply_velocity_bc, build_operators,
                      interior_divergence, momentum_predict, nusselt_average, pressure_solve, run,

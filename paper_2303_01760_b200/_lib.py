@@ -75,6 +75,9 @@ SIGNATURES: dict[str, tuple] = {
     "hn_host_block_levels": (_i, [_vp, _vp, _i64, _i, _i64, _vp, _vp, _vp]),
     "hn_partition_methods": (_i, [_vp, _i64, _vp, _vp, _vp, _vp]),
     "hn_permute": (_i, [_i, _vp, _vp, _i64, _vp, _vp]),
+    "hn_halo_gather": (_i, [_vp, _vp, _i64, _vp, _vp]),
+    "hn_halo_scatter": (_i, [_vp, _vp, _i64, _vp, _vp]),
+    "hn_remap_indices": (_i, [_vp, _vp, _i64, _vp, _vp, _vp]),
     "hn_condition_numbers": (_i, [_vp, _i, _i, _vp, _i64, _i64, _vp, _i64, _i, _i, _vp, _vp]),
     "hn_pressure_setup": (_i, [_i64, _vp, _vp, _vp, C.POINTER(TriPlan), C.POINTER(TriPlan), _vp, _vp, _i, _c_i64_p]),
     "hn_pressure_solve": (_i, [_i64, _vp, _vp, _vp, _d, _i, _vp, _vp]),

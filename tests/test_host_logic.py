@@ -200,36 +200,28 @@ def test_host_pack_panels_hold_every_dense_block(lower, cap):
 
 
 def test_run_builds_the_domain_spec_for_cold_origins(monkeypatch):
-    """run(config, nodeset=...) builds the reference's domain spec before cold_origins(spec)
-    (reference solver.py:412-415) when the reference config module is importable: obstacle
-    cases read spec.obstacles there."""
-    import sys
-    import types
+    """run(config, nodeset=...) builds the domain spec before cold_origins(spec) (reference
+    solver.py:412-415), with the package's own build_domain: obstacle cases read
+    spec.obstacles there."""
+    import paper_2303_01760_b200 as hn
     from paper_2303_01760_b200 import solver as S
-
-    spec_obj = object()
-    fake_cfg = types.ModuleType("hybridnodes.config")
-    fake_cfg.build_domain = lambda config: spec_obj
-    fake_pkg = types.ModuleType("hybridnodes")
-    fake_pkg.config = fake_cfg
-    monkeypatch.setitem(sys.modules, "hybridnodes", fake_pkg)
-    monkeypatch.setitem(sys.modules, "hybridnodes.config", fake_cfg)
 
     class Reached(Exception):
         pass
 
     seen = {}
 
-    class Cfg:
-        poisson_tol, poisson_maxiter = 1e-8, 2000
-
+    class Cfg(hn.CaseConfig):
         def cold_origins(self, spec):
             seen["spec"] = spec
+            seen["cold"] = super().cold_origins(spec)
             raise Reached
 
     with pytest.raises(Reached):
-        S.run(Cfg(), nodeset=nodesets.jittered_box(8, seed=0))
-    assert seen["spec"] is spec_obj
+        S.run(Cfg(case="dvd", h_r=0.05), nodeset=nodesets.jittered_box(8, seed=0))
+    assert isinstance(seen["spec"], hn.DomainSpec) and seen["cold"] == {"wall:x-"}
+    # (the obstacle case, whose placement runs on the device, is covered by
+    # tests/test_gpu_solver.py::test_run_obstacle_case_with_precomputed_node_set)
 
 
 def test_write_outputs_matches_reference_artifacts(tmp_path):
