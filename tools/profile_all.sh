@@ -26,6 +26,16 @@ cap() {  # name config kernel-regex count [extra bench args]
   $NCU --set full --import-source on -k "regex:$rx" --launch-skip 2 -c $cnt -f -o $OUT/${TAG}_$name \
     python bench.py --config $cfg --steps 2 --warmup 3 --no-cpu-baseline "$@" > $OUT/ncu_$name.log 2>&1
   python tools/ncu_summary.py report $OUT/${TAG}_$name.ncu-rep $OUT/${TAG}_${name}_full > /dev/null 2>> $OUT/ncu_$name.log
+  keep_source $name
+}
+# gpurun copies back <= 64 MiB: keep the summaries, the per-line source page (gzip) of the
+# kernels being tuned, and drop the reports themselves
+keep_source() {
+  case $1 in
+    c4_rbf|c4_knn|c1_rbf|c3_trisolve)
+      ncu -i $OUT/${TAG}_$1.ncu-rep --page source --csv 2>/dev/null | gzip -9 > $OUT/${TAG}_$1_source.csv.gz ;;
+  esac
+  rm -f $OUT/${TAG}_$1.ncu-rep
 }
 cap c0_mon 0 'mon_weights_kernel' 1
 cap c0_apply 0 'apply_ell_kernel' 1
@@ -43,6 +53,7 @@ cap3() {  # name kernel-regex count
   HN_PRESSURE_EAGER=1 $NCU --set full --import-source on -k "regex:$2" --launch-skip 4 -c $3 -f -o $OUT/${TAG}_$1 \
     python tools/prof_step_eager.py 4 > $OUT/ncu_$1.log 2>&1
   python tools/ncu_summary.py report $OUT/${TAG}_$1.ncu-rep $OUT/${TAG}_${1}_full > /dev/null 2>> $OUT/ncu_$1.log
+  keep_source $1
 }
 cap3 c3_explicit 'momentum_fused_kernel|div_rhs_fused_kernel|correct_temp_fused_kernel|temperature_bc_kernel' 4
 cap3 c3_trisolve 'sptrsv_super_kernel' 2
