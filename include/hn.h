@@ -264,6 +264,17 @@ typedef struct hn_tri_plan {
   const double* vals;
   const double* diag;    /* U only */
   const double* packed;
+  /* Dense tail (optional, tail_inv != NULL): the tasks above cover rows [0, n - tail_n) only
+   * (for U their rows keep the tail columns: x of the tail is final before they run); the last
+   * tail_n rows are solved as x_T = tail_inv * y_T, tail_inv the row-major tail_n x tail_n
+   * inverse of the factor's trailing triangle (unit diagonal for L, U's diagonal included).
+   * L: y_T = b_T - C x with C = rows [n - tail_n, n) restricted to columns < n - tail_n (CSR:
+   * tail_rowptr (tail_n + 1), tail_cols, tail_vals); U: y_T = b_T. */
+  int64_t tail_n;
+  const int64_t* tail_rowptr;
+  const int* tail_cols;
+  const double* tail_vals;
+  const double* tail_inv;
 } hn_tri_plan;
 
 int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
@@ -271,6 +282,10 @@ int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int
                     const int* cols, const double* vals, const double* diag, const double* packed, int inv,
                     const double* b, double* x, double* ysum, int64_t n, unsigned long long* ticket,
                     int ctas_per_sm, void* stream);
+
+/* hn_sptrsv_super from a plan struct, dense tail included. */
+int hn_sptrsv_plan(const hn_tri_plan* plan, const double* b, double* x, double* ysum, int64_t n,
+                   unsigned long long* ticket, int ctas_per_sm, void* stream);
 
 /* Setup helpers on HOST arrays: dense-triangle row blocks (returns the count; blocks in row
  * order, w <= cap <= 256), their dependency levels, and the packed dense triangles of the

@@ -28,7 +28,8 @@ class TriPlan(C.Structure):
     """hn_tri_plan (include/hn.h): one triangular factor's supernodal task list."""
     _fields_ = [("lower", _i), ("inv", _i), ("ntasks", _i64), ("kind", _vp), ("r0", _vp), ("w", _vp), ("rb", _vp),
                 ("rc", _vp), ("off", _vp), ("rw", _vp), ("rowptr", _vp), ("cols", _vp), ("vals", _vp), ("diag", _vp),
-                ("packed", _vp)]
+                ("packed", _vp), ("tail_n", _i64), ("tail_rowptr", _vp), ("tail_cols", _vp), ("tail_vals", _vp),
+                ("tail_inv", _vp)]
 
 
 # name -> (restype, argtypes); mirrors include/hn.h exactly (tests check the export list)
@@ -75,6 +76,7 @@ SIGNATURES: dict[str, tuple] = {
     "hn_host_block_levels": (_i, [_vp, _vp, _i64, _i, _i64, _vp, _vp, _vp]),
     "hn_partition_methods": (_i, [_vp, _i64, _vp, _vp, _vp, _vp]),
     "hn_permute": (_i, [_i, _vp, _vp, _i64, _vp, _vp]),
+    "hn_sptrsv_plan": (_i, [C.POINTER(TriPlan), _vp, _vp, _vp, _i64, _vp, _i, _vp]),
     "hn_halo_gather": (_i, [_vp, _vp, _i64, _vp, _vp]),
     "hn_halo_scatter": (_i, [_vp, _vp, _i64, _vp, _vp]),
     "hn_remap_indices": (_i, [_vp, _vp, _i64, _vp, _vp, _vp]),

@@ -632,6 +632,86 @@ __global__ void sptrsv_reset_kernel(double* __restrict__ x, double* __restrict__
 
 constexpr int kNbuf = 32 * kSnMaxW * static_cast<int>(sizeof(double));  // one panel (dynamic smem)
 
+// ---- dense tail -----------------------------------------------------------------------
+// The last T rows of a SuperLU factor are (nearly) dense supernodes solved one 256-wide block
+// after the other: at config 3 the last 8192 rows hold 54 of L's 96 block levels and 49 of
+// U's 77, each a ~13 us hop on one CTA.  They are replaced by the explicit inverse of the
+// trailing T x T triangle (computed once at setup): x_T = inv * y_T is one dense
+// matrix-vector product over every SM (8 T^2 / 2 bytes from HBM) instead of a dependency
+// chain.  Lower: the task kernel solves rows [0, n-T), then y_T = b_T - L[T rows, leading
+// columns] x (tail_coupling_kernel), then x_T = inv y_T.  Upper: x_T = inv b_T first; the
+// leading rows read those columns as ordinary (already final) dependencies.
+// One CTA per row, fixed column striding and a fixed reduction tree: deterministic.
+constexpr int kTailThreads = 256;
+
+__device__ __forceinline__ double tail_block_sum(double v, double* s_red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) s_red[warp] = v;
+  __syncthreads();
+  double tot = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < kTailThreads / 32; ++k) tot += s_red[k];
+  }
+  return tot;  // valid on thread 0
+}
+
+__global__ void __launch_bounds__(kTailThreads) tail_coupling_kernel(
+    const int64_t* __restrict__ rowptr, const int* __restrict__ cols, const double* __restrict__ vals,
+    const double* __restrict__ b_tail, const double* __restrict__ x, double* __restrict__ y,
+    const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double s_red[kTailThreads / 32];
+  const int r = blockIdx.x;
+  const int64_t e0 = __ldg(rowptr + r), e1 = __ldg(rowptr + r + 1);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += 4 * kTailThreads) {
+    const int64_t ea = e + kTailThreads, eb = e + 2 * kTailThreads, ec = e + 3 * kTailThreads;
+    const int c0 = __ldg(cols + e);
+    const int c1 = ea < e1 ? __ldg(cols + ea) : -1;
+    const int c2 = eb < e1 ? __ldg(cols + eb) : -1;
+    const int c3 = ec < e1 ? __ldg(cols + ec) : -1;
+    const double v0 = __ldg(vals + e);
+    const double v1 = c1 >= 0 ? __ldg(vals + ea) : 0.0;
+    const double v2 = c2 >= 0 ? __ldg(vals + eb) : 0.0;
+    const double v3 = c3 >= 0 ? __ldg(vals + ec) : 0.0;
+    a0 = fma(v0, x[c0], a0);
+    a1 = fma(v1, c1 >= 0 ? x[c1] : 0.0, a1);
+    a2 = fma(v2, c2 >= 0 ? x[c2] : 0.0, a2);
+    a3 = fma(v3, c3 >= 0 ? x[c3] : 0.0, a3);
+  }
+  const double tot = tail_block_sum((a0 + a1) + (a2 + a3), s_red);
+  if (threadIdx.x == 0) y[r] = __ldg(b_tail + r) - tot;
+}
+
+template <bool LOWER>
+__global__ void __launch_bounds__(kTailThreads) tail_gemv_kernel(const double* __restrict__ inv, int T,
+                                                                 const double* __restrict__ y,
+                                                                 double* __restrict__ x_tail,
+                                                                 const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double s_red[kTailThreads / 32];
+  // long rows first: the grid drains evenly
+  const int r = LOWER ? T - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+  const int c_lo = LOWER ? 0 : r, c_hi = LOWER ? r + 1 : T;
+  const double* row = inv + static_cast<int64_t>(r) * T;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (int c = c_lo + threadIdx.x; c < c_hi; c += 4 * kTailThreads) {
+    const int ca = c + kTailThreads, cb = c + 2 * kTailThreads, cc = c + 3 * kTailThreads;
+    const double m0 = __ldg(row + c);
+    const double m1 = ca < c_hi ? __ldg(row + ca) : 0.0;
+    const double m2 = cb < c_hi ? __ldg(row + cb) : 0.0;
+    const double m3 = cc < c_hi ? __ldg(row + cc) : 0.0;
+    a0 = fma(m0, y[c], a0);
+    a1 = fma(m1, ca < c_hi ? y[ca] : 0.0, a1);
+    a2 = fma(m2, cb < c_hi ? y[cb] : 0.0, a2);
+    a3 = fma(m3, cc < c_hi ? y[cc] : 0.0, a3);
+  }
+  const double tot = tail_block_sum((a0 + a1) + (a2 + a3), s_red);
+  if (threadIdx.x == 0) x_tail[r] = tot;
+}
+
 cudaError_t sptrsv_prepare() {
   // per-device function attributes: set on every call (cheap), so any device a process
   // drives gets the opt-in; never called inside a stream capture
@@ -642,17 +722,29 @@ cudaError_t sptrsv_prepare() {
 
 cudaError_t sptrsv_enqueue(const hn_tri_plan& p, const double* b, double* x, double* ysum, int64_t n,
                            unsigned long long* ticket, int ctas_per_sm, const int* skip, cudaStream_t s) {
-  if (p.ntasks == 0 || n == 0) return cudaSuccess;
+  const int64_t T = p.tail_inv ? p.tail_n : 0, k = n - T;
+  if ((p.ntasks == 0 && T == 0) || n == 0 || k < 0) return cudaSuccess;
   sptrsv_reset_kernel<<<ceil_div(n, 256), 256, 0, s>>>(x, ysum, n, ticket, skip);
+  if (!p.lower && T > 0)  // upper: the tail is solved first, straight from its inverse
+    tail_gemv_kernel<false><<<static_cast<int>(T), kTailThreads, 0, s>>>(p.tail_inv, static_cast<int>(T), b + k,
+                                                                         x + k, skip);
   const int blocks = sm_count() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
-  if (p.lower)
-    sptrsv_super_kernel<true><<<blocks, kSnThreads, kNbuf, s>>>(p.kind, p.r0, p.w, p.rb, p.rc, p.off, p.rw, p.ntasks,
-                                                                p.rowptr, p.cols, p.vals, p.diag, p.packed, p.inv, b,
-                                                                x, ysum, ticket, skip);
-  else
-    sptrsv_super_kernel<false><<<blocks, kSnThreads, kNbuf, s>>>(p.kind, p.r0, p.w, p.rb, p.rc, p.off, p.rw, p.ntasks,
-                                                                 p.rowptr, p.cols, p.vals, p.diag, p.packed, p.inv,
-                                                                 b, x, ysum, ticket, skip);
+  if (p.ntasks > 0) {
+    if (p.lower)
+      sptrsv_super_kernel<true><<<blocks, kSnThreads, kNbuf, s>>>(p.kind, p.r0, p.w, p.rb, p.rc, p.off, p.rw,
+                                                                  p.ntasks, p.rowptr, p.cols, p.vals, p.diag,
+                                                                  p.packed, p.inv, b, x, ysum, ticket, skip);
+    else
+      sptrsv_super_kernel<false><<<blocks, kSnThreads, kNbuf, s>>>(p.kind, p.r0, p.w, p.rb, p.rc, p.off, p.rw,
+                                                                   p.ntasks, p.rowptr, p.cols, p.vals, p.diag,
+                                                                   p.packed, p.inv, b, x, ysum, ticket, skip);
+  }
+  if (p.lower && T > 0) {  // lower: the tail last -- its coupling to the solved rows, then the inverse
+    tail_coupling_kernel<<<static_cast<int>(T), kTailThreads, 0, s>>>(p.tail_rowptr, p.tail_cols, p.tail_vals, b + k,
+                                                                      x, ysum + k, skip);
+    tail_gemv_kernel<true><<<static_cast<int>(T), kTailThreads, 0, s>>>(p.tail_inv, static_cast<int>(T), ysum + k,
+                                                                        x + k, skip);
+  }
   return cudaGetLastError();
 }
 
@@ -671,8 +763,19 @@ HN_EXPORT int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0,
   if (nblk == 0) return 0;
   HN_TRY(sptrsv_prepare());
   const hn_tri_plan p{lower, inv, nblk, blk_kind, blk_r0, blk_w, blk_rb, blk_rc, blk_off, blk_rw, rowptr, cols, vals,
-                      diag, packed};
+                      diag, packed, 0, nullptr, nullptr, nullptr, nullptr};
   HN_TRY(sptrsv_enqueue(p, b, x, ysum, n, ticket, ctas_per_sm, nullptr, as_stream(stream)));
+  return 0;
+}
+
+// The same solve from a plan struct, including the plan's dense tail (tail_n rows through
+// tail_inv) when it has one.
+HN_EXPORT int hn_sptrsv_plan(const hn_tri_plan* plan, const double* b, double* x, double* ysum, int64_t n,
+                             unsigned long long* ticket, int ctas_per_sm, void* stream) {
+  if (!plan) return 1;
+  if (plan->tail_inv && (plan->tail_n < 0 || plan->tail_n > n)) return 2;
+  HN_TRY(sptrsv_prepare());
+  HN_TRY(sptrsv_enqueue(*plan, b, x, ysum, n, ticket, ctas_per_sm, nullptr, as_stream(stream)));
   return 0;
 }
 

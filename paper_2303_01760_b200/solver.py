@@ -116,14 +116,17 @@ def _split_by_chunks(outside: np.ndarray, bounds: np.ndarray) -> np.ndarray:
 
 
 def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, helper_nnz: int = 4096,
-                           batch: int = 8, batch_row_nnz: int = 32, rect: bool = True) -> dict:
+                           batch: int = 8, batch_row_nnz: int = 32, rect: bool = True,
+                           extra_outside: np.ndarray | None = None) -> dict:
     """Host planning of hn_sptrsv_super: dense-triangle row blocks in dependency-level order.
     Consecutive small blocks (w <= 32, every row's outside part <= batch_row_nnz) of one
     level are grouped `batch` to a task (kind 3, one warp each); heavy blocks get helper
     tasks (kind 1) for their outside sums.  rect: a block task whose rows all couple densely
     to the adjacent predecessor block (the pieces of one supernode cut at `cap`) takes those
     columns off its off-block sums and applies them itself from packed rectangle panels, tile
-    by tile as the predecessor solves them (t_rw = the rectangle's width)."""
+    by tile as the predecessor solves them (t_rw = the rectangle's width).  extra_outside: per
+    row, off-block entries the device rows carry beyond `m` (the dense-tail columns of U's
+    leading rows) -- counted into the outside sums' work, not into the structure."""
     n = m.shape[0]
     rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
     cols = np.ascontiguousarray(m.indices, dtype=np.int32)
@@ -148,7 +151,8 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, he
     inside = rr if lower else owner_w - 1 - rr
     outside = rowlen[rows] - inside
     starts = np.concatenate([[0], np.cumsum(w)[:-1]]) if nb else np.empty(0, np.int64)
-    block_maxout = np.maximum.reduceat(outside, starts) if nb else np.empty(0)
+    extra = np.asarray(extra_outside, dtype=outside.dtype)[rows] if extra_outside is not None and nb else 0
+    block_maxout = np.maximum.reduceat(outside + extra, starts) if nb else np.empty(0)
     small = (w <= 32) & (block_maxout <= batch_row_nnz) if batch else np.zeros(nb, bool)
     rect_w = np.zeros(nb, dtype=np.int64)
     if rect and nb:
@@ -170,6 +174,7 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, he
             if (cols[e_first] == c_first).all() and (cols[e_last] == c_first + pw - 1).all():
                 rect_w[k] = pw
                 outside[sl] -= pw
+    outside = outside + extra
     block_out = np.add.reduceat(outside, starts) if nb else np.empty(0)
     kinds, tr0, tw, trb, trc, trw = [], [], [], [], [], []
     members = []  # (r0, w) of batched small blocks, appended after the task list (kind 3)
@@ -221,18 +226,33 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, he
 
 class _SuperSchedule:
     """Device task list of one supernodal triangular solve: the planned tasks plus the packed
-    dense triangles of the block tasks (hn_host_pack_panels)."""
+    dense triangles of the block tasks (hn_host_pack_panels), and optionally the dense tail:
+    the factor's last `tail` rows leave the task list and are solved through the explicit
+    inverse of the trailing triangle (csrc/pressure.cu, 'dense tail')."""
 
     def __init__(self, m: sparse.csr_matrix, lower: bool, diag: np.ndarray | None = None, inverse: bool = False,
-                 **plan_kw):
-        plan = plan_supernodal_blocks(m, lower, **plan_kw)
+                 tail: int = 0, **plan_kw):
+        n = m.shape[0]
+        tail = int(tail) if 0 < int(tail) < n else 0
+        k = n - tail
+        self.n, self.lower, self.tail = n, bool(lower), tail
+        lead_sq = m[:k, :k].tocsr() if tail else m
+        lead_sq.sort_indices()
+        # the rows the task kernel reads: the leading rows with every column (U rows keep their
+        # tail columns: they sort after the in-block and rectangle entries, so the planner's
+        # entry positions hold, and x of the tail is final before the tasks run)
+        lead = m[:k].tocsr() if tail else m
+        lead.sort_indices()
+        extra = (np.diff(lead.indptr) - np.diff(lead_sq.indptr)) if tail and not lower else None
+        plan = plan_supernodal_blocks(lead_sq, lower, extra_outside=extra, **plan_kw)
+        self.csr = DeviceCSR(lead)
         self.inverse = bool(inverse)
         self.nblk, self.depth, self.ntasks = plan["nblk"], plan["depth"], plan["ntasks"]
         kind, r0, w, rw = plan["kind"], plan["t_r0"], plan["t_w"], plan["t_rw"]
         vp = L._vp
-        rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
-        cols = np.ascontiguousarray(m.indices, dtype=np.int32)
-        vals = np.ascontiguousarray(m.data, dtype=np.float64)
+        rowptr = np.ascontiguousarray(lead.indptr, dtype=np.int64)
+        cols = np.ascontiguousarray(lead.indices, dtype=np.int32)
+        vals = np.ascontiguousarray(lead.data, dtype=np.float64)
         off = np.empty(len(kind), dtype=np.int64)
         dg = np.ascontiguousarray(diag if diag is not None else np.ones(1), dtype=np.float64)
         args = (rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), vals.ctypes.data_as(vp), dg.ctypes.data_as(vp),
@@ -249,6 +269,44 @@ class _SuperSchedule:
         self.rw = L.to_device(rw)
         self.rects = plan["rects"]
         self.packed_bytes = 8 * total
+        self.nnz = int(lead.nnz)
+        self.d_diag = L.to_device(dg) if diag is not None else None
+        self.coupling = self.tail_inv = None
+        self.tail_bytes = 0
+        if tail:
+            self._build_tail(m, k, diag)
+        self._plan = L.TriPlan(
+            1 if lower else 0, 1 if self.inverse else 0, self.ntasks, self.kind.data_ptr(), self.r0.data_ptr(),
+            self.w.data_ptr(), self.rb.data_ptr(), self.rc.data_ptr(), self.off.data_ptr(), self.rw.data_ptr(),
+            self.csr.rowptr.data_ptr(), self.csr.cols.data_ptr(), self.csr.vals.data_ptr(),
+            self.d_diag.data_ptr() if self.d_diag is not None else None, self.packed.data_ptr(), tail,
+            self.coupling.rowptr.data_ptr() if self.coupling is not None else None,
+            self.coupling.cols.data_ptr() if self.coupling is not None else None,
+            self.coupling.vals.data_ptr() if self.coupling is not None else None,
+            self.tail_inv.data_ptr() if self.tail_inv is not None else None)
+
+    def _build_tail(self, m, k: int, diag):
+        """The trailing triangle's inverse (row-major, one-time: a dense triangular solve
+        against the identity on the device) and, for L, the tail rows' coupling to the
+        leading columns."""
+        t = L.torch()
+        T = self.tail
+        tri = np.asarray(m[k:, k:].todense(), dtype=np.float64)
+        tri[np.diag_indices(T)] = 1.0 if self.lower else np.asarray(diag, dtype=np.float64)[k:]
+        d_tri = L.to_device(tri)
+        eye = t.eye(T, dtype=t.float64, device=d_tri.device)
+        self.tail_inv = t.linalg.solve_triangular(d_tri, eye, upper=not self.lower).contiguous()
+        del d_tri, eye
+        self.tail_bytes = 8 * T * (T + 1) // 2
+        if self.lower:
+            cpl = m[k:, :k].tocsr()
+            cpl.sort_indices()
+            self.coupling = DeviceCSR(cpl)
+            self.nnz += int(cpl.nnz)
+            self.tail_bytes += 12 * int(cpl.nnz)
+
+    def plan_struct(self):
+        return self._plan
 
 
 class _DeviceLU:
@@ -262,12 +320,16 @@ class _DeviceLU:
     # norm, random rhs) and the fields after 50 full steps by <= 1.1e-12 (relative).
     TILE_INVERSE_L = True
     TILE_INVERSE_U = True
+    # dense tail: the factors' last TAIL rows (at most a quarter of the matrix) are solved through
+    # the explicit inverse of the trailing triangle instead of the block chain -- at config 3
+    # the last 8192 rows hold 54 of L's 96 and 49 of U's 77 block levels.  0 = off.
+    TAIL = 8192
     # max-norm relative distance to SuperLU's solve on a random rhs (tests): U is ill-conditioned
     # (block kappa up to 7e7), two exact substitution orders differ by ~6e-11; the diagonal-tile
     # inverses move it to ~1.1e-10 (fields: <= 1.1e-12 after 50 steps, see above)
     PARITY_TOL = {False: 1e-10, True: 1e-9}
 
-    def __init__(self, lu, inverse: bool | None = None, **plan_kw):
+    def __init__(self, lu, inverse: bool | None = None, tail: int | None = None, **plan_kw):
         Lm = sparse.csr_matrix(lu.L)
         Um = sparse.csr_matrix(lu.U)
         self.n = Lm.shape[0]
@@ -275,13 +337,16 @@ class _DeviceLU:
         Us = sparse.triu(Um, k=1, format="csr")
         Ls.sort_indices()
         Us.sort_indices()
-        self.L = DeviceCSR(Ls)
-        self.U = DeviceCSR(Us)
         udiag = np.asarray(Um.diagonal(), dtype=np.float64)
-        self.sL = _SuperSchedule(Ls, lower=True, inverse=self.TILE_INVERSE_L if inverse is None else inverse, **plan_kw)
+        tail = self.TAIL if tail is None else int(tail)
+        tail = min(tail, self.n // 4)
+        self.tail = tail if tail >= 64 else 0
+        self.sL = _SuperSchedule(Ls, lower=True, inverse=self.TILE_INVERSE_L if inverse is None else inverse,
+                                 tail=self.tail, **plan_kw)
         self.sU = _SuperSchedule(Us, lower=False, diag=udiag, inverse=self.TILE_INVERSE_U if inverse is None else inverse,
-                                 **plan_kw)
-        self.diag = L.to_device(udiag)
+                                 tail=self.tail, **plan_kw)
+        self.L, self.U = self.sL.csr, self.sU.csr  # the rows the task kernels read (leading rows)
+        self.diag = self.sU.d_diag
         self.perm_r = L.to_device(np.asarray(lu.perm_r, dtype=np.int32))
         self.perm_c = L.to_device(np.asarray(lu.perm_c, dtype=np.int32))
         t = L.torch()
@@ -290,18 +355,16 @@ class _DeviceLU:
         self.w = L.empty(self.n, t.float64)
         self.ticket = L.zeros(1, t.int64)
         self.ysum = L.empty(self.n, t.float64)
-        self.nnz = self.L.nnz + self.U.nnz + self.n
-        self.parity_tol = self.PARITY_TOL[self.sL.inverse or self.sU.inverse]
+        self.nnz = int(Ls.nnz + Us.nnz + self.n)  # the factors as SuperLU holds them
+        # bytes one application reads: 12 B per sparse entry the kernels touch + 8 B per entry of
+        # the tail inverses' triangles (what replaced the tail's own 12 B entries)
+        self.solve_bytes = 12 * (self.sL.nnz + self.sU.nnz) + self.sL.tail_bytes - (
+            12 * int(self.sL.coupling.nnz) if self.sL.coupling is not None else 0) + self.sU.tail_bytes + 8 * self.n
+        self.parity_tol = self.PARITY_TOL[self.sL.inverse or self.sU.inverse or bool(self.tail)]
 
     def plans(self):
         """(L, U) as hn_tri_plan structs for hn_pressure_setup (the arrays stay owned here)."""
-        def mk(sch, m, diag, lower):
-            return L.TriPlan(1 if lower else 0, 1 if sch.inverse else 0, sch.ntasks, sch.kind.data_ptr(),
-                             sch.r0.data_ptr(), sch.w.data_ptr(), sch.rb.data_ptr(), sch.rc.data_ptr(),
-                             sch.off.data_ptr(), sch.rw.data_ptr(), m.rowptr.data_ptr(), m.cols.data_ptr(),
-                             m.vals.data_ptr(),
-                             diag.data_ptr() if diag is not None else None, sch.packed.data_ptr())
-        return mk(self.sL, self.L, None, True), mk(self.sU, self.U, self.diag, False)
+        return self.sL.plan_struct(), self.sU.plan_struct()
 
     def solve(self, b, x):
         """x = Pc U^-1 L^-1 Pr b (scipy SuperLU.solve semantics)."""
@@ -313,9 +376,9 @@ class _DeviceLU:
         return x
 
     def _tri(self, sch, m, diag, b, x, s):
-        L.call("hn_sptrsv_super", 1 if diag is None else 0, L.ptr(sch.kind), L.ptr(sch.r0), L.ptr(sch.w),
-               L.ptr(sch.rb), L.ptr(sch.rc), L.ptr(sch.off), L.ptr(sch.rw), sch.ntasks, L.ptr(m.rowptr), L.ptr(m.cols),
-               L.ptr(m.vals), L.ptr(diag), L.ptr(sch.packed), 1 if sch.inverse else 0, L.ptr(b), L.ptr(x), L.ptr(self.ysum), self.n,
+        """One triangular solve (m and diag are the schedule's own arrays; kept in the signature
+        for the dev tools)."""
+        L.call("hn_sptrsv_plan", C.byref(sch.plan_struct()), L.ptr(b), L.ptr(x), L.ptr(self.ysum), self.n,
                L.ptr(self.ticket), self.CTAS_PER_SM, s)
 
 

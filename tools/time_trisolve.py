@@ -1,13 +1,18 @@
-"""Time the L and U supernodal solves and one full preconditioner application on config 3
-(dev tool; CUDA events, median of 20)."""
+"""Time the L and U supernodal solves and one full preconditioner application on config 3 for a
+list of dense-tail widths, with the distance to SuperLU's own solve (dev tool; CUDA events,
+median of 20).
+  python tools/time_trisolve.py [M=500] [tails, e.g. 0,1694,4096,8192]"""
 import sys
+import time
 from pathlib import Path
 
 import numpy as np
+from scipy.sparse import linalg as spla
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2303_01760_b200 as hn  # noqa: E402
 from paper_2303_01760_b200 import _lib as L, nodesets  # noqa: E402
+from paper_2303_01760_b200.solver import _DeviceLU  # noqa: E402
 
 
 def timeit(fn, reps=20):
@@ -27,16 +32,29 @@ def timeit(fn, reps=20):
 def main():
     t = L.torch()
     M = int(sys.argv[1]) if len(sys.argv) > 1 else 500
+    tails = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 2048, 4096, 8192, 12288]
     ns = nodesets.hybrid_hole_2d(M, seed=2)
-    ops = hn.build_operators(ns, {"wall:x-"}, hn.PoissonSolveSettings())
-    lu = ops._d_lu
-    b = L.to_device(np.random.default_rng(0).normal(size=lu.n))
-    x = L.empty(lu.n, t.float64)
-    s = L.stream_handle()
-    tl = timeit(lambda: lu._tri(lu.sL, lu.L, None, b, lu.z, s))
-    tu = timeit(lambda: lu._tri(lu.sU, lu.U, lu.diag, b, lu.w, s))
-    tp = timeit(lambda: lu.solve(b, x))
-    print(f"L {tl:.3f} ms  U {tu:.3f} ms  precond {tp:.3f} ms  (L+U nnz {lu.L.nnz + lu.U.nnz})", flush=True)
+    ops = hn.build_operators(ns, {"wall:x-"}, hn.PoissonSolveSettings(), factorize=True)
+    host_lu = spla.splu(ops.poisson_matrix.tocsc())
+    rhs = np.random.default_rng(0).normal(size=host_lu.shape[0])
+    ref = host_lu.solve(rhs)
+    b = L.to_device(rhs)
+    for tail in tails:
+        t0 = time.perf_counter()
+        lu = _DeviceLU(host_lu, tail=tail)
+        t.cuda.synchronize()
+        setup = time.perf_counter() - t0
+        x = L.empty(lu.n, t.float64)
+        s = L.stream_handle()
+        tl = timeit(lambda: lu._tri(lu.sL, lu.L, None, b, lu.z, s))
+        tu = timeit(lambda: lu._tri(lu.sU, lu.U, lu.diag, b, lu.w, s))
+        tp = timeit(lambda: lu.solve(b, x))
+        err = np.abs(x.cpu().numpy() - ref).max() / np.abs(ref).max()
+        print(f"tail {lu.tail:6d}: L {tl:.3f} ms  U {tu:.3f} ms  precond {tp:.3f} ms  vs SuperLU {err:.2e}  "
+              f"depth L {lu.sL.depth} U {lu.sU.depth}  bytes {lu.solve_bytes / 1e6:.0f} MB  setup {setup:.1f} s",
+              flush=True)
+        del lu, x
+        t.cuda.empty_cache()
 
 
 if __name__ == "__main__":
