@@ -240,7 +240,8 @@ int hn_csr_residual(const int64_t* rowptr, const int* cols, const double* vals, 
  * computing the outside sums of block rows [rb, rb+rc) into ysum (heavy blocks); kind 2:
  * dense part of a heavy block, fed by its helpers (scheduled just before it); kind 3: up to
  * 8 small blocks (w <= 32) of one level, one warp each (members listed after the tasks).
- * inv: the packed diagonal tiles are inverses (x = T^-1 y per tile instead of substitution).
+ * inv: 1 = the packed diagonal tiles are inverses (x = T^-1 y per tile instead of substitution),
+ * 2 = the packed triangle is the whole block's inverse (x = B^-1 y, no tile-to-tile chain).
  * blk_rw (may be NULL): per task, the width of the dense rectangle coupling the block to its
  * adjacent predecessor (lower: the rw rows before r0, upper: after r0 + w); those columns are
  * left out of the off-block sums and applied from packed rectangle panels as the
@@ -250,7 +251,7 @@ int hn_csr_residual(const int64_t* rowptr, const int* cols, const double* vals, 
 /* One triangular factor's supernodal task list (all device pointers; see hn_sptrsv_super). */
 typedef struct hn_tri_plan {
   int lower;             /* 1: unit-lower L, 0: upper U (divides by diag) */
-  int inv;               /* packed diagonal tiles are inverses */
+  int inv;               /* 0 substitution, 1 diagonal-tile inverses, 2 whole-block inverses */
   int64_t ntasks;
   const int* kind;
   const int* r0;
@@ -292,9 +293,11 @@ int hn_sptrsv_plan(const hn_tri_plan* plan, const double* b, double* x, double* 
  * tasks of kind 0/2 (panels of 32 columns, column-major; off[t] in doubles, -1 for other
  * kinds; packed == NULL computes offsets only; returns the total, -1 if a block's in-block
  * triangle or rectangle is not dense; rw_host may be NULL).  Rectangle panels (rw_host[t] > 0)
- * come first: the predecessor's columns in its tile order, all w rows.  inverse != 0: every
- * diagonal tile's rows hold that tile's inverse
- * (diag_host = U's diagonal for upper) and hn_sptrsv_super must be called with inv = 1. */
+ * come first: the predecessor's columns in its tile order, all w rows.  inverse = 1: every
+ * diagonal tile's rows hold that tile's inverse; inverse = 2: the triangle panels hold the
+ * inverse of the block's whole triangle (diagonal included), the block is then x = B^-1 y panel
+ * by panel (diag_host = U's diagonal for upper); hn_sptrsv_super must be called with inv =
+ * the same value. */
 int64_t hn_host_supernodes(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower, int cap,
                            int* blk_r0_host, int* blk_w_host);
 int hn_host_block_levels(const int64_t* rowptr_host, const int* cols_host, int64_t n, int lower, int64_t nblk,

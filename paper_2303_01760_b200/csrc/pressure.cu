@@ -423,6 +423,7 @@ __global__ void __launch_bounds__(kSnThreads, 2) sptrsv_super_kernel(
     seq_geom(LOWER, w, rw, 0, rect, t0, tw, rbase, rows, rp);
     const double* panel = P;
     double cur[32];
+    double acc = 0.0;  // inv == 2: this row of x = B^-1 y, summed panel by panel
     {
       const int rr = tid - rbase;
       const bool in = has && rr >= 0 && rr < rows;
@@ -453,6 +454,21 @@ __global__ void __launch_bounds__(kSnThreads, 2) sptrsv_super_kernel(
             a3 = fma(cur[k + 3], s_xr[k + 3], a3);
           }
           ys[tid] -= (a0 + a1) + (a2 + a3);
+        }
+      } else if (inv == 2) {
+        // whole-block inverse: the panels hold B^-1 (B = the block's triangle with its diagonal),
+        // so every panel is an independent slice of x = B^-1 y -- no tile-to-tile chain, no
+        // barrier besides the panel hand-over.  ys keeps y (the rectangle panels came first).
+        if (has) {
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) {
+            a0 = fma(cur[k], ys[t0 + k], a0);
+            a1 = fma(cur[k + 1], ys[t0 + k + 1], a1);
+            a2 = fma(cur[k + 2], ys[t0 + k + 2], a2);
+            a3 = fma(cur[k + 3], ys[t0 + k + 3], a3);
+          }
+          acc += (a0 + a1) + (a2 + a3);
         }
       } else {
         if (warp == t0 / 32 && inv) {  // x = T^-1 y: 32 independent products, no chain
@@ -512,6 +528,7 @@ __global__ void __launch_bounds__(kSnThreads, 2) sptrsv_super_kernel(
       }
       __syncthreads();
     }
+    if (inv == 2 && has) st_release_dbl(x + i, acc);
 #ifdef HN_TRACE
     if (tid == 0) {
       SN_TRACE(2, gtime());
@@ -634,7 +651,7 @@ constexpr int kNbuf = 32 * kSnMaxW * static_cast<int>(sizeof(double));  // one p
 
 // ---- dense tail -----------------------------------------------------------------------
 // The last T rows of a SuperLU factor are (nearly) dense supernodes solved one 256-wide block
-// after the other: at config 3 the last 8192 rows hold 54 of L's 96 block levels and 49 of
+// after the other: at config 3 the last 4096 rows hold 23 of L's 96 block levels and 22 of
 // U's 77, each a ~13 us hop on one CTA.  They are replaced by the explicit inverse of the
 // trailing T x T triangle (computed once at setup): x_T = inv * y_T is one dense
 // matrix-vector product over every SM (8 T^2 / 2 bytes from HBM) instead of a dependency
@@ -798,6 +815,44 @@ HN_EXPORT int64_t hn_host_pack_panels(const int64_t* rowptr_host, const int* col
     const int64_t r0 = r0_host[t];
     const int64_t pr0 = lower ? r0 - rw : r0 + w;  // the rectangle's predecessor rows
     const int npanels = (rw + 31) / 32 + (w + 31) / 32;
+    // inverse == 2: X = B^-1 of the whole block triangle B (unit / U's diagonal included), by
+    // substitution on the identity; the triangle panels then hold X instead of B
+    static thread_local double* Bm = nullptr;
+    static thread_local double* Xm = nullptr;
+    if (inverse == 2 && packed_host) {
+      if (!Bm) {
+        Bm = new double[kSnMaxW * kSnMaxW];
+        Xm = new double[kSnMaxW * kSnMaxW];
+      }
+      for (int row = 0; row < w; ++row) {
+        const int64_t i = r0 + row;
+        const int64_t a = rowptr_host[i], z = rowptr_host[i + 1];
+        for (int c = 0; c < w; ++c) Bm[row * w + c] = 0.0;
+        Bm[row * w + row] = lower ? 1.0 : diag_host[i];
+        for (int c = (lower ? 0 : row + 1); c < (lower ? row : w); ++c) {
+          const int64_t e = lower ? (z - row) + c : a + (c - row - 1);
+          if (e < a || e >= z || cols_host[e] != r0 + c) return -1;  // not dense
+          Bm[row * w + c] = vals_host[e];
+        }
+      }
+      for (int j = 0; j < w; ++j) {
+        if (lower) {
+          for (int l = 0; l < w; ++l) {
+            if (l < j) { Xm[l * w + j] = 0.0; continue; }
+            double v = l == j ? 1.0 : 0.0;
+            for (int k = j; k < l; ++k) v -= Bm[l * w + k] * Xm[k * w + j];
+            Xm[l * w + j] = v;
+          }
+        } else {
+          for (int l = w - 1; l >= 0; --l) {
+            if (l > j) { Xm[l * w + j] = 0.0; continue; }
+            double v = l == j ? 1.0 : 0.0;
+            for (int k = l + 1; k <= j; ++k) v -= Bm[l * w + k] * Xm[k * w + j];
+            Xm[l * w + j] = v / Bm[l * w + l];
+          }
+        }
+      }
+    }
     for (int pi = 0; pi < npanels; ++pi) {
       bool rect;
       int t0, tw, rbase, rows, rp;
@@ -817,6 +872,9 @@ HN_EXPORT int64_t hn_host_pack_panels(const int64_t* rowptr_host, const int* col
             if (rect) {  // predecessor column pr0 + c: the last rw outside entries (lower) / the first (upper)
               e = lower ? (z - inside - rw) + c : a + inside + c;
               want = pr0 + c;
+            } else if (inverse == 2) {
+              if (lower ? c <= row : c >= row) pn[static_cast<int64_t>(k) * rp + rr] = Xm[row * w + c];
+              continue;
             } else {
               if (!(lower ? c < row : c > row)) continue;
               e = lower ? (z - row) + c : a + (c - row - 1);
@@ -826,7 +884,7 @@ HN_EXPORT int64_t hn_host_pack_panels(const int64_t* rowptr_host, const int* col
             pn[static_cast<int64_t>(k) * rp + rr] = vals_host[e];
           }
         }
-        if (inverse && !rect) {  // the diagonal tile's rows hold T^-1 (substitution on the identity)
+        if (inverse == 1 && !rect) {  // the diagonal tile's rows hold T^-1 (substitution on the identity)
           double T[32][32], X[32][32];
           const int d0 = t0 - rbase;  // first diagonal-tile row inside the panel
           for (int l = 0; l < tw; ++l)

@@ -230,7 +230,7 @@ class _SuperSchedule:
     the factor's last `tail` rows leave the task list and are solved through the explicit
     inverse of the trailing triangle (csrc/pressure.cu, 'dense tail')."""
 
-    def __init__(self, m: sparse.csr_matrix, lower: bool, diag: np.ndarray | None = None, inverse: bool = False,
+    def __init__(self, m: sparse.csr_matrix, lower: bool, diag: np.ndarray | None = None, inverse: int = 0,
                  tail: int = 0, **plan_kw):
         n = m.shape[0]
         tail = int(tail) if 0 < int(tail) < n else 0
@@ -246,7 +246,7 @@ class _SuperSchedule:
         extra = (np.diff(lead.indptr) - np.diff(lead_sq.indptr)) if tail and not lower else None
         plan = plan_supernodal_blocks(lead_sq, lower, extra_outside=extra, **plan_kw)
         self.csr = DeviceCSR(lead)
-        self.inverse = bool(inverse)
+        self.inverse = int(inverse)  # 0 substitution, 1 diagonal-tile inverses, 2 whole-block inverses
         self.nblk, self.depth, self.ntasks = plan["nblk"], plan["depth"], plan["ntasks"]
         kind, r0, w, rw = plan["kind"], plan["t_r0"], plan["t_w"], plan["t_rw"]
         vp = L._vp
@@ -256,7 +256,7 @@ class _SuperSchedule:
         off = np.empty(len(kind), dtype=np.int64)
         dg = np.ascontiguousarray(diag if diag is not None else np.ones(1), dtype=np.float64)
         args = (rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), vals.ctypes.data_as(vp), dg.ctypes.data_as(vp),
-                1 if lower else 0, 1 if inverse else 0, self.ntasks, kind.ctypes.data_as(vp), r0.ctypes.data_as(vp),
+                1 if lower else 0, int(inverse), self.ntasks, kind.ctypes.data_as(vp), r0.ctypes.data_as(vp),
                 w.ctypes.data_as(vp), rw.ctypes.data_as(vp), off.ctypes.data_as(vp))
         total = int(L.lib().hn_host_pack_panels(*args, None))
         packed = np.empty(max(total, 2), dtype=np.float64)
@@ -276,7 +276,7 @@ class _SuperSchedule:
         if tail:
             self._build_tail(m, k, diag)
         self._plan = L.TriPlan(
-            1 if lower else 0, 1 if self.inverse else 0, self.ntasks, self.kind.data_ptr(), self.r0.data_ptr(),
+            1 if lower else 0, self.inverse, self.ntasks, self.kind.data_ptr(), self.r0.data_ptr(),
             self.w.data_ptr(), self.rb.data_ptr(), self.rc.data_ptr(), self.off.data_ptr(), self.rw.data_ptr(),
             self.csr.rowptr.data_ptr(), self.csr.cols.data_ptr(), self.csr.vals.data_ptr(),
             self.d_diag.data_ptr() if self.d_diag is not None else None, self.packed.data_ptr(), tail,
@@ -318,18 +318,25 @@ class _DeviceLU:
     # no substitution chain) for the L / U solve.  Config 3 (tools/ab_inverse.py): L 1.10 ->
     # 0.91 ms, U 1.27 -> 1.06 ms; the solve moves from 1.2e-11 to 1.1e-10 of SuperLU's (max
     # norm, random rhs) and the fields after 50 full steps by <= 1.1e-12 (relative).
-    TILE_INVERSE_L = True
-    TILE_INVERSE_U = True
+    # (2 = whole-block inverses -- the packed panels hold the inverse of a block's entire dense
+    # triangle, x = B^-1 y panel by panel with no tile-to-tile chain -- measured slower: L 0.726
+    # -> 0.777 ms with the dense tail, 5e-10 from SuperLU: a block's x is then published only
+    # at its end, while the tile scheme feeds the next piece of a supernode tile by tile.)
+    TILE_INVERSE_L = 1
+    TILE_INVERSE_U = 1
     # dense tail: the factors' last TAIL rows (at most a quarter of the matrix) are solved through
     # the explicit inverse of the trailing triangle instead of the block chain -- at config 3
-    # the last 8192 rows hold 54 of L's 96 and 49 of U's 77 block levels.  0 = off.
-    TAIL = 8192
+    # the last 8192 rows hold 54 of L's 96 and 49 of U's 77 block levels, the last 4096 rows 23
+    # and 22.  Measured (tools/time_trisolve.py, L + U): no tail 1.944 ms, 1694 (the fully dense
+    # triangle) 1.839, 4096 1.556, 8192 1.564, 12288 1.673 -- beyond ~4096 rows the remaining
+    # depth sits in other branches of the elimination tree and the inverse only adds bytes.  0 = off.
+    TAIL = 4096
     # max-norm relative distance to SuperLU's solve on a random rhs (tests): U is ill-conditioned
     # (block kappa up to 7e7), two exact substitution orders differ by ~6e-11; the diagonal-tile
     # inverses move it to ~1.1e-10 (fields: <= 1.1e-12 after 50 steps, see above)
     PARITY_TOL = {False: 1e-10, True: 1e-9}
 
-    def __init__(self, lu, inverse: bool | None = None, tail: int | None = None, **plan_kw):
+    def __init__(self, lu, inverse: int | None = None, tail: int | None = None, **plan_kw):
         Lm = sparse.csr_matrix(lu.L)
         Um = sparse.csr_matrix(lu.U)
         self.n = Lm.shape[0]
@@ -360,7 +367,7 @@ class _DeviceLU:
         # the tail inverses' triangles (what replaced the tail's own 12 B entries)
         self.solve_bytes = 12 * (self.sL.nnz + self.sU.nnz) + self.sL.tail_bytes - (
             12 * int(self.sL.coupling.nnz) if self.sL.coupling is not None else 0) + self.sU.tail_bytes + 8 * self.n
-        self.parity_tol = self.PARITY_TOL[self.sL.inverse or self.sU.inverse or bool(self.tail)]
+        self.parity_tol = self.PARITY_TOL[bool(self.sL.inverse or self.sU.inverse or self.tail)]
 
     def plans(self):
         """(L, U) as hn_tri_plan structs for hn_pressure_setup (the arrays stay owned here)."""

@@ -359,8 +359,8 @@ class TestRun:
         npt.assert_array_equal(a.state.temperature[mask], ns.bc_value[mask])
 
 
-@pytest.mark.parametrize("inverse,tail,tol", [(False, 0, 1e-12), (True, 0, 1e-9), (False, 900, 1e-10),
-                                              (True, None, 1e-9)])
+@pytest.mark.parametrize("inverse,tail,tol", [(False, 0, 1e-12), (True, 0, 1e-9), (2, 0, 1e-9), (False, 900, 1e-10),
+                                              (True, None, 1e-9), (None, None, 1e-9)])
 def test_device_lu_solve_matches_superlu(inverse, tail, tol):
     """The GPU preconditioner (SuperLU factors, supernodal sync-free solves over packed dense
     panels) against SuperLU's own solve: substitution to rounding, diagonal-tile inverses and
@@ -387,7 +387,7 @@ def test_device_lu_solve_matches_superlu(inverse, tail, tol):
 
 
 @pytest.mark.parametrize("cap,helper", [(32, 64), (96, 512), (256, 4096)])
-@pytest.mark.parametrize("inverse,tail", [(False, 0), (True, 0), (False, 333), (True, 750)])
+@pytest.mark.parametrize("inverse,tail", [(False, 0), (True, 0), (2, 0), (False, 333), (True, 750), (2, 750)])
 def test_device_lu_random_fill_all_block_shapes(cap, helper, inverse, tail):
     """Random sparse matrix with heavy fill: blocks of every width up to the cap (partial last
     panels, upper and lower), helper-fed blocks and batched small blocks, vs SuperLU."""
