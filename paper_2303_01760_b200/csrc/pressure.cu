@@ -472,15 +472,17 @@ __global__ void __launch_bounds__(kSnThreads, 2) sptrsv_super_kernel(
         }
       } else {
         if (warp == t0 / 32 && inv) {  // x = T^-1 y: 32 independent products, no chain
-          const double yv = lane < tw ? ys[tid] : 0.0;
+          // y of the tile's rows straight from shared memory (broadcast reads; columns past tw
+          // are zero in the panel and ys beyond w is zeroed above): no 32-shuffle sequence
           double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
           for (int k = 0; k < 32; k += 4) {
-            a0 = fma(cur[k], __shfl_sync(0xffffffffu, yv, k), a0);
-            a1 = fma(cur[k + 1], __shfl_sync(0xffffffffu, yv, k + 1), a1);
-            a2 = fma(cur[k + 2], __shfl_sync(0xffffffffu, yv, k + 2), a2);
-            a3 = fma(cur[k + 3], __shfl_sync(0xffffffffu, yv, k + 3), a3);
+            a0 = fma(cur[k], ys[t0 + k], a0);
+            a1 = fma(cur[k + 1], ys[t0 + k + 1], a1);
+            a2 = fma(cur[k + 2], ys[t0 + k + 2], a2);
+            a3 = fma(cur[k + 3], ys[t0 + k + 3], a3);
           }
+          __syncwarp();  // every lane has read the tile's y before any lane overwrites its entry
           if (lane < tw) {
             ys[tid] = (a0 + a1) + (a2 + a3);
             st_release_dbl(x + i, ys[tid]);
