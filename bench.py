@@ -519,8 +519,8 @@ def _explicit_roofline(L, stepper, ns, steps, flush):
 def pressure_bytes(ops) -> int:
     """Algorithmic HBM bytes of one warm pressure solve (one BiCGStab half-step, SURVEY §8(a)
     A17): 2 A-matvecs (12 B/nnz + int64 row pointer + x gather/y write), one preconditioner
-    application (L and U: 12 B per sparse entry the task kernels and the tail coupling read, 8 B per
-    entry of the dense-tail inverses' triangles, the U diagonal, the two permutations in and out) and the
+    application (L and U: 12 B per sparse entry the task kernels and the dense groups' coupling read,
+    8 B per entry of the groups' inverse triangles, the U diagonal, the two permutations in and out) and the
     BiCGStab vector algebra (~12 vector passes of 8 B/element)."""
     n1 = ops.n + 1
     a_nnz = int(ops._d_poisson.nnz)

@@ -265,17 +265,26 @@ typedef struct hn_tri_plan {
   const double* vals;
   const double* diag;    /* U only */
   const double* packed;
-  /* Dense tail (optional, tail_inv != NULL): the tasks above cover rows [0, n - tail_n) only
-   * (for U their rows keep the tail columns: x of the tail is final before they run); the last
-   * tail_n rows are solved as x_T = tail_inv * y_T, tail_inv the row-major tail_n x tail_n
-   * inverse of the factor's trailing triangle (unit diagonal for L, U's diagonal included).
-   * L: y_T = b_T - C x with C = rows [n - tail_n, n) restricted to columns < n - tail_n (CSR:
-   * tail_rowptr (tail_n + 1), tail_cols, tail_vals); U: y_T = b_T. */
-  int64_t tail_n;
-  const int64_t* tail_rowptr;
-  const int* tail_cols;
-  const double* tail_vals;
-  const double* tail_inv;
+  /* Dense groups (optional, g_inv != NULL): row runs at the top of the elimination tree that
+   * leave the task list (their rows are empty in rowptr/cols/vals; for U their diag entries
+   * are 1) and are solved as x_G = inv(T_GG) (b_G - C_G x), phase by phase (<= 16 phases; the
+   * runs of one phase are independent): rows [phase_ptr[p], phase_ptr[p+1]) of the arrays
+   * below.  g_row: row id; g_cpl_*: CSR of C_G (the row's entries outside its run: columns
+   * before it for L, after it for U) over the same row order; x[row] = sum_{c < g_cnt}
+   * g_inv[g_inv_off + c] * y[g_ystart + c], the row's slice of its run's inverse triangle
+   * (row-packed).  L: after the tasks; U: before them, and b's group entries are overwritten
+   * with the solution. */
+  int n_phases;
+  int64_t phase_ptr[17];
+  const int* g_row;
+  const int64_t* g_cpl_rowptr;
+  const int* g_cpl_cols;
+  const double* g_cpl_vals;
+  const int64_t* g_inv_off;
+  const int* g_cnt;
+  const int* g_ystart;
+  const double* g_inv;
+  double* g_y;           /* scratch, n fp64, owned by the plan's creator (y of the group rows) */
 } hn_tri_plan;
 
 int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int* blk_w, const int* blk_rb,
@@ -284,8 +293,9 @@ int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0, const int
                     const double* b, double* x, double* ysum, int64_t n, unsigned long long* ticket,
                     int ctas_per_sm, void* stream);
 
-/* hn_sptrsv_super from a plan struct, dense tail included. */
-int hn_sptrsv_plan(const hn_tri_plan* plan, const double* b, double* x, double* ysum, int64_t n,
+/* hn_sptrsv_super from a plan struct, dense groups included (an upper plan with groups
+ * overwrites the groups' entries of b). */
+int hn_sptrsv_plan(const hn_tri_plan* plan, double* b, double* x, double* ysum, int64_t n,
                    unsigned long long* ticket, int ctas_per_sm, void* stream);
 
 /* Setup helpers on HOST arrays: dense-triangle row blocks (returns the count; blocks in row

@@ -28,8 +28,9 @@ class TriPlan(C.Structure):
     """hn_tri_plan (include/hn.h): one triangular factor's supernodal task list."""
     _fields_ = [("lower", _i), ("inv", _i), ("ntasks", _i64), ("kind", _vp), ("r0", _vp), ("w", _vp), ("rb", _vp),
                 ("rc", _vp), ("off", _vp), ("rw", _vp), ("rowptr", _vp), ("cols", _vp), ("vals", _vp), ("diag", _vp),
-                ("packed", _vp), ("tail_n", _i64), ("tail_rowptr", _vp), ("tail_cols", _vp), ("tail_vals", _vp),
-                ("tail_inv", _vp)]
+                ("packed", _vp), ("n_phases", _i), ("phase_ptr", _i64 * 17), ("g_row", _vp), ("g_cpl_rowptr", _vp),
+                ("g_cpl_cols", _vp), ("g_cpl_vals", _vp), ("g_inv_off", _vp), ("g_cnt", _vp), ("g_ystart", _vp),
+                ("g_inv", _vp), ("g_y", _vp)]
 
 
 # name -> (restype, argtypes); mirrors include/hn.h exactly (tests check the export list)

@@ -651,19 +651,25 @@ __global__ void sptrsv_reset_kernel(double* __restrict__ x, double* __restrict__
 
 constexpr int kNbuf = 32 * kSnMaxW * static_cast<int>(sizeof(double));  // one panel (dynamic smem)
 
-// ---- dense tail -----------------------------------------------------------------------
-// The last T rows of a SuperLU factor are (nearly) dense supernodes solved one 256-wide block
-// after the other: at config 3 the last 4096 rows hold 23 of L's 96 block levels and 22 of
-// U's 77, each a ~13 us hop on one CTA.  They are replaced by the explicit inverse of the
-// trailing T x T triangle (computed once at setup): x_T = inv * y_T is one dense
-// matrix-vector product over every SM (8 T^2 / 2 bytes from HBM) instead of a dependency
-// chain.  Lower: the task kernel solves rows [0, n-T), then y_T = b_T - L[T rows, leading
-// columns] x (tail_coupling_kernel), then x_T = inv y_T.  Upper: x_T = inv b_T first; the
-// leading rows read those columns as ordinary (already final) dependencies.
+// ---- dense groups ---------------------------------------------------------------------
+// The top of the elimination tree -- the separators' (nearly) dense supernodes -- is a chain
+// of 256-wide pieces that can only run one after the other: at config 3 the block levels >= 40
+// of L (56 of its 96 levels, 26 K rows in 24 contiguous row runs) cost ~10 us each on a
+// single CTA while the other 295 wait.  Those rows leave the task list (their rows are empty
+// in the task kernel's matrix: x = b, overwritten here).  Each run G = [a, b) is solved through
+// the explicit inverse of its triangle, formed once at setup:
+//     x_G = inv(T_GG) * (b_G - C_G x),   C_G = G's rows restricted to the columns outside G
+// = one CSR product and one dense triangular product, each a single launch over every SM for
+// all runs of one phase (runs of a phase do not depend on each other; a run's phase = 1 + the
+// highest phase among the runs it reads).  Lower: after the task kernel, phases ascending
+// (C_G = columns < a: leaves and earlier runs, all final).  Upper: before the task kernel,
+// phases ascending from the root run (C_G = columns >= b); the other rows then read these
+// columns as ordinary, already final, dependencies.  The runs are closed under the solves'
+// dependencies (no other row of L reads them; they read no other row of U).
 // One CTA per row, fixed column striding and a fixed reduction tree: deterministic.
-constexpr int kTailThreads = 256;
+constexpr int kGroupThreads = 256;
 
-__device__ __forceinline__ double tail_block_sum(double v, double* s_red) {
+__device__ __forceinline__ double group_block_sum(double v, double* s_red) {
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) s_red[warp] = v;
@@ -671,22 +677,23 @@ __device__ __forceinline__ double tail_block_sum(double v, double* s_red) {
   double tot = 0.0;
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < kTailThreads / 32; ++k) tot += s_red[k];
+    for (int k = 0; k < kGroupThreads / 32; ++k) tot += s_red[k];
   }
   return tot;  // valid on thread 0
 }
 
-__global__ void __launch_bounds__(kTailThreads) tail_coupling_kernel(
-    const int64_t* __restrict__ rowptr, const int* __restrict__ cols, const double* __restrict__ vals,
-    const double* __restrict__ b_tail, const double* __restrict__ x, double* __restrict__ y,
-    const int* __restrict__ skip) {
+// y[row] = b[row] - sum_e vals[e] * x[cols[e]] over the row's entries outside its run
+__global__ void __launch_bounds__(kGroupThreads) group_coupling_kernel(
+    const int* __restrict__ g_row, const int64_t* __restrict__ rowptr, const int* __restrict__ cols,
+    const double* __restrict__ vals, int64_t q0, const double* __restrict__ b, const double* __restrict__ x,
+    double* __restrict__ y, const int* __restrict__ skip) {
   if (skip && *skip) return;
-  __shared__ double s_red[kTailThreads / 32];
-  const int r = blockIdx.x;
-  const int64_t e0 = __ldg(rowptr + r), e1 = __ldg(rowptr + r + 1);
+  __shared__ double s_red[kGroupThreads / 32];
+  const int64_t q = q0 + blockIdx.x;
+  const int64_t e0 = __ldg(rowptr + q), e1 = __ldg(rowptr + q + 1);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += 4 * kTailThreads) {
-    const int64_t ea = e + kTailThreads, eb = e + 2 * kTailThreads, ec = e + 3 * kTailThreads;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += 4 * kGroupThreads) {
+    const int64_t ea = e + kGroupThreads, eb = e + 2 * kGroupThreads, ec = e + 3 * kGroupThreads;
     const int c0 = __ldg(cols + e);
     const int c1 = ea < e1 ? __ldg(cols + ea) : -1;
     const int c2 = eb < e1 ? __ldg(cols + eb) : -1;
@@ -700,35 +707,44 @@ __global__ void __launch_bounds__(kTailThreads) tail_coupling_kernel(
     a2 = fma(v2, c2 >= 0 ? x[c2] : 0.0, a2);
     a3 = fma(v3, c3 >= 0 ? x[c3] : 0.0, a3);
   }
-  const double tot = tail_block_sum((a0 + a1) + (a2 + a3), s_red);
-  if (threadIdx.x == 0) y[r] = __ldg(b_tail + r) - tot;
+  const double tot = group_block_sum((a0 + a1) + (a2 + a3), s_red);
+  if (threadIdx.x == 0) {
+    const int row = __ldg(g_row + q);
+    y[row] = __ldg(b + row) - tot;
+  }
 }
 
-template <bool LOWER>
-__global__ void __launch_bounds__(kTailThreads) tail_gemv_kernel(const double* __restrict__ inv, int T,
-                                                                 const double* __restrict__ y,
-                                                                 double* __restrict__ x_tail,
-                                                                 const int* __restrict__ skip) {
+// x[row] = sum_c inv[off + c] * y[ystart + c], c < cnt (the row's part of its run's inverse);
+// echo (upper): the rhs entry takes the solution too, so the task kernel's trivial row
+// (x = b / 1) reproduces it
+__global__ void __launch_bounds__(kGroupThreads) group_gemv_kernel(
+    const int* __restrict__ g_row, const int64_t* __restrict__ g_off, const int* __restrict__ g_cnt,
+    const int* __restrict__ g_ystart, const double* __restrict__ inv, int64_t q0, const double* __restrict__ y,
+    double* __restrict__ x, double* __restrict__ echo, const int* __restrict__ skip) {
   if (skip && *skip) return;
-  __shared__ double s_red[kTailThreads / 32];
-  // long rows first: the grid drains evenly
-  const int r = LOWER ? T - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
-  const int c_lo = LOWER ? 0 : r, c_hi = LOWER ? r + 1 : T;
-  const double* row = inv + static_cast<int64_t>(r) * T;
+  __shared__ double s_red[kGroupThreads / 32];
+  const int64_t q = q0 + blockIdx.x;
+  const double* row = inv + __ldg(g_off + q);
+  const int cnt = __ldg(g_cnt + q);
+  const double* yv = y + __ldg(g_ystart + q);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  for (int c = c_lo + threadIdx.x; c < c_hi; c += 4 * kTailThreads) {
-    const int ca = c + kTailThreads, cb = c + 2 * kTailThreads, cc = c + 3 * kTailThreads;
+  for (int c = threadIdx.x; c < cnt; c += 4 * kGroupThreads) {
+    const int ca = c + kGroupThreads, cb = c + 2 * kGroupThreads, cc = c + 3 * kGroupThreads;
     const double m0 = __ldg(row + c);
-    const double m1 = ca < c_hi ? __ldg(row + ca) : 0.0;
-    const double m2 = cb < c_hi ? __ldg(row + cb) : 0.0;
-    const double m3 = cc < c_hi ? __ldg(row + cc) : 0.0;
-    a0 = fma(m0, y[c], a0);
-    a1 = fma(m1, ca < c_hi ? y[ca] : 0.0, a1);
-    a2 = fma(m2, cb < c_hi ? y[cb] : 0.0, a2);
-    a3 = fma(m3, cc < c_hi ? y[cc] : 0.0, a3);
+    const double m1 = ca < cnt ? __ldg(row + ca) : 0.0;
+    const double m2 = cb < cnt ? __ldg(row + cb) : 0.0;
+    const double m3 = cc < cnt ? __ldg(row + cc) : 0.0;
+    a0 = fma(m0, yv[c], a0);
+    a1 = fma(m1, ca < cnt ? yv[ca] : 0.0, a1);
+    a2 = fma(m2, cb < cnt ? yv[cb] : 0.0, a2);
+    a3 = fma(m3, cc < cnt ? yv[cc] : 0.0, a3);
   }
-  const double tot = tail_block_sum((a0 + a1) + (a2 + a3), s_red);
-  if (threadIdx.x == 0) x_tail[r] = tot;
+  const double tot = group_block_sum((a0 + a1) + (a2 + a3), s_red);
+  if (threadIdx.x == 0) {
+    const int r = __ldg(g_row + q);
+    x[r] = tot;
+    if (echo) echo[r] = tot;
+  }
 }
 
 cudaError_t sptrsv_prepare() {
@@ -739,14 +755,27 @@ cudaError_t sptrsv_prepare() {
   return cudaFuncSetAttribute(sptrsv_super_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNbuf);
 }
 
-cudaError_t sptrsv_enqueue(const hn_tri_plan& p, const double* b, double* x, double* ysum, int64_t n,
+static void group_phases(const hn_tri_plan& p, double* b, double* x, const int* skip, cudaStream_t s) {
+  // y lives in the plan's own scratch (g_y), never in ysum: there a non-sentinel value means
+  // "the helpers' sum is ready", and an upper block may end in a group row (an empty row joins
+  // the supernode of the rows before it), whose dense task would take the groups' y for it
+  for (int ph = 0; ph < p.n_phases; ++ph) {
+    const int64_t q0 = p.phase_ptr[ph], rows = p.phase_ptr[ph + 1] - q0;
+    if (rows <= 0) continue;
+    group_coupling_kernel<<<static_cast<unsigned>(rows), kGroupThreads, 0, s>>>(p.g_row, p.g_cpl_rowptr, p.g_cpl_cols,
+                                                                                p.g_cpl_vals, q0, b, x, p.g_y, skip);
+    group_gemv_kernel<<<static_cast<unsigned>(rows), kGroupThreads, 0, s>>>(p.g_row, p.g_inv_off, p.g_cnt, p.g_ystart,
+                                                                            p.g_inv, q0, p.g_y, x,
+                                                                            p.lower ? nullptr : b, skip);
+  }
+}
+
+cudaError_t sptrsv_enqueue(const hn_tri_plan& p, double* b, double* x, double* ysum, int64_t n,
                            unsigned long long* ticket, int ctas_per_sm, const int* skip, cudaStream_t s) {
-  const int64_t T = p.tail_inv ? p.tail_n : 0, k = n - T;
-  if ((p.ntasks == 0 && T == 0) || n == 0 || k < 0) return cudaSuccess;
+  const bool groups = p.g_inv != nullptr && p.g_y != nullptr && p.n_phases > 0;
+  if ((p.ntasks == 0 && !groups) || n == 0) return cudaSuccess;
   sptrsv_reset_kernel<<<ceil_div(n, 256), 256, 0, s>>>(x, ysum, n, ticket, skip);
-  if (!p.lower && T > 0)  // upper: the tail is solved first, straight from its inverse
-    tail_gemv_kernel<false><<<static_cast<int>(T), kTailThreads, 0, s>>>(p.tail_inv, static_cast<int>(T), b + k,
-                                                                         x + k, skip);
+  if (!p.lower && groups) group_phases(p, b, x, skip, s);  // upper: the top of the tree first
   const int blocks = sm_count() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
   if (p.ntasks > 0) {
     if (p.lower)
@@ -758,12 +787,7 @@ cudaError_t sptrsv_enqueue(const hn_tri_plan& p, const double* b, double* x, dou
                                                                    p.ntasks, p.rowptr, p.cols, p.vals, p.diag,
                                                                    p.packed, p.inv, b, x, ysum, ticket, skip);
   }
-  if (p.lower && T > 0) {  // lower: the tail last -- its coupling to the solved rows, then the inverse
-    tail_coupling_kernel<<<static_cast<int>(T), kTailThreads, 0, s>>>(p.tail_rowptr, p.tail_cols, p.tail_vals, b + k,
-                                                                      x, ysum + k, skip);
-    tail_gemv_kernel<true><<<static_cast<int>(T), kTailThreads, 0, s>>>(p.tail_inv, static_cast<int>(T), ysum + k,
-                                                                        x + k, skip);
-  }
+  if (p.lower && groups) group_phases(p, b, x, skip, s);  // lower: the top of the tree last
   return cudaGetLastError();
 }
 
@@ -782,17 +806,17 @@ HN_EXPORT int hn_sptrsv_super(int lower, const int* blk_kind, const int* blk_r0,
   if (nblk == 0) return 0;
   HN_TRY(sptrsv_prepare());
   const hn_tri_plan p{lower, inv, nblk, blk_kind, blk_r0, blk_w, blk_rb, blk_rc, blk_off, blk_rw, rowptr, cols, vals,
-                      diag, packed, 0, nullptr, nullptr, nullptr, nullptr};
-  HN_TRY(sptrsv_enqueue(p, b, x, ysum, n, ticket, ctas_per_sm, nullptr, as_stream(stream)));
+                      diag, packed, 0, {0}, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  HN_TRY(sptrsv_enqueue(p, const_cast<double*>(b), x, ysum, n, ticket, ctas_per_sm, nullptr, as_stream(stream)));
   return 0;
 }
 
-// The same solve from a plan struct, including the plan's dense tail (tail_n rows through
-// tail_inv) when it has one.
-HN_EXPORT int hn_sptrsv_plan(const hn_tri_plan* plan, const double* b, double* x, double* ysum, int64_t n,
+// The same solve from a plan struct, dense groups included.  An upper plan with groups
+// overwrites the groups' entries of b with their solution (see group_gemv_kernel).
+HN_EXPORT int hn_sptrsv_plan(const hn_tri_plan* plan, double* b, double* x, double* ysum, int64_t n,
                              unsigned long long* ticket, int ctas_per_sm, void* stream) {
   if (!plan) return 1;
-  if (plan->tail_inv && (plan->tail_n < 0 || plan->tail_n > n)) return 2;
+  if (plan->n_phases < 0 || plan->n_phases > 16) return 2;
   HN_TRY(sptrsv_prepare());
   HN_TRY(sptrsv_enqueue(*plan, b, x, ysum, n, ticket, ctas_per_sm, nullptr, as_stream(stream)));
   return 0;

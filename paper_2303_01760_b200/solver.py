@@ -125,8 +125,8 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, he
     to the adjacent predecessor block (the pieces of one supernode cut at `cap`) takes those
     columns off its off-block sums and applies them itself from packed rectangle panels, tile
     by tile as the predecessor solves them (t_rw = the rectangle's width).  extra_outside: per
-    row, off-block entries the device rows carry beyond `m` (the dense-tail columns of U's
-    leading rows) -- counted into the outside sums' work, not into the structure."""
+    row, off-block entries the device rows carry beyond `m` -- counted into the outside sums'
+    work, not into the structure."""
     n = m.shape[0]
     rowptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
     cols = np.ascontiguousarray(m.indices, dtype=np.int32)
@@ -224,27 +224,152 @@ def plan_supernodal_blocks(m: sparse.csr_matrix, lower: bool, cap: int = 256, he
             "rects": int((rect_w > 0).sum())}
 
 
+def dense_group_runs(m: sparse.csr_matrix, lower_plan: dict, keep_levels: int, upper: sparse.csr_matrix | None = None,
+                     max_bytes: float = 3e9):
+    """Row runs at the top of the elimination tree: the rows of L's blocks at level >=
+    keep_levels (everything above them is then `keep_levels` cheap levels deep), closed under
+    both solves' dependencies (no other row of L reads a chosen row; a chosen row of U reads
+    only chosen rows), as maximal contiguous ranges.  keep_levels rises until the runs' inverse
+    triangles fit max_bytes.  Returns (starts, ends) or None."""
+    n = m.shape[0]
+    r0, w, lev = lower_plan["r0"], lower_plan["w"], lower_plan["levels"]
+    depth = int(lower_plan["depth"])
+    rows_l = np.repeat(np.arange(n), np.diff(m.indptr))
+    rows_u = np.repeat(np.arange(n), np.diff(upper.indptr)) if upper is not None else None
+    keep = int(keep_levels)
+    while keep < depth:
+        sel = lev >= keep
+        chosen = np.zeros(n, dtype=bool)
+        chosen[np.concatenate([np.arange(a, a + b) for a, b in zip(r0[sel], w[sel])])] = True
+        for _ in range(64):  # closure (a fixed point in one or two rounds: the set is the tree's top)
+            before = int(chosen.sum())
+            chosen[rows_l[chosen[m.indices]]] = True            # a row of L reading a chosen column
+            if upper is not None:
+                chosen[upper.indices[chosen[rows_u]]] = True    # a column a chosen row of U reads
+            if int(chosen.sum()) == before:
+                break
+        idx = np.nonzero(chosen)[0]
+        if len(idx) == 0:
+            return None
+        brk = np.nonzero(np.diff(idx) > 1)[0]
+        starts = np.concatenate([[idx[0]], idx[brk + 1]]).astype(np.int64)
+        ends = np.concatenate([idx[brk] + 1, [idx[-1] + 1]]).astype(np.int64)
+        if 4.0 * float(((ends - starts).astype(np.float64) ** 2).sum()) <= max_bytes and len(idx) <= n // 2:
+            return starts, ends
+        keep += max(1, (depth - keep) // 4)
+    return None
+
+
+def group_arrays(m: sparse.csr_matrix, g: dict, lower: bool) -> dict:
+    """Host arrays of the dense groups (pure numpy): the coupling CSR over the chosen rows in
+    (phase, row) order -- a row's entries outside its run are a prefix (L: columns < a) or a
+    suffix (U: columns >= b) of its sorted CSR row -- and, per row, where its slice of the
+    run's row-packed inverse triangle starts (g_off), how long it is (g_cnt) and which y entry
+    its first column multiplies (g_ystart)."""
+    rows, starts, ends, run_of = g["rows"], g["starts"], g["ends"], g["run_of"]
+    n = m.shape[0]
+    a_of, b_of = starts[run_of[rows]], ends[run_of[rows]]
+    indptr = np.asarray(m.indptr, dtype=np.int64)
+    cnt_out = np.zeros(len(rows), dtype=np.int64)
+    e0 = np.zeros(len(rows), dtype=np.int64)
+    for q, r in enumerate(rows):  # searchsorted in each chosen row (26 K rows at config 3)
+        c = m.indices[indptr[r]: indptr[r + 1]]
+        if lower:
+            k = int(np.searchsorted(c, a_of[q], side="left"))
+            cnt_out[q], e0[q] = k, indptr[r]
+        else:
+            k = int(np.searchsorted(c, b_of[q], side="left"))
+            cnt_out[q], e0[q] = len(c) - k, indptr[r] + k
+    cpl_ptr = np.concatenate([[0], np.cumsum(cnt_out)]).astype(np.int64)
+    take = np.repeat(e0 - cpl_ptr[:-1], cnt_out) + np.arange(cpl_ptr[-1], dtype=np.int64)
+    widths = (ends - starts)[g["order"]]
+    tri = widths * (widths + 1) // 2
+    run_off = np.zeros(len(starts), dtype=np.int64)
+    run_off[g["order"]] = np.concatenate([[0], np.cumsum(tri)[:-1]])
+    i = rows - a_of  # row inside its run
+    wv = b_of - a_of
+    if lower:
+        g_off = run_off[run_of[rows]] + i * (i + 1) // 2
+        g_cnt, g_ystart = i + 1, a_of
+    else:
+        g_off = run_off[run_of[rows]] + i * wv - i * (i - 1) // 2
+        g_cnt, g_ystart = wv - i, rows
+    return {"cpl_ptr": cpl_ptr, "cpl_cols": np.ascontiguousarray(m.indices[take], dtype=np.int32),
+            "cpl_vals": np.ascontiguousarray(m.data[take], dtype=np.float64), "run_off": run_off,
+            "inv_entries": int(tri.sum()), "g_off": g_off.astype(np.int64), "g_cnt": g_cnt.astype(np.int32),
+            "g_ystart": g_ystart.astype(np.int32)}
+
+
+def group_task_matrix(m: sparse.csr_matrix, chosen: np.ndarray) -> sparse.csr_matrix:
+    """The task kernel's matrix once the groups took their rows: the chosen rows are empty
+    (trivial tasks x = b / 1; for U the groups put their solution into b first, so the trivial
+    task reproduces it).  The other rows of U keep their group columns: x of the groups is
+    final before the tasks run.  (Moving those columns into a streaming product ahead of the
+    tasks -- 23 M entries, 87 us -- was built and measured: the task kernel did not get
+    shorter, U 0.837 -> 0.866 ms; dropped.)"""
+    n = m.shape[0]
+    ent_row = np.repeat(np.arange(n), np.diff(m.indptr))
+    ent = ~chosen[ent_row]
+    indptr = np.concatenate([[0], np.cumsum(np.bincount(ent_row[ent], minlength=n))]).astype(np.int64)
+    return sparse.csr_matrix((m.data[ent], m.indices[ent], indptr), shape=m.shape)
+
+
+def plan_groups(m: sparse.csr_matrix, groups, lower: bool, max_phases: int = 16):
+    """Phases of the runs for one factor: a run's phase = 1 + the highest phase among the runs
+    it reads (L: earlier rows, U: later rows); rows ordered by (phase, row)."""
+    starts, ends = (np.asarray(v, dtype=np.int64) for v in groups)
+    n, nr = m.shape[0], len(starts)
+    if nr == 0:
+        return None
+    run_of = np.full(n, -1, dtype=np.int64)
+    chosen = np.zeros(n, dtype=bool)
+    for k, (a, b) in enumerate(zip(starts, ends)):
+        run_of[a:b] = k
+        chosen[a:b] = True
+    phase = np.zeros(nr, dtype=np.int64)
+    for k in (range(nr) if lower else range(nr - 1, -1, -1)):
+        a, b = starts[k], ends[k]
+        cols = m.indices[m.indptr[a]: m.indptr[b]]
+        out = cols[cols < a] if lower else cols[cols >= b]
+        deps = np.unique(run_of[out])
+        deps = deps[deps >= 0]
+        if len(deps):
+            phase[k] = phase[deps].max() + 1
+    if int(phase.max()) + 1 > max_phases:
+        return None
+    order = np.lexsort((starts, phase))
+    rows = np.concatenate([np.arange(starts[k], ends[k]) for k in order])
+    counts = np.bincount(phase, weights=(ends - starts).astype(float), minlength=int(phase.max()) + 1)
+    return {"starts": starts, "ends": ends, "order": order, "phase": phase, "rows": rows, "chosen": chosen,
+            "run_of": run_of, "phase_ptr": np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)}
+
+
 class _SuperSchedule:
     """Device task list of one supernodal triangular solve: the planned tasks plus the packed
-    dense triangles of the block tasks (hn_host_pack_panels), and optionally the dense tail:
-    the factor's last `tail` rows leave the task list and are solved through the explicit
-    inverse of the trailing triangle (csrc/pressure.cu, 'dense tail')."""
+    dense triangles of the block tasks (hn_host_pack_panels), and optionally the dense groups:
+    row runs at the top of the elimination tree that leave the task list and are solved
+    through the explicit inverses of their triangles (csrc/pressure.cu, 'dense groups')."""
+
+    MAX_PHASES = 16
 
     def __init__(self, m: sparse.csr_matrix, lower: bool, diag: np.ndarray | None = None, inverse: int = 0,
-                 tail: int = 0, **plan_kw):
+                 groups=None, **plan_kw):
         n = m.shape[0]
-        tail = int(tail) if 0 < int(tail) < n else 0
-        k = n - tail
-        self.n, self.lower, self.tail = n, bool(lower), tail
-        lead_sq = m[:k, :k].tocsr() if tail else m
-        lead_sq.sort_indices()
-        # the rows the task kernel reads: the leading rows with every column (U rows keep their
-        # tail columns: they sort after the in-block and rectangle entries, so the planner's
-        # entry positions hold, and x of the tail is final before the tasks run)
-        lead = m[:k].tocsr() if tail else m
+        self.n, self.lower = n, bool(lower)
+        self.groups = None
+        g = self._plan_groups(m, groups) if groups is not None else None
+        dg = np.ascontiguousarray(diag if diag is not None else np.ones(1), dtype=np.float64)
+        if g is not None:
+            # the task kernel's matrix: the chosen rows are empty (trivial tasks x = b / 1; for U
+            # the groups put their solution into b first, so the trivial task reproduces it)
+            lead = group_task_matrix(m, g["chosen"])
+            if diag is not None:
+                dg = dg.copy()
+                dg[g["chosen"]] = 1.0
+        else:
+            lead = m
         lead.sort_indices()
-        extra = (np.diff(lead.indptr) - np.diff(lead_sq.indptr)) if tail and not lower else None
-        plan = plan_supernodal_blocks(lead_sq, lower, extra_outside=extra, **plan_kw)
+        plan = plan_supernodal_blocks(lead, lower, **plan_kw)
         self.csr = DeviceCSR(lead)
         self.inverse = int(inverse)  # 0 substitution, 1 diagonal-tile inverses, 2 whole-block inverses
         self.nblk, self.depth, self.ntasks = plan["nblk"], plan["depth"], plan["ntasks"]
@@ -254,7 +379,6 @@ class _SuperSchedule:
         cols = np.ascontiguousarray(lead.indices, dtype=np.int32)
         vals = np.ascontiguousarray(lead.data, dtype=np.float64)
         off = np.empty(len(kind), dtype=np.int64)
-        dg = np.ascontiguousarray(diag if diag is not None else np.ones(1), dtype=np.float64)
         args = (rowptr.ctypes.data_as(vp), cols.ctypes.data_as(vp), vals.ctypes.data_as(vp), dg.ctypes.data_as(vp),
                 1 if lower else 0, int(inverse), self.ntasks, kind.ctypes.data_as(vp), r0.ctypes.data_as(vp),
                 w.ctypes.data_as(vp), rw.ctypes.data_as(vp), off.ctypes.data_as(vp))
@@ -271,39 +395,55 @@ class _SuperSchedule:
         self.packed_bytes = 8 * total
         self.nnz = int(lead.nnz)
         self.d_diag = L.to_device(dg) if diag is not None else None
-        self.coupling = self.tail_inv = None
-        self.tail_bytes = 0
-        if tail:
-            self._build_tail(m, k, diag)
+        self.inv_entries = 0
+        self.n_phases, self.group_rows = 0, 0
+        phase_ptr = (C.c_int64 * 17)()
+        gp = [None] * 9
+        if g is not None:
+            gp = self._upload_groups(m, g, diag) + [L.empty(n, L.torch().float64)]  # + the y scratch
+            for k, v in enumerate(g["phase_ptr"]):
+                phase_ptr[k] = int(v)
         self._plan = L.TriPlan(
             1 if lower else 0, self.inverse, self.ntasks, self.kind.data_ptr(), self.r0.data_ptr(),
             self.w.data_ptr(), self.rb.data_ptr(), self.rc.data_ptr(), self.off.data_ptr(), self.rw.data_ptr(),
             self.csr.rowptr.data_ptr(), self.csr.cols.data_ptr(), self.csr.vals.data_ptr(),
-            self.d_diag.data_ptr() if self.d_diag is not None else None, self.packed.data_ptr(), tail,
-            self.coupling.rowptr.data_ptr() if self.coupling is not None else None,
-            self.coupling.cols.data_ptr() if self.coupling is not None else None,
-            self.coupling.vals.data_ptr() if self.coupling is not None else None,
-            self.tail_inv.data_ptr() if self.tail_inv is not None else None)
+            self.d_diag.data_ptr() if self.d_diag is not None else None, self.packed.data_ptr(),
+            self.n_phases, phase_ptr, *[t.data_ptr() if t is not None else None for t in gp])
+        self._group_tensors = gp
 
-    def _build_tail(self, m, k: int, diag):
-        """The trailing triangle's inverse (row-major, one-time: a dense triangular solve
-        against the identity on the device) and, for L, the tail rows' coupling to the
-        leading columns."""
+    # ---- dense groups ----
+    def _plan_groups(self, m, groups):
+        return plan_groups(m, groups, self.lower, self.MAX_PHASES)
+
+    def _upload_groups(self, m, g, diag):
+        """Coupling CSR (the chosen rows' entries outside their run), the runs' inverse
+        triangles (row-packed; one dense triangular solve per run on the device, setup only) and
+        the per-row descriptors."""
         t = L.torch()
-        T = self.tail
-        tri = np.asarray(m[k:, k:].todense(), dtype=np.float64)
-        tri[np.diag_indices(T)] = 1.0 if self.lower else np.asarray(diag, dtype=np.float64)[k:]
-        d_tri = L.to_device(tri)
-        eye = t.eye(T, dtype=t.float64, device=d_tri.device)
-        self.tail_inv = t.linalg.solve_triangular(d_tri, eye, upper=not self.lower).contiguous()
-        del d_tri, eye
-        self.tail_bytes = 8 * T * (T + 1) // 2
-        if self.lower:
-            cpl = m[k:, :k].tocsr()
-            cpl.sort_indices()
-            self.coupling = DeviceCSR(cpl)
-            self.nnz += int(cpl.nnz)
-            self.tail_bytes += 12 * int(cpl.nnz)
+        lower = self.lower
+        arr = group_arrays(m, g, lower)
+        starts, ends = g["starts"], g["ends"]
+        inv = L.empty(int(arr["inv_entries"]), t.float64)
+        for k in g["order"]:
+            a, b = int(starts[k]), int(ends[k])
+            wk = b - a
+            blk = np.asarray(m[a:b, a:b].todense(), dtype=np.float64)
+            blk[np.diag_indices(wk)] = 1.0 if lower else np.asarray(diag, dtype=np.float64)[a:b]
+            d_blk = L.to_device(blk)
+            x = t.linalg.solve_triangular(d_blk, t.eye(wk, dtype=t.float64, device=d_blk.device), upper=not lower)
+            mask = t.ones((wk, wk), dtype=t.bool, device=d_blk.device)
+            mask = t.tril(mask) if lower else t.triu(mask)
+            o = int(arr["run_off"][k])
+            inv[o: o + wk * (wk + 1) // 2].copy_(x[mask])
+            del d_blk, x, mask
+        self.n_phases = len(g["phase_ptr"]) - 1
+        self.group_rows = len(g["rows"])
+        self.nnz += int(arr["cpl_ptr"][-1])
+        self.inv_entries = int(arr["inv_entries"])
+        self.groups = g
+        return [L.to_device(g["rows"].astype(np.int32)), L.to_device(arr["cpl_ptr"]), L.to_device(arr["cpl_cols"]),
+                L.to_device(arr["cpl_vals"]), L.to_device(arr["g_off"]), L.to_device(arr["g_cnt"]),
+                L.to_device(arr["g_ystart"]), inv]
 
     def plan_struct(self):
         return self._plan
@@ -320,23 +460,23 @@ class _DeviceLU:
     # norm, random rhs) and the fields after 50 full steps by <= 1.1e-12 (relative).
     # (2 = whole-block inverses -- the packed panels hold the inverse of a block's entire dense
     # triangle, x = B^-1 y panel by panel with no tile-to-tile chain -- measured slower: L 0.726
-    # -> 0.777 ms with the dense tail, 5e-10 from SuperLU: a block's x is then published only
+    # -> 0.777 ms with a 4096-row dense tail, 5e-10 from SuperLU: a block's x is then published only
     # at its end, while the tile scheme feeds the next piece of a supernode tile by tile.)
     TILE_INVERSE_L = 1
     TILE_INVERSE_U = 1
-    # dense tail: the factors' last TAIL rows (at most a quarter of the matrix) are solved through
-    # the explicit inverse of the trailing triangle instead of the block chain -- at config 3
-    # the last 8192 rows hold 54 of L's 96 and 49 of U's 77 block levels, the last 4096 rows 23
-    # and 22.  Measured (tools/time_trisolve.py, L + U): no tail 1.944 ms, 1694 (the fully dense
-    # triangle) 1.839, 4096 1.556, 8192 1.564, 12288 1.673 -- beyond ~4096 rows the remaining
-    # depth sits in other branches of the elimination tree and the inverse only adds bytes.  0 = off.
-    TAIL = 4096
+    # dense groups: the rows of L's block levels >= KEEP_LEVELS (the top of the elimination tree:
+    # separators, nearly dense supernodes that can only be solved one 256-wide piece after the
+    # other) leave the task chain and are solved through explicit inverses, phase by phase
+    # (csrc/pressure.cu).  Config 3 at 50: 12.4 K rows in 8 runs, 4 phases, L's 96 and U's 77 block
+    # levels -> 50 and 44.  Measured L + U (tools/time_trisolve.py): none 1.913 ms, keep 60 1.509, 50
+    # 1.469, 40 1.536, 30 1.573 (more rows = more inverse bytes and phases).  0 = off.
+    KEEP_LEVELS = 50
     # max-norm relative distance to SuperLU's solve on a random rhs (tests): U is ill-conditioned
     # (block kappa up to 7e7), two exact substitution orders differ by ~6e-11; the diagonal-tile
     # inverses move it to ~1.1e-10 (fields: <= 1.1e-12 after 50 steps, see above)
     PARITY_TOL = {False: 1e-10, True: 1e-9}
 
-    def __init__(self, lu, inverse: int | None = None, tail: int | None = None, **plan_kw):
+    def __init__(self, lu, inverse: int | None = None, keep_levels: int | None = None, **plan_kw):
         Lm = sparse.csr_matrix(lu.L)
         Um = sparse.csr_matrix(lu.U)
         self.n = Lm.shape[0]
@@ -345,14 +485,18 @@ class _DeviceLU:
         Ls.sort_indices()
         Us.sort_indices()
         udiag = np.asarray(Um.diagonal(), dtype=np.float64)
-        tail = self.TAIL if tail is None else int(tail)
-        tail = min(tail, self.n // 4)
-        self.tail = tail if tail >= 64 else 0
+        keep = self.KEEP_LEVELS if keep_levels is None else int(keep_levels)
+        groups = None
+        if keep > 0:
+            full = plan_supernodal_blocks(Ls, True, **plan_kw)
+            if full["depth"] > keep + 4:
+                groups = dense_group_runs(Ls, full, keep, upper=Us)
         self.sL = _SuperSchedule(Ls, lower=True, inverse=self.TILE_INVERSE_L if inverse is None else inverse,
-                                 tail=self.tail, **plan_kw)
+                                 groups=groups, **plan_kw)
         self.sU = _SuperSchedule(Us, lower=False, diag=udiag, inverse=self.TILE_INVERSE_U if inverse is None else inverse,
-                                 tail=self.tail, **plan_kw)
-        self.L, self.U = self.sL.csr, self.sU.csr  # the rows the task kernels read (leading rows)
+                                 groups=groups, **plan_kw)
+        self.group_rows = self.sL.group_rows
+        self.L, self.U = self.sL.csr, self.sU.csr  # the rows the task kernels read
         self.diag = self.sU.d_diag
         self.perm_r = L.to_device(np.asarray(lu.perm_r, dtype=np.int32))
         self.perm_c = L.to_device(np.asarray(lu.perm_c, dtype=np.int32))
@@ -363,11 +507,11 @@ class _DeviceLU:
         self.ticket = L.zeros(1, t.int64)
         self.ysum = L.empty(self.n, t.float64)
         self.nnz = int(Ls.nnz + Us.nnz + self.n)  # the factors as SuperLU holds them
-        # bytes one application reads: 12 B per sparse entry the kernels touch + 8 B per entry of
-        # the tail inverses' triangles (what replaced the tail's own 12 B entries)
-        self.solve_bytes = 12 * (self.sL.nnz + self.sU.nnz) + self.sL.tail_bytes - (
-            12 * int(self.sL.coupling.nnz) if self.sL.coupling is not None else 0) + self.sU.tail_bytes + 8 * self.n
-        self.parity_tol = self.PARITY_TOL[bool(self.sL.inverse or self.sU.inverse or self.tail)]
+        # bytes one application reads: 12 B per sparse entry the kernels touch (task rows and the
+        # groups' coupling) + 8 B per entry of the groups' inverse triangles + the U diagonal
+        self.solve_bytes = 12 * (self.sL.nnz + self.sU.nnz) + 8 * (self.sL.inv_entries + self.sU.inv_entries) \
+            + 8 * self.n
+        self.parity_tol = self.PARITY_TOL[bool(self.sL.inverse or self.sU.inverse or self.group_rows)]
 
     def plans(self):
         """(L, U) as hn_tri_plan structs for hn_pressure_setup (the arrays stay owned here)."""
@@ -384,7 +528,8 @@ class _DeviceLU:
 
     def _tri(self, sch, m, diag, b, x, s):
         """One triangular solve (m and diag are the schedule's own arrays; kept in the signature
-        for the dev tools)."""
+        for the dev tools).  The upper solve with dense groups overwrites the groups' entries of
+        b with their solution (solve() passes its own scratch)."""
         L.call("hn_sptrsv_plan", C.byref(sch.plan_struct()), L.ptr(b), L.ptr(x), L.ptr(self.ysum), self.n,
                L.ptr(self.ticket), self.CTAS_PER_SM, s)
 

@@ -359,21 +359,25 @@ class TestRun:
         npt.assert_array_equal(a.state.temperature[mask], ns.bc_value[mask])
 
 
-@pytest.mark.parametrize("inverse,tail,tol", [(False, 0, 1e-12), (True, 0, 1e-9), (2, 0, 1e-9), (False, 900, 1e-10),
-                                              (True, None, 1e-9), (None, None, 1e-9)])
-def test_device_lu_solve_matches_superlu(inverse, tail, tol):
+@pytest.mark.parametrize("inverse,keep,tol", [(False, 0, 1e-12), (True, 0, 1e-9), (2, 0, 1e-9), (False, 12, 1e-10),
+                                              (True, 6, 1e-9), (None, None, 1e-9)])
+def test_device_lu_solve_matches_superlu(inverse, keep, tol):
     """The GPU preconditioner (SuperLU factors, supernodal sync-free solves over packed dense
     panels) against SuperLU's own solve: substitution to rounding, diagonal-tile inverses and
-    the dense-tail inverse (the defaults; tail=None) to the drift DESIGN.md states; twice in a
-    row: bitwise reproducible."""
+    the dense groups (explicit inverses of the top-of-tree row runs; keep = the block levels
+    left to the task chain) to the drift DESIGN.md states; twice in a row: bitwise reproducible."""
     from paper_2303_01760_b200 import _lib as L
     from paper_2303_01760_b200.solver import _DeviceLU
     from scipy.sparse import linalg as spla
     ns = nodesets.hybrid_hole_2d(60, seed=2)
     ops = hn.build_operators(ns, {"wall:x-"}, PoissonSolveSettings())
     lu = spla.splu(ops.poisson_matrix.tocsc())  # the factorisation build_operators makes
-    dlu = _DeviceLU(lu, inverse=inverse, tail=tail)
-    assert dlu.tail == (0 if tail == 0 else (900 if tail else dlu.n // 4))
+    dlu = _DeviceLU(lu, inverse=inverse, keep_levels=keep)
+    if keep:
+        assert dlu.group_rows > 0 and dlu.sL.n_phases >= 1
+        assert dlu.sU.group_rows == dlu.sL.group_rows
+    elif keep == 0:
+        assert dlu.group_rows == 0
     assert int((dlu.sL.w.cpu().numpy() > 32).sum()) > 0  # multi-tile blocks exercised
     b = np.random.default_rng(3).normal(size=dlu.n)
     ref = lu.solve(b)
@@ -387,10 +391,11 @@ def test_device_lu_solve_matches_superlu(inverse, tail, tol):
 
 
 @pytest.mark.parametrize("cap,helper", [(32, 64), (96, 512), (256, 4096)])
-@pytest.mark.parametrize("inverse,tail", [(False, 0), (True, 0), (2, 0), (False, 333), (True, 750), (2, 750)])
-def test_device_lu_random_fill_all_block_shapes(cap, helper, inverse, tail):
+@pytest.mark.parametrize("inverse,keep", [(False, 0), (True, 0), (2, 0), (False, 5), (True, 20), (2, 60)])
+def test_device_lu_random_fill_all_block_shapes(cap, helper, inverse, keep):
     """Random sparse matrix with heavy fill: blocks of every width up to the cap (partial last
-    panels, upper and lower), helper-fed blocks and batched small blocks, vs SuperLU."""
+    panels, upper and lower), helper-fed blocks and batched small blocks, dense groups cut at
+    several depths (many runs and phases), vs SuperLU."""
     from paper_2303_01760_b200 import _lib as L
     from paper_2303_01760_b200.solver import _DeviceLU
     from scipy import sparse
@@ -398,13 +403,14 @@ def test_device_lu_random_fill_all_block_shapes(cap, helper, inverse, tail):
     n = 3000
     a = sparse.random(n, n, density=0.004, random_state=7, format="csc") + sparse.eye(n) * 2.0
     lu = spla.splu(a.tocsc())
-    dlu = _DeviceLU(lu, inverse=inverse, tail=tail, cap=cap, helper_nnz=helper)  # tails cut supernodes anywhere
+    dlu = _DeviceLU(lu, inverse=inverse, keep_levels=keep, cap=cap, helper_nnz=helper)
+    assert dlu.group_rows == 0 if keep == 0 else (dlu.group_rows > 0 or keep > 20)
     b = np.random.default_rng(5).normal(size=n)
     t = L.torch()
     xd = L.empty(n, t.float64)
     dlu.solve(L.to_device(b), xd)
     ref = lu.solve(b)
-    assert np.abs(xd.cpu().numpy() - ref).max() / np.abs(ref).max() <= (1e-9 if inverse or tail else 1e-11)
+    assert np.abs(xd.cpu().numpy() - ref).max() / np.abs(ref).max() <= (1e-9 if inverse or keep else 1e-11)
 
 
 # ---------------------------------------------------------------- run(): reference loop semantics

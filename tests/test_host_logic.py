@@ -247,3 +247,86 @@ def test_write_outputs_matches_reference_artifacts(tmp_path):
     rows = list(csv.reader(open(tmp_path / "out" / "fields_0p25.csv")))
     assert rows[0] == ["x", "y", "u", "v", "p", "T", "h"] and len(rows) == n + 1
     np.testing.assert_allclose(np.array(rows[1:], dtype=float)[:, :2], ns.positions)
+
+
+@pytest.mark.parametrize("keep", [3, 8, 20])
+def test_dense_groups_host_arrays_solve_both_factors(keep):
+    """The dense-group setup (solver.dense_group_runs / plan_groups / group_arrays, pure numpy)
+    emulated in numpy exactly as csrc/pressure.cu executes it: the task rows by substitution
+    (chosen rows empty), then per phase the coupling product and the row-packed inverse
+    triangles -- against scipy's triangular solves, for L (groups last) and U (groups first)."""
+    from scipy.sparse import linalg as spla
+
+    from paper_2303_01760_b200.solver import (dense_group_runs, group_arrays, group_task_matrix, plan_groups,
+                                              plan_supernodal_blocks)
+    n = 700
+    a = sp.random(n, n, density=0.012, random_state=3, format="csc") + sp.eye(n) * 3
+    lu = spla.splu(a.tocsc())
+    Ls = sp.tril(sp.csr_matrix(lu.L), k=-1, format="csr")
+    Us = sp.triu(sp.csr_matrix(lu.U), k=1, format="csr")
+    Ls.sort_indices()
+    Us.sort_indices()
+    udiag = sp.csr_matrix(lu.U).diagonal()
+    full = plan_supernodal_blocks(Ls, True)
+    assert full["depth"] > keep + 4
+    groups = dense_group_runs(Ls, full, keep, upper=Us)
+    assert groups is not None
+    rng = np.random.default_rng(0)
+    for m, lower in ((Ls, True), (Us, False)):
+        g = plan_groups(m, groups, lower)
+        arr = group_arrays(m, g, lower)
+        chosen = g["chosen"]
+        # closure: no other row of L reads a chosen row; a chosen row of U reads only chosen rows
+        rows_of = np.repeat(np.arange(n), np.diff(m.indptr))
+        if lower:
+            assert not chosen[m.indices[~chosen[rows_of]]].any()
+        else:
+            assert chosen[m.indices[chosen[rows_of]]].all()
+        full_tri = (m + sp.eye(n)) if lower else (m + sp.diags(udiag))
+        b = rng.normal(size=n)
+        want = spsolve_triangular(full_tri.tocsr(), b, lower=lower)
+        # inverse triangles, row-packed in execution order
+        inv = np.zeros(arr["inv_entries"])
+        for k in g["order"]:
+            s0, s1 = int(g["starts"][k]), int(g["ends"][k])
+            blk = full_tri.tocsr()[s0:s1, s0:s1].toarray()
+            x = np.linalg.inv(blk)
+            mask = np.tril(np.ones_like(x, dtype=bool)) if lower else np.triu(np.ones_like(x, dtype=bool))
+            o = int(arr["run_off"][k])
+            inv[o: o + mask.sum()] = x[mask]
+        x = np.full(n, np.nan)
+        rhs = b.copy()
+
+        def phases():
+            y = np.full(n, np.nan)
+            for ph in range(len(g["phase_ptr"]) - 1):
+                q0, q1 = int(g["phase_ptr"][ph]), int(g["phase_ptr"][ph + 1])
+                for q in range(q0, q1):  # group_coupling_kernel
+                    e0, e1 = arr["cpl_ptr"][q], arr["cpl_ptr"][q + 1]
+                    xv = x[arr["cpl_cols"][e0:e1]]
+                    assert not np.isnan(xv).any(), "coupling read an unsolved row"
+                    y[g["rows"][q]] = rhs[g["rows"][q]] - np.dot(arr["cpl_vals"][e0:e1], xv)
+                for q in range(q0, q1):  # group_gemv_kernel
+                    o, c, ys = int(arr["g_off"][q]), int(arr["g_cnt"][q]), int(arr["g_ystart"][q])
+                    x[g["rows"][q]] = np.dot(inv[o: o + c], y[ys: ys + c])
+                    if not lower:
+                        rhs[g["rows"][q]] = x[g["rows"][q]]  # echo
+
+        lead = group_task_matrix(m, chosen)
+        assert not np.diff(lead.indptr)[chosen].any()            # chosen rows are empty
+
+        def tasks():  # the task kernel's rows (x = rhs / 1 on the empty chosen rows)
+            order = range(n) if lower else range(n - 1, -1, -1)
+            for i in order:
+                c = lead.indices[lead.indptr[i]: lead.indptr[i + 1]]
+                v = lead.data[lead.indptr[i]: lead.indptr[i + 1]]
+                assert not np.isnan(x[c]).any()
+                x[i] = (rhs[i] - np.dot(v, x[c])) / (1.0 if lower or chosen[i] else udiag[i])
+
+        if lower:
+            tasks()
+            phases()
+        else:
+            phases()
+            tasks()
+        np.testing.assert_allclose(x, want, rtol=1e-8, atol=1e-10)

@@ -1,7 +1,7 @@
 """Time the L and U supernodal solves and one full preconditioner application on config 3 for a
-list of dense-tail widths, with the distance to SuperLU's own solve (dev tool; CUDA events,
+list of dense-group depths (block levels left to the task chain; 0 = no groups), with the distance to SuperLU's own solve (dev tool; CUDA events,
 median of 20).
-  python tools/time_trisolve.py [M=500] [tails, e.g. 0,1694,4096,8192] [inverse modes, e.g. 0,1,2]"""
+  python tools/time_trisolve.py [M=500] [keep_levels, e.g. 0,60,40,30] [inverse modes, e.g. 0,1,2] [helper_nnz, e.g. 4096,16384]"""
 import sys
 import time
 from pathlib import Path
@@ -32,26 +32,28 @@ def timeit(fn, reps=20):
 def main():
     t = L.torch()
     M = int(sys.argv[1]) if len(sys.argv) > 1 else 500
-    tails = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 2048, 4096, 8192, 12288]
+    tails = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 60, 50, 40, 30]
     modes = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else [None]
+    helpers = [int(v) for v in sys.argv[4].split(",")] if len(sys.argv) > 4 else [4096]
     ns = nodesets.hybrid_hole_2d(M, seed=2)
     ops = hn.build_operators(ns, {"wall:x-"}, hn.PoissonSolveSettings(), factorize=True)
     host_lu = spla.splu(ops.poisson_matrix.tocsc())
     rhs = np.random.default_rng(0).normal(size=host_lu.shape[0])
     ref = host_lu.solve(rhs)
     b = L.to_device(rhs)
-    for tail, mode in [(a, b) for a in tails for b in modes]:
+    for tail, mode, hz in [(a, b, c) for a in tails for b in modes for c in helpers]:
         t0 = time.perf_counter()
-        lu = _DeviceLU(host_lu, tail=tail, inverse=mode)
+        lu = _DeviceLU(host_lu, keep_levels=tail, inverse=mode, helper_nnz=hz)
         t.cuda.synchronize()
         setup = time.perf_counter() - t0
         x = L.empty(lu.n, t.float64)
         s = L.stream_handle()
         tl = timeit(lambda: lu._tri(lu.sL, lu.L, None, b, lu.z, s))
-        tu = timeit(lambda: lu._tri(lu.sU, lu.U, lu.diag, b, lu.w, s))
+        bu = b.clone()  # an upper plan with dense groups overwrites the groups' rhs entries
+        tu = timeit(lambda: lu._tri(lu.sU, lu.U, lu.diag, bu, lu.w, s))
         tp = timeit(lambda: lu.solve(b, x))
         err = np.abs(x.cpu().numpy() - ref).max() / np.abs(ref).max()
-        print(f"tail {lu.tail:6d} inverse {lu.sL.inverse}: L {tl:.3f} ms  U {tu:.3f} ms  precond {tp:.3f} ms  vs SuperLU {err:.2e}  "
+        print(f"keep {tail:3d} rows {lu.group_rows:6d} phases {lu.sL.n_phases}/{lu.sU.n_phases} inverse {lu.sL.inverse} helper {hz} tasks {lu.sL.ntasks}/{lu.sU.ntasks}: L {tl:.3f} ms  U {tu:.3f} ms  precond {tp:.3f} ms  vs SuperLU {err:.2e}  "
               f"depth L {lu.sL.depth} U {lu.sU.depth}  bytes {lu.solve_bytes / 1e6:.0f} MB  setup {setup:.1f} s",
               flush=True)
         del lu, x
