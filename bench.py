@@ -196,8 +196,11 @@ def measure_dfma_peak(L):
 
 class LaunchCounter:
     """Kernels each libhn entry point launches (fixed per call; see csrc/*.cu)."""
-    # hn_pressure_solve: 6 set-up kernels + one WHILE-body pass (24 kernels; the complete-LU
-    # preconditioner converges at its first half-step check) + 1 finish kernel
+    # hn_pressure_solve: 6 set-up kernels + one WHILE-body pass (12 Krylov kernels + 2
+    # preconditioner applications; the complete-LU preconditioner converges at its first
+    # half-step check, the second application's kernels launch and return) + 1 finish kernel.
+    # One application = 2 permutes + per factor (reset + task kernel + 2 kernels per dense-group
+    # phase): 31 without groups; steps_measure sets the entry from the factors' phase counts.
     KERNELS = {"hn_celllist_build": 5, "hn_partition_methods": 6, "hn_sptrsv_super": 2,
                "hn_knn": 1, "hn_knn_spacing": 1, "hn_classify": 1, "hn_mon_stencils": 1, "hn_weights_mon": 2,
                "hn_weights_rbf": 1, "hn_apply_ell": 1, "hn_momentum": 1, "hn_div_rhs": 1,
@@ -550,6 +553,9 @@ def steps_measure(args, rank, world, cfg=3, flush=None, with_cpu=True):
     t_setup = time.perf_counter()
     stepper, ops, dt = _stepper(hn, ns, True, Ra, rbf_n=30 if cfg == 4 else None)
     t_setup = time.perf_counter() - t_setup
+    lu_dev = ops._d_lu
+    counter.KERNELS = dict(counter.KERNELS, hn_pressure_solve=19 + 2 * (6 + 2 * (lu_dev.sL.n_phases + lu_dev.sU.n_phases)),
+                           hn_sptrsv_plan=2 + 2 * max(lu_dev.sL.n_phases, lu_dev.sU.n_phases))
     steps = args.steps_steps
     # a step is one CUDA-graph replay (no libhn call from the host), so the kernels of a step
     # are counted where they are enqueued: the warm-up steps (eager first step, then the

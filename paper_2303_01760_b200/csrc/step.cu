@@ -382,8 +382,14 @@ __device__ __forceinline__ double csr_row_seq32_neu(const int* __restrict__ cols
     c[k] = k < len ? __ldg(cols + e + k) : -1;
     v[k] = k < len ? __ldg(vals + e + k) : 0.0;
   }
+  // the gather and the mask byte are requested together (one round trip, not two); a masked
+  // entry's value is read and dropped (it may be another row's Neumann node, written meanwhile)
 #pragma unroll
-  for (int k = 0; k < 32; ++k) xv[k] = (c[k] >= 0 && !__ldg(is_neu + c[k])) ? x[c[k]] : 0.0;
+  for (int k = 0; k < 32; ++k) {
+    const double xr = c[k] >= 0 ? x[c[k]] : 0.0;
+    const bool masked = c[k] >= 0 && __ldg(is_neu + c[k]);
+    xv[k] = masked ? 0.0 : xr;
+  }
   double acc = 0.0;
 #pragma unroll
   for (int k = 0; k < 32; ++k)

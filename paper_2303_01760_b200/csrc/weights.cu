@@ -1463,12 +1463,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
           if (jj + 1 < NQ) st_pred2(isp[r], pbase + 8u * jj, pp[r][jj], pp[r][jj + 1]);
           else st_pred1(isp[r], pbase + 8u * jj, pp[r][jj]);
         }
-        if (isp[r]) {
-#pragma unroll
-          for (int a = 0; a < D; ++a) sm.yp[m][a] = yo[r][a];
-          sm.sidp[m] = sido[r];
-          step_of[r] = m;
-        }
+        if (isp[r]) step_of[r] = m;  // its coordinates and id go to slot m after the loop
       }
       __syncwarp();
       const double* prow = su + m * NQP;
@@ -1478,12 +1473,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
       st_pred1(lane_live && s == 0, hist + 8u * m, inv);
 #pragma unroll
       for (int r = 0; r < PA; ++r) {
-        const double l = (vm[r] == 0u) ? 0.0 : pp[r][m] * inv;  // rows still unpivoted
-        if (vm[r] != 0u && !isp[r]) lm[r][m] = l;
-        const double le = isp[r] ? 0.0 : l;
+        // no masks: a row pivoted at step i only keeps its multipliers m < i (L_I is unit lower),
+        // and its pp entries are never read again (vm = 0 keeps it out of every later search),
+        // so eliminating it like any other row is harmless and saves the selects
+        const double l = pp[r][m] * inv;
+        lm[r][m] = l;
         vm[r] = isp[r] ? 0u : vm[r];
 #pragma unroll
-        for (int cc = m + 1; cc < NQ; ++cc) pp[r][cc] = fma(-le, prow[cc], pp[r][cc]);
+        for (int cc = m + 1; cc < NQ; ++cc) pp[r][cc] = fma(-l, prow[cc], pp[r][cc]);
       }
       chosen |= 1u << (63u - ptag);
     });
@@ -1501,6 +1498,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_ns_kernel(
         for (int m = 0; m < NQ; ++m) slj[jr * NQ + m] = lm[r][m];
       } else {
         const int i = step_of[r];
+#pragma unroll
+        for (int a = 0; a < D; ++a) sm.yp[i][a] = yo[r][a];
+        sm.sidp[i] = sido[r];
 #pragma unroll
         for (int m = 0; m < NQ; ++m) sli[i * NQP + m] = m < i ? lm[r][m] : (m == i ? 1.0 : 0.0);
       }
