@@ -475,7 +475,7 @@ __device__ unsigned long long g_knn_fb_stats[4];  // dev builds: [fallbacks, > c
 #endif
 
 template <int D>
-__global__ void __launch_bounds__(kWarpKnnWarps * 32) knn_warp_kernel(
+__global__ void __launch_bounds__(kWarpKnnWarps * 32, 8) knn_warp_kernel(
     Grid g, const double* __restrict__ pos, const int* __restrict__ cell_start, const int* __restrict__ cell_items,
     const double* __restrict__ cell_pos, const int* __restrict__ queries, int64_t nq, int n,
     const uint8_t* __restrict__ exclude, double r0, const double* __restrict__ qh, double rscale,
