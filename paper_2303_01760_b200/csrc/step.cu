@@ -293,22 +293,29 @@ constexpr int64_t kFuseRows = 600000;
   else if (WB > 0 && w == WB) ROWFN<D, (WB > 0 ? WB : WA)>(b, bin, k, __VA_ARGS__); \
   else ROWFN<D, 0>(b, bin, k, __VA_ARGS__);
 
+// launch bounds: the 2D stencils (W <= 12) run best at 6 / 8 CTAs per SM (80 / 64 registers, no
+// spills): config-3 explicit part 43.0 -> 39.0 us (59 % of HBM); 8 / 10 CTAs: 41.0 us; the 3D
+// widths keep 3 / 4 (W = 20, 30 gathers per row need the registers: 4 / 6 CTAs measured 78.5 -> 76.6 %
+// of HBM on the config-4 explicit part)
+template <int WA, int WB>
+constexpr bool kNarrowBins = (WA > WB ? WA : WB) <= 12;
+
 template <int D, int WA, int WB>
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(128, (kNarrowBins<WA, WB> ? 6 : 3))
 momentum_fused_kernel(StepBins b, const double* __restrict__ v, const double* __restrict__ T, int64_t N,
                       MomentumCoef c, double* __restrict__ vstar) {
   HN_FUSED_BODY(momentum_row, v, T, N, c, vstar)
 }
 
 template <int D, int WA, int WB>
-__global__ void __launch_bounds__(128, 4)
+__global__ void __launch_bounds__(128, (kNarrowBins<WA, WB> ? 8 : 4))
 div_rhs_fused_kernel(StepBins b, const double* __restrict__ vs, int64_t N, double dt, double* __restrict__ rhs) {
   if (blockIdx.x == 0 && threadIdx.x == 0) rhs[N] = 0.0;  // bordered gauge equation
   HN_FUSED_BODY(div_row, vs, N, 0.0, dt, rhs)
 }
 
 template <int D, int WA, int WB>
-__global__ void __launch_bounds__(128, 4)
+__global__ void __launch_bounds__(128, (kNarrowBins<WA, WB> ? 8 : 4))
 correct_temp_fused_kernel(StepBins b, const double* __restrict__ vs, const double* __restrict__ p,
                           const double* __restrict__ T, int64_t N, double dt, double* __restrict__ vout,
                           double* __restrict__ Tout, int* __restrict__ flags, HyperT hy) {
