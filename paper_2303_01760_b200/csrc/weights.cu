@@ -966,16 +966,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
       for (int m = 0; m < NQ; ++m) pp[r][m] = mono_val<D>(m, yo[r]);
       vm[r] = (lane_live && j < NST) ? (0x7fffffc0u | static_cast<unsigned>(63 - j)) : 0u;
     }
+    int step_of[PA];  // step that chose the slot's node (its I index)
+#pragma unroll
+    for (int r = 0; r < PA; ++r) step_of[r] = 0;
     // column 0 (monomial 1) is all ones: partial pivoting takes the first node, the centre,
     // whose monomial row is [1, 0, ..] (y = 0 exactly), so step 0 eliminates nothing
     unsigned chosen = 1u;
     vm[0] = s == 0 ? 0u : vm[0];
-    if (lane_live && s == 0) {
-#pragma unroll
-      for (int a = 0; a < D; ++a) sm.yp[0][a] = yo[0][a];
-      sm.sidp[0] = sido[0];
-      sm.inv_hist[0] = 1.0;
-    }
+    if (lane_live && s == 0) sm.inv_hist[0] = 1.0;
     static_for<NQ - 1>([&](auto mc) {
       constexpr int m = decltype(mc)::value + 1;
       unsigned key = 0;
@@ -996,11 +994,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
           if (jj + 1 < NQ) st_pred2(isp[r], pbase + 8u * jj, pp[r][jj], pp[r][jj + 1]);
           else st_pred1(isp[r], pbase + 8u * jj, pp[r][jj]);
         }
-        if (isp[r]) {
-#pragma unroll
-          for (int a = 0; a < D; ++a) sm.yp[m][a] = yo[r][a];
-          sm.sidp[m] = sido[r];
-        }
+        if (isp[r]) step_of[r] = m;  // its coordinates and id go to slot m after the loop
       }
       __syncwarp();
       const double* prow = sm.prow[m & 1];
@@ -1010,19 +1004,20 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rbf_static_kernel(
       st_pred1(lane_live && s == 0, hist + 8u * m, inv);
 #pragma unroll
       for (int r = 0; r < PA; ++r) {
-        const double l = isp[r] ? 0.0 : pp[r][m] * inv;
+        // no mask on the pivot row: it eliminates itself to zero and is never read again
+        const double l = pp[r][m] * inv;
         vm[r] = isp[r] ? 0u : vm[r];
 #pragma unroll
         for (int cc = m + 1; cc < NQ; ++cc) pp[r][cc] = fma(-l, prow[cc], pp[r][cc]);
       }
       chosen |= 1u << (63u - ptag);
     });
-    // J: the unchosen nodes in stencil order
+    // renumbering: I = the chosen nodes by step, J = the others in stencil order
 #pragma unroll
     for (int r = 0; r < PA; ++r) {
       const int j = s + r * LPS;
-      if (lane_live && j < NST && !((chosen >> j) & 1u)) {
-        const int ni = NQ + __popc(~chosen & ((1u << j) - 1u));
+      if (lane_live && j < NST) {
+        const int ni = ((chosen >> j) & 1u) ? step_of[r] : NQ + __popc(~chosen & ((1u << j) - 1u));
 #pragma unroll
         for (int a = 0; a < D; ++a) sm.yp[ni][a] = yo[r][a];
         sm.sidp[ni] = sido[r];
