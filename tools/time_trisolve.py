@@ -35,15 +35,17 @@ def main():
     tails = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 60, 50, 40, 30]
     modes = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else [None]
     helpers = [int(v) for v in sys.argv[4].split(",")] if len(sys.argv) > 4 else [4096]
+    extra = [dict(kv.split("=") for kv in a.split(";")) for a in sys.argv[5:]] or [{}]  # plan kwargs, e.g. cap=128;batch=4
+    extra = [{k: int(v) for k, v in e.items()} for e in extra]
     ns = nodesets.hybrid_hole_2d(M, seed=2)
     ops = hn.build_operators(ns, {"wall:x-"}, hn.PoissonSolveSettings(), factorize=True)
     host_lu = spla.splu(ops.poisson_matrix.tocsc())
     rhs = np.random.default_rng(0).normal(size=host_lu.shape[0])
     ref = host_lu.solve(rhs)
     b = L.to_device(rhs)
-    for tail, mode, hz in [(a, b, c) for a in tails for b in modes for c in helpers]:
+    for tail, mode, hz, kw in [(a, b, c, e) for a in tails for b in modes for c in helpers for e in extra]:
         t0 = time.perf_counter()
-        lu = _DeviceLU(host_lu, keep_levels=tail, inverse=mode, helper_nnz=hz)
+        lu = _DeviceLU(host_lu, keep_levels=tail, inverse=mode, helper_nnz=hz, **kw)
         t.cuda.synchronize()
         setup = time.perf_counter() - t0
         x = L.empty(lu.n, t.float64)
@@ -53,7 +55,7 @@ def main():
         tu = timeit(lambda: lu._tri(lu.sU, lu.U, lu.diag, bu, lu.w, s))
         tp = timeit(lambda: lu.solve(b, x))
         err = np.abs(x.cpu().numpy() - ref).max() / np.abs(ref).max()
-        print(f"keep {tail:3d} rows {lu.group_rows:6d} phases {lu.sL.n_phases}/{lu.sU.n_phases} inverse {lu.sL.inverse} helper {hz} tasks {lu.sL.ntasks}/{lu.sU.ntasks}: L {tl:.3f} ms  U {tu:.3f} ms  precond {tp:.3f} ms  vs SuperLU {err:.2e}  "
+        print(f"keep {tail:3d} rows {lu.group_rows:6d} phases {lu.sL.n_phases}/{lu.sU.n_phases} inverse {lu.sL.inverse} helper {hz} {kw} tasks {lu.sL.ntasks}/{lu.sU.ntasks}: L {tl:.3f} ms  U {tu:.3f} ms  precond {tp:.3f} ms  vs SuperLU {err:.2e}  "
               f"depth L {lu.sL.depth} U {lu.sU.depth}  bytes {lu.solve_bytes / 1e6:.0f} MB  setup {setup:.1f} s",
               flush=True)
         del lu, x
