@@ -196,16 +196,17 @@ def measure_dfma_peak(L):
 
 class LaunchCounter:
     """Kernels each libhn entry point launches (fixed per call; see csrc/*.cu)."""
-    # hn_pressure_solve: 6 set-up kernels + one WHILE-body pass (12 Krylov kernels + 2
-    # preconditioner applications; the complete-LU preconditioner converges at its first
-    # half-step check, the second application's kernels launch and return) + 1 finish kernel.
-    # One application = 2 permutes + per factor (reset + task kernel + 2 kernels per dense-group
-    # phase): 31 without groups; steps_measure sets the entry from the factors' phase counts.
+    # hn_pressure_solve: 6 set-up kernels + one WHILE-body pass + 1 finish kernel.  The
+    # complete-LU preconditioner converges at its first half-step check, so a pass is its
+    # first half (7 Krylov kernels + 1 preconditioner application), the IF-condition kernel and
+    # the end-of-pass kernel; the second half sits in an IF node that is not entered.  One
+    # application = 2 permutes + per factor (reset + task kernel + 2 kernels per dense-group
+    # phase); steps_measure sets the entry from the factors' phase counts.
     KERNELS = {"hn_celllist_build": 5, "hn_partition_methods": 6, "hn_sptrsv_super": 2,
                "hn_knn": 1, "hn_knn_spacing": 1, "hn_classify": 1, "hn_mon_stencils": 1, "hn_weights_mon": 2,
                "hn_weights_rbf": 1, "hn_apply_ell": 1, "hn_momentum": 1, "hn_div_rhs": 1,
                "hn_correct_temperature": 1, "hn_temperature_bc": 1, "hn_csr_matvec": 1, "hn_csr_residual": 1,
-               "hn_pressure_solve": 31, "hn_permute": 1, "hn_reduce": 2, "hn_bicg_update": 1, "hn_bench_dfma": 1}
+               "hn_pressure_solve": 22, "hn_permute": 1, "hn_reduce": 2, "hn_bicg_update": 1, "hn_bench_dfma": 1}
 
     def __init__(self, L):
         self.L = L
@@ -554,7 +555,7 @@ def steps_measure(args, rank, world, cfg=3, flush=None, with_cpu=True):
     stepper, ops, dt = _stepper(hn, ns, True, Ra, rbf_n=30 if cfg == 4 else None)
     t_setup = time.perf_counter() - t_setup
     lu_dev = ops._d_lu
-    counter.KERNELS = dict(counter.KERNELS, hn_pressure_solve=19 + 2 * (6 + 2 * (lu_dev.sL.n_phases + lu_dev.sU.n_phases)),
+    counter.KERNELS = dict(counter.KERNELS, hn_pressure_solve=16 + (6 + 2 * (lu_dev.sL.n_phases + lu_dev.sU.n_phases)),
                            hn_sptrsv_plan=2 + 2 * max(lu_dev.sL.n_phases, lu_dev.sU.n_phases))
     steps = args.steps_steps
     # a step is one CUDA-graph replay (no libhn call from the host), so the kernels of a step

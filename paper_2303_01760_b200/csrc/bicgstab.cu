@@ -325,6 +325,12 @@ __global__ void end_pass_kernel(double* __restrict__ sc, int* __restrict__ st, i
   if constexpr (GRAPH) cudaGraphSetConditional(cond, st[kDone] ? 0u : 1u);
 }
 
+// the IF condition around a pass's second half: it runs only while the solve is not done
+// (the complete-LU preconditioner converges at the first half-step check of nearly every step)
+__global__ void second_half_cond_kernel(const int* __restrict__ st, cudaGraphConditionalHandle cond) {
+  if (threadIdx.x == 0) cudaGraphSetConditional(cond, st[kDone] ? 0u : 1u);
+}
+
 // after the loop: special right-hand sides, status out
 __global__ void finish_kernel(double* __restrict__ x, const double* __restrict__ b, int64_t n,
                               const int* __restrict__ st, int* __restrict__ status) {
@@ -355,7 +361,8 @@ struct PressureSolver {
   double *r = nullptr, *rt = nullptr, *p = nullptr, *phat = nullptr, *v = nullptr, *shat = nullptr, *t = nullptr;
   double *part = nullptr, *sc = nullptr;
   int* st = nullptr;
-  cudaStream_t cap = nullptr;  // private capture stream for the loop body
+  cudaStream_t cap = nullptr;   // private capture stream for the loop body
+  cudaStream_t cap2 = nullptr;  // ... and for the IF body inside it (a pass's second half)
   // cached standalone graph (calls outside a stream capture)
   cudaGraphExec_t exec = nullptr;
   const double* kb = nullptr;
@@ -462,12 +469,50 @@ cudaError_t enqueue_pass(PressureSolver& S, double* x, double rtol, int maxiter,
   s_update_kernel<<<kParts, kThr, 0, c>>>(S.r, S.v, n, S.sc, S.part, S.st);
   ctrl_kernel<kCtrlHalf><<<1, kThr, 0, c>>>(S.part, S.sc, S.st, rtol);
   half_x_kernel<<<kParts, kThr, 0, c>>>(x, S.phat, n, S.sc, S.st);
-  if (e == cudaSuccess) e = precond(S, S.r, S.shat, c);
-  matvec_dot_kernel<<<kParts, kThr, 0, c>>>(S.a_rowptr, S.a_cols, S.a_vals, S.shat, n, S.t, S.r, S.t, S.part, S.st);
-  ctrl_kernel<kCtrlOmega><<<1, kThr, 0, c>>>(S.part, S.sc, S.st, rtol);
-  xr_update_kernel<<<kParts, kThr, 0, c>>>(x, S.phat, S.shat, S.r, S.t, S.rt, n, S.sc, S.part, S.st);
-  end_pass_kernel<GRAPH><<<1, 32, 0, c>>>(S.sc, S.st, maxiter, cond);
   if (e != cudaSuccess) return e;
+  auto second_half = [&](cudaStream_t q) {
+    cudaError_t e2 = precond(S, S.r, S.shat, q);
+    matvec_dot_kernel<<<kParts, kThr, 0, q>>>(S.a_rowptr, S.a_cols, S.a_vals, S.shat, n, S.t, S.r, S.t, S.part, S.st);
+    ctrl_kernel<kCtrlOmega><<<1, kThr, 0, q>>>(S.part, S.sc, S.st, rtol);
+    xr_update_kernel<<<kParts, kThr, 0, q>>>(x, S.phat, S.shat, S.r, S.t, S.rt, n, S.sc, S.part, S.st);
+    return e2;
+  };
+  if constexpr (GRAPH) {
+    // the second half as the body of an IF node (nested in the WHILE body): when the half-step
+    // check converged -- nearly every step -- its ~27 kernels are not launched at all instead
+    // of launching and returning
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    if ((e = cudaStreamGetCaptureInfo(c, &cs, nullptr, &g, &deps, &ndeps)) != cudaSuccess) return e;
+    if (cs != cudaStreamCaptureStatusActive) return cudaErrorStreamCaptureInvalidated;
+    cudaGraphConditionalHandle cond2;
+    if ((e = cudaGraphConditionalHandleCreate(&cond2, g, 0, 0)) != cudaSuccess) return e;
+    second_half_cond_kernel<<<1, 32, 0, c>>>(S.st, cond2);
+    if ((e = cudaStreamGetCaptureInfo(c, &cs, nullptr, &g, &deps, &ndeps)) != cudaSuccess) return e;
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond2;
+    np.conditional.type = cudaGraphCondTypeIf;
+    np.conditional.size = 1;
+    cudaGraphNode_t ifnode;
+    if ((e = cudaGraphAddNode(&ifnode, g, deps, ndeps, &np)) != cudaSuccess) return e;
+    cudaGraph_t ifbody = np.conditional.phGraph_out[0];
+    if ((e = cudaStreamBeginCaptureToGraph(S.cap2, ifbody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) !=
+        cudaSuccess)
+      return e;
+    e = second_half(S.cap2);
+    cudaError_t e3 = cudaStreamEndCapture(S.cap2, &ifbody);
+    if (e != cudaSuccess) return e;
+    if (e3 != cudaSuccess) return e3;
+    if ((e = cudaStreamUpdateCaptureDependencies(c, &ifnode, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
+      return e;
+  } else {
+    e = second_half(c);
+    if (e != cudaSuccess) return e;
+  }
+  end_pass_kernel<GRAPH><<<1, 32, 0, c>>>(S.sc, S.st, maxiter, cond);
   return cudaGetLastError();
 }
 
@@ -507,6 +552,7 @@ HN_EXPORT int hn_pressure_setup(int64_t n, const int64_t* a_rowptr, const int* a
   if (e == cudaSuccess) e = cudaMemset(S->p, 0, sizeof(double) * n);
   if (e == cudaSuccess) e = cudaMemset(S->v, 0, sizeof(double) * n);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&S->cap, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&S->cap2, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     *handle_out = reinterpret_cast<int64_t>(S);
     return -static_cast<int>(e);
@@ -580,6 +626,7 @@ HN_EXPORT int hn_pressure_free(int64_t handle) {
                   static_cast<void*>(S->sc), static_cast<void*>(S->st), static_cast<void*>(S->ticket)})
     if (q) cudaFree(q);
   if (S->cap) cudaStreamDestroy(S->cap);
+  if (S->cap2) cudaStreamDestroy(S->cap2);
   delete S;
   return 0;
 }
