@@ -174,11 +174,15 @@ __global__ void __launch_bounds__(kThr) matvec_dot_kernel(const int64_t* __restr
   __shared__ double sm[32];
   if (st[kDone]) return;
   double s1 = 0.0, s2 = 0.0;
+  // a2 may be y itself (t.t of the omega step): the product then uses the value just formed --
+  // reading it back through the restrict-qualified a2 may be scheduled before the store to y
+  // and return the previous contents of the buffer
+  const bool a2_is_y = a2 == y;
   GRID_LOOP(i, n) {
     const double v = row_dot(rowptr, cols, vals, x, i);
     y[i] = v;
     s1 += a1[i] * v;
-    if (a2) s2 += a2[i] * v;
+    if (a2) s2 += (a2_is_y ? v : a2[i]) * v;
   }
   s1 = block_sum(s1, sm);
   if (a2) s2 = block_sum(s2, sm);
